@@ -1,0 +1,161 @@
+"""Seeded synthetic workloads for the five BASELINE.json configs.
+
+Shapes and distributions (BASELINE.json `configs`):
+
+  tiny_a / tiny_b  N=2^12, q = 40/30/30-bit + one 40-bit special prime,
+                   Delta = 2^30, lookup level 2.  tiny_a: one 256x16 table,
+                   U[-1,1], never compressed.  tiny_b: the same index, base 16,
+                   two 16x16 sub-tables U[-1,1].  Index ~ U{0..255}.
+  uci              N=2^14, 8x40-bit q + 2x40-bit p, Delta = 2^36, level 7.
+                   Vocab [2,2,3,4,4,5,8,16], d=16, entries N(0, 0.1^2),
+                   base 4; 13 dense features U[0,1].
+  criteo           N=2^16, 24x50-bit q + 4x50-bit p (dnum 6), Delta = 2^40,
+                   level 23.  26 tables, CRITEO_VOCAB below, d=16, entries
+                   N(0, 0.05^2), base 64; indices Zipf(1.1) per table.
+  llm              N=2^16, 20x50-bit q + 4x50-bit p (dnum 5), Delta = 2^40,
+                   level 19.  One 50257x768 table compressed base 256 into
+                   2 sub-tables 256x768, entries N(0, 0.02^2); 128 token ids
+                   U[0, 50257); layout L2 (token stride 1024 in and out).
+  microbench       N=2^16, Criteo's primes; 1024 ciphertexts of uniform limbs
+                   (drawn by the D9 PRNG, purpose 9 -- see microbench_seed).
+
+Draw order from numpy.random.default_rng(seed): table weights in block order,
+then indices (query-major, block order within a query), then dense features.
+No arithmetic of the method lives here (no digit decomposition, packing,
+encoding or modular arithmetic).  `subtable_rows` is the one shape rule the
+generator needs to know how many rows to draw; both the oracle and the
+library re-derive and check it independently.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+# Criteo-shaped vocabulary: the first seed s >= 0 for
+# which round(exp(default_rng(s).uniform(ln 3, ln 1e7, 26))) sums into
+# [3.25e7, 3.35e7] with max <= 1e7 is s = 230; stored so that a NumPy stream
+# change cannot alter it (tests/test_synth.py re-derives it).
+CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431, 2246483,
+                415, 9, 213122, 1215, 66731, 214456, 425, 55, 240, 3613143, 4875, 17,
+                495595, 10, 822, 1375]
+CRITEO_VOCAB_SEED = 230
+
+CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "llm", "microbench")
+
+
+def subtable_rows(k: int, p: int) -> int:
+    """Number of weight rows drawn for a table of k rows at base p.
+
+    k rows if the table stays uncompressed (p == 0 or k <= p), else p * l with
+    l the smallest integer such that p**l >= k (section 5.1).
+    """
+    if p == 0 or k <= p:
+        return k
+    l, cap = 1, p
+    while cap < k:
+        cap *= p
+        l += 1
+    return p * l
+
+
+@dataclasses.dataclass
+class Table:
+    k: int                      # rows of the (virtual) original table
+    d: int                      # embedding dimension
+    p: int                      # digit base, 0 = never compress
+    weights: np.ndarray         # (subtable_rows(k, p), d) float64, row-major
+    in_off: int = -1            # explicit input slot offset, -1 = contiguous default
+    out_off: int = -1           # explicit output slot offset, -1 = contiguous default
+    weight_id: int = -1         # blocks sharing one weight array carry the same id
+
+
+@dataclasses.dataclass
+class Config:
+    name: str
+    log_n: int
+    q_groups: List[Tuple[int, int]]   # (bits, count) ciphertext groups, in order
+    p_groups: List[Tuple[int, int]]   # (bits, count) special group(s)
+    log_scale: int
+    level: int
+    seed: int
+    batch: int = 1
+
+    @property
+    def N(self) -> int:
+        return 1 << self.log_n
+
+    @property
+    def n_slots(self) -> int:
+        return 1 << (self.log_n - 1)
+
+
+@dataclasses.dataclass
+class Workload:
+    config: Config
+    tables: List[Table]
+    n_dense: int
+    indices: np.ndarray               # (batch, n_blocks) int64
+    dense: np.ndarray                 # (batch, n_dense) float64
+
+
+_CONFIGS = {
+    "tiny_a": Config("tiny_a", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    "tiny_b": Config("tiny_b", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    "uci": Config("uci", 14, [(40, 8)], [(40, 2)], 36, 7, 1),
+    "criteo": Config("criteo", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
+    "criteo_b64": Config("criteo_b64", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=64),
+    "llm": Config("llm", 16, [(50, 20)], [(50, 4)], 40, 19, 1),
+    "microbench": Config("microbench", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=1024),
+}
+
+
+def config_by_name(name: str) -> Config:
+    return dataclasses.replace(_CONFIGS[name])
+
+
+def _zipf_index(rng: np.random.Generator, k: int, a: float = 1.1) -> int:
+    while True:
+        r = int(rng.zipf(a))
+        if r <= k:
+            return r - 1
+
+
+def make_workload(name: str, batch: Optional[int] = None) -> Workload:
+    cfg = config_by_name(name)
+    if batch is not None:
+        cfg.batch = batch
+    rng = np.random.default_rng(cfg.seed)
+    B = cfg.batch
+    if name in ("tiny_a", "tiny_b"):
+        if name == "tiny_a":
+            w = rng.uniform(-1.0, 1.0, size=(256, 16))
+            tables = [Table(256, 16, 0, w)]
+        else:
+            w = rng.uniform(-1.0, 1.0, size=(subtable_rows(256, 16), 16))
+            tables = [Table(256, 16, 16, w)]
+        idx = rng.integers(0, 256, size=(B, 1))
+        return Workload(cfg, tables, 0, idx.astype(np.int64), np.zeros((B, 0)))
+    if name == "uci":
+        vocab = [2, 2, 3, 4, 4, 5, 8, 16]
+        tables = [Table(k, 16, 4, rng.normal(0.0, 0.1, size=(subtable_rows(k, 4), 16))) for k in vocab]
+        idx = np.array([[rng.integers(0, k) for k in vocab] for _ in range(B)], dtype=np.int64)
+        dense = rng.uniform(0.0, 1.0, size=(B, 13))
+        return Workload(cfg, tables, 13, idx, dense)
+    if name in ("criteo", "criteo_b64"):
+        tables = [Table(k, 16, 64, rng.normal(0.0, 0.05, size=(subtable_rows(k, 64), 16))) for k in CRITEO_VOCAB]
+        idx = np.array([[_zipf_index(rng, k) for k in CRITEO_VOCAB] for _ in range(B)], dtype=np.int64)
+        return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))
+    if name == "llm":
+        V, d, p, m, stride = 50257, 768, 256, 128, 1024
+        w = rng.normal(0.0, 0.02, size=(subtable_rows(V, p), d))
+        tables = [Table(V, d, p, w, in_off=stride * t, out_off=stride * t, weight_id=0) for t in range(m)]
+        idx = rng.integers(0, V, size=(B, m)).astype(np.int64)
+        return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))
+    raise KeyError(name)
+
+
+def microbench_seed() -> int:
+    """Seed of the microbench's uniform limbs (D9 purpose 9 streams)."""
+    return _CONFIGS["microbench"].seed

@@ -1,0 +1,225 @@
+"""Pins of the oracle's lookup layer (S0, D19-D22) against the paper's worked
+examples and counts, the plain definition (float64 gather / dense W x), and
+exact identities.  CPU only."""
+import types
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import core
+from oracle import lookup as lk
+
+
+def test_digit_decomposition_paper_examples():
+    assert lk.digit_decompose(14, 4, 2) == (2, 3)             # PAPER.md:329, Fig. 6
+    assert lk.digit_decompose(50256, 16, 4) == (0, 5, 4, 12)
+    assert lk.digit_decompose(0, 7, 3) == (0, 0, 0)
+    with pytest.raises(ValueError):
+        lk.digit_decompose(16, 4, 2)
+    assert lk.n_digits(10**6, 4) == 10
+    assert lk.n_digits(50257, 16) == 4 and lk.n_digits(50257, 256) == 2
+
+
+@pytest.mark.parametrize("p,l", [(2, 16), (4, 8), (16, 4), (256, 2), (7, 5)])
+def test_digit_recomposition_exhaustive(p, l):
+    for i in range(min(p ** l, 1 << 16)):
+        d = lk.digit_decompose(i, p, l)
+        assert sum(x * p ** t for t, x in enumerate(d)) == i and all(0 <= x < p for x in d)
+
+
+def test_uci_layout_paper_slot_count():
+    """5 dense + one-hots of widths [2,4,2,3,2,3,4,3] need 28
+    slots (uncompressed).  Our UCI-shaped config (BASELINE.json) instead has 13
+    dense and base-4 digits: widths [2,2,3,4,4,8,8,8], K = 52."""
+    paper = types.SimpleNamespace(n_dense=5, tables=[synth.Table(k, 4, 0, np.zeros((k, 4)))
+                                                     for k in [2, 4, 2, 3, 2, 3, 4, 3]])
+    assert lk.layout(paper).K == 28
+    lay = lk.layout(synth.make_workload("uci"))
+    assert [b.w for b in lay.blocks] == [2, 2, 3, 4, 4, 8, 8, 8] and lay.K == 52 and lay.M == 128
+
+
+def test_encode_query_invariants():
+    w = synth.make_workload("criteo")
+    lay = lk.layout(w)
+    x = lk.encode_query(lay, w.indices[0], w.dense[0])
+    assert lay.K == 4126 and x.sum() == 68
+    for b, i in zip(lay.blocks, w.indices[0]):
+        seg = x[b.I: b.I + b.w]
+        assert seg.sum() == b.l                              # popcount = l per segment
+        if b.compressed:
+            for t in range(b.l):
+                assert seg[t * b.p:(t + 1) * b.p].sum() == 1
+    with pytest.raises(ValueError):
+        lk.encode_query(lay, [10**8] * 26, [])
+
+
+@pytest.mark.parametrize("slots,cts", [(569545, 18), (2772109, 85), (128 * 512, 2), (1096, 1), (47759, 2)])
+def test_input_ciphertext_counts(slots, cts):
+    """PAPER.md:462-463, :472 (18 and 85 cts at n = 2^15), :553 (m p l / n = 2)."""
+    lay = lk.Layout([lk.Block(slots, 1, 0, False, 1, slots, 0, 0, np.zeros((1, 1)))], 0, slots, 1)
+    assert -(-lay.K // (1 << 15)) == cts
+    # the planner's own count
+    w = types.SimpleNamespace(n_dense=0, tables=[synth.Table(1, 1, 0, np.ones((1, 1)), in_off=slots - 1)])
+    mbar, O, C, diags = lk.hybrid_diagonals(lk.layout(w), 1 << 15)
+    assert C == cts
+
+
+def test_criteo_plan_matches_paper_diagonal_count():
+    """the 10^4x / 10^5x Criteo models have 512 non-zero
+    diagonals; our Criteo-shaped draw (26 tables of width <= 256, d = 16) under
+    the hybrid layout gives exactly 512, span 512 ->
+    n1 = 32, n2 = 16, <= 46 BSGS rotations."""
+    lay = lk.layout(synth.make_workload("criteo"))
+    plan = lk.make_plan(lay, 1 << 15, 23)
+    assert plan.n_diag == 512 and len(plan.u_slots) == 512
+    assert (plan.mbar, plan.O, plan.C, plan.n1, plan.n2, plan.t0) == (512, 1, 1, 32, [16], [0])
+    P = types.SimpleNamespace(n=1 << 15)
+    amts = plan.rotation_amounts(P)
+    bsgs = [a for a in amts if a < 512]
+    assert len(bsgs) <= 46 and len(bsgs) <= plan.n1 + plan.n2[0] - 2
+    assert len(amts) == 52                                   # 31 + 15 + 6 RotSum
+
+
+def test_uci_and_tiny_plans():
+    P = types.SimpleNamespace(n=1 << 13)
+    plan = lk.make_plan(lk.layout(synth.make_workload("uci")), 1 << 13, 7)
+    assert plan.n_diag == 98 and (plan.n1, plan.n2) == (16, [8]) and len(plan.rotation_amounts(P)) == 27
+    for name in ("tiny_a", "tiny_b"):
+        plan = lk.make_plan(lk.layout(synth.make_workload(name)), 1 << 11, 2)
+        assert plan.n_diag == 16 and (plan.n1, plan.n2) == (4, [4])
+        assert len(plan.rotation_amounts(types.SimpleNamespace(n=1 << 11))) == 13
+
+
+@pytest.mark.parametrize("name", ["tiny_a", "tiny_b", "uci", "criteo"])
+def test_plan_slot_simulation_equals_dense_matvec(name):
+    """The exact D19/D20 schedule run on float64 slots (ckks-vm semantics,
+    SPEC.md:101, :246) equals the dense W x and the gather, periodic in mbar."""
+    w = synth.make_workload(name)
+    lay = lk.layout(w)
+    n = w.config.n_slots
+    plan = lk.make_plan(lay, n, w.config.level)
+    rng = np.random.default_rng(0)
+    W = lk.dense_matrix(lay)
+    for trial in range(3):
+        x = rng.normal(size=lay.K) if trial else lk.encode_query(lay, w.indices[0], w.dense[0])
+        y = lk.simulate_plan_slots(plan, x, n)
+        assert np.abs(y[: lay.M] - W @ x).max() < 1e-9
+        assert np.abs(y[lay.M: plan.mbar]).max(initial=0) < 1e-12
+        assert np.allclose(y[: plan.mbar], y[plan.mbar: 2 * plan.mbar] if plan.mbar < n else y[: plan.mbar])
+    x = lk.encode_query(lay, w.indices[0], w.dense[0])
+    assert np.abs(W @ x - lk.gather(lay, w.indices[0])).max() < 1e-12
+
+
+def test_plan_scaled_llm_l2_layout():
+    """Scaled LLM-L2 (n = 2048, stride 128, shared 32x48 table, 64 tokens):
+    4 in / 4 out cts, 79 shared diagonals, t0 = -47 mod n."""
+    n, stride, rows, d, m = 2048, 128, 32, 48, 64
+    wts = np.random.default_rng(1).normal(size=(rows, d))
+    tables = [synth.Table(rows, d, 0, wts, in_off=stride * t, out_off=stride * t) for t in range(m)]
+    w = types.SimpleNamespace(n_dense=0, tables=tables)
+    lay = lk.layout(w)
+    plan = lk.make_plan(lay, n, 1)
+    assert (plan.C, plan.O, len(plan.u_slots)) == (4, 4, 79) and plan.t0[0] == n - 47
+    x = np.random.default_rng(2).normal(size=lay.K)
+    y = lk.simulate_plan_slots(plan, x, n)
+    assert np.abs(y[: lay.M] - lk.dense_matrix(lay) @ x).max() < 1e-9
+
+
+def test_hs_and_bsgs_agree_on_random_matrices():
+    """Halevi-Shoup (n1 = 1, every offset a giant) == BSGS == dense."""
+    rng = np.random.default_rng(3)
+    for trial in range(20):
+        k, d = int(rng.integers(1, 40)), int(rng.integers(1, 20))
+        w = types.SimpleNamespace(n_dense=int(rng.integers(0, 5)),
+                                  tables=[synth.Table(k, d, 0, rng.normal(size=(k, d)))])
+        lay = lk.layout(w)
+        n = 64
+        x = rng.normal(size=lay.K)
+        ref = lk.dense_matrix(lay) @ x
+        for n1 in (1, 0, 2, 8):
+            y = lk.simulate_plan_slots(lk.make_plan(lay, n, 1, n1=n1), x, n)
+            assert np.abs(y[: lay.M] - ref).max() < 1e-9
+
+
+def test_digit_decomposition_identity_exhaustive():
+    """North star: per-digit partial lookups sum to the full lookup, which is
+    E^[i] = sum_t T_t[digit_t(i)] -- exact on plaintext slots, all i of Tiny-B."""
+    w = synth.make_workload("tiny_b")
+    lay = lk.layout(w)
+    b = lay.blocks[0]
+    W = lk.dense_matrix(lay)
+    for i in range(256):
+        x = lk.encode_query(lay, [i], [])
+        full = W @ x
+        parts = np.zeros_like(full)
+        for t in range(b.l):
+            xt = np.zeros_like(x)
+            seg = slice(b.I + t * b.p, b.I + (t + 1) * b.p)
+            xt[seg] = x[seg]
+            parts += W @ xt
+        assert np.array_equal(parts, full)
+        d = lk.digit_decompose(i, 16, 2)
+        assert np.array_equal(full, b.S[d[0]] + b.S[16 + d[1]])
+
+
+@pytest.fixture(scope="module")
+def uci_run():
+    return lk.run_config(synth.make_workload("uci"))
+
+
+@pytest.mark.parametrize("name", ["tiny_a", "tiny_b"])
+def test_tiny_lookup_decrypts_to_gather(name):
+    w = synth.make_workload(name)
+    run = lk.run_config(w)
+    out = run.outs[0][0]
+    assert out.level == w.config.level - 1 and out.scale == w.config.N // w.config.N * (1 << 30)
+    z = core.decrypt_decode(run.P, run.sk, out)
+    y = lk.gather(run.lay, w.indices[0])
+    assert np.abs(z[: run.lay.M] - y).max() < 1e-3
+    # slot s holds y[s mod mbar] everywhere (RotSum periodicity, R20)
+    mb = run.plan.mbar
+    zz = z.reshape(-1, mb)
+    assert np.abs(zz[:, : run.lay.M] - y).max() < 1e-3 and np.abs(zz[:, run.lay.M:]).max(initial=0) < 1e-3
+
+
+def test_uci_lookup_decrypts_to_gather_and_ignores_dense(uci_run):
+    run = uci_run
+    w = synth.make_workload("uci")
+    z = core.decrypt_decode(run.P, run.sk, run.outs[0][0])
+    y = lk.gather(run.lay, w.indices[0])
+    assert np.abs(z[: run.lay.M] - y).max() < 1e-3
+    # dense slots do not influence y (R19): change them, same decrypted result within noise
+    ct2 = lk.query_cts(run.P, run.pk, run.lay, run.plan, w.indices[0], 1 - w.dense[0], 7, 1, 0)
+    out2 = lk.lookup(run.P, run.plan, run.u_ntt, run.rk, ct2)[0]
+    z2 = core.decrypt_decode(run.P, run.sk, out2)
+    assert np.abs(z2[: run.lay.M] - y).max() < 1e-3
+
+
+def test_single_and_double_modes_agree(uci_run):
+    run = uci_run
+    w = synth.make_workload("uci")
+    plan_s = lk.make_plan(run.lay, run.P.n, 7, mode=lk.MODE_SINGLE)
+    u_s = lk.encode_plan(run.P, plan_s)
+    out_s = lk.lookup(run.P, plan_s, u_s, run.rk, run.cts[0])[0]
+    zs = core.decrypt_decode(run.P, run.sk, out_s)
+    zd = core.decrypt_decode(run.P, run.sk, run.outs[0][0])
+    assert np.abs(zs - zd).max() < 1e-3
+    assert not np.array_equal(out_s.c0, run.outs[0][0].c0)   # different bits, same values (D22)
+
+
+def test_per_digit_partial_lookups_sum_encrypted():
+    """The digit-decomposition identity under encryption (within noise)."""
+    w = synth.make_workload("tiny_b")
+    run = lk.run_config(w)
+    b = run.lay.blocks[0]
+    x = lk.encode_query(run.lay, w.indices[0], [])
+    total = np.zeros(run.P.n)
+    for t in range(b.l):
+        xt = np.zeros(run.P.n)
+        seg = slice(b.I + t * b.p, b.I + (t + 1) * b.p)
+        xt[seg] = x[seg]
+        ct = core.encrypt(run.P, run.pk, xt, 2, 1000 + t)
+        total += core.decrypt_decode(run.P, run.sk, lk.lookup(run.P, run.plan, run.u_ntt, run.rk, [ct])[0])
+    y = lk.gather(run.lay, w.indices[0])
+    assert np.abs(total[: run.lay.M] - y).max() < 2e-3
