@@ -1,0 +1,1359 @@
+// api.cu -- the C ABI (include/helrm.h): context and device tables, client
+// keys and ciphertexts, server setup (plan), and the lookup engine.
+//
+// The lookup (helrm_lookup) follows SURVEY.md D20 (double-hoisted BSGS,
+// PAPER.md:289, :584) step by step:
+//   L1 ModUp of each input c1 (hoist #1)        -> modup()
+//   L2 lazy baby steps (a_j, b_j) over Q_l P     -> launch_kip (fused phi + KIP)
+//   L3 inner sums with the pre-rotated diagonals  -> launch_diag_mac
+//   L4 giant steps: ModDown(B), ModUp, KIP, +phi(A) (hoist #2)
+//   L6 ModDown, L7 rescale, L8 RotSum
+// Every arithmetic step runs in the kernels of kernels_ntt.cu / kernels_rns.cu;
+// the host only schedules launches on the context stream.
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <set>
+#include <tuple>
+#include <unordered_map>
+
+#include "internal.h"
+
+using namespace helrm;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+helrm_status guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return HELRM_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return HELRM_ERR_ALLOC;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HELRM_ERR_ARG;
+  }
+}
+
+void need(bool ok, helrm_status code, const char* msg) {
+  if (!ok) throw Error(code, msg);
+}
+}  // namespace
+
+// ============================================================================
+// handles
+// ============================================================================
+struct helrm_params {
+  Params P;
+};
+
+struct ConvEntry {
+  ConvDev* d = nullptr;
+  int nt = 0;
+  std::vector<int16_t> rows;
+};
+
+struct LevelConst {
+  uint64_t* pmod = nullptr;       // [l+1] P mod q_i, shoup companions
+  uint64_t* pmods = nullptr;
+  uint64_t* pinv = nullptr;       // [l+1] P^-1 mod q_i
+  uint64_t* pinvs = nullptr;
+  uint64_t* qlinv = nullptr;      // [l] q_l^-1 mod q_i
+  uint64_t* qlinvs = nullptr;
+};
+
+struct helrm_ctx {
+  Params P;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<PrimeDev> hprimes;
+  PrimeDev* dprimes = nullptr;
+  uint64_t* dtw = nullptr;
+  uint32_t* dslotpos = nullptr;
+  uint64_t* dcdt = nullptr;
+  uint64_t* scratch = nullptr;
+  std::map<std::pair<int, int>, ConvEntry> conv;
+  std::map<int, LevelConst> lconst;
+  std::vector<void*> owned;       // device allocations freed at destroy
+  uint64_t launches = 0;
+  std::vector<uint32_t> dlog5;    // dlog5[g] for odd g < 2N (0xffffffff if not a power of 5)
+
+  DevCtx dc() { return DevCtx{dprimes, dslotpos, P.log_n, P.N, stream, &launches}; }
+
+  void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 8;
+    cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+    if (e != cudaSuccess) throw Error(HELRM_ERR_ALLOC, std::string("device allocation failed: ") + cudaGetErrorString(e));
+    return p;
+  }
+  void dfree(void* p) {
+    if (p) cudaFreeAsync(p, stream);
+  }
+  uint64_t* upload_u64(const std::vector<uint64_t>& v) {
+    uint64_t* d = (uint64_t*)dalloc(v.size() * 8);
+    HCUDA(cudaMemcpyAsync(d, v.data(), v.size() * 8, cudaMemcpyHostToDevice, stream));
+    HCUDA(cudaStreamSynchronize(stream));
+    owned.push_back(d);
+    return d;
+  }
+};
+
+// RAII device buffer on the context stream
+struct DBuf {
+  helrm_ctx* c;
+  uint64_t* p;
+  DBuf(helrm_ctx* c_, size_t words) : c(c_), p((uint64_t*)c_->dalloc(words * 8)) {}
+  ~DBuf() { c->dfree(p); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+
+struct helrm_sk {
+  helrm_ctx* c;
+  uint64_t* sntt;                 // [L+1+K][N]
+  std::vector<int64_t> s;         // coefficients (host copy)
+};
+struct helrm_pk {
+  helrm_ctx* c;
+  uint64_t* d;                    // [2][L+1][N]: b, a
+};
+struct helrm_rotkeys {
+  helrm_ctx* c;
+  std::map<uint64_t, uint64_t*> keys;   // galois -> [dnum][2][L+1+K][N]
+  size_t words_per_key = 0;
+};
+struct helrm_ct {
+  helrm_ctx* c;
+  uint32_t level;
+  double scale;
+  uint64_t* d;                    // [2][level+1][N]
+};
+
+struct Block {
+  int64_t k, d, p, l, w, I, R;
+  bool comp;
+  int wid;                        // index into weights store
+};
+struct helrm_tables {
+  Params P;
+  std::vector<Block> blocks;
+  std::vector<std::vector<double>> weights;
+  uint32_t n_dense;
+  int64_t K, M;
+};
+
+struct Entry {
+  int c, j, uid;
+};
+struct helrm_plan {
+  helrm_ctx* c;
+  uint32_t level, mode;
+  int64_t K, M, mbar, O, C, n1;
+  std::vector<int64_t> t0, span, n2;
+  std::vector<std::vector<std::vector<Entry>>> entries;  // [o][i]
+  std::vector<std::vector<int64_t>> giants;               // [o][i]
+  std::vector<std::vector<int>> babies;                   // [c] sorted j used
+  int64_t n_diag = 0;
+  uint64_t* diag = nullptr;                               // [n_unique][nl][N]
+  int64_t n_unique = 0;
+  uint32_t nl = 0;
+  std::vector<int64_t> rotations;
+};
+
+// ============================================================================
+// context helpers
+// ============================================================================
+static uint64_t* ct_c0(const helrm_ct* ct) { return ct->d; }
+static uint64_t* ct_c1(const helrm_ct* ct) { return ct->d + (size_t)(ct->level + 1) * ct->c->P.N; }
+
+static helrm_ct* new_ct(helrm_ctx* c, uint32_t level, double scale) {
+  helrm_ct* ct = new helrm_ct{c, level, scale, nullptr};
+  ct->d = (uint64_t*)c->dalloc((size_t)2 * (level + 1) * c->P.N * 8);
+  return ct;
+}
+
+static LimbMap sub_map(const LimbMap& m, int first, int count) {
+  LimbMap r{};
+  r.n = count;
+  for (int i = 0; i < count; i++) r.pr[i] = m.pr[first + i];
+  return r;
+}
+
+static void ntt_fwd(helrm_ctx* c, const uint64_t* src, uint64_t* dst, size_t n, const LimbMap& map) {
+  if (n) launch_ntt_fwd(c->dc(), src, dst, c->scratch, n, map);
+}
+static void ntt_inv(helrm_ctx* c, const uint64_t* src, uint64_t* dst, size_t n, const LimbMap& map) {
+  if (n) launch_ntt_inv(c->dc(), src, dst, c->scratch, n, map);
+}
+
+static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
+  auto it = c->lconst.find((int)l);
+  if (it != c->lconst.end()) return it->second;
+  const Params& P = c->P;
+  std::vector<uint64_t> pm(l + 1), pms(l + 1), pi(l + 1), pis(l + 1), qi(l + 1, 0), qis(l + 1, 0);
+  for (uint32_t i = 0; i <= l; i++) {
+    uint64_t q = P.primes[i], pmod = 1;
+    for (uint32_t j = 0; j < P.K; j++) pmod = mulm(pmod, P.primes[P.L + 1 + j] % q, q);
+    pm[i] = pmod;
+    pms[i] = shoup_pre(pmod, q);
+    pi[i] = inv_mod(pmod, q);
+    pis[i] = shoup_pre(pi[i], q);
+    if (i < l) {
+      qi[i] = inv_mod(P.primes[l] % q, q);
+      qis[i] = shoup_pre(qi[i], q);
+    }
+  }
+  LevelConst lc;
+  lc.pmod = c->upload_u64(pm);
+  lc.pmods = c->upload_u64(pms);
+  lc.pinv = c->upload_u64(pi);
+  lc.pinvs = c->upload_u64(pis);
+  lc.qlinv = c->upload_u64(qi);
+  lc.qlinvs = c->upload_u64(qis);
+  return c->lconst.emplace((int)l, lc).first->second;
+}
+
+// D14 tables: digit >= 0: ModUp digit at level l; digit = -1: ModDown P -> Q_l
+static const ConvEntry& conv_entry(helrm_ctx* c, uint32_t l, int digit) {
+  auto key = std::make_pair((int)l, digit);
+  auto it = c->conv.find(key);
+  if (it != c->conv.end()) return it->second;
+  const Params& P = c->P;
+  std::vector<uint32_t> src, tgt;
+  std::vector<int16_t> rows;
+  if (digit >= 0) {
+    uint32_t lo = digit * P.alpha, hi = std::min((uint32_t)(digit + 1) * P.alpha, l + 1);
+    for (uint32_t i = lo; i < hi; i++) src.push_back(i);
+    for (uint32_t r = 0; r < l + 1 + P.K; r++) {
+      if (r >= lo && r < hi) continue;
+      tgt.push_back(P.qp_chain(l, r));
+      rows.push_back((int16_t)r);
+    }
+  } else {
+    for (uint32_t j = 0; j < P.K; j++) src.push_back(P.L + 1 + j);
+    for (uint32_t r = 0; r <= l; r++) {
+      tgt.push_back(r);
+      rows.push_back((int16_t)r);
+    }
+  }
+  need(src.size() <= (size_t)kMaxDigitPrimes && tgt.size() <= (size_t)kMaxLimbs, HELRM_ERR_CONFIG, "too many primes");
+  ConvDev h{};
+  h.nb = (int)src.size();
+  h.nt = (int)tgt.size();
+  for (size_t b = 0; b < src.size(); b++) {
+    uint64_t qb = P.primes[src[b]], hat = 1;
+    for (size_t b2 = 0; b2 < src.size(); b2++)
+      if (b2 != b) hat = mulm(hat, P.primes[src[b2]] % qb, qb);
+    h.bpr[b] = (uint8_t)src[b];
+    h.binv[b] = inv_mod(hat, qb);
+    h.binvs[b] = shoup_pre(h.binv[b], qb);
+  }
+  for (size_t t = 0; t < tgt.size(); t++) {
+    uint64_t qt = P.primes[tgt[t]];
+    h.tpr[t] = (uint8_t)tgt[t];
+    for (size_t b = 0; b < src.size(); b++) {
+      uint64_t hat = 1;
+      for (size_t b2 = 0; b2 < src.size(); b2++)
+        if (b2 != b) hat = mulm(hat, P.primes[src[b2]] % qt, qt);
+      h.bmod[t][b] = hat;
+    }
+  }
+  ConvEntry e;
+  e.d = (ConvDev*)c->dalloc(sizeof(ConvDev));
+  HCUDA(cudaMemcpyAsync(e.d, &h, sizeof(ConvDev), cudaMemcpyHostToDevice, c->stream));
+  HCUDA(cudaStreamSynchronize(c->stream));
+  c->owned.push_back(e.d);
+  e.nt = h.nt;
+  e.rows = rows;
+  return c->conv.emplace(key, e).first->second;
+}
+
+// D15: in [l+1][N] NTT -> out [l+1+K][N] NTT
+static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t* out) {
+  const Params& P = c->P;
+  const size_t N = P.N;
+  const uint32_t lo = k * P.alpha, hi = std::min((uint32_t)(k + 1) * P.alpha, l + 1), nb = hi - lo;
+  const uint32_t nl = l + 1 + P.K;
+  need(lo <= l, HELRM_ERR_LEVEL, "digit beyond level");
+  DBuf x(c, nb * N);
+  ntt_inv(c, in + lo * N, x.p, nb, P.map_range(lo, nb));
+  const ConvEntry& ce = conv_entry(c, l, k);
+  launch_conv(c->dc(), ce.d, ce.nt, ce.rows.data(), x.p, out);
+  LimbMap m = P.map_qp(l);
+  ntt_fwd(c, out, out, lo, sub_map(m, 0, lo));
+  ntt_fwd(c, out + hi * N, out + hi * N, nl - hi, sub_map(m, hi, nl - hi));
+  HCUDA(cudaMemcpyAsync(out + lo * N, in + lo * N, nb * N * 8, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// D16: y [l+1+K][N] -> out [l+1][N]
+static void moddown(helrm_ctx* c, const uint64_t* y, uint32_t l, uint64_t* out) {
+  const Params& P = c->P;
+  const size_t N = P.N;
+  DBuf yp(c, P.K * N), t(c, (l + 1) * N);
+  ntt_inv(c, y + (l + 1) * N, yp.p, P.K, P.map_range(P.L + 1, P.K));
+  const ConvEntry& ce = conv_entry(c, l, -1);
+  launch_conv(c->dc(), ce.d, ce.nt, ce.rows.data(), yp.p, t.p);
+  ntt_fwd(c, t.p, t.p, l + 1, P.map_q(l));
+  const LevelConst& lc = level_const(c, l);
+  launch_sub_scale(c->dc(), y, t.p, out, P.map_q(l), lc.pinv, lc.pinvs);
+}
+
+// D17 on one polynomial x [l+1][N] -> out [l][N]
+static void rescale_poly(helrm_ctx* c, const uint64_t* x, uint32_t l, uint64_t* out) {
+  const Params& P = c->P;
+  const size_t N = P.N;
+  DBuf xl(c, N), r(c, l * N);
+  ntt_inv(c, x + l * N, xl.p, 1, P.map_range(l, 1));
+  launch_rescale_prep(c->dc(), xl.p, P.primes[l], r.p, P.map_q(l - 1));
+  ntt_fwd(c, r.p, r.p, l, P.map_q(l - 1));
+  const LevelConst& lc = level_const(c, l);
+  launch_sub_scale(c->dc(), x, r.p, out, P.map_q(l - 1), lc.qlinv, lc.qlinvs);
+}
+
+static uint32_t rot_of_galois(helrm_ctx* c, uint64_t g) {
+  need(g < 2 * (uint64_t)c->P.N && (g & 1), HELRM_ERR_CONFIG, "bad Galois element");
+  uint32_t r = c->dlog5[g];
+  need(r != 0xffffffffu, HELRM_ERR_CONFIG, "Galois element is not a power of 5");
+  return r;
+}
+
+static uint64_t galois_of_rot(helrm_ctx* c, int64_t k) {
+  const uint64_t n = c->P.n, twoN = 2 * (uint64_t)c->P.N;
+  uint64_t r = (uint64_t)(((k % (int64_t)n) + (int64_t)n) % (int64_t)n);
+  return pow_mod(5, r, twoN);
+}
+
+static const uint64_t* key_for(const helrm_rotkeys* rk, uint64_t g) {
+  auto it = rk->keys.find(g);
+  if (it == rk->keys.end()) throw Error(HELRM_ERR_LAYOUT, "missing rotation key for Galois element " + std::to_string(g));
+  return it->second;
+}
+
+// KS_g over precomputed digits D [dnum][l+1+K][N]; with c0 != null computes the
+// lazy rotation (P phi(c0) + KS0, KS1).
+static void kip(helrm_ctx* c, const uint64_t* D, uint32_t l, const helrm_rotkeys* rk, uint64_t g, const uint64_t* c0,
+                uint64_t* out0, uint64_t* out1, bool accumulate) {
+  const Params& P = c->P;
+  KipArgs a{};
+  a.digits = D;
+  a.dnum = (int)P.dnum(l);
+  a.key = key_for(rk, g);
+  a.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * P.N;
+  a.key_half_stride = (size_t)(P.L + 1 + P.K) * P.N;
+  a.c0 = c0;
+  a.p_mod = c0 ? level_const(c, l).pmod : nullptr;
+  a.rot = rot_of_galois(c, g);
+  a.out0 = out0;
+  a.out1 = out1;
+  a.accumulate = accumulate ? 1 : 0;
+  a.level = l;
+  launch_kip(c->dc(), a, P.map_qp(l));
+}
+
+static void modup_all(helrm_ctx* c, const uint64_t* c1, uint32_t l, uint64_t* D) {
+  const size_t nlN = (size_t)(l + 1 + c->P.K) * c->P.N;
+  for (uint32_t k = 0; k < c->P.dnum(l); k++) modup(c, c1, l, (int)k, D + k * nlN);
+}
+
+// Rotate(ct, k) from digits D of ct.c1 (hoisted): out = ModDown(P phi(c0) + KS0), ModDown(KS1)
+static void rotate_from_digits(helrm_ctx* c, const helrm_ct* in, const uint64_t* D, const helrm_rotkeys* rk, int64_t k,
+                               helrm_ct* out) {
+  const Params& P = c->P;
+  const uint32_t l = in->level;
+  const size_t N = P.N, nl = l + 1 + P.K;
+  const uint64_t g = galois_of_rot(c, k);
+  if (g == 1) {
+    HCUDA(cudaMemcpyAsync(out->d, in->d, (size_t)2 * (l + 1) * N * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return;
+  }
+  DBuf t0(c, nl * N), t1(c, nl * N);
+  kip(c, D, l, rk, g, ct_c0(in), t0.p, t1.p, false);
+  moddown(c, t0.p, l, ct_c0(out));
+  moddown(c, t1.p, l, ct_c1(out));
+}
+
+static void rotate(helrm_ctx* c, const helrm_ct* in, const helrm_rotkeys* rk, int64_t k, helrm_ct* out) {
+  const uint32_t l = in->level;
+  if (galois_of_rot(c, k) == 1) {
+    HCUDA(cudaMemcpyAsync(out->d, in->d, (size_t)2 * (l + 1) * c->P.N * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return;
+  }
+  DBuf D(c, (size_t)c->P.dnum(l) * (l + 1 + c->P.K) * c->P.N);
+  modup_all(c, ct_c1(in), l, D.p);
+  rotate_from_digits(c, in, D.p, rk, k, out);
+}
+
+static void ct_add_inplace(helrm_ctx* c, helrm_ct* acc, const helrm_ct* x) {
+  LimbMap m = c->P.map_q(acc->level);
+  launch_binary(c->dc(), 0, ct_c0(acc), ct_c0(x), ct_c0(acc), m);
+  launch_binary(c->dc(), 0, ct_c1(acc), ct_c1(x), ct_c1(acc), m);
+}
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* helrm_last_error(void) { return g_last_error.c_str(); }
+const char* helrm_version(void) { return "helrm-b200 0.1 (sm_100a)"; }
+
+helrm_status helrm_params_create(const helrm_params_desc* d, helrm_params** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(d && out, HELRM_ERR_ARG, "null argument");
+    need(d->log_n >= 10 && d->log_n <= 16, HELRM_ERR_CONFIG, "log_n must be in [10, 16]");
+    std::vector<std::pair<uint32_t, uint32_t>> qg, pg;
+    need(d->n_q_groups >= 1 && d->n_q_groups <= 8 && d->n_p_groups >= 1 && d->n_p_groups <= 4, HELRM_ERR_CONFIG,
+         "bad prime group counts");
+    for (uint32_t i = 0; i < d->n_q_groups; i++) qg.push_back({d->q_bits[i], d->q_count[i]});
+    for (uint32_t i = 0; i < d->n_p_groups; i++) pg.push_back({d->p_bits[i], d->p_count[i]});
+    Params P;
+    P.log_n = d->log_n;
+    P.N = 1u << d->log_n;
+    P.n = P.N / 2;
+    auto q = find_primes(qg, P.N, {});
+    auto p = find_primes(pg, P.N, q);
+    need(q.size() + p.size() <= (size_t)kMaxLimbs, HELRM_ERR_CONFIG, "too many primes");
+    need(p.size() <= (size_t)kMaxDigitPrimes, HELRM_ERR_CONFIG, "at most 8 special primes");
+    P.L = (uint32_t)q.size() - 1;
+    P.K = (uint32_t)p.size();
+    P.alpha = P.K;
+    P.log_scale = d->log_scale;
+    need(d->log_scale >= 1 && d->log_scale < 62, HELRM_ERR_CONFIG, "bad log_scale");
+    P.primes = q;
+    P.primes.insert(P.primes.end(), p.begin(), p.end());
+    for (uint64_t x : P.primes) P.psi.push_back(min_psi(x, P.N));
+    *out = new helrm_params{P};
+  });
+}
+
+void helrm_params_destroy(helrm_params* p) { delete p; }
+
+helrm_status helrm_params_info(const helrm_params* p, helrm_params_info_t* out) {
+  return guard([&] {
+    need(p && out, HELRM_ERR_ARG, "null argument");
+    *out = {p->P.N, p->P.n, p->P.L, p->P.K, p->P.dnum(p->P.L), p->P.log_scale};
+  });
+}
+
+helrm_status helrm_params_moduli(const helrm_params* p, uint64_t* q, uint64_t* pp, uint64_t* psi) {
+  return guard([&] {
+    need(p, HELRM_ERR_ARG, "null argument");
+    const Params& P = p->P;
+    if (q) std::copy(P.primes.begin(), P.primes.begin() + P.L + 1, q);
+    if (pp) std::copy(P.primes.begin() + P.L + 1, P.primes.end(), pp);
+    if (psi) std::copy(P.psi.begin(), P.psi.end(), psi);
+  });
+}
+
+helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t stream, helrm_ctx** out) {
+  if (out) *out = nullptr;
+  helrm_ctx* c = nullptr;
+  helrm_status st = guard([&] {
+    need(p && out, HELRM_ERR_ARG, "null argument");
+    HCUDA(cudaSetDevice(device));
+    c = new helrm_ctx();
+    c->P = p->P;
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    cudaMemPool_t pool;
+    HCUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    HCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    const Params& P = c->P;
+    const size_t N = P.N, np = P.primes.size();
+    // twiddles: per prime 4 arrays of N words
+    std::vector<uint64_t> tw(np * 4 * N);
+    std::vector<uint32_t> br(N);
+    for (uint32_t k = 0; k < N; k++) {
+      uint32_t r = 0;
+      for (uint32_t b = 0; b < P.log_n; b++) r |= ((k >> b) & 1u) << (P.log_n - 1 - b);
+      br[k] = r;
+    }
+#pragma omp parallel for
+    for (size_t i = 0; i < np; i++) {
+      uint64_t q = P.primes[i], psi = P.psi[i], ipsi = inv_mod(psi, q);
+      uint64_t* w = &tw[i * 4 * N];
+      std::vector<uint64_t> pw(N), ipw(N);
+      pw[0] = ipw[0] = 1;
+      for (size_t k = 1; k < N; k++) {
+        pw[k] = mulm(pw[k - 1], psi, q);
+        ipw[k] = mulm(ipw[k - 1], ipsi, q);
+      }
+      for (size_t k = 0; k < N; k++) {
+        w[k] = pw[br[k]];
+        w[N + k] = shoup_pre(w[k], q);
+        w[2 * N + k] = ipw[br[k]];
+        w[3 * N + k] = shoup_pre(w[2 * N + k], q);
+      }
+    }
+    c->dtw = c->upload_u64(tw);
+    c->hprimes.resize(np);
+    for (size_t i = 0; i < np; i++) {
+      PrimeDev& d = c->hprimes[i];
+      uint64_t q = P.primes[i];
+      d.rc.q = q;
+      d.rc.mu = (uint64_t)(~0ull / q);
+      d.rc.r64 = (uint64_t)(((unsigned __int128)1 << 64) % q);
+      d.rc.r64s = shoup_pre(d.rc.r64, q);
+      d.ninv = inv_mod(N % q, q);
+      d.ninvs = shoup_pre(d.ninv, q);
+      d.tw = c->dtw + i * 4 * N;
+      d.tws = d.tw + N;
+      d.itw = d.tw + 2 * N;
+      d.itws = d.tw + 3 * N;
+    }
+    c->dprimes = (PrimeDev*)c->dalloc(np * sizeof(PrimeDev));
+    c->owned.push_back(c->dprimes);
+    HCUDA(cudaMemcpyAsync(c->dprimes, c->hprimes.data(), np * sizeof(PrimeDev), cudaMemcpyHostToDevice, c->stream));
+    auto sp = slot_of_bitrev(P.log_n);
+    c->dslotpos = (uint32_t*)c->dalloc(N * 4);
+    c->owned.push_back(c->dslotpos);
+    HCUDA(cudaMemcpyAsync(c->dslotpos, sp.data(), N * 4, cudaMemcpyHostToDevice, c->stream));
+    c->dcdt = c->upload_u64(gauss_cdt_table());
+    c->scratch = (uint64_t*)c->dalloc(ntt_scratch_words(P.log_n) * 8);
+    c->owned.push_back(c->scratch);
+    c->dlog5.assign(2 * N, 0xffffffffu);
+    uint64_t e = 1;
+    for (uint32_t j = 0; j < P.n; j++) {
+      c->dlog5[e] = j;
+      e = e * 5 % (2 * N);
+    }
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = c;
+  });
+  if (st != HELRM_OK) delete c;
+  return st;
+}
+
+void helrm_ctx_destroy(helrm_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  for (void* p : c->owned) cudaFreeAsync(p, c->stream);
+  cudaStreamSynchronize(c->stream);
+  delete c;
+}
+
+helrm_status helrm_ctx_sync(helrm_ctx* c) {
+  return guard([&] {
+    need(c, HELRM_ERR_ARG, "null argument");
+    HCUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+uint64_t helrm_ctx_launches(const helrm_ctx* c) { return c ? c->launches : 0; }
+
+// ---------------------------------------------------------------------------
+// keys
+// ---------------------------------------------------------------------------
+static void sample_small_ntt(helrm_ctx* c, uint64_t seed, uint64_t stream, int kind, uint64_t* out, const LimbMap& m,
+                             int64_t* keep = nullptr) {
+  const size_t N = c->P.N;
+  DBuf s(c, N);
+  launch_sample_small(c->dc(), (int64_t*)s.p, prng_base(seed, stream), kind, c->dcdt);
+  launch_reduce_signed(c->dc(), (int64_t*)s.p, out, m);
+  if (keep) {
+    HCUDA(cudaMemcpyAsync(keep, s.p, N * 8, cudaMemcpyDeviceToHost, c->stream));
+    HCUDA(cudaStreamSynchronize(c->stream));
+  }
+  ntt_fwd(c, out, out, m.n, m);
+}
+
+helrm_status helrm_sk_gen(helrm_ctx* c, uint64_t seed, helrm_sk** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && out, HELRM_ERR_ARG, "null argument");
+    const Params& P = c->P;
+    helrm_sk* sk = new helrm_sk{c, nullptr, std::vector<int64_t>(P.N)};
+    const uint32_t nall = P.L + 1 + P.K;
+    sk->sntt = (uint64_t*)c->dalloc((size_t)nall * P.N * 8);
+    sample_small_ntt(c, seed, prng_stream(1, 0, 0, 0), 0, sk->sntt, P.map_range(0, nall), sk->s.data());
+    *out = sk;
+  });
+}
+
+void helrm_sk_destroy(helrm_sk* s) {
+  if (!s) return;
+  s->c->dfree(s->sntt);
+  delete s;
+}
+
+helrm_status helrm_pk_gen(helrm_ctx* c, const helrm_sk* sk, uint64_t seed, helrm_pk** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && sk && out, HELRM_ERR_ARG, "null argument");
+    const Params& P = c->P;
+    const size_t N = P.N, nq = P.L + 1;
+    helrm_pk* pk = new helrm_pk{c, (uint64_t*)c->dalloc(2 * nq * N * 8)};
+    uint64_t* b = pk->d;
+    uint64_t* a = pk->d + nq * N;
+    LimbMap m = P.map_q(P.L);
+    launch_sample_uniform_ntt(c->dc(), a, m, seed, 2, 0, 0, m);
+    DBuf e(c, nq * N), t(c, nq * N);
+    sample_small_ntt(c, seed, prng_stream(3, 0, 0, 0), 1, e.p, m);
+    launch_binary(c->dc(), 2, a, sk->sntt, t.p, m);   // a s
+    launch_binary(c->dc(), 1, e.p, t.p, b, m);        // e - a s
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = pk;
+  });
+}
+
+void helrm_pk_destroy(helrm_pk* p) {
+  if (!p) return;
+  p->c->dfree(p->d);
+  delete p;
+}
+
+helrm_status helrm_rotkeys_gen(helrm_ctx* c, const helrm_sk* sk, const uint64_t* galois, size_t n, uint64_t seed,
+                               helrm_rotkeys** out) {
+  if (out) *out = nullptr;
+  helrm_rotkeys* rk = nullptr;
+  helrm_status st = guard([&] {
+    need(c && sk && out && (galois || n == 0), HELRM_ERR_ARG, "null argument");
+    const Params& P = c->P;
+    const size_t N = P.N, nall = P.L + 1 + P.K, dn = P.dnum(P.L);
+    rk = new helrm_rotkeys{c, {}, dn * 2 * nall * N};
+    LimbMap m = P.map_range(0, (uint32_t)nall);
+    DBuf e(c, nall * N), t(c, nall * N), phis(c, nall * N);
+    const LevelConst& lc = level_const(c, P.L);
+    for (size_t gi = 0; gi < n; gi++) {
+      const uint64_t g = galois[gi];
+      if (rk->keys.count(g)) continue;
+      const uint32_t r = rot_of_galois(c, g);
+      uint64_t* key = (uint64_t*)c->dalloc(rk->words_per_key * 8);
+      rk->keys[g] = key;
+      launch_automorph(c->dc(), sk->sntt, phis.p, m, r, 0);   // phi_g(s)
+      for (size_t k = 0; k < dn; k++) {
+        uint64_t* b = key + k * 2 * nall * N;
+        uint64_t* a = b + nall * N;
+        launch_sample_uniform_ntt(c->dc(), a, m, seed, 4, g, k, m);
+        sample_small_ntt(c, seed, prng_stream(5, g, k, 0), 1, e.p, m);
+        launch_binary(c->dc(), 2, a, sk->sntt, t.p, m);
+        launch_binary(c->dc(), 1, e.p, t.p, b, m);            // -a s + e
+        // + [q_i in digit k] [P]_{q_i} phi_g(s)
+        const uint32_t lo = k * P.alpha, hi = std::min((uint32_t)(k + 1) * P.alpha, P.L + 1);
+        LimbMap dm = P.map_range(lo, hi - lo);
+        launch_scalar_mul(c->dc(), phis.p + lo * N, t.p, dm, lc.pmod + lo, lc.pmods + lo);
+        launch_binary(c->dc(), 0, b + lo * N, t.p, b + lo * N, dm);
+      }
+    }
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = rk;
+  });
+  if (st != HELRM_OK && rk) helrm_rotkeys_destroy(rk);
+  return st;
+}
+
+void helrm_rotkeys_destroy(helrm_rotkeys* r) {
+  if (!r) return;
+  for (auto& kv : r->keys) r->c->dfree(kv.second);
+  delete r;
+}
+
+size_t helrm_rotkeys_bytes(const helrm_rotkeys* r) { return r ? r->keys.size() * r->words_per_key * 8 : 0; }
+
+helrm_status helrm_sk_export(helrm_ctx* c, const helrm_sk* s, int64_t* coeff, size_t n_words) {
+  return guard([&] {
+    need(c && s && coeff && n_words >= c->P.N, HELRM_ERR_ARG, "bad argument");
+    std::copy(s->s.begin(), s->s.end(), coeff);
+  });
+}
+
+static void export_ntt(helrm_ctx* c, const uint64_t* d, size_t npolys, const LimbMap& m, uint64_t* host) {
+  const size_t N = c->P.N;
+  DBuf t(c, npolys * m.n * N);
+  ntt_inv(c, d, t.p, npolys * m.n, m);
+  HCUDA(cudaMemcpyAsync(host, t.p, npolys * m.n * N * 8, cudaMemcpyDeviceToHost, c->stream));
+  HCUDA(cudaStreamSynchronize(c->stream));
+}
+
+helrm_status helrm_pk_export(helrm_ctx* c, const helrm_pk* p, uint64_t* coeff, size_t n_words) {
+  return guard([&] {
+    need(c && p && coeff && n_words >= (size_t)2 * (c->P.L + 1) * c->P.N, HELRM_ERR_ARG, "bad argument");
+    export_ntt(c, p->d, 2, c->P.map_q(c->P.L), coeff);
+  });
+}
+
+helrm_status helrm_rotkeys_export(helrm_ctx* c, const helrm_rotkeys* r, uint64_t g, uint64_t* coeff, size_t n_words) {
+  return guard([&] {
+    need(c && r && coeff && n_words >= r->words_per_key, HELRM_ERR_ARG, "bad argument");
+    const Params& P = c->P;
+    export_ntt(c, key_for(r, g), 2 * P.dnum(P.L), P.map_range(0, P.L + 1 + P.K), coeff);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// tables and query encoding (S0)
+// ---------------------------------------------------------------------------
+helrm_status helrm_tables_create(const helrm_params* p, const helrm_table_desc* t, size_t n_tables, uint32_t n_dense,
+                                 helrm_tables** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(p && t && out && n_tables > 0, HELRM_ERR_ARG, "null argument");
+    helrm_tables* T = new helrm_tables();
+    T->P = p->P;
+    T->n_dense = n_dense;
+    std::map<const double*, int> seen;
+    int64_t I = n_dense, R = 0;
+    for (size_t b = 0; b < n_tables; b++) {
+      const helrm_table_desc& d = t[b];
+      need(d.k >= 1 && d.d >= 1 && d.p >= 0 && d.w, HELRM_ERR_CONFIG, "bad table description");
+      Block B{};
+      B.k = d.k;
+      B.d = d.d;
+      B.p = d.p;
+      B.comp = d.p != 0 && d.k > d.p;
+      B.l = 1;
+      if (B.comp) {
+        need(d.p >= 2, HELRM_ERR_CONFIG, "digit base must be >= 2");
+        __int128 cap = d.p;
+        while (cap < d.k) { cap *= d.p; B.l++; }
+      }
+      B.w = B.comp ? d.p * B.l : d.k;
+      B.I = d.in_off < 0 ? I : d.in_off;
+      B.R = d.out_off < 0 ? R : d.out_off;
+      auto it = seen.find(d.w);
+      if (it == seen.end()) {
+        T->weights.emplace_back(d.w, d.w + (size_t)B.w * d.d);
+        B.wid = (int)T->weights.size() - 1;
+        seen[d.w] = B.wid;
+      } else {
+        B.wid = it->second;
+        need((int64_t)T->weights[B.wid].size() == B.w * B.d, HELRM_ERR_LAYOUT, "shared weights with different shapes");
+      }
+      I = B.I + B.w;
+      R = B.R + B.d;
+      T->blocks.push_back(B);
+    }
+    T->K = 0;
+    T->M = 0;
+    for (auto& B : T->blocks) {
+      T->K = std::max(T->K, B.I + B.w);
+      T->M = std::max(T->M, B.R + B.d);
+    }
+    // overlapping segments / outputs are a layout error
+    std::vector<std::pair<int64_t, int64_t>> in, outv;
+    for (auto& B : T->blocks) {
+      in.push_back({B.I, B.I + B.w});
+      outv.push_back({B.R, B.R + B.d});
+    }
+    in.push_back({0, (int64_t)n_dense});
+    for (auto* v : {&in, &outv}) {
+      std::sort(v->begin(), v->end());
+      for (size_t i = 1; i < v->size(); i++)
+        need((*v)[i].first >= (*v)[i - 1].second, HELRM_ERR_LAYOUT, "overlapping table offsets");
+    }
+    *out = T;
+  });
+}
+
+void helrm_tables_destroy(helrm_tables* t) { delete t; }
+
+helrm_status helrm_tables_info(const helrm_tables* t, int64_t* K, int64_t* M) {
+  return guard([&] {
+    need(t, HELRM_ERR_ARG, "null argument");
+    if (K) *K = t->K;
+    if (M) *M = t->M;
+  });
+}
+
+helrm_status helrm_encode_query(const helrm_tables* t, const int64_t* idx, const double* dense, double* slots,
+                                size_t n_slots) {
+  return guard([&] {
+    need(t && idx && slots, HELRM_ERR_ARG, "null argument");
+    need((int64_t)n_slots >= t->K, HELRM_ERR_CAPACITY, "slot buffer smaller than K");
+    std::fill(slots, slots + n_slots, 0.0);
+    for (uint32_t i = 0; i < t->n_dense; i++) slots[i] = dense ? dense[i] : 0.0;
+    for (size_t b = 0; b < t->blocks.size(); b++) {
+      const Block& B = t->blocks[b];
+      int64_t i = idx[b];
+      need(i >= 0 && i < B.k, HELRM_ERR_RANGE, "index outside [0, k)");
+      if (!B.comp) {
+        slots[B.I + i] = 1.0;
+      } else {
+        for (int64_t dgt = 0; dgt < B.l; dgt++) {  // least-significant digit first
+          slots[B.I + dgt * B.p + i % B.p] = 1.0;
+          i /= B.p;
+        }
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// ciphertexts
+// ---------------------------------------------------------------------------
+static void encode_to_device(helrm_ctx* c, const double* slots, size_t n_slots, double delta, uint64_t* out,
+                             const LimbMap& m) {
+  const Params& P = c->P;
+  std::vector<double> z(P.n, 0.0);
+  std::copy(slots, slots + n_slots, z.begin());
+  std::vector<int64_t> coef(P.N);
+  int st = encode_slots(z.data(), n_slots, P.log_n, delta, coef.data());
+  need(st == 0, HELRM_ERR_CONFIG, "|encoded coefficient| >= 2^62");
+  DBuf d(c, P.N);
+  HCUDA(cudaMemcpyAsync(d.p, coef.data(), P.N * 8, cudaMemcpyHostToDevice, c->stream));
+  launch_reduce_signed(c->dc(), (const int64_t*)d.p, out, m);
+  ntt_fwd(c, out, out, m.n, m);
+  HCUDA(cudaStreamSynchronize(c->stream));
+}
+
+helrm_status helrm_encrypt(helrm_ctx* c, const helrm_pk* pk, const double* slots, size_t n_slots, uint32_t level,
+                           uint64_t seed, helrm_ct** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && pk && slots && out, HELRM_ERR_ARG, "null argument");
+    const Params& P = c->P;
+    need(n_slots <= P.n, HELRM_ERR_CAPACITY, "more slots than N/2");
+    need(level <= P.L, HELRM_ERR_LEVEL, "level above L");
+    const size_t N = P.N, nq = level + 1;
+    LimbMap m = P.map_q(level);
+    helrm_ct* ct = new_ct(c, level, std::ldexp(1.0, P.log_scale));
+    DBuf mm(c, nq * N), v(c, nq * N), e0(c, nq * N), e1(c, nq * N);
+    encode_to_device(c, slots, n_slots, std::ldexp(1.0, P.log_scale), mm.p, m);
+    sample_small_ntt(c, seed, prng_stream(6, 0, 0, 0), 0, v.p, m);
+    sample_small_ntt(c, seed, prng_stream(7, 0, 0, 0), 1, e0.p, m);
+    sample_small_ntt(c, seed, prng_stream(8, 0, 0, 0), 1, e1.p, m);
+    const uint64_t* pkb = pk->d;
+    const uint64_t* pka = pk->d + (size_t)(P.L + 1) * N;
+    launch_binary(c->dc(), 2, v.p, pkb, ct_c0(ct), m);
+    launch_binary(c->dc(), 0, ct_c0(ct), e0.p, ct_c0(ct), m);
+    launch_binary(c->dc(), 0, ct_c0(ct), mm.p, ct_c0(ct), m);
+    launch_binary(c->dc(), 2, v.p, pka, ct_c1(ct), m);
+    launch_binary(c->dc(), 0, ct_c1(ct), e1.p, ct_c1(ct), m);
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = ct;
+  });
+}
+
+helrm_status helrm_ct_alloc(helrm_ctx* c, uint32_t level, double scale, helrm_ct** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && out, HELRM_ERR_ARG, "null argument");
+    need(level <= c->P.L, HELRM_ERR_LEVEL, "level above L");
+    *out = new_ct(c, level, scale);
+  });
+}
+
+helrm_status helrm_ct_import(helrm_ctx* c, const uint64_t* coeff, uint32_t level, double scale, helrm_ct** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && coeff && out, HELRM_ERR_ARG, "null argument");
+    need(level <= c->P.L, HELRM_ERR_LEVEL, "level above L");
+    helrm_ct* ct = new_ct(c, level, scale);
+    const size_t words = (size_t)2 * (level + 1) * c->P.N;
+    HCUDA(cudaMemcpyAsync(ct->d, coeff, words * 8, cudaMemcpyHostToDevice, c->stream));
+    ntt_fwd(c, ct->d, ct->d, 2 * (level + 1), c->P.map_q(level));
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = ct;
+  });
+}
+
+helrm_status helrm_ct_export(helrm_ctx* c, const helrm_ct* ct, uint64_t* coeff, size_t n_words) {
+  return guard([&] {
+    need(c && ct && coeff, HELRM_ERR_ARG, "null argument");
+    need(n_words >= (size_t)2 * (ct->level + 1) * c->P.N, HELRM_ERR_ARG, "buffer too small");
+    export_ntt(c, ct->d, 2, c->P.map_q(ct->level), coeff);
+  });
+}
+
+helrm_status helrm_ct_info(const helrm_ct* ct, uint32_t* level, double* scale) {
+  return guard([&] {
+    need(ct, HELRM_ERR_ARG, "null argument");
+    if (level) *level = ct->level;
+    if (scale) *scale = ct->scale;
+  });
+}
+
+helrm_status helrm_ct_device_ptr(const helrm_ct* ct, uint64_t** dev) {
+  return guard([&] {
+    need(ct && dev, HELRM_ERR_ARG, "null argument");
+    *dev = ct->d;
+  });
+}
+
+void helrm_ct_destroy(helrm_ct* ct) {
+  if (!ct) return;
+  ct->c->dfree(ct->d);
+  delete ct;
+}
+
+helrm_status helrm_decrypt_decode(helrm_ctx* c, const helrm_sk* sk, const helrm_ct* ct, double* slots,
+                                  size_t n_slots) {
+  return guard([&] {
+    need(c && sk && ct && slots, HELRM_ERR_ARG, "null argument");
+    const Params& P = c->P;
+    const size_t N = P.N, nq = ct->level + 1;
+    LimbMap m = P.map_q(ct->level);
+    DBuf t(c, nq * N);
+    launch_binary(c->dc(), 2, ct_c1(ct), sk->sntt, t.p, m);
+    launch_binary(c->dc(), 0, t.p, ct_c0(ct), t.p, m);
+    ntt_inv(c, t.p, t.p, nq, m);
+    std::vector<uint64_t> h(nq * N);
+    HCUDA(cudaMemcpyAsync(h.data(), t.p, nq * N * 8, cudaMemcpyDeviceToHost, c->stream));
+    HCUDA(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> mm(N);
+    crt_small(h.data(), P.primes.data(), nq, N, mm.data());
+    decode_coeffs(mm.data(), P.log_n, ct->scale, slots, std::min(n_slots, (size_t)P.n));
+  });
+}
+
+// ---------------------------------------------------------------------------
+// plan (server setup, D19)
+// ---------------------------------------------------------------------------
+static int64_t next_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p *= 2;
+  return p;
+}
+
+helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t level, uint32_t n1_req, uint32_t mode,
+                               helrm_plan** out) {
+  if (out) *out = nullptr;
+  helrm_plan* pl = nullptr;
+  helrm_status st = guard([&] {
+    need(c && T && out, HELRM_ERR_ARG, "null argument");
+    const Params& P = c->P;
+    need(level >= 1 && level <= P.L, HELRM_ERR_LEVEL, "lookup needs 1 <= level <= L");
+    need(mode == HELRM_MODE_DOUBLE || mode == HELRM_MODE_SINGLE, HELRM_ERR_ARG, "bad mode");
+    const int64_t n = P.n;
+    pl = new helrm_plan();
+    pl->c = c;
+    pl->level = level;
+    pl->mode = mode;
+    pl->K = T->K;
+    pl->M = T->M;
+    pl->mbar = std::min(next_pow2(T->M), n);
+    pl->O = (T->M + n - 1) / n;
+    pl->C = (T->K + n - 1) / n;
+    // hybrid diagonals: each non-zero W[r][u] lands in exactly one (o, c, t, s)
+    std::map<std::tuple<int64_t, int64_t, int64_t>, std::vector<double>> diags;
+    for (const Block& B : T->blocks) {
+      const std::vector<double>& S = T->weights[B.wid];
+      for (int64_t row = 0; row < B.w; row++)
+        for (int64_t col = 0; col < B.d; col++) {
+          const double v = S[row * B.d + col];
+          if (v == 0.0) continue;
+          const int64_t r = B.R + col, u = B.I + row;
+          const int64_t o = r / n, cc = u / n, ul = u % n;
+          int64_t t, s;
+          if (pl->mbar < n) {
+            t = ((ul - r % pl->mbar) % pl->mbar + pl->mbar) % pl->mbar;
+            s = ((ul - t) % n + n) % n;
+          } else {
+            s = r % n;
+            t = ((ul - s) % n + n) % n;
+          }
+          auto& vec = diags[{o, cc, t}];
+          if (vec.empty()) vec.assign(n, 0.0);
+          vec[s] += v;
+        }
+    }
+    for (auto it = diags.begin(); it != diags.end();) {
+      bool nz = std::any_of(it->second.begin(), it->second.end(), [](double x) { return x != 0.0; });
+      it = nz ? std::next(it) : diags.erase(it);
+    }
+    pl->n_diag = (int64_t)diags.size();
+    need(pl->n_diag > 0, HELRM_ERR_LAYOUT, "the packed matrix is zero");
+    // BSGS split per output block: minimal cyclic interval, n1, n2
+    std::vector<std::pair<int64_t, int64_t>> iv(pl->O);
+    int64_t maxspan = 0;
+    for (int64_t o = 0; o < pl->O; o++) {
+      std::vector<int64_t> ts;
+      for (auto& kv : diags)
+        if (std::get<0>(kv.first) == o) ts.push_back(std::get<2>(kv.first));
+      std::sort(ts.begin(), ts.end());
+      ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+      int64_t best_span = -1, best_t0 = 0;
+      for (size_t a = 0; a < ts.size(); a++) {
+        const int64_t prev = ts[(a + ts.size() - 1) % ts.size()];
+        const int64_t span = ts.size() == 1 ? 1 : ((prev - ts[a]) % n + n) % n + 1;
+        if (best_span < 0 || span < best_span || (span == best_span && ts[a] < best_t0)) {
+          best_span = span;
+          best_t0 = ts[a];
+        }
+      }
+      iv[o] = {best_t0, best_span};
+      maxspan = std::max(maxspan, best_span);
+    }
+    int64_t n1 = n1_req;
+    if (n1 == 0) {
+      n1 = 1;
+      while (n1 * n1 < maxspan) n1 *= 2;
+    }
+    pl->n1 = n1;
+    std::vector<std::vector<double>> uniq;
+    std::unordered_map<uint64_t, std::vector<int>> by_hash;
+    std::vector<std::set<int>> bab(pl->C);
+    pl->entries.resize(pl->O);
+    pl->giants.resize(pl->O);
+    for (int64_t o = 0; o < pl->O; o++) {
+      const int64_t t0 = iv[o].first, span = iv[o].second, n2 = (span + n1 - 1) / n1;
+      pl->t0.push_back(t0);
+      pl->span.push_back(span);
+      pl->n2.push_back(n2);
+      pl->entries[o].resize(n2);
+      for (int64_t i = 0; i < n2; i++) pl->giants[o].push_back((t0 + i * n1) % n);
+      for (auto& kv : diags) {
+        if (std::get<0>(kv.first) != o) continue;
+        const int64_t cc = std::get<1>(kv.first), t = std::get<2>(kv.first);
+        const int64_t r = ((t - t0) % n + n) % n, j = r % n1, i = r / n1, g = pl->giants[o][i];
+        std::vector<double> u(n);
+        for (int64_t s = 0; s < n; s++) u[s] = kv.second[((s - g) % n + n) % n];  // rot(diag, -g)
+        uint64_t h = 1469598103934665603ull;
+        const unsigned char* bytes = (const unsigned char*)u.data();
+        for (size_t b = 0; b < u.size() * 8; b++) h = (h ^ bytes[b]) * 1099511628211ull;
+        int uid = -1;
+        for (int cand : by_hash[h])
+          if (uniq[cand] == u) { uid = cand; break; }
+        if (uid < 0) {
+          uid = (int)uniq.size();
+          uniq.push_back(std::move(u));
+          by_hash[h].push_back(uid);
+        }
+        pl->entries[o][i].push_back(Entry{(int)cc, (int)j, uid});
+        bab[cc].insert((int)j);
+      }
+    }
+    for (auto& s : bab) pl->babies.emplace_back(s.begin(), s.end());
+    // rotation amounts: babies != 0, non-empty giants != 0, RotSum
+    std::set<int64_t> am;
+    for (auto& bl : pl->babies)
+      for (int j : bl)
+        if (j) am.insert(j);
+    for (int64_t o = 0; o < pl->O; o++)
+      for (size_t i = 0; i < pl->giants[o].size(); i++)
+        if (pl->giants[o][i] % n && !pl->entries[o][i].empty()) am.insert(pl->giants[o][i]);
+    for (int64_t r = pl->mbar; r < n; r *= 2) am.insert(r);
+    pl->rotations.assign(am.begin(), am.end());
+    // encode the unique pre-rotated diagonals at Delta_pt = q_level, upload, NTT
+    pl->n_unique = (int64_t)uniq.size();
+    pl->nl = mode == HELRM_MODE_DOUBLE ? level + 1 + P.K : level + 1;
+    LimbMap m = mode == HELRM_MODE_DOUBLE ? P.map_qp(level) : P.map_q(level);
+    const size_t N = P.N;
+    pl->diag = (uint64_t*)c->dalloc((size_t)pl->n_unique * pl->nl * N * 8);
+    const double delta_pt = (double)P.primes[level];
+    const int64_t chunk = 64;
+    std::vector<int64_t> coef((size_t)chunk * N);
+    DBuf dcoef(c, (size_t)chunk * N);
+    for (int64_t u0 = 0; u0 < pl->n_unique; u0 += chunk) {
+      const int64_t cnt = std::min(chunk, pl->n_unique - u0);
+      int bad = 0;
+#pragma omp parallel for schedule(dynamic) reduction(| : bad)
+      for (int64_t k = 0; k < cnt; k++) bad |= encode_slots(uniq[u0 + k].data(), 0, P.log_n, delta_pt, &coef[k * N]);
+      need(bad == 0, HELRM_ERR_CONFIG, "|encoded diagonal coefficient| >= 2^62");
+      HCUDA(cudaStreamSynchronize(c->stream));
+      HCUDA(cudaMemcpyAsync(dcoef.p, coef.data(), (size_t)cnt * N * 8, cudaMemcpyHostToDevice, c->stream));
+      for (int64_t k = 0; k < cnt; k++) {
+        uint64_t* dst = pl->diag + (size_t)(u0 + k) * pl->nl * N;
+        launch_reduce_signed(c->dc(), (const int64_t*)(dcoef.p + k * N), dst, m);
+      }
+      ntt_fwd(c, pl->diag + (size_t)u0 * pl->nl * N, pl->diag + (size_t)u0 * pl->nl * N, (size_t)cnt * pl->nl, m);
+    }
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = pl;
+  });
+  if (st != HELRM_OK && pl) helrm_plan_destroy(pl);
+  return st;
+}
+
+void helrm_plan_destroy(helrm_plan* p) {
+  if (!p) return;
+  p->c->dfree(p->diag);
+  delete p;
+}
+
+helrm_status helrm_plan_info(const helrm_plan* p, helrm_plan_info_t* out) {
+  return guard([&] {
+    need(p && out, HELRM_ERR_ARG, "null argument");
+    helrm_plan_info_t r{};
+    r.K = p->K;
+    r.M = p->M;
+    r.mbar = p->mbar;
+    r.n_in_cts = p->C;
+    r.n_out_cts = p->O;
+    r.n_diag = p->n_diag;
+    r.n_unique = p->n_unique;
+    r.n1 = p->n1;
+    r.n2_max = *std::max_element(p->n2.begin(), p->n2.end());
+    r.n_rotations = (int64_t)p->rotations.size();
+    r.level = p->level;
+    r.mode = p->mode;
+    r.diag_bytes = (uint64_t)p->n_unique * p->nl * p->c->P.N * 8;
+    *out = r;
+  });
+}
+
+helrm_status helrm_plan_rotations(const helrm_plan* p, int64_t* amounts, size_t cap, size_t* n) {
+  return guard([&] {
+    need(p && n, HELRM_ERR_ARG, "null argument");
+    *n = p->rotations.size();
+    if (amounts) {
+      need(cap >= p->rotations.size(), HELRM_ERR_ARG, "buffer too small");
+      std::copy(p->rotations.begin(), p->rotations.end(), amounts);
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// the lookup (D20 / D22, D21)
+// ---------------------------------------------------------------------------
+static void rot_sum(helrm_ctx* c, helrm_ct* ct, int64_t mbar, const helrm_rotkeys* rk) {
+  const int64_t n = c->P.n;
+  if (mbar >= n) return;
+  helrm_ct* tmp = new_ct(c, ct->level, ct->scale);
+  for (int64_t r = mbar; r < n; r *= 2) {
+    rotate(c, ct, rk, r, tmp);
+    ct_add_inplace(c, ct, tmp);
+  }
+  helrm_ct_destroy(tmp);
+}
+
+static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                          helrm_ct** out) {
+  const Params& P = c->P;
+  const uint32_t l = pl->level;
+  const size_t N = P.N, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
+  const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
+  const LevelConst& lc = level_const(c, l);
+  // L1 + L2: digits and baby steps per input ct
+  std::vector<std::map<int, std::pair<uint64_t*, uint64_t*>>> ab(pl->C);
+  std::vector<std::unique_ptr<DBuf>> keep;
+  for (int64_t ci = 0; ci < pl->C; ci++) {
+    const helrm_ct* ct = in[ci];
+    auto D = std::make_unique<DBuf>(c, dn * nlN);
+    modup_all(c, ct_c1(ct), l, D->p);
+    for (int j : pl->babies[ci]) {
+      auto buf = std::make_unique<DBuf>(c, 2 * nlN);
+      uint64_t* a = buf->p;
+      uint64_t* b = buf->p + nlN;
+      if (j == 0) {  // (P c0, P c1): Q limbs scaled by [P]_q, P limbs 0
+        HCUDA(cudaMemsetAsync(a, 0, 2 * nlN * 8, c->stream));
+        launch_scalar_mul(c->dc(), ct_c0(ct), a, mq, lc.pmod, lc.pmods);
+        launch_scalar_mul(c->dc(), ct_c1(ct), b, mq, lc.pmod, lc.pmods);
+      } else {
+        kip(c, D->p, l, rk, galois_of_rot(c, j), ct_c0(ct), a, b, false);
+      }
+      ab[ci][j] = {a, b};
+      keep.push_back(std::move(buf));
+    }
+    keep.push_back(std::move(D));
+  }
+  // host list of MAC terms for every (o, i); one upload
+  std::vector<MacTerm> terms;
+  std::vector<std::vector<std::pair<size_t, size_t>>> ranges(pl->O);
+  for (int64_t o = 0; o < pl->O; o++)
+    for (auto& ent : pl->entries[o]) {
+      size_t s0 = terms.size();
+      for (const Entry& e : ent) {
+        auto& x = ab[e.c].at(e.j);
+        terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nlN, x.first, x.second});
+      }
+      ranges[o].push_back({s0, terms.size() - s0});
+    }
+  MacTerm* dterms = (MacTerm*)c->dalloc(std::max<size_t>(1, terms.size()) * sizeof(MacTerm));
+  HCUDA(cudaMemcpyAsync(dterms, terms.data(), terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice, c->stream));
+  DBuf AB(c, 2 * nlN), Bp(c, (l + 1) * N), D2(c, dn * nlN), O(c, 2 * nlN);
+  for (int64_t o = 0; o < pl->O; o++) {
+    HCUDA(cudaMemsetAsync(O.p, 0, 2 * nlN * 8, c->stream));
+    for (size_t i = 0; i < pl->entries[o].size(); i++) {
+      auto [s0, cnt] = ranges[o][i];
+      if (cnt == 0) continue;
+      // L3
+      launch_diag_mac(c->dc(), dterms + s0, (int)cnt, AB.p, AB.p + nlN, mqp);
+      const int64_t gi = pl->giants[o][i];
+      if (gi % (int64_t)P.n == 0) {
+        launch_binary(c->dc(), 0, O.p, AB.p, O.p, mqp);
+        launch_binary(c->dc(), 0, O.p + nlN, AB.p + nlN, O.p + nlN, mqp);
+      } else {
+        // L4: B' = ModDown(B); (G0, G1) = KS(B'); O0 += phi(A) + G0; O1 += G1
+        moddown(c, AB.p + nlN, l, Bp.p);
+        modup_all(c, Bp.p, l, D2.p);
+        kip(c, D2.p, l, rk, galois_of_rot(c, gi), nullptr, O.p, O.p + nlN, true);
+        launch_automorph(c->dc(), AB.p, O.p, mqp, (uint32_t)gi, 1);
+      }
+    }
+    // L6 + L7 + L8
+    helrm_ct* r = new_ct(c, l, in[0]->scale * (double)P.primes[l]);
+    moddown(c, O.p, l, ct_c0(r));
+    moddown(c, O.p + nlN, l, ct_c1(r));
+    helrm_ct* s = new_ct(c, l - 1, in[0]->scale);
+    rescale_poly(c, ct_c0(r), l, ct_c0(s));
+    rescale_poly(c, ct_c1(r), l, ct_c1(s));
+    helrm_ct_destroy(r);
+    rot_sum(c, s, pl->mbar, rk);
+    out[o] = s;
+  }
+  c->dfree(dterms);
+}
+
+static void lookup_single(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                          helrm_ct** out) {
+  const Params& P = c->P;
+  const uint32_t l = pl->level;
+  const size_t N = P.N, nq = l + 1, nqN = nq * N;
+  const LimbMap mq = P.map_q(l);
+  std::vector<std::map<int, helrm_ct*>> rots(pl->C);
+  for (int64_t ci = 0; ci < pl->C; ci++) {
+    const helrm_ct* ct = in[ci];
+    DBuf D(c, (size_t)P.dnum(l) * (l + 1 + P.K) * N);
+    modup_all(c, ct_c1(ct), l, D.p);
+    for (int j : pl->babies[ci]) {
+      helrm_ct* r = new_ct(c, l, ct->scale);
+      rotate_from_digits(c, ct, D.p, rk, j, r);
+      rots[ci][j] = r;
+    }
+  }
+  std::vector<MacTerm> terms;
+  std::vector<std::vector<std::pair<size_t, size_t>>> ranges(pl->O);
+  for (int64_t o = 0; o < pl->O; o++)
+    for (auto& ent : pl->entries[o]) {
+      size_t s0 = terms.size();
+      for (const Entry& e : ent) {
+        helrm_ct* x = rots[e.c].at(e.j);
+        terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nqN, ct_c0(x), ct_c1(x)});
+      }
+      ranges[o].push_back({s0, terms.size() - s0});
+    }
+  MacTerm* dterms = (MacTerm*)c->dalloc(std::max<size_t>(1, terms.size()) * sizeof(MacTerm));
+  HCUDA(cudaMemcpyAsync(dterms, terms.data(), terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice, c->stream));
+  helrm_ct* AB = new_ct(c, l, in[0]->scale);
+  helrm_ct* R = new_ct(c, l, in[0]->scale);
+  for (int64_t o = 0; o < pl->O; o++) {
+    helrm_ct* acc = new_ct(c, l, in[0]->scale * (double)P.primes[l]);
+    HCUDA(cudaMemsetAsync(acc->d, 0, 2 * nqN * 8, c->stream));
+    for (size_t i = 0; i < pl->entries[o].size(); i++) {
+      auto [s0, cnt] = ranges[o][i];
+      if (cnt == 0) continue;
+      launch_diag_mac(c->dc(), dterms + s0, (int)cnt, ct_c0(AB), ct_c1(AB), mq);
+      rotate(c, AB, rk, pl->giants[o][i], R);
+      ct_add_inplace(c, acc, R);
+    }
+    helrm_ct* s = new_ct(c, l - 1, in[0]->scale);
+    rescale_poly(c, ct_c0(acc), l, ct_c0(s));
+    rescale_poly(c, ct_c1(acc), l, ct_c1(s));
+    helrm_ct_destroy(acc);
+    rot_sum(c, s, pl->mbar, rk);
+    out[o] = s;
+  }
+  helrm_ct_destroy(AB);
+  helrm_ct_destroy(R);
+  c->dfree(dterms);
+  for (auto& m : rots)
+    for (auto& kv : m) helrm_ct_destroy(kv.second);
+}
+
+helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                          size_t batch, helrm_ct** out) {
+  if (out)
+    for (size_t i = 0; i < batch * (p ? p->O : 0); i++) out[i] = nullptr;
+  return guard([&] {
+    need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
+    for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
+    for (size_t q = 0; q < batch; q++) {
+      for (int64_t ci = 0; ci < p->C; ci++) {
+        need(in[q * p->C + ci] != nullptr, HELRM_ERR_ARG, "null input ciphertext");
+        need(in[q * p->C + ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's level");
+      }
+      if (p->mode == HELRM_MODE_DOUBLE)
+        lookup_double(c, p, rk, in + q * p->C, out + q * p->O);
+      else
+        lookup_single(c, p, rk, in + q * p->C, out + q * p->O);
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// primitives
+// ---------------------------------------------------------------------------
+helrm_status helrm_ntt_fwd(helrm_ctx* c, uint64_t* dev, uint32_t first, uint32_t n_limbs, size_t n_polys) {
+  return guard([&] {
+    need(c && dev, HELRM_ERR_ARG, "null argument");
+    need(first + n_limbs <= c->P.primes.size() && n_limbs >= 1, HELRM_ERR_ARG, "prime range outside the chain");
+    ntt_fwd(c, dev, dev, (size_t)n_limbs * n_polys, c->P.map_range(first, n_limbs));
+  });
+}
+
+helrm_status helrm_ntt_inv(helrm_ctx* c, uint64_t* dev, uint32_t first, uint32_t n_limbs, size_t n_polys) {
+  return guard([&] {
+    need(c && dev, HELRM_ERR_ARG, "null argument");
+    need(first + n_limbs <= c->P.primes.size() && n_limbs >= 1, HELRM_ERR_ARG, "prime range outside the chain");
+    ntt_inv(c, dev, dev, (size_t)n_limbs * n_polys, c->P.map_range(first, n_limbs));
+  });
+}
+
+helrm_status helrm_modup(helrm_ctx* c, const uint64_t* in, uint32_t level, uint32_t digit, uint64_t* out) {
+  return guard([&] {
+    need(c && in && out, HELRM_ERR_ARG, "null argument");
+    need(level <= c->P.L && digit < c->P.dnum(level), HELRM_ERR_LEVEL, "bad level/digit");
+    modup(c, in, level, (int)digit, out);
+  });
+}
+
+helrm_status helrm_moddown(helrm_ctx* c, const uint64_t* in, uint32_t level, uint64_t* out) {
+  return guard([&] {
+    need(c && in && out, HELRM_ERR_ARG, "null argument");
+    need(level <= c->P.L, HELRM_ERR_LEVEL, "bad level");
+    moddown(c, in, level, out);
+  });
+}
+
+helrm_status helrm_rescale(helrm_ctx* c, const helrm_ct* in, helrm_ct** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && in && out, HELRM_ERR_ARG, "null argument");
+    need(in->level >= 1, HELRM_ERR_LEVEL, "rescale at level 0");
+    helrm_ct* r = new_ct(c, in->level - 1, in->scale / (double)c->P.primes[in->level]);
+    rescale_poly(c, ct_c0(in), in->level, ct_c0(r));
+    rescale_poly(c, ct_c1(in), in->level, ct_c1(r));
+    *out = r;
+  });
+}
+
+helrm_status helrm_rotate(helrm_ctx* c, const helrm_rotkeys* rk, const helrm_ct* in, int64_t k, helrm_ct** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && rk && in && out, HELRM_ERR_ARG, "null argument");
+    helrm_ct* r = new_ct(c, in->level, in->scale);
+    rotate(c, in, rk, k, r);
+    *out = r;
+  });
+}
+
+helrm_status helrm_rotate_hoisted(helrm_ctx* c, const helrm_rotkeys* rk, const helrm_ct* in, const int64_t* amounts,
+                                  size_t n_amounts, helrm_ct* const* ring, size_t n_ring) {
+  return guard([&] {
+    need(c && rk && in && amounts && ring && n_ring > 0, HELRM_ERR_ARG, "null argument");
+    const uint32_t l = in->level;
+    for (size_t i = 0; i < n_ring; i++) need(ring[i] && ring[i]->level == l, HELRM_ERR_LEVEL, "ring ct level");
+    DBuf D(c, (size_t)c->P.dnum(l) * (l + 1 + c->P.K) * c->P.N);
+    modup_all(c, ct_c1(in), l, D.p);
+    for (size_t i = 0; i < n_amounts; i++) rotate_from_digits(c, in, D.p, rk, amounts[i], ring[i % n_ring]);
+  });
+}
+
+helrm_status helrm_ct_random(helrm_ctx* c, uint64_t seed, uint32_t ct_index, uint32_t level, helrm_ct** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && out, HELRM_ERR_ARG, "null argument");
+    need(level <= c->P.L, HELRM_ERR_LEVEL, "level above L");
+    helrm_ct* ct = new_ct(c, level, std::ldexp(1.0, c->P.log_scale));
+    LimbMap m = c->P.map_q(level);
+    for (int poly = 0; poly < 2; poly++)
+      launch_sample_uniform_ntt(c->dc(), ct->d + (size_t)poly * (level + 1) * c->P.N, m, seed, 9, ct_index, poly, m);
+    *out = ct;
+  });
+}
+
+}  // extern "C"

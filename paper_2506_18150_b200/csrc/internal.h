@@ -1,0 +1,157 @@
+// internal.h -- library-internal types shared by the host engine and the
+// kernels.  Nothing here crosses the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "arith.cuh"
+#include "../../include/helrm.h"
+
+namespace helrm {
+
+constexpr int kMaxLimbs = 64;
+constexpr int kMaxDigitPrimes = 8;
+
+struct Error : std::runtime_error {
+  helrm_status code;
+  Error(helrm_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define HCUDA(x)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess)                                                                    \
+      throw ::helrm::Error(HELRM_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+// Constants of one prime of the chain q_0..q_L, p_0..p_{K-1}, on the device.
+struct PrimeDev {
+  RedConst rc;
+  uint64_t ninv, ninvs;         // N^-1 and its shoup companion
+  const uint64_t* tw;           // [N] psi^bitrev(k)
+  const uint64_t* tws;          // [N] shoup companions
+  const uint64_t* itw;          // [N] psi^-bitrev(k)
+  const uint64_t* itws;
+};
+
+// Global chain index of each limb of a polynomial (by value as kernel arg).
+struct LimbMap {
+  int n;
+  uint8_t pr[kMaxLimbs];
+};
+
+// Fast base conversion tables (D14), device resident.
+struct ConvDev {
+  int nb, nt;
+  uint8_t bpr[kMaxDigitPrimes];           // chain index of each source prime
+  uint8_t tpr[kMaxLimbs];                 // chain index of each target prime
+  uint64_t binv[kMaxDigitPrimes], binvs[kMaxDigitPrimes];   // [(B/b)^-1]_b
+  uint64_t bmod[kMaxLimbs][kMaxDigitPrimes];                // (B/b) mod t
+};
+
+struct Params {
+  uint32_t log_n = 0, N = 0, n = 0, L = 0, K = 0, alpha = 0, log_scale = 0;
+  std::vector<uint64_t> primes;  // q_0..q_L, p_0..p_{K-1}
+  std::vector<uint64_t> psi;
+  uint32_t dnum(uint32_t level) const { return (level + 1 + alpha - 1) / alpha; }
+  // chain index of limb `l` of an R_{Q_level P} polynomial
+  uint32_t qp_chain(uint32_t level, uint32_t l) const { return l <= level ? l : L + 1 + (l - level - 1); }
+  LimbMap map_q(uint32_t level) const {
+    LimbMap m{};
+    m.n = level + 1;
+    for (uint32_t i = 0; i <= level; i++) m.pr[i] = (uint8_t)i;
+    return m;
+  }
+  LimbMap map_qp(uint32_t level) const {
+    LimbMap m{};
+    m.n = level + 1 + K;
+    for (uint32_t i = 0; i < (uint32_t)m.n; i++) m.pr[i] = (uint8_t)qp_chain(level, i);
+    return m;
+  }
+  LimbMap map_range(uint32_t first, uint32_t count) const {
+    LimbMap m{};
+    m.n = count;
+    for (uint32_t i = 0; i < count; i++) m.pr[i] = (uint8_t)(first + i);
+    return m;
+  }
+};
+
+// host math (host_math.cpp)
+bool is_prime_u64(uint64_t n);
+std::vector<uint64_t> find_primes(const std::vector<std::pair<uint32_t, uint32_t>>& groups, uint64_t N,
+                                  std::vector<uint64_t> taken);
+uint64_t min_psi(uint64_t q, uint64_t N);
+uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t q);
+uint64_t inv_mod(uint64_t a, uint64_t q);
+uint64_t mulm(uint64_t a, uint64_t b, uint64_t q);
+// D6: correctly rounded encode (double-double FFT + binary128 recheck)
+int encode_slots(const double* z, size_t n_nonzero_hint, uint32_t log_n, double delta, int64_t* out);
+// D7 decode (fp64)
+void decode_coeffs(const int64_t* m, uint32_t log_n, double delta, double* z, size_t n_slots);
+// centered CRT of small values into int64 (|m| < 2^62 assumed)
+void crt_small(const uint64_t* res, const uint64_t* primes, size_t n_limbs, size_t N, int64_t* out);
+// the slot-order permutation: slot position of bit-reversed NTT index r
+std::vector<uint32_t> slot_of_bitrev(uint32_t log_n);
+std::vector<uint64_t> gauss_cdt_table();
+
+// ---------------- kernel launchers (kernels_*.cu) ----------------
+struct DevCtx {
+  const PrimeDev* primes;     // device array, chain-indexed
+  const uint32_t* slotpos;    // [N] slot position of bitrev index r
+  uint32_t log_n, N;
+  cudaStream_t stream;
+  uint64_t* launches;         // host counter
+};
+
+void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total_limbs,
+                    const LimbMap& map);
+void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total_limbs,
+                    const LimbMap& map);
+
+void launch_reduce_signed(const DevCtx& c, const int64_t* m, uint64_t* out, const LimbMap& map);
+void launch_sample_uniform_ntt(const DevCtx& c, uint64_t* out, const LimbMap& map, uint64_t seed, uint64_t purpose,
+                               uint64_t a, uint64_t b, const LimbMap& ids);
+void launch_sample_small(const DevCtx& c, int64_t* out, uint64_t base, int kind, const uint64_t* cdt);
+// op 0: a + b, 1: a - b, 2: a * b, 3: -a
+void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, const LimbMap& map);
+void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
+                       const uint64_t* sp);
+void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
+                      int accumulate);
+void launch_conv(const DevCtx& c, const ConvDev* cv, int nt, const int16_t* rows, const uint64_t* in, uint64_t* out);
+void launch_sub_scale(const DevCtx& c, const uint64_t* y, const uint64_t* t, uint64_t* out, const LimbMap& map,
+                      const uint64_t* s, const uint64_t* sp);
+void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, uint64_t ql, uint64_t* out, const LimbMap& map);
+size_t ntt_scratch_words(int log_n);
+
+struct KipArgs {
+  const uint64_t* digits;     // [dnum][nl][N] (Q_l P, NTT slot order)
+  int dnum;
+  const uint64_t* key;        // key for g: [digit][2][L+1+K][N]
+  size_t key_digit_stride;    // words between digits of the key
+  size_t key_half_stride;     // words between b and a of a digit
+  const uint64_t* c0;         // optional: add P.phi(c0) on Q limbs ([level+1][N]), may be null
+  const uint64_t* p_mod;      // [level+1] P mod q_l (device), used with c0
+  uint32_t rot;               // slot rotation amount (phi_{5^rot})
+  uint64_t* out0;             // [nl][N]
+  uint64_t* out1;
+  int accumulate;             // out += result (else out = result)
+  uint32_t level;
+};
+void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map);
+
+struct MacTerm {
+  const uint64_t* u;          // plaintext [nl][N]
+  const uint64_t* x0;         // [nl][N]
+  const uint64_t* x1;
+};
+void launch_diag_mac(const DevCtx& c, const MacTerm* terms_dev, int n_terms, uint64_t* out0, uint64_t* out1,
+                     const LimbMap& map);
+
+}  // namespace helrm

@@ -1,0 +1,260 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bit-exact for every integer result (NTT, keys, ciphertexts, ModUp/ModDown,
+rescale, rotations, lookups); decrypted lookups within 1e-3 of the float64
+gather (BASELINE.json north star).  GPU tests are marked `gpu`; the symbol
+export check runs on CPU."""
+import re
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import core
+from oracle import lookup as lk
+
+ROOT_H = __import__("os").path.join(__import__("os").path.dirname(__file__), "..", "include", "helrm.h")
+
+
+def _cuda_ok():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def test_library_exports_every_declared_symbol():
+    """CPU: libhelrm.so loads and exports every function include/helrm.h declares."""
+    from paper_2506_18150_b200 import helrm
+    decl = set(re.findall(r"\b(helrm_[a-z0-9_]+)\s*\(", open(ROOT_H).read()))
+    assert len(decl) > 30
+    for name in sorted(decl):
+        assert hasattr(helrm._L, name), name
+    assert set(helrm.EXPORTED) <= decl
+
+
+def test_host_side_matches_oracle_on_cpu():
+    """CPU: primes/psi (D2/D3), table layout and the client query (S0)."""
+    from paper_2506_18150_b200 import helrm
+    for name in ("tiny_a", "tiny_b", "uci", "criteo"):
+        w = synth.make_workload(name)
+        P = helrm.params_from_config(w.config)
+        PO = core.params_from_config(w.config)
+        q, p, psi = P.moduli()
+        assert q == PO.q and p == PO.p and psi == [PO.psi[x] for x in PO.q + PO.p]
+        T = helrm.tables_create(P, w.tables, w.n_dense)
+        lay = lk.layout(w)
+        assert T.info() == (lay.K, lay.M)
+        for qi in range(w.indices.shape[0]):
+            x = helrm.encode_query(T, w.indices[qi], w.dense[qi], lay.K)
+            assert np.array_equal(x, lk.encode_query(lay, w.indices[qi], w.dense[qi]))
+    with pytest.raises(helrm.HelrmError) as e:
+        helrm.encode_query(T, [10**9] * 26, [], lay.K)
+    assert e.value.code == 5
+
+
+gpu = pytest.mark.gpu
+
+
+def _slot_to_natural(N):
+    """Library NTT slot order -> oracle natural order (D4/D5): position s < N/2
+    holds the evaluation at psi^(5^s), N/2 + s the one at psi^(-5^s)."""
+    n = N // 2
+    idx = np.zeros(N, dtype=np.int64)      # idx[natural i] = slot position
+    e = 1
+    for s in range(n):
+        idx[(e - 1) // 2] = s
+        idx[(2 * N - e - 1) // 2] = n + s
+        e = e * 5 % (2 * N)
+    return idx
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    if not _cuda_ok():
+        pytest.skip("no CUDA device")
+    import torch
+    return torch
+
+
+class Env:
+    def __init__(self, name, torch):
+        from paper_2506_18150_b200 import helrm
+        self.h = helrm
+        self.w = synth.make_workload(name)
+        self.cfg = self.w.config
+        self.PO = core.params_from_config(self.cfg)
+        self.P = helrm.params_from_config(self.cfg)
+        self.ctx = helrm.Context(self.P, 0, 0)
+        self.torch = torch
+
+    def dev(self, arr):
+        t = self.torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint64)).cuda()
+        return t
+
+    def host(self, t):
+        self.ctx.sync()
+        return t.cpu().numpy()
+
+
+_envs = {}
+
+
+def env(name, torch):
+    if name not in _envs:
+        _envs[name] = Env(name, torch)
+    return _envs[name]
+
+
+@gpu
+@pytest.mark.parametrize("name", ["tiny_a", "uci", "criteo"])
+def test_ntt_matches_oracle(name, torch_mod):
+    E = env(name, torch_mod)
+    PO = E.PO
+    primes = PO.q + PO.p
+    rng = np.random.default_rng(11)
+    a = np.stack([rng.integers(0, q, size=PO.N, dtype=np.uint64) for q in primes])
+    # 3 polys x all limbs in one launch (several tiles and chunks)
+    d = E.dev(np.concatenate([a, a, a]))
+    E.h.ntt_fwd(E.ctx, d, 0, len(primes), 3)
+    got = E.host(d).reshape(3, len(primes), PO.N)
+    want = core.ntt(a, primes, PO)
+    perm = _slot_to_natural(PO.N)
+    for k in range(3):
+        assert np.array_equal(got[k][:, perm], want)
+    E.h.ntt_inv(E.ctx, d, 0, len(primes), 3)
+    assert np.array_equal(E.host(d).reshape(3, len(primes), PO.N)[1], a)
+
+
+@gpu
+@pytest.mark.parametrize("name", ["tiny_a", "uci"])
+def test_keys_and_encryption_match_oracle(name, torch_mod):
+    E = env(name, torch_mod)
+    h, PO, cfg = E.h, E.PO, E.cfg
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    osk = core.sk_gen(PO, cfg.seed)
+    opk = core.pk_gen(PO, osk, cfg.seed)
+    assert np.array_equal(h.sk_export(E.ctx, sk), osk.s)
+    gpk = h.pk_export(E.ctx, pk)
+    assert np.array_equal(gpk[0], core.intt(opk.b, PO.q, PO)) and np.array_equal(gpk[1], core.intt(opk.a, PO.q, PO))
+    gs = [core.galois_elt(3, PO), core.galois_elt(PO.n - 1, PO)]
+    rk = h.rotkeys_gen(E.ctx, sk, gs, cfg.seed)
+    ork = core.rotkeys_gen(PO, osk, gs, cfg.seed)
+    allp = PO.q + PO.p
+    for g in gs:
+        got = h.rotkeys_export(E.ctx, rk, g)
+        for k, (b, a) in enumerate(ork.keys[g]):
+            assert np.array_equal(got[k, 0], core.intt(b, allp, PO))
+            assert np.array_equal(got[k, 1], core.intt(a, allp, PO))
+    z = np.random.default_rng(5).uniform(-1, 1, PO.n)
+    for level in (PO.L, 1):
+        ct = h.encrypt(E.ctx, pk, z, level, 1234)
+        oct_ = core.encrypt(PO, opk, z, level, 1234)
+        assert np.array_equal(h.ct_export(E.ctx, ct), core.ct_to_coeff(PO, oct_))
+        dec = h.decrypt_decode(E.ctx, sk, ct)
+        assert np.abs(dec - z).max() < 1e-3
+
+
+def _rand_ct(PO, level, seed):
+    rng = np.random.default_rng(seed)
+    Q = PO.q[: level + 1]
+    return np.stack([np.stack([rng.integers(0, q, size=PO.N, dtype=np.uint64) for q in Q]) for _ in range(2)])
+
+
+@gpu
+@pytest.mark.parametrize("name", ["tiny_a", "uci", "criteo"])
+def test_modup_moddown_rescale_match_oracle(name, torch_mod):
+    E = env(name, torch_mod)
+    h, PO = E.h, E.PO
+    level = PO.L - 1 if PO.L > 1 else PO.L
+    coeff = _rand_ct(PO, level, 3)
+    Q = PO.q[: level + 1]
+    qp = PO.qp(level)
+    c1_ntt = core.ntt(coeff[1], Q, PO)
+    ct = h.ct_import(E.ctx, coeff, level, 2.0 ** 30)
+    perm = _slot_to_natural(PO.N)
+    dptr = ct.device_ptr()
+    torch = E.torch
+    for k in range(PO.dnum(level)):
+        out = torch.zeros(len(qp) * PO.N, dtype=torch.uint64, device="cuda")
+        h.modup(E.ctx, dptr + (level + 1) * PO.N * 8, level, k, out)
+        got = E.host(out).reshape(len(qp), PO.N)[:, perm]
+        assert np.array_equal(got, core.modup(PO, c1_ntt, level, k)), k
+    y = np.stack([np.random.default_rng(4).integers(0, q, size=PO.N, dtype=np.uint64) for q in qp])
+    yd = E.dev(core.intt(y, qp, PO))          # coefficient form -> library NTT
+    _ntt_limbs(E, yd, level, len(qp))
+    out = torch.zeros((level + 1) * PO.N, dtype=torch.uint64, device="cuda")
+    h.moddown(E.ctx, yd, level, out)
+    got = E.host(out).reshape(level + 1, PO.N)[:, perm]
+    assert np.array_equal(got, core.moddown(PO, y, level))
+    r = h.rescale(E.ctx, ct)
+    oct_ = core.Ciphertext(core.ntt(coeff[0], Q, PO), c1_ntt, level, 2 ** 30)
+    assert np.array_equal(h.ct_export(E.ctx, r), core.ct_to_coeff(PO, core.rescale(PO, oct_)))
+
+
+def _ntt_limbs(E, d, level, nl):
+    """library NTT of a Q_l P polynomial (limb i uses its chain prime)."""
+    PO = E.PO
+    E.h.ntt_fwd(E.ctx, d, 0, level + 1, 1)
+    E.h.ntt_fwd(E.ctx, d.data_ptr() + (level + 1) * PO.N * 8, PO.L + 1, PO.K, 1)
+
+
+@gpu
+@pytest.mark.parametrize("name", ["tiny_a", "uci"])
+def test_rotation_matches_oracle(name, torch_mod):
+    E = env(name, torch_mod)
+    h, PO, cfg = E.h, E.PO, E.cfg
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    osk = core.sk_gen(PO, cfg.seed)
+    ks = [1, 7, PO.n - 3]
+    gs = [core.galois_elt(k, PO) for k in ks]
+    rk = h.rotkeys_gen(E.ctx, sk, gs, cfg.seed)
+    ork = core.rotkeys_gen(PO, osk, gs, cfg.seed)
+    for level in (PO.L, 1):
+        coeff = _rand_ct(PO, level, 7 + level)
+        Q = PO.q[: level + 1]
+        ct = h.ct_import(E.ctx, coeff, level, 1.0)
+        oct_ = core.Ciphertext(core.ntt(coeff[0], Q, PO), core.ntt(coeff[1], Q, PO), level, 1)
+        ring = [h.ct_alloc(E.ctx, level) for _ in ks]
+        h.rotate_hoisted(E.ctx, rk, ct, ks, ring)
+        for k, rct in zip(ks, ring):
+            want = core.ct_to_coeff(PO, core.rotate(PO, oct_, k, ork))
+            assert np.array_equal(h.ct_export(E.ctx, h.rotate(E.ctx, rk, ct, k)), want)
+            assert np.array_equal(h.ct_export(E.ctx, rct), want)
+
+
+def _gpu_lookup(E, w, mode=0, n1=0):
+    h, cfg = E.h, w.config
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    plan = h.plan_create(E.ctx, T, cfg.level, n1, mode)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N), cfg.seed)
+    info = plan.info()
+    outs = []
+    for q in range(w.indices.shape[0]):
+        x = h.encode_query(T, w.indices[q], w.dense[q], info.n_in_cts * cfg.n_slots)
+        cts = [h.encrypt(E.ctx, pk, x[c * cfg.n_slots:(c + 1) * cfg.n_slots], cfg.level,
+                         (cfg.seed << 20) | (q * info.n_in_cts + c)) for c in range(info.n_in_cts)]
+        outs.append(h.lookup(E.ctx, plan, rk, cts))
+    return plan, sk, outs
+
+
+@gpu
+@pytest.mark.parametrize("name,mode", [("tiny_a", 0), ("tiny_b", 0), ("uci", 0), ("uci", 1), ("tiny_b", 1)])
+def test_lookup_bit_exact_vs_oracle(name, mode, torch_mod):
+    E = env(name, torch_mod)
+    w = synth.make_workload(name)
+    ref = lk.run_config(w, mode=mode)
+    plan, sk, outs = _gpu_lookup(E, w, mode)
+    info = plan.info()
+    assert (info.n_diag, info.n_unique, info.n1, info.mbar) == (ref.plan.n_diag, len(ref.plan.u_slots),
+                                                                ref.plan.n1, ref.plan.mbar)
+    assert plan.rotations() == ref.plan.rotation_amounts(ref.P)
+    got = E.h.ct_export(E.ctx, outs[0][0])
+    assert np.array_equal(got, core.ct_to_coeff(ref.P, ref.outs[0][0]))
+    z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
+    y = lk.gather(ref.lay, w.indices[0])
+    assert np.abs(z[: ref.lay.M] - y).max() < 1e-3
