@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""bench.py -- HE-LRM server-side encrypted embedding lookup on B200.
+
+One step = one Criteo-shaped encrypted lookup (BASELINE.json configs[2],
+batch 1): the whole hot path S3-S10 of SURVEY.md section 8(a) -- ModUp,
+31 hoisted baby key switches, 512 plaintext-diagonal MACs, 15 giant steps
+(ModDown, ModUp, key switch), final ModDown, rescale and 6 RotSum rotations --
+on a ciphertext already resident in HBM.  The 15.5 GiB of diagonals and
+rotation keys it streams are far larger than L2 (126 MB), so no L2 flush is
+needed between steps.
+
+Also measured on the same run (secondary, BASELINE.json metric list): NTT
+GB/s (configs[4] microbench, forward and inverse over 1024 ciphertexts) and
+hoisted key-switch rotations/s (amounts 1..64).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun): every rank runs its own independent lookups on its own
+GPU (replicas, no data-path collective; "scaling": "weak"); the time is the
+max over ranks.  `--impl reference` times the CPU oracle (the parity
+reference, oracle/) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clock / throttle-reason sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.out = ""
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        loaded = [s for s, _, _ in rows if s > 0] or [rows[0][0]]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_lookup_seconds(threads: int = 0):
+    """CPU oracle (oracle/, as it stands) on a bounded sample of the Criteo
+    lookup: each primitive the double-hoisted lookup is made of is timed once
+    on Criteo parameters (random residues and random key material -- validity
+    is irrelevant to the arithmetic), then composed with the exact operation
+    counts of the Criteo plan.  Returns (seconds per lookup, sample text, cores)."""
+    import synth
+    from oracle import core
+    from oracle import lookup as lk
+    if threads:
+        core.set_threads(threads)
+    cfg = synth.config_by_name("criteo")
+    w = synth.make_workload("criteo")
+    P = core.params_from_config(cfg)
+    plan = lk.make_plan(lk.layout(w), P.n, cfg.level)
+    l = cfg.level
+    qp = P.qp(l)
+    rng = np.random.default_rng(0)
+    rand = lambda primes: np.stack([rng.integers(0, q, size=P.N, dtype=np.uint64) for q in primes])
+    c0, c1 = rand(P.q[: l + 1]), rand(P.q[: l + 1])
+    g = core.galois_elt(1, P)
+    rk = core.RotKeys(P)
+    allp = P.q + P.p
+    key = [(rand(allp), rand(allp)) for _ in range(P.dnum(l))]
+    rk.keys[g] = key
+    t = {}
+    for _ in range(2):                     # second pass is the timed one (first warms allocations)
+        t.update(_oracle_parts(P, core, l, qp, c0, c1, g, rk))
+    n_baby = sum(1 for j in plan.babies[0] if j)
+    n_mac = sum(len(e) for e in plan.entries[0])
+    n_giant = sum(1 for i, e in enumerate(plan.entries[0]) if e and plan.giants[0][i])
+    n_rotsum = int(round(math.log2(P.n // plan.mbar)))
+    rot_full = t["modup_all"] + t["baby_kip"] + 2 * t["moddown"]
+    total = (t["modup_all"] + n_baby * t["baby_kip"] + n_mac * t["mac"]
+             + n_giant * (t["moddown"] + t["modup_all"] + t["giant_kip"])
+             + 2 * t["moddown"] + t["rescale"] + n_rotsum * rot_full)
+    sample = (f"oracle primitives timed on Criteo parameters (ModUp x{P.dnum(l)} digits, 1 baby key switch, "
+              f"1 diagonal MAC, ModDown, 1 giant key switch, rescale; 2nd of 2 passes), composed by the plan's "
+              f"counts: {n_baby} baby KS + {n_mac} MACs + {n_giant} giants + {n_rotsum} RotSum rotations")
+    return total, sample, core.threads(), {k: round(v, 4) for k, v in t.items()}
+
+
+def _oracle_parts(P, core, l, qp, c0, c1, g, rk):
+    t = {}
+    t0 = time.perf_counter()
+    D = [core.modup(P, c1, l, k) for k in range(P.dnum(l))]
+    t["modup_all"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    a, b = core.rotate_lazy(P, core.Ciphertext(c0, c1, l, 1), 1, rk, D=D)
+    t["baby_kip"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    A = core.vadd(a, core.vmul(a, b, qp), qp)
+    B = core.vadd(b, core.vmul(b, a, qp), qp)
+    t["mac"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Bp = core.moddown(P, B, l)
+    t["moddown"] = time.perf_counter() - t0
+    D2 = [core.modup(P, Bp, l, k) for k in range(P.dnum(l))]
+    t0 = time.perf_counter()
+    G0, G1 = core.keyswitch_digits(P, D2, g, rk, l)
+    core.vadd(core.automorph_ntt(A, g, P.N), G0, qp)
+    t["giant_kip"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    core.rescale(P, core.Ciphertext(Bp, Bp, l, 1))
+    t["rescale"] = time.perf_counter() - t0
+    return t
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args, world, rank, local):
+    import torch
+    import synth
+    from paper_2506_18150_b200 import helrm
+
+    dev = local
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    w = synth.make_workload("criteo", batch=4)
+    cfg = w.config
+    P = helrm.params_from_config(cfg)
+    ctx = helrm.Context(P, dev, stream.cuda_stream)
+    t_setup = time.time()
+    T = helrm.tables_create(P, w.tables, w.n_dense)
+    plan = helrm.plan_create(ctx, T, cfg.level)
+    info = plan.info()
+    sk = helrm.sk_gen(ctx, cfg.seed)
+    pk = helrm.pk_gen(ctx, sk, cfg.seed)
+    rk = helrm.rotkeys_gen(ctx, sk, plan.galois(cfg.N), cfg.seed)
+    cts = []
+    for q in range(w.indices.shape[0]):
+        x = helrm.encode_query(T, w.indices[q], w.dense[q], cfg.n_slots)
+        cts.append(helrm.encrypt(ctx, pk, x, cfg.level, (cfg.seed << 20) | (rank * 1000 + q)))
+    ctx.sync()
+    t_setup = time.time() - t_setup
+    log(f"[rank {rank}] setup {t_setup:.1f}s: diag {info.diag_bytes / 2**30:.2f} GiB, keys "
+        f"{rk.nbytes() / 2**30:.2f} GiB, {info.n_diag} diagonals, n1={info.n1}, rotations={info.n_rotations}")
+
+    def step(i):
+        out = helrm.lookup(ctx, plan, rk, [cts[i % len(cts)]])
+        for o in out:
+            o.close()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if args.ncu_step:
+        # one lookup inside a profiler range (ncu --profile-from-start off)
+        torch.cuda.profiler.start()
+        step(0)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        log(f"[rank {rank}] ncu step done")
+        sys.exit(0)
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local, world)
+    value = world * args.steps / (ms / 1e3)
+
+    # per-kernel breakdown on a second, profiled pass (CUDA events per launch)
+    ctx.profile(True)
+    for i in range(args.steps):
+        step(i)
+    stats = ctx.profile_stats()
+    ctx.profile(False)
+    top = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    peak, peak_src = hbm_peak()
+    total_kernel_ms = sum(v["ms"] for v in stats.values())
+    achieved = top[1]["bytes"] / (top[1]["ms"] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "share_of_step": round(top[1]["ms"] / total_kernel_ms, 3),
+                "bytes_per_launch": round(top[1]["bytes"] / top[1]["count"]),
+                "avg_launch_us": round(top[1]["ms"] * 1e3 / top[1]["count"], 2)}
+    step_bytes = sum(v["bytes"] for v in stats.values()) / args.steps
+    kernels = {k: {"count": v["count"] // args.steps, "ms_per_step": round(v["ms"] / args.steps, 4),
+                   "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in
+               sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+
+    # e2e through the public API: pinned host coefficient-form ct in, result out
+    N, L = cfg.N, cfg.level
+    ct_host = [helrm.ct_export(ctx, c) for c in cts]
+    pin_in = [torch.empty(c.size, dtype=torch.uint64, pin_memory=True) for c in ct_host]
+    for p_, c in zip(pin_in, ct_host):
+        p_.numpy()[:] = c.ravel()
+    pin_out = torch.empty(2 * L * N, dtype=torch.uint64, pin_memory=True)
+
+    def e2e_step(i):
+        ci = helrm.ct_import(ctx, pin_in[i % len(pin_in)].numpy(), L, 2.0 ** cfg.log_scale)
+        out = helrm.lookup(ctx, plan, rk, [ci])
+        helrm_ct_export_into(helrm, ctx, out[0], pin_out.numpy())
+        for o in out:
+            o.close()
+        ci.close()
+
+    for i in range(max(1, args.warmup // 2)):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        e2e_step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e = {"value": round(world * args.steps / (e2e_ms / 1e3), 3), "unit": "lookups/s",
+           "h2d_bytes_per_step": int(2 * (L + 1) * N * 8), "d2h_bytes_per_step": int(2 * L * N * 8),
+           "path": "helrm_ct_import (pinned host, coefficient form) -> helrm_lookup -> helrm_ct_export"}
+
+    secondary = {}
+    if not args.skip_micro:
+        secondary = micro(args, ctx, helrm, torch, stream, sk, cfg, world)
+
+    return {
+        "value": value, "ms": ms / args.steps, "launches": launches, "clocks": clk.summary(),
+        "roofline": roofline, "kernels": kernels, "e2e": e2e, "secondary": secondary,
+        "setup_s": round(t_setup, 1), "info": info, "step_bytes": step_bytes, "total_kernel_ms": total_kernel_ms,
+        "rk_bytes": rk.nbytes(),
+    }
+
+
+def helrm_ct_export_into(helrm, ctx, ct, host: np.ndarray):
+    import ctypes
+    helrm._check(helrm._L.helrm_ct_export(ctx.h, ct.h, host.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                         host.size))
+
+
+def micro(args, ctx, helrm, torch, stream, sk, cfg, world):
+    """configs[4]: NTT GB/s over 1024 cts x 2 x 24 limbs; hoisted rotations/s."""
+    N, L = cfg.N, cfg.level
+    n_cts = args.micro_cts
+    limbs = n_cts * 2 * (L + 1)
+    buf = torch.randint(0, 2**49, (limbs * N,), dtype=torch.int64, device="cuda").view(torch.uint64)
+    torch.cuda.synchronize()
+    ptr = buf.data_ptr()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    helrm.ntt_fwd(ctx, ptr, 0, L + 1, 2 * n_cts)
+    helrm.ntt_inv(ctx, ptr, 0, L + 1, 2 * n_cts)
+    torch.cuda.synchronize()
+    reps = 3
+    ev[0].record(stream)
+    for _ in range(reps):
+        helrm.ntt_fwd(ctx, ptr, 0, L + 1, 2 * n_cts)
+    ev[1].record(stream)
+    for _ in range(reps):
+        helrm.ntt_inv(ctx, ptr, 0, L + 1, 2 * n_cts)
+    ev[2].record(stream)
+    torch.cuda.synchronize()
+    fwd_ms = ev[0].elapsed_time(ev[1]) / reps
+    inv_ms = ev[1].elapsed_time(ev[2]) / reps
+    nbytes = 16.0 * N * limbs
+    del buf
+    torch.cuda.empty_cache()
+    # hoisted rotations: amounts 1..64, keys for all of them
+    amounts = list(range(1, 65))
+    rk = helrm.rotkeys_gen(ctx, sk, sorted({pow(5, a, 2 * N) for a in amounts}), cfg.seed)
+    n_rot_cts = args.rot_cts
+    cts = [helrm.ct_random(ctx, cfg.seed, i, L) for i in range(n_rot_cts)]
+    ring = [helrm.ct_alloc(ctx, L) for _ in range(4)]
+    helrm.rotate_hoisted(ctx, rk, cts[0], amounts[:4], ring)
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for c in cts:
+        helrm.rotate_hoisted(ctx, rk, c, amounts, ring)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    rot_ms = ev[0].elapsed_time(ev[1])
+    rot_ms = max_over_ranks(rot_ms, world)
+    fwd_ms = max_over_ranks(fwd_ms, world)
+    inv_ms = max_over_ranks(inv_ms, world)
+    peak, _ = hbm_peak()
+    return {
+        "ntt_fwd_GBps": round(world * nbytes / (fwd_ms / 1e3) / 1e9, 1),
+        "ntt_inv_GBps": round(world * nbytes / (inv_ms / 1e3) / 1e9, 1),
+        "ntt_fwd_frac_hbm": round(nbytes / (fwd_ms / 1e3) / 1e9 / peak, 4),
+        "ntt_limbs_per_pass": limbs,
+        "ntt_cts": n_cts,
+        "rotations_per_s": round(world * n_rot_cts * len(amounts) / (rot_ms / 1e3), 1),
+        "rotation_cts": n_rot_cts,
+        "rotation_keys_GiB": round(rk.nbytes() / 2**30, 2),
+    }
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip-micro", action="store_true")
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--micro-cts", type=int, default=1024)
+    ap.add_argument("--rot-cts", type=int, default=8)
+    ap.add_argument("--ncu-step", action="store_true", help="profile one lookup in a cudaProfiler range and exit")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    metric = "encrypted lookups/sec"
+    config = {"workload": "criteo_b1_lookup", "model": "HE-LRM Criteo-shaped 26-table lookup (synthetic)",
+              "N": 65536, "L": 23, "K": 4, "dnum": 6, "log_scale": 40, "batch": 1, "n_tables": 26,
+              "n_diag": 512, "n1": 32, "n2": 16, "parallelism": f"replicas{world}",
+              "l2": "inputs larger than L2: 15.5 GiB of diagonals + keys streamed per step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        secs = []
+        last = None
+        for i in range(args.warmup + args.steps):
+            s, sample, cores, parts = oracle_lookup_seconds()
+            if i >= args.warmup:
+                secs.append(s)
+            last = (sample, cores, parts)
+        t = statistics.mean(secs)
+        v = 1.0 / t
+        line = {"metric": metric, "value": round(v, 6), "unit": "lookups/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic", "config": config, "impl": "reference",
+                "cpu_baseline": {"value": round(v, 6), "unit": "lookups/s", "cores": last[1], "kind": "oracle",
+                                 "sample": last[0], "parts_s": last[2]},
+                "e2e": {"value": round(v, 6), "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    world, rank, local = dist_setup(args.gpus)
+    r = run_gpu(args, world, rank, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu_baseline:
+        s, sample, cores, parts = oracle_lookup_seconds()
+        cpu = {"value": round(1.0 / s, 6), "unit": "lookups/s", "cores": cores, "kind": "oracle", "sample": sample,
+               "parts_s": parts}
+    if rank == 0:
+        info = r["info"]
+        line = {"metric": metric, "value": round(r["value"], 3), "unit": "lookups/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms"], 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic", "config": config, "roofline": r["roofline"], "cpu_baseline": cpu,
+                "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
+                "secondary": r["secondary"],
+                "step": {"kernel_ms": round(r["total_kernel_ms"] / args.steps, 4),
+                         "algorithmic_GB": round(r["step_bytes"] / 1e9, 3),
+                         "floor_GB": round((info.diag_bytes + r["rk_bytes"]) / 1e9, 3),
+                         "kernels": r["kernels"]},
+                "setup_s": r["setup_s"]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

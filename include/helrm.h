@@ -98,6 +98,12 @@ void helrm_ctx_destroy(helrm_ctx* c);
 helrm_status helrm_ctx_sync(helrm_ctx* c);
 /* Number of library kernels launched on this context since creation. */
 uint64_t helrm_ctx_launches(const helrm_ctx* c);
+/* Per-kernel timing: when enabled, every library launch is bracketed by CUDA
+ * events on the context stream; enabling/disabling clears the records.
+ * helrm_ctx_profile_json returns {"kernel": {"count": n, "ms": total}, ...}
+ * for the records so far (synchronises; string owned by the context). */
+helrm_status helrm_ctx_profile(helrm_ctx* c, int enable);
+const char* helrm_ctx_profile_json(helrm_ctx* c);
 
 /* ---- client keys (D9-D11) --------------------- */
 /* Deterministic in the seed (counter-based SplitMix64 streams, D9).  Key

@@ -59,7 +59,7 @@ struct helrm_params {
 
 struct ConvEntry {
   ConvDev* d = nullptr;
-  int nt = 0;
+  int nb = 0, nt = 0;
   std::vector<int16_t> rows;
 };
 
@@ -88,7 +88,10 @@ struct helrm_ctx {
   uint64_t launches = 0;
   std::vector<uint32_t> dlog5;    // dlog5[g] for odd g < 2N (0xffffffff if not a power of 5)
 
-  DevCtx dc() { return DevCtx{dprimes, dslotpos, P.log_n, P.N, stream, &launches}; }
+  Profiler prof;
+  std::string prof_json;
+
+  DevCtx dc() { return DevCtx{dprimes, dslotpos, P.log_n, P.N, stream, &launches, &prof}; }
 
   void* dalloc(size_t bytes) {
     void* p = nullptr;
@@ -170,6 +173,33 @@ struct helrm_plan {
   uint32_t nl = 0;
   std::vector<int64_t> rotations;
 };
+
+// ============================================================================
+// profiler (per-kernel CUDA events on the context stream)
+// ============================================================================
+namespace helrm {
+cudaEvent_t Profiler::get() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  HCUDA(cudaEventCreate(&e));
+  return e;
+}
+ProfScope::ProfScope(const DevCtx& c_, const char* name, double bytes) : c(c_) {
+  if (c.prof && c.prof->on) {
+    Profiler::Rec r{name, c.prof->get(), c.prof->get(), bytes};
+    HCUDA(cudaEventRecord(r.a, c.stream));
+    idx = (int)c.prof->recs.size();
+    c.prof->recs.push_back(r);
+  }
+}
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(c.prof->recs[idx].b, c.stream);
+}
+}  // namespace helrm
 
 // ============================================================================
 // context helpers
@@ -274,6 +304,7 @@ static const ConvEntry& conv_entry(helrm_ctx* c, uint32_t l, int digit) {
   HCUDA(cudaMemcpyAsync(e.d, &h, sizeof(ConvDev), cudaMemcpyHostToDevice, c->stream));
   HCUDA(cudaStreamSynchronize(c->stream));
   c->owned.push_back(e.d);
+  e.nb = h.nb;
   e.nt = h.nt;
   e.rows = rows;
   return c->conv.emplace(key, e).first->second;
@@ -289,7 +320,7 @@ static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t*
   DBuf x(c, nb * N);
   ntt_inv(c, in + lo * N, x.p, nb, P.map_range(lo, nb));
   const ConvEntry& ce = conv_entry(c, l, k);
-  launch_conv(c->dc(), ce.d, ce.nt, ce.rows.data(), x.p, out);
+  launch_conv(c->dc(), ce.d, ce.nb, ce.nt, ce.rows.data(), x.p, out);
   LimbMap m = P.map_qp(l);
   ntt_fwd(c, out, out, lo, sub_map(m, 0, lo));
   ntt_fwd(c, out + hi * N, out + hi * N, nl - hi, sub_map(m, hi, nl - hi));
@@ -303,7 +334,7 @@ static void moddown(helrm_ctx* c, const uint64_t* y, uint32_t l, uint64_t* out) 
   DBuf yp(c, P.K * N), t(c, (l + 1) * N);
   ntt_inv(c, y + (l + 1) * N, yp.p, P.K, P.map_range(P.L + 1, P.K));
   const ConvEntry& ce = conv_entry(c, l, -1);
-  launch_conv(c->dc(), ce.d, ce.nt, ce.rows.data(), yp.p, t.p);
+  launch_conv(c->dc(), ce.d, ce.nb, ce.nt, ce.rows.data(), yp.p, t.p);
   ntt_fwd(c, t.p, t.p, l + 1, P.map_q(l));
   const LevelConst& lc = level_const(c, l);
   launch_sub_scale(c->dc(), y, t.p, out, P.map_q(l), lc.pinv, lc.pinvs);
@@ -553,6 +584,48 @@ helrm_status helrm_ctx_sync(helrm_ctx* c) {
 }
 
 uint64_t helrm_ctx_launches(const helrm_ctx* c) { return c ? c->launches : 0; }
+
+helrm_status helrm_ctx_profile(helrm_ctx* c, int enable) {
+  return guard([&] {
+    need(c, HELRM_ERR_ARG, "null argument");
+    HCUDA(cudaStreamSynchronize(c->stream));
+    for (auto& r : c->prof.recs) {
+      c->prof.pool.push_back(r.a);
+      c->prof.pool.push_back(r.b);
+    }
+    c->prof.recs.clear();
+    c->prof.on = enable != 0;
+  });
+}
+
+const char* helrm_ctx_profile_json(helrm_ctx* c) {
+  if (!c) return "{}";
+  cudaStreamSynchronize(c->stream);
+  struct Agg {
+    uint64_t n = 0;
+    double ms = 0, bytes = 0;
+  };
+  std::map<std::string, Agg> agg;
+  for (auto& r : c->prof.recs) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto& a = agg[r.name];
+    a.n++;
+    a.ms += ms;
+    a.bytes += r.bytes;
+  }
+  std::string j = "{";
+  for (auto& kv : agg) {
+    if (j.size() > 1) j += ", ";
+    char buf[200];
+    snprintf(buf, sizeof buf, "\"%s\": {\"count\": %llu, \"ms\": %.6f, \"bytes\": %.0f}", kv.first.c_str(),
+             (unsigned long long)kv.second.n, kv.second.ms, kv.second.bytes);
+    j += buf;
+  }
+  j += "}";
+  c->prof_json = j;
+  return c->prof_json.c_str();
+}
 
 // ---------------------------------------------------------------------------
 // keys

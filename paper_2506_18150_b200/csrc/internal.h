@@ -101,12 +101,35 @@ std::vector<uint32_t> slot_of_bitrev(uint32_t log_n);
 std::vector<uint64_t> gauss_cdt_table();
 
 // ---------------- kernel launchers (kernels_*.cu) ----------------
+// Optional per-kernel CUDA-event timing (helrm_ctx_profile): each launcher
+// brackets its launch with events on the context stream.
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    const char* name;
+    cudaEvent_t a, b;
+    double bytes;                 // algorithmic HBM bytes of the launch
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get();
+};
+
 struct DevCtx {
   const PrimeDev* primes;     // device array, chain-indexed
   const uint32_t* slotpos;    // [N] slot position of bitrev index r
   uint32_t log_n, N;
   cudaStream_t stream;
   uint64_t* launches;         // host counter
+  Profiler* prof;
+};
+
+// RAII: records a start event now and a stop event at scope exit
+struct ProfScope {
+  const DevCtx& c;
+  int idx = -1;
+  ProfScope(const DevCtx& c_, const char* name, double bytes = 0);
+  ~ProfScope();
 };
 
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total_limbs,
@@ -124,7 +147,8 @@ void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const 
                        const uint64_t* sp);
 void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
                       int accumulate);
-void launch_conv(const DevCtx& c, const ConvDev* cv, int nt, const int16_t* rows, const uint64_t* in, uint64_t* out);
+void launch_conv(const DevCtx& c, const ConvDev* cv, int nb, int nt, const int16_t* rows, const uint64_t* in,
+                 uint64_t* out);
 void launch_sub_scale(const DevCtx& c, const uint64_t* y, const uint64_t* t, uint64_t* out, const LimbMap& map,
                       const uint64_t* s, const uint64_t* sp);
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, uint64_t ql, uint64_t* out, const LimbMap& map);

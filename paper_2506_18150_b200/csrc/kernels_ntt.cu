@@ -173,9 +173,15 @@ void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
   const size_t smem = kTile * sizeof(uint64_t);
   for (size_t off = 0; off < n_total; off += ch) {
     unsigned cnt = (unsigned)std::min(ch, n_total - off);
-    k_ntt_fwd_p1<<<dim3(g.G1, cnt), kThreads, smem, c.stream>>>(src + off * g.N, scratch, c.primes, map, off, g);
-    k_ntt_fwd_p2<<<dim3(g.G2, cnt), kThreads, smem, c.stream>>>(scratch, dst + off * g.N, c.primes, map, off, g,
-                                                                c.slotpos);
+    {
+      ProfScope ps_(c, "ntt_fwd_p1", 8.0 * g.N * cnt);
+      k_ntt_fwd_p1<<<dim3(g.G1, cnt), kThreads, smem, c.stream>>>(src + off * g.N, scratch, c.primes, map, off, g);
+    }
+    {
+      ProfScope ps_(c, "ntt_fwd_p2", 8.0 * g.N * cnt);
+      k_ntt_fwd_p2<<<dim3(g.G2, cnt), kThreads, smem, c.stream>>>(scratch, dst + off * g.N, c.primes, map, off, g,
+                                                                  c.slotpos);
+    }
     *c.launches += 2;
   }
   HCUDA(cudaGetLastError());
@@ -188,9 +194,15 @@ void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
   const size_t smem = kTile * sizeof(uint64_t);
   for (size_t off = 0; off < n_total; off += ch) {
     unsigned cnt = (unsigned)std::min(ch, n_total - off);
-    k_ntt_inv_pa<<<dim3(g.G2, cnt), kThreads, smem, c.stream>>>(src + off * g.N, scratch, c.primes, map, off, g,
-                                                                c.slotpos);
-    k_ntt_inv_pb<<<dim3(g.G1, cnt), kThreads, smem, c.stream>>>(scratch, dst + off * g.N, c.primes, map, off, g);
+    {
+      ProfScope ps_(c, "ntt_inv_pa", 8.0 * g.N * cnt);
+      k_ntt_inv_pa<<<dim3(g.G2, cnt), kThreads, smem, c.stream>>>(src + off * g.N, scratch, c.primes, map, off, g,
+                                                                  c.slotpos);
+    }
+    {
+      ProfScope ps_(c, "ntt_inv_pb", 8.0 * g.N * cnt);
+      k_ntt_inv_pb<<<dim3(g.G1, cnt), kThreads, smem, c.stream>>>(scratch, dst + off * g.N, c.primes, map, off, g);
+    }
     *c.launches += 2;
   }
   HCUDA(cudaGetLastError());

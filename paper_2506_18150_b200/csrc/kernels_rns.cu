@@ -230,6 +230,7 @@ __global__ void k_diag_mac(const MacTerm* __restrict__ terms, int n_terms, uint6
 static dim3 grid_for(uint32_t N, int limbs) { return dim3((N + kT - 1) / kT, limbs); }
 
 void launch_reduce_signed(const DevCtx& c, const int64_t* m, uint64_t* out, const LimbMap& map) {
+  ProfScope ps_(c, "reduce_signed", 8.0 * c.N * (1 + map.n));
   k_reduce_signed<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(m, out, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
@@ -237,6 +238,7 @@ void launch_reduce_signed(const DevCtx& c, const int64_t* m, uint64_t* out, cons
 
 void launch_sample_uniform_ntt(const DevCtx& c, uint64_t* out, const LimbMap& map, uint64_t seed, uint64_t purpose,
                                uint64_t a, uint64_t b, const LimbMap& ids) {
+  ProfScope ps_(c, "sample_uniform", 8.0 * c.N * map.n);
   k_sample_uniform_ntt<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(out, c.primes, map, c.log_n, c.slotpos, seed,
                                                                   purpose, a, b, ids);
   (*c.launches)++;
@@ -244,12 +246,14 @@ void launch_sample_uniform_ntt(const DevCtx& c, uint64_t* out, const LimbMap& ma
 }
 
 void launch_sample_small(const DevCtx& c, int64_t* out, uint64_t base, int kind, const uint64_t* cdt) {
+  ProfScope ps_(c, "sample_small", 8.0 * c.N);
   k_sample_small<<<(c.N + kT - 1) / kT, kT, 0, c.stream>>>(out, c.N, base, kind, cdt);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, const LimbMap& map) {
+  ProfScope ps_(c, "binary", 8.0 * c.N * map.n * (op == 3 ? 2 : 3));
   k_binary<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(op, a, b, out, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
@@ -257,6 +261,7 @@ void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b
 
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
                        const uint64_t* sp) {
+  ProfScope ps_(c, "scalar_mul", 16.0 * c.N * map.n);
   k_scalar_mul<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
@@ -264,12 +269,15 @@ void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const 
 
 void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
                       int accumulate) {
+  ProfScope ps_(c, "automorph", 8.0 * c.N * map.n * (accumulate ? 3 : 2));
   k_automorph<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, rot, accumulate);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
-void launch_conv(const DevCtx& c, const ConvDev* cv, int nt, const int16_t* rows, const uint64_t* in, uint64_t* out) {
+void launch_conv(const DevCtx& c, const ConvDev* cv, int nb, int nt, const int16_t* rows, const uint64_t* in,
+                 uint64_t* out) {
+  ProfScope ps_(c, "conv", 8.0 * c.N * (nt + nb));
   ConvRows r{};
   for (int t = 0; t < nt; t++) r.row[t] = rows[t];
   const int tpb = 4;
@@ -280,18 +288,21 @@ void launch_conv(const DevCtx& c, const ConvDev* cv, int nt, const int16_t* rows
 
 void launch_sub_scale(const DevCtx& c, const uint64_t* y, const uint64_t* t, uint64_t* out, const LimbMap& map,
                       const uint64_t* s, const uint64_t* sp) {
+  ProfScope ps_(c, "sub_scale", 24.0 * c.N * map.n);
   k_sub_scale<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(y, t, out, c.primes, map, c.N, s, sp);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, uint64_t ql, uint64_t* out, const LimbMap& map) {
+  ProfScope ps_(c, "rescale_prep", 8.0 * c.N * (1 + map.n));
   k_rescale_prep<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(xl, ql, out, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
+  ProfScope ps_(c, "kip", 8.0 * c.N * (3.0 * a.dnum * map.n + (a.c0 ? a.level + 1 : 0) + (a.accumulate ? 4 : 2) * map.n));
   k_kip<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
@@ -299,6 +310,7 @@ void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
 
 void launch_diag_mac(const DevCtx& c, const MacTerm* terms, int n_terms, uint64_t* out0, uint64_t* out1,
                      const LimbMap& map) {
+  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (3.0 * n_terms + 2));
   k_diag_mac<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(terms, n_terms, out0, out1, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());

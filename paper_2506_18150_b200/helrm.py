@@ -110,13 +110,17 @@ _L.helrm_last_error.restype = ctypes.c_char_p
 _L.helrm_version.restype = ctypes.c_char_p
 _L.helrm_ctx_launches.argtypes = [_vp]
 _L.helrm_ctx_launches.restype = _u64
+_L.helrm_ctx_profile.argtypes = [_vp, ctypes.c_int]
+_L.helrm_ctx_profile.restype = ctypes.c_int
+_L.helrm_ctx_profile_json.argtypes = [_vp]
+_L.helrm_ctx_profile_json.restype = ctypes.c_char_p
 _L.helrm_rotkeys_bytes.argtypes = [_vp]
 _L.helrm_rotkeys_bytes.restype = _sz
 
 EXPORTED = sorted(list(_SIGS) + ["helrm_params_destroy", "helrm_ctx_destroy", "helrm_sk_destroy", "helrm_pk_destroy",
                                  "helrm_rotkeys_destroy", "helrm_tables_destroy", "helrm_ct_destroy",
                                  "helrm_plan_destroy", "helrm_last_error", "helrm_version", "helrm_ctx_launches",
-                                 "helrm_rotkeys_bytes"])
+                                 "helrm_rotkeys_bytes", "helrm_ctx_profile", "helrm_ctx_profile_json"])
 
 
 def _check(code: int):
@@ -252,6 +256,13 @@ class Context(_Handle):
 
     def launches(self) -> int:
         return int(_L.helrm_ctx_launches(self.h))
+
+    def profile(self, on: bool):
+        _check(_L.helrm_ctx_profile(self.h, 1 if on else 0))
+
+    def profile_stats(self) -> dict:
+        import json
+        return json.loads(_L.helrm_ctx_profile_json(self.h).decode())
 
 
 class SecretKey(_Handle):

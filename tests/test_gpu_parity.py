@@ -258,3 +258,40 @@ def test_lookup_bit_exact_vs_oracle(name, mode, torch_mod):
     z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
     y = lk.gather(ref.lay, w.indices[0])
     assert np.abs(z[: ref.lay.M] - y).max() < 1e-3
+
+
+@gpu
+def test_criteo_full_size_matches_oracle_golden(torch_mod):
+    """Criteo-shaped lookup at full size (N = 2^16, 24 + 4 primes, 512
+    diagonals, 52 rotation keys) against digests of the oracle's own outputs
+    (tests/golden/criteo.json, written by tests/golden/make_golden.py from
+    oracle/ only): rotation key, encrypted query, output ciphertext; plus the
+    decrypted output against the float64 gather."""
+    import hashlib
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "criteo.json")))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype="<u8").tobytes()).hexdigest()
+    E = env("criteo", torch_mod)
+    w = synth.make_workload("criteo")
+    plan, sk, outs = _gpu_lookup(E, w)
+    info = plan.info()
+    assert (info.n_diag, info.n1, info.n2_max, info.n_rotations) == (512, 32, 16, 52)
+    # rotation key of the first Galois element, digit by digit
+    T = E.h.tables_create(E.P, w.tables, w.n_dense)
+    rk = E.h.rotkeys_gen(E.ctx, sk, [gold["rotkey_g0"]], w.config.seed)
+    kk = E.h.rotkeys_export(E.ctx, rk, gold["rotkey_g0"])
+    assert [sha(kk[k]) for k in range(kk.shape[0])] == gold["rotkey_g0_sha"]
+    q0 = gold["queries"][0]
+    pk = E.h.pk_gen(E.ctx, sk, w.config.seed)
+    x = E.h.encode_query(T, w.indices[0], w.dense[0], w.config.n_slots)
+    ct = E.h.encrypt(E.ctx, pk, x, w.config.level, (w.config.seed << 20) | 0)
+    assert sha(E.h.ct_export(E.ctx, ct)) == q0["in_sha"][0]
+    assert sha(E.h.ct_export(E.ctx, outs[0][0])) == q0["out_sha"][0]
+    z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
+    lay = lk.layout(w)
+    y = lk.gather(lay, w.indices[0])
+    assert np.abs(z[: lay.M] - y).max() < 1e-3
+    # slot s holds y[s mod mbar] in every period (RotSum, R20)
+    zz = z.reshape(-1, info.mbar)
+    assert np.abs(zz[:, : lay.M] - y).max() < 1e-3
