@@ -70,7 +70,7 @@ typedef struct helrm_plan helrm_plan;
 
 /* ---- parameters (D1-D3) ------------------------------- */
 typedef struct {
-  uint32_t log_n;          /* ring degree N = 2^log_n, 10 <= log_n <= 16 */
+  uint32_t log_n;          /* ring degree N = 2^log_n, 12 <= log_n <= 16 */
   uint32_t n_q_groups;     /* ciphertext prime groups, in order q_0, q_1, ... */
   uint32_t q_bits[8], q_count[8];
   uint32_t n_p_groups;     /* special prime groups (alpha = K = total count) */

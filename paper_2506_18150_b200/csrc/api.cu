@@ -80,6 +80,8 @@ struct helrm_ctx {
   PrimeDev* dprimes = nullptr;
   uint64_t* dtw = nullptr;
   uint32_t* dslotpos = nullptr;
+  uint32_t* dgrp = nullptr;
+  uint8_t* deinv = nullptr;
   uint64_t* dcdt = nullptr;
   uint64_t* scratch = nullptr;
   std::map<std::pair<int, int>, ConvEntry> conv;
@@ -91,7 +93,7 @@ struct helrm_ctx {
   Profiler prof;
   std::string prof_json;
 
-  DevCtx dc() { return DevCtx{dprimes, dslotpos, P.log_n, P.N, stream, &launches, &prof}; }
+  DevCtx dc() { return DevCtx{dprimes, dslotpos, dgrp, deinv, P.log_n, P.N, stream, &launches, &prof}; }
 
   void* dalloc(size_t bytes) {
     void* p = nullptr;
@@ -443,7 +445,7 @@ helrm_status helrm_params_create(const helrm_params_desc* d, helrm_params** out)
   if (out) *out = nullptr;
   return guard([&] {
     need(d && out, HELRM_ERR_ARG, "null argument");
-    need(d->log_n >= 10 && d->log_n <= 16, HELRM_ERR_CONFIG, "log_n must be in [10, 16]");
+    need(d->log_n >= 12 && d->log_n <= 16, HELRM_ERR_CONFIG, "log_n must be in [12, 16]");
     std::vector<std::pair<uint32_t, uint32_t>> qg, pg;
     need(d->n_q_groups >= 1 && d->n_q_groups <= 8 && d->n_p_groups >= 1 && d->n_p_groups <= 4, HELRM_ERR_CONFIG,
          "bad prime group counts");
@@ -504,32 +506,50 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
     HCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     const Params& P = c->P;
     const size_t N = P.N, np = P.primes.size();
-    // twiddles: per prime 4 arrays of N words
-    std::vector<uint64_t> tw(np * 4 * N);
+    // NTT twiddles as (w, w/q) double pairs; per prime [tw1 256][tw2 N][itw1 256][itw2 N]
+    const size_t per = 2 * (2 * N + 512);  // doubles per prime
+    std::vector<double> tw(np * per);
     std::vector<uint32_t> br(N);
     for (uint32_t k = 0; k < N; k++) {
       uint32_t r = 0;
       for (uint32_t b = 0; b < P.log_n; b++) r |= ((k >> b) & 1u) << (P.log_n - 1 - b);
       br[k] = r;
     }
+    const uint32_t s1 = P.log_n - 8;
 #pragma omp parallel for
     for (size_t i = 0; i < np; i++) {
-      uint64_t q = P.primes[i], psi = P.psi[i], ipsi = inv_mod(psi, q);
-      uint64_t* w = &tw[i * 4 * N];
+      const uint64_t q = P.primes[i], psi = P.psi[i], ipsi = inv_mod(psi, q);
       std::vector<uint64_t> pw(N), ipw(N);
       pw[0] = ipw[0] = 1;
       for (size_t k = 1; k < N; k++) {
         pw[k] = mulm(pw[k - 1], psi, q);
         ipw[k] = mulm(ipw[k - 1], ipsi, q);
       }
-      for (size_t k = 0; k < N; k++) {
-        w[k] = pw[br[k]];
-        w[N + k] = shoup_pre(w[k], q);
-        w[2 * N + k] = ipw[br[k]];
-        w[3 * N + k] = shoup_pre(w[2 * N + k], q);
+      double* base = &tw[i * per];
+      auto put = [&](double* dst, size_t j, size_t idx) {
+        dst[2 * j] = (double)pw[br[idx]];
+        dst[2 * j + 1] = (double)pw[br[idx]] / (double)q;
+        dst[2 * N + 512 + 2 * j] = (double)ipw[br[idx]];
+        dst[2 * N + 512 + 2 * j + 1] = (double)ipw[br[idx]] / (double)q;
+      };
+      for (size_t idx = 0; idx < 256; idx++) put(base, idx, idx);  // pass 1 (natural index < 256)
+      double* t2 = base + 512;
+      for (size_t B = 0; B < N / 256; B++) {
+        for (uint32_t st = 0; st < 4; st++)
+          for (uint32_t ii = 0; ii < (1u << st); ii++)
+            put(t2, B * 256 + (1u << st) - 1 + ii, (1ull << (s1 + st)) + (B << st) + ii);
+        for (uint32_t t = 0; t < 16; t++)
+          for (uint32_t st = 4; st < 8; st++)
+            for (uint32_t ii = 0; ii < (1u << (st - 4)); ii++)
+              put(t2, B * 256 + 15 + 15 * t + (1u << (st - 4)) - 1 + ii,
+                  (1ull << (s1 + st)) + (B << st) + t * (1ull << (st - 4)) + ii);
       }
     }
-    c->dtw = c->upload_u64(tw);
+    {
+      std::vector<uint64_t> bits(tw.size());
+      std::memcpy(bits.data(), tw.data(), tw.size() * 8);
+      c->dtw = c->upload_u64(bits);
+    }
     c->hprimes.resize(np);
     for (size_t i = 0; i < np; i++) {
       PrimeDev& d = c->hprimes[i];
@@ -540,10 +560,14 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       d.rc.r64s = shoup_pre(d.rc.r64, q);
       d.ninv = inv_mod(N % q, q);
       d.ninvs = shoup_pre(d.ninv, q);
-      d.tw = c->dtw + i * 4 * N;
-      d.tws = d.tw + N;
-      d.itw = d.tw + 2 * N;
-      d.itws = d.tw + 3 * N;
+      d.qd = (double)q;
+      d.qinv = 1.0 / (double)q;
+      d.ninvd = make_double2((double)d.ninv, (double)d.ninv / (double)q);
+      const double* b = reinterpret_cast<const double*>(c->dtw) + i * per;
+      d.tw1 = reinterpret_cast<const double2*>(b);
+      d.tw2 = reinterpret_cast<const double2*>(b + 512);
+      d.itw1 = reinterpret_cast<const double2*>(b + 2 * N + 512);
+      d.itw2 = reinterpret_cast<const double2*>(b + 2 * N + 1024);
     }
     c->dprimes = (PrimeDev*)c->dalloc(np * sizeof(PrimeDev));
     c->owned.push_back(c->dprimes);
@@ -552,6 +576,36 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
     c->dslotpos = (uint32_t*)c->dalloc(N * 4);
     c->owned.push_back(c->dslotpos);
     HCUDA(cudaMemcpyAsync(c->dslotpos, sp.data(), N * 4, cudaMemcpyHostToDevice, c->stream));
+    {
+      // pass-2 grouping: 256-blocks ordered by (half, slot position mod n/256);
+      // per block, elements ordered by slot position
+      const uint32_t nb = N / 256, stride = P.n / 256;
+      std::vector<std::pair<uint64_t, uint32_t>> key(nb);
+      std::vector<uint8_t> einv(N);
+      for (uint32_t B = 0; B < nb; B++) {
+        const uint32_t p0 = sp[B * 256];
+        const uint32_t sig = p0 >= P.n, j = (p0 % P.n) % stride;
+        std::vector<std::pair<uint32_t, uint32_t>> pe(256);
+        for (uint32_t e = 0; e < 256; e++) {
+          const uint32_t p = sp[B * 256 + e];
+          need((p >= P.n) == (bool)sig && (p % P.n) % stride == j, HELRM_ERR_CONFIG, "slot grouping invariant");
+          pe[e] = {p, e};
+        }
+        std::sort(pe.begin(), pe.end());
+        for (uint32_t tp = 0; tp < 256; tp++) einv[B * 256 + tp] = (uint8_t)pe[tp].second;
+        key[B] = {((uint64_t)sig << 32) | j, B};
+      }
+      std::sort(key.begin(), key.end());
+      std::vector<uint32_t> grp(nb);
+      for (uint32_t i = 0; i < nb; i++) grp[i] = key[i].second;
+      c->dgrp = (uint32_t*)c->dalloc(nb * 4);
+      c->owned.push_back(c->dgrp);
+      HCUDA(cudaMemcpyAsync(c->dgrp, grp.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
+      c->deinv = (uint8_t*)c->dalloc(N);
+      c->owned.push_back(c->deinv);
+      HCUDA(cudaMemcpyAsync(c->deinv, einv.data(), N, cudaMemcpyHostToDevice, c->stream));
+      HCUDA(cudaStreamSynchronize(c->stream));
+    }
     c->dcdt = c->upload_u64(gauss_cdt_table());
     c->scratch = (uint64_t*)c->dalloc(ntt_scratch_words(P.log_n) * 8);
     c->owned.push_back(c->scratch);

@@ -34,10 +34,13 @@ struct Error : std::runtime_error {
 struct PrimeDev {
   RedConst rc;
   uint64_t ninv, ninvs;         // N^-1 and its shoup companion
-  const uint64_t* tw;           // [N] psi^bitrev(k)
-  const uint64_t* tws;          // [N] shoup companions
-  const uint64_t* itw;          // [N] psi^-bitrev(k)
-  const uint64_t* itws;
+  double qd, qinv;              // q and 1/q as doubles (NTT butterflies on the FP64 pipe)
+  double2 ninvd;                // (N^-1, N^-1 / q)
+  // NTT twiddles as (w, w/q) doubles, w = psi^(+-bitrev_logN(idx)):
+  const double2* tw1;           // [256] pass 1, natural index idx < 256
+  const double2* tw2;           // [N] pass 2, per 256-block B: [B][j], j in per-thread order
+  const double2* itw1;          // inverse twiddles, same layouts
+  const double2* itw2;
 };
 
 // Global chain index of each limb of a polynomial (by value as kernel arg).
@@ -118,6 +121,8 @@ struct Profiler {
 struct DevCtx {
   const PrimeDev* primes;     // device array, chain-indexed
   const uint32_t* slotpos;    // [N] slot position of bitrev index r
+  const uint32_t* ntt_grp;    // [N/256] 256-blocks ordered by (half, slot residue): 16 per pass-2 CTA
+  const uint8_t* ntt_einv;    // [N] per block: element index of its tp-th smallest slot position
   uint32_t log_n, N;
   cudaStream_t stream;
   uint64_t* launches;         // host counter

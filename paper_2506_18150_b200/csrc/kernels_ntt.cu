@@ -6,208 +6,365 @@
 // automorphism phi_{5^r} is a cyclic shift by r inside each half -- the
 // rotations of the lookup become offset loads instead of gathers.
 //
-// Forward: Cooley-Tukey with merged psi-twist (twiddle psi^bitrev(m+i)),
-// natural input -> bit-reversed output, split in two passes so each CTA
-// works on a 32 KB tile in shared memory:
-//   pass 1: the first s1 = log N - 8 stages act on columns {c + 256 h};
-//           a CTA loads C consecutive columns (128-byte row segments).
-//   pass 2: the last 8 stages act inside contiguous 256-element blocks;
-//           the result is written through the bit-reversed -> slot-order
-//           permutation.
-// Inverse: Gentleman-Sande mirror (gather from slot order, blocks first,
-// then columns, times N^-1).
-// Between the passes the data live in a scratch buffer that the launcher
-// sizes to stay L2-resident (<= 32 MiB per chunk of limbs), so HBM sees one
-// read and one write per coefficient.
+// Forward = Cooley-Tukey with the psi-twist merged into the twiddles
+// (psi^bitrev(m+i)), natural input -> bit-reversed output, in two passes of
+// batched 2^s-point sub-transforms (N = 2^s1 x 2^8):
+//   pass 1: 2^8 column transforms of 2^s1 points (stride 2^8), the first s1
+//           stages;  pass 2: 2^s1 row transforms of 256 contiguous points,
+//           the last 8 stages, written through bit-reversed -> slot order.
+// Each sub-transform is held by S/16 threads x 16 registers: 4 radix-2 stages
+// in registers, one shared-memory transpose, the remaining stages in
+// registers.  Pass-2 CTAs own the 16 blocks whose slot positions interleave
+// (same half, consecutive residues mod N/512), so the permuted stores are
+// contiguous runs; pass-2 twiddles are stored in per-block, per-thread order
+// so each thread reads its 15 phase-B twiddles contiguously.  Inverse = the
+// Gentleman-Sande mirror.  Between the passes the data live in a scratch
+// buffer of <= 32 MiB per chunk of limbs, which stays L2-resident: HBM sees
+// one read and one write per coefficient per transform.
+//
+// Butterfly arithmetic runs on the FP64 pipe (q < 2^51): residues are exact
+// integer-valued doubles, the product Y W = h + l is split exactly with an
+// FMA, the quotient k = rint(Y W / q) comes from one FMA against the
+// precomputed W/q (round-to-nearest via the 1.5 2^52 shift), and
+// r = (h - k q) + l is exact; values stay in (-2q, 2q) by centred
+// reductions.  Measured on B200: ~2.7x the modmul throughput of 64-bit
+// integer Shoup (profiles/r01_peak_int.txt).
 #include "internal.h"
 
 namespace helrm {
 
 namespace {
-constexpr int kTile = 4096;   // elements per CTA (32 KB of shared memory)
-constexpr int kThreads = 512;
-constexpr int kS2 = 8;        // log2 of the pass-2 block
+constexpr int kEPT = 16;                     // elements per thread
+constexpr int kTileElems = 4096;             // elements per CTA
+constexpr int kThreads = kTileElems / kEPT;  // 256
+constexpr int kBlkPad = 256 + 16;            // pass-2 smem block stride (1 pad word per 16)
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;
 
-struct Geo {
-  int log_n, N, s1, s2, R, W2, C, G1, NB, G2;
-};
+__device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
 
-Geo geometry(int log_n) {
-  Geo g;
-  g.log_n = log_n;
-  g.N = 1 << log_n;
-  g.s2 = log_n < kS2 ? log_n : kS2;
-  g.s1 = log_n - g.s2;
-  g.R = 1 << g.s1;
-  g.W2 = 1 << g.s2;
-  g.C = kTile / g.R;
-  if (g.C > g.W2) g.C = g.W2;
-  g.G1 = g.W2 / g.C;
-  g.NB = kTile / g.W2;
-  if (g.NB > g.N / g.W2) g.NB = g.N / g.W2;
-  g.G2 = (g.N / g.W2) / g.NB;
-  return g;
+__device__ __forceinline__ double u2d(uint64_t x) {  // x < 2^52
+  return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - kTwo52;
+}
+__device__ __forceinline__ double rnd(double x) { return (x + kMagic) - kMagic; }  // |x| < 2^51
+// centred reduction: |x| < 2^51 q-multiples -> [-q/2, q/2]
+__device__ __forceinline__ double cred(double x, double q, double qi) {
+  const double k = __fma_rn(x, qi, kMagic) - kMagic;
+  return __fma_rn(-k, q, x);
+}
+// Y W mod q, exact, in [-q/2 - 1, q/2 + 1] (|Y| < 2^51)
+__device__ __forceinline__ double mmul(double y, double w, double wq, double q) {
+  const double h = y * w;
+  const double k = __fma_rn(y, wq, kMagic) - kMagic;
+  const double l = __fma_rn(y, w, -h);
+  return __fma_rn(-k, q, h) + l;
+}
+// canonical uint64 in [0, q) from an integer-valued double with |x| <= q
+__device__ __forceinline__ uint64_t d2u(double x, double q, double qi, uint64_t qint) {
+  x = cred(x, q, qi);
+  const long long v = (long long)(__double_as_longlong(x + kMagic) & 0xFFFFFFFFFFFFFull) - (1ll << 51);
+  return (uint64_t)(v < 0 ? v + (long long)qint : v);
+}
+__device__ __forceinline__ void ct_bfly(double& x, double& y, double2 w, double q) {
+  const double r = mmul(y, w.x, w.y, q);
+  const double a = x;
+  x = a + r;
+  y = a - r;
+}
+__device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double q, double qi) {
+  const double s = x + y, dd = x - y;
+  x = cred(s, q, qi);
+  y = mmul(dd, w.x, w.y, q);
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads) k_ntt_fwd_p1(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
-                                                         const PrimeDev* __restrict__ primes, LimbMap map,
-                                                         size_t limb0, Geo g) {
-  extern __shared__ uint64_t sm[];
+// Forward sub-transforms of S = 2^SLOG points, 16 per thread, TS = S/16
+// threads per sub-transform.
+//   MODE 0 (pass 1): sub-transform = column (stride 256); twiddles tw1[2^st + i].
+//   MODE 1 (pass 2): sub-transform = 256-block B; twiddles tw2[B][...]:
+//     [0, 15): phase A, 2^st - 1 + i_loc;  [15 + 15 t, ...): thread t's phase B.
+template <int SLOG, int MODE>
+__global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                                      const PrimeDev* __restrict__ primes,
+                                                      const __grid_constant__ LimbMap map, size_t limb0, int log_n,
+                                                      const uint32_t* __restrict__ grp,
+                                                      const uint8_t* __restrict__ einv) {
+  constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
+  __shared__ double sm[MODE == 0 ? kTileElems : 16 * kBlkPad];
+  const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
   const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
-  const uint64_t q = P.rc.q;
-  const uint64_t* s = src + limb * g.N;
-  uint64_t* d = dst + limb * g.N;
-  const int c0 = blockIdx.x * g.C, tile = g.R * g.C;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[e] = s[(size_t)(e / g.C) * g.W2 + c0 + e % g.C];
-  __syncthreads();
-  for (int st = 0; st < g.s1; st++) {
-    const int m = 1 << st, T = g.R >> (st + 1);
-    for (int b = threadIdx.x; b < tile / 2; b += blockDim.x) {
-      const int c = b % g.C, bb = b / g.C;
-      const int i = bb / T, h = 2 * i * T + bb % T;
-      const uint64_t w = P.tw[m + i], wp = P.tws[m + i];
-      const uint64_t U = sm[h * g.C + c];
-      const uint64_t V = shoup(sm[(h + T) * g.C + c], w, wp, q);
-      sm[h * g.C + c] = add_mod(U, V, q);
-      sm[(h + T) * g.C + c] = sub_mod(U, V, q);
+  const double q = P.qd, qi = P.qinv;
+  const uint64_t* s = src + limb * N;
+  uint64_t* d = dst + limb * N;
+  const int tid = threadIdx.x;
+  const int sub = MODE == 0 ? tid % SUBS : tid / TS;
+  const int t = MODE == 0 ? tid / SUBS : tid % TS;
+  const int gsub = MODE == 0 ? blockIdx.x * SUBS + sub : (int)grp[blockIdx.x * SUBS + sub];
+  const double2* __restrict__ twA = MODE == 0 ? P.tw1 : P.tw2 + (size_t)gsub * 256;
+  double r[kEPT];
+#pragma unroll
+  for (int k = 0; k < kEPT; k++) {
+    const int e = t + TS * k;
+    if (MODE == 0) r[k] = u2d(s[(size_t)e * 256 + gsub]);
+    else r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
+  }
+  // phase A: stages 0..3 on layout e = t + TS k (twiddles independent of t)
+#pragma unroll
+  for (int st = 0; st < 4; st++) {
+    const int half = 8 >> st;
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      if ((k & half) == 0) {
+        // MODE 0: tw1[2^st + i]; MODE 1: tw2[B][2^st - 1 + i]
+        const double2 w = MODE == 0 ? twA[(1 << st) + (k >> (4 - st))] : twA[(1 << st) - 1 + (k >> (4 - st))];
+        ct_bfly(r[k], r[k + half], w, q);
+      }
+    }
+    if (st & 1) {
+#pragma unroll
+      for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
+    }
+  }
+  if (SLOG > 4) {
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const int e = t + TS * k;
+      if (MODE == 0) sm[e * SUBS + sub] = r[k];
+      else sm[sub * kBlkPad + pidx(e)] = r[k];
     }
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const int e = kEPT * t + k;
+      r[k] = MODE == 0 ? sm[e * SUBS + sub] : sm[sub * kBlkPad + pidx(e)];
+    }
+    const double2* __restrict__ twB = MODE == 0 ? P.tw1 : twA + 15 + 15 * t;
+#pragma unroll
+    for (int st = 4; st < SLOG; st++) {
+      const int half = S >> (st + 1);
+#pragma unroll
+      for (int k = 0; k < kEPT; k++) {
+        if ((k & half) == 0) {
+          const int e = kEPT * t + k;
+          double2 w;
+          if (MODE == 0) w = twB[(1 << st) + (e >> (SLOG - st))];
+          else w = twB[(1 << (st - 4)) - 1 + (k >> (SLOG - st))];
+          ct_bfly(r[k], r[k + half], w, q);
+        }
+      }
+      if ((st & 1) || st == SLOG - 1) {
+#pragma unroll
+        for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
   }
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) d[(size_t)(e / g.C) * g.W2 + c0 + e % g.C] = sm[e];
+  if (MODE == 0) {
+    // centred doubles into the (L2-resident) scratch, natural row positions
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const int e = SLOG > 4 ? kEPT * t + k : t + TS * k;
+      d[(size_t)e * 256 + gsub] = (uint64_t)__double_as_longlong(r[k]);
+    }
+  } else {
+    __syncthreads();
+    uint64_t* smu = reinterpret_cast<uint64_t*>(sm);
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) smu[sub * kBlkPad + pidx(kEPT * t + k)] = d2u(r[k], q, qi, P.rc.q);
+    __syncthreads();
+    // permuted store: block of rank g = 16 cta + i lives at slot positions
+    // (g / stride) n + (g % stride) + stride tp; for a given tp the 16 blocks are adjacent
+    const int n = N >> 1, stride = N >> 9;
+#pragma unroll 4
+    for (int idx = tid; idx < kTileElems; idx += kThreads) {
+      const int i = idx % 16, tp = idx / 16;
+      const int g = blockIdx.x * 16 + i;
+      const int B = grp[g];
+      const int e = einv[B * 256 + tp];
+      d[(g / stride) * n + (g % stride) + stride * tp] = smu[i * kBlkPad + pidx(e)];
+    }
+  }
 }
 
-__global__ void __launch_bounds__(kThreads) k_ntt_fwd_p2(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
-                                                         const PrimeDev* __restrict__ primes, LimbMap map,
-                                                         size_t limb0, Geo g, const uint32_t* __restrict__ slotpos) {
-  extern __shared__ uint64_t sm[];
+// Inverse (Gentleman-Sande), mirror of k_ntt_fwd.
+//   MODE 1 (pass A): blocks gathered from slot order, the last 8 stages;
+//   MODE 0 (pass B): columns, the first s1 stages, times N^-1, natural order.
+template <int SLOG, int MODE>
+__global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                                      const PrimeDev* __restrict__ primes,
+                                                      const __grid_constant__ LimbMap map, size_t limb0, int log_n,
+                                                      const uint32_t* __restrict__ grp,
+                                                      const uint8_t* __restrict__ einv) {
+  constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
+  __shared__ double sm[MODE == 0 ? kTileElems : 16 * kBlkPad];
+  const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
   const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
-  const uint64_t q = P.rc.q;
-  const uint64_t* s = src + limb * g.N;
-  uint64_t* d = dst + limb * g.N;
-  const int tile = g.NB * g.W2, base = blockIdx.x * tile;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[e] = s[base + e];
-  __syncthreads();
-  for (int st = g.s1; st < g.log_n; st++) {
-    const int m = 1 << st, t = g.N >> (st + 1);
-    for (int b = threadIdx.x; b < tile / 2; b += blockDim.x) {
-      const int B = base / 2 + b;
-      const int i = B / t, j = 2 * i * t + B % t - base;
-      const uint64_t w = P.tw[m + i], wp = P.tws[m + i];
-      const uint64_t U = sm[j];
-      const uint64_t V = shoup(sm[j + t], w, wp, q);
-      sm[j] = add_mod(U, V, q);
-      sm[j + t] = sub_mod(U, V, q);
+  const double q = P.qd, qi = P.qinv;
+  const uint64_t* s = src + limb * N;
+  uint64_t* d = dst + limb * N;
+  const int tid = threadIdx.x;
+  const int sub = MODE == 0 ? tid % SUBS : tid / TS;
+  const int t = MODE == 0 ? tid / SUBS : tid % TS;
+  const int gsub = MODE == 0 ? blockIdx.x * SUBS + sub : (int)grp[blockIdx.x * SUBS + sub];
+  const double2* __restrict__ twA = MODE == 0 ? P.itw1 : P.itw2 + (size_t)gsub * 256;
+  double r[kEPT];
+  if (MODE == 1) {
+    const int n = N >> 1, stride = N >> 9;
+#pragma unroll 4
+    for (int idx = tid; idx < kTileElems; idx += kThreads) {
+      const int i = idx % 16, tp = idx / 16;
+      const int g = blockIdx.x * 16 + i;
+      const int B = grp[g];
+      const int e = einv[B * 256 + tp];
+      sm[i * kBlkPad + pidx(e)] = u2d(s[(g / stride) * n + (g % stride) + stride * tp]);
     }
     __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) r[k] = sm[sub * kBlkPad + pidx(kEPT * t + k)];
+  } else {
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const int e = SLOG > 4 ? kEPT * t + k : t + TS * k;
+      r[k] = __longlong_as_double((long long)s[(size_t)e * 256 + gsub]);
+    }
   }
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) d[slotpos[base + e]] = sm[e];
-}
-
-__global__ void __launch_bounds__(kThreads) k_ntt_inv_pa(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
-                                                         const PrimeDev* __restrict__ primes, LimbMap map,
-                                                         size_t limb0, Geo g, const uint32_t* __restrict__ slotpos) {
-  extern __shared__ uint64_t sm[];
-  const size_t limb = blockIdx.y;
-  const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
-  const uint64_t q = P.rc.q;
-  const uint64_t* s = src + limb * g.N;
-  uint64_t* d = dst + limb * g.N;
-  const int tile = g.NB * g.W2, base = blockIdx.x * tile;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[e] = s[slotpos[base + e]];
-  __syncthreads();
-  for (int st = g.log_n - 1; st >= g.s1; st--) {
-    const int m = 1 << st, t = g.N >> (st + 1);
-    for (int b = threadIdx.x; b < tile / 2; b += blockDim.x) {
-      const int B = base / 2 + b;
-      const int i = B / t, j = 2 * i * t + B % t - base;
-      const uint64_t w = P.itw[m + i], wp = P.itws[m + i];
-      const uint64_t U = sm[j], V = sm[j + t];
-      sm[j] = add_mod(U, V, q);
-      sm[j + t] = shoup(sub_mod(U, V, q), w, wp, q);
+  if (SLOG > 4) {
+    const double2* __restrict__ twB = MODE == 0 ? P.itw1 : twA + 15 + 15 * t;
+#pragma unroll
+    for (int st = SLOG - 1; st >= 4; st--) {
+      const int half = S >> (st + 1);
+#pragma unroll
+      for (int k = 0; k < kEPT; k++) {
+        if ((k & half) == 0) {
+          const int e = kEPT * t + k;
+          double2 w;
+          if (MODE == 0) w = twB[(1 << st) + (e >> (SLOG - st))];
+          else w = twB[(1 << (st - 4)) - 1 + (k >> (SLOG - st))];
+          gs_bfly(r[k], r[k + half], w, q, qi);
+        }
+      }
+    }
+    if (MODE == 1) __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const int e = kEPT * t + k;
+      if (MODE == 0) sm[e * SUBS + sub] = r[k];
+      else sm[sub * kBlkPad + pidx(e)] = r[k];
     }
     __syncthreads();
-  }
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) d[base + e] = sm[e];
-}
-
-__global__ void __launch_bounds__(kThreads) k_ntt_inv_pb(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
-                                                         const PrimeDev* __restrict__ primes, LimbMap map,
-                                                         size_t limb0, Geo g) {
-  extern __shared__ uint64_t sm[];
-  const size_t limb = blockIdx.y;
-  const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
-  const uint64_t q = P.rc.q;
-  const uint64_t* s = src + limb * g.N;
-  uint64_t* d = dst + limb * g.N;
-  const int c0 = blockIdx.x * g.C, tile = g.R * g.C;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) sm[e] = s[(size_t)(e / g.C) * g.W2 + c0 + e % g.C];
-  __syncthreads();
-  for (int st = g.s1 - 1; st >= 0; st--) {
-    const int m = 1 << st, T = g.R >> (st + 1);
-    for (int b = threadIdx.x; b < tile / 2; b += blockDim.x) {
-      const int c = b % g.C, bb = b / g.C;
-      const int i = bb / T, h = 2 * i * T + bb % T;
-      const uint64_t w = P.itw[m + i], wp = P.itws[m + i];
-      const uint64_t U = sm[h * g.C + c], V = sm[(h + T) * g.C + c];
-      sm[h * g.C + c] = add_mod(U, V, q);
-      sm[(h + T) * g.C + c] = shoup(sub_mod(U, V, q), w, wp, q);
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const int e = t + TS * k;
+      r[k] = MODE == 0 ? sm[e * SUBS + sub] : sm[sub * kBlkPad + pidx(e)];
     }
-    __syncthreads();
   }
-  for (int e = threadIdx.x; e < tile; e += blockDim.x)
-    d[(size_t)(e / g.C) * g.W2 + c0 + e % g.C] = shoup(sm[e], P.ninv, P.ninvs, q);
+#pragma unroll
+  for (int st = 3; st >= 0; st--) {
+    const int half = 8 >> st;
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      if ((k & half) == 0) {
+        const double2 w = MODE == 0 ? twA[(1 << st) + (k >> (4 - st))] : twA[(1 << st) - 1 + (k >> (4 - st))];
+        gs_bfly(r[k], r[k + half], w, q, qi);
+      }
+    }
+  }
+  if (MODE == 1) {
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) d[(size_t)gsub * 256 + t + TS * k] = (uint64_t)__double_as_longlong(r[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const double v = mmul(r[k], P.ninvd.x, P.ninvd.y, q);
+      d[(size_t)(t + TS * k) * 256 + gsub] = d2u(v, q, qi, P.rc.q);
+    }
+  }
 }
 
+// ---------------------------------------------------------------- launchers
 static size_t chunk_limbs(int N) {
   size_t ch = ((size_t)64 << 16) / (size_t)N;  // 32 MiB of scratch per chunk
   return ch > 65535 ? 65535 : ch;
 }
 
+size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)1 << log_n); }
+
+template <int SLOG>
+static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
+                      const LimbMap& map, size_t off) {
+  constexpr int TS = (1 << SLOG) / kEPT;
+  const int g1 = TS, g2 = (c.N / 256) / 16;
+  {
+    ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
+    k_ntt_fwd<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, c.log_n,
+                                                                  c.ntt_grp, c.ntt_einv);
+  }
+  {
+    ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
+    k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, c.log_n, c.ntt_grp,
+                                                               c.ntt_einv);
+  }
+  *c.launches += 2;
+}
+
+template <int SLOG>
+static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
+                      const LimbMap& map, size_t off) {
+  constexpr int TS = (1 << SLOG) / kEPT;
+  const int g1 = TS, g2 = (c.N / 256) / 16;
+  {
+    ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
+    k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, c.log_n, c.ntt_grp,
+                                                               c.ntt_einv);
+  }
+  {
+    ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
+    k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, c.log_n,
+                                                                  c.ntt_grp, c.ntt_einv);
+  }
+  *c.launches += 2;
+}
+
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map) {
-  Geo g = geometry(c.log_n);
-  const size_t ch = chunk_limbs(g.N);
-  const size_t smem = kTile * sizeof(uint64_t);
+  const size_t ch = chunk_limbs(c.N);
   for (size_t off = 0; off < n_total; off += ch) {
-    unsigned cnt = (unsigned)std::min(ch, n_total - off);
-    {
-      ProfScope ps_(c, "ntt_fwd_p1", 8.0 * g.N * cnt);
-      k_ntt_fwd_p1<<<dim3(g.G1, cnt), kThreads, smem, c.stream>>>(src + off * g.N, scratch, c.primes, map, off, g);
+    const unsigned cnt = (unsigned)std::min(ch, n_total - off);
+    const uint64_t* s = src + off * c.N;
+    uint64_t* d = dst + off * c.N;
+    switch (c.log_n) {
+      case 12: fwd_chunk<4>(c, s, d, scratch, cnt, map, off); break;
+      case 13: fwd_chunk<5>(c, s, d, scratch, cnt, map, off); break;
+      case 14: fwd_chunk<6>(c, s, d, scratch, cnt, map, off); break;
+      case 15: fwd_chunk<7>(c, s, d, scratch, cnt, map, off); break;
+      case 16: fwd_chunk<8>(c, s, d, scratch, cnt, map, off); break;
+      default: throw Error(HELRM_ERR_CONFIG, "NTT supports 12 <= log N <= 16");
     }
-    {
-      ProfScope ps_(c, "ntt_fwd_p2", 8.0 * g.N * cnt);
-      k_ntt_fwd_p2<<<dim3(g.G2, cnt), kThreads, smem, c.stream>>>(scratch, dst + off * g.N, c.primes, map, off, g,
-                                                                  c.slotpos);
-    }
-    *c.launches += 2;
   }
   HCUDA(cudaGetLastError());
 }
 
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map) {
-  Geo g = geometry(c.log_n);
-  const size_t ch = chunk_limbs(g.N);
-  const size_t smem = kTile * sizeof(uint64_t);
+  const size_t ch = chunk_limbs(c.N);
   for (size_t off = 0; off < n_total; off += ch) {
-    unsigned cnt = (unsigned)std::min(ch, n_total - off);
-    {
-      ProfScope ps_(c, "ntt_inv_pa", 8.0 * g.N * cnt);
-      k_ntt_inv_pa<<<dim3(g.G2, cnt), kThreads, smem, c.stream>>>(src + off * g.N, scratch, c.primes, map, off, g,
-                                                                  c.slotpos);
+    const unsigned cnt = (unsigned)std::min(ch, n_total - off);
+    const uint64_t* s = src + off * c.N;
+    uint64_t* d = dst + off * c.N;
+    switch (c.log_n) {
+      case 12: inv_chunk<4>(c, s, d, scratch, cnt, map, off); break;
+      case 13: inv_chunk<5>(c, s, d, scratch, cnt, map, off); break;
+      case 14: inv_chunk<6>(c, s, d, scratch, cnt, map, off); break;
+      case 15: inv_chunk<7>(c, s, d, scratch, cnt, map, off); break;
+      case 16: inv_chunk<8>(c, s, d, scratch, cnt, map, off); break;
+      default: throw Error(HELRM_ERR_CONFIG, "NTT supports 12 <= log N <= 16");
     }
-    {
-      ProfScope ps_(c, "ntt_inv_pb", 8.0 * g.N * cnt);
-      k_ntt_inv_pb<<<dim3(g.G1, cnt), kThreads, smem, c.stream>>>(scratch, dst + off * g.N, c.primes, map, off, g);
-    }
-    *c.launches += 2;
   }
   HCUDA(cudaGetLastError());
 }
-
-size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)1 << log_n); }
 
 }  // namespace helrm

@@ -24,7 +24,7 @@ __device__ __forceinline__ uint32_t rot_src(uint32_t p, uint32_t rot, uint32_t n
 }  // namespace
 
 __global__ void k_reduce_signed(const int64_t* __restrict__ m, uint64_t* __restrict__ out,
-                                const PrimeDev* __restrict__ primes, LimbMap map, uint32_t N) {
+                                const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
@@ -42,9 +42,9 @@ __global__ void k_reduce_signed(const int64_t* __restrict__ m, uint64_t* __restr
 
 // UniformMod(q) of natural NTT index i = (w_{2i} 2^64 + w_{2i+1}) mod q, placed
 // at its slot-order position.
-__global__ void k_sample_uniform_ntt(uint64_t* __restrict__ out, const PrimeDev* __restrict__ primes, LimbMap map,
+__global__ void k_sample_uniform_ntt(uint64_t* __restrict__ out, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map,
                                      uint32_t log_n, const uint32_t* __restrict__ slotpos, uint64_t seed,
-                                     uint64_t purpose, uint64_t a, uint64_t b, LimbMap ids) {
+                                     uint64_t purpose, uint64_t a, uint64_t b, const __grid_constant__ LimbMap ids) {
   const uint32_t N = 1u << log_n;
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
@@ -76,7 +76,7 @@ __global__ void k_sample_small(int64_t* __restrict__ out, uint32_t N, uint64_t b
 
 // op 0: a + b, 1: a - b, 2: a * b, 3: -a
 __global__ void k_binary(int op, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
-                         uint64_t* __restrict__ out, const PrimeDev* __restrict__ primes, LimbMap map, uint32_t N) {
+                         uint64_t* __restrict__ out, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
@@ -95,7 +95,7 @@ __global__ void k_binary(int op, const uint64_t* __restrict__ a, const uint64_t*
 
 // out[l] = a[l] * s[l] (shoup constants per limb)
 __global__ void k_scalar_mul(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
-                             const PrimeDev* __restrict__ primes, LimbMap map, uint32_t N,
+                             const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N,
                              const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
@@ -107,7 +107,7 @@ __global__ void k_scalar_mul(const uint64_t* __restrict__ a, uint64_t* __restric
 
 // out[l][p] = a[l][rot_src(p)]  (+ out if accumulate)
 __global__ void k_automorph(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
-                            const PrimeDev* __restrict__ primes, LimbMap map, uint32_t N, uint32_t rot,
+                            const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N, uint32_t rot,
                             int accumulate) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
@@ -122,7 +122,7 @@ struct ConvRows {
   int16_t row[kMaxLimbs];
 };
 __global__ void k_conv(const ConvDev* __restrict__ cv, const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
-                       const PrimeDev* __restrict__ primes, uint32_t N, ConvRows rows, int t_per_block) {
+                       const PrimeDev* __restrict__ primes, uint32_t N, const __grid_constant__ ConvRows rows, int t_per_block) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int nb = cv->nb;
@@ -148,7 +148,7 @@ __global__ void k_conv(const ConvDev* __restrict__ cv, const uint64_t* __restric
 
 // out[l] = (y[l] - t[l]) * s[l] mod q_l  (ModDown / rescale finish)
 __global__ void k_sub_scale(const uint64_t* __restrict__ y, const uint64_t* __restrict__ t, uint64_t* __restrict__ out,
-                            const PrimeDev* __restrict__ primes, LimbMap map, uint32_t N,
+                            const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N,
                             const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
@@ -160,7 +160,7 @@ __global__ void k_sub_scale(const uint64_t* __restrict__ y, const uint64_t* __re
 
 // D17: r = ((x + h) mod q_l) - h, then r mod q_i for the remaining limbs
 __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, uint64_t ql, uint64_t* __restrict__ out,
-                               const PrimeDev* __restrict__ primes, LimbMap map, uint32_t N) {
+                               const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
@@ -180,7 +180,7 @@ __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, uint64_t ql, uin
 // D18 key inner product with the automorphism fused into the loads:
 //   out0[l][p] (+)= [c0] P phi(c0)[l][p] + sum_k phi(D_k)[l][p] b_k[l][p]
 //   out1[l][p] (+)= sum_k phi(D_k)[l][p] a_k[l][p]
-__global__ void k_kip(KipArgs a, const PrimeDev* __restrict__ primes, LimbMap map, uint32_t N) {
+__global__ void k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (p >= N) return;
@@ -208,7 +208,7 @@ __global__ void k_kip(KipArgs a, const PrimeDev* __restrict__ primes, LimbMap ma
 
 // D20 L3: (A, B)[l][p] = sum_t u_t[l][p] (x0_t, x1_t)[l][p]
 __global__ void k_diag_mac(const MacTerm* __restrict__ terms, int n_terms, uint64_t* __restrict__ out0,
-                           uint64_t* __restrict__ out1, const PrimeDev* __restrict__ primes, LimbMap map,
+                           uint64_t* __restrict__ out1, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map,
                            uint32_t N) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
