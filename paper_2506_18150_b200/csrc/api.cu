@@ -57,12 +57,6 @@ struct helrm_params {
   Params P;
 };
 
-struct ConvEntry {
-  ConvDev* d = nullptr;
-  int nb = 0, nt = 0;
-  std::vector<int16_t> rows;
-};
-
 struct LevelConst {
   uint64_t* pmod = nullptr;       // [l+1] P mod q_i, shoup companions
   uint64_t* pmods = nullptr;
@@ -70,6 +64,12 @@ struct LevelConst {
   uint64_t* pinvs = nullptr;
   uint64_t* qlinv = nullptr;      // [l] q_l^-1 mod q_i
   uint64_t* qlinvs = nullptr;
+  // fused base conversions (D14 inside the NTT): INTT post-factors
+  // N^-1 [(B/b)^-1]_b (y-form) and per-output-row coefficient tables
+  double2* modup_post = nullptr;   // [l+1]
+  ConvRowDev* modup_tab = nullptr; // [dnum(l)][l+1+K]
+  double2* moddown_post = nullptr; // [K]
+  ConvRowDev* moddown_tab = nullptr; // [l+1]
 };
 
 struct helrm_ctx {
@@ -84,7 +84,6 @@ struct helrm_ctx {
   uint8_t* deinv = nullptr;
   uint64_t* dcdt = nullptr;
   uint64_t* scratch = nullptr;
-  std::map<std::pair<int, int>, ConvEntry> conv;
   std::map<int, LevelConst> lconst;
   std::vector<void*> owned;       // device allocations freed at destroy
   uint64_t launches = 0;
@@ -222,11 +221,13 @@ static LimbMap sub_map(const LimbMap& m, int first, int count) {
   return r;
 }
 
-static void ntt_fwd(helrm_ctx* c, const uint64_t* src, uint64_t* dst, size_t n, const LimbMap& map) {
-  if (n) launch_ntt_fwd(c->dc(), src, dst, c->scratch, n, map);
+static void ntt_fwd(helrm_ctx* c, const uint64_t* src, uint64_t* dst, size_t n, const LimbMap& map, size_t ss = 0,
+                    size_t ds = 0) {
+  if (n) launch_ntt_fwd(c->dc(), src, dst, c->scratch, n, map, ss, ds);
 }
-static void ntt_inv(helrm_ctx* c, const uint64_t* src, uint64_t* dst, size_t n, const LimbMap& map) {
-  if (n) launch_ntt_inv(c->dc(), src, dst, c->scratch, n, map);
+static void ntt_inv(helrm_ctx* c, const uint64_t* src, uint64_t* dst, size_t n, const LimbMap& map, size_t ss = 0,
+                    size_t ds = 0) {
+  if (n) launch_ntt_inv(c->dc(), src, dst, c->scratch, n, map, ss, ds);
 }
 
 static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
@@ -247,6 +248,65 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
     }
   }
   LevelConst lc;
+  {
+    const uint32_t nl = l + 1 + P.K, dn = P.dnum(l);
+    const uint64_t ninv_base = 0;
+    (void)ninv_base;
+    auto hat_mod = [&](const std::vector<uint32_t>& B, size_t skip, uint64_t t) {
+      uint64_t h = 1;
+      for (size_t b = 0; b < B.size(); b++)
+        if (b != skip) h = mulm(h, P.primes[B[b]] % t, t);
+      return h;
+    };
+    auto pair = [&](uint64_t w, uint64_t q) { return make_double2((double)w, (double)w / (double)q); };
+    std::vector<double2> upost(l + 1), dpost(P.K);
+    std::vector<ConvRowDev> utab((size_t)dn * nl), dtab(l + 1);
+    for (uint32_t k = 0; k < dn; k++) {
+      std::vector<uint32_t> B;
+      const uint32_t lo = k * P.alpha, hi = std::min((k + 1) * P.alpha, l + 1);
+      for (uint32_t i = lo; i < hi; i++) B.push_back(i);
+      for (size_t b = 0; b < B.size(); b++) {
+        const uint64_t q = P.primes[B[b]];
+        const uint64_t binv = inv_mod(hat_mod(B, b, q), q);
+        upost[B[b]] = pair(mulm(inv_mod(P.N % q, q), binv, q), q);
+      }
+      for (uint32_t r = 0; r < nl; r++) {
+        ConvRowDev& cr = utab[(size_t)k * nl + r];
+        cr = ConvRowDev{};
+        cr.src_row0 = (int)lo;
+        cr.nb = (int)B.size();
+        const uint64_t qr = P.primes[P.qp_chain(l, r)];
+        for (size_t b = 0; b < B.size(); b++) {
+          if (r >= lo && r < hi) cr.cf[b] = (r - lo == b) ? hat_mod(B, b, qr) : 0;  // undo the y-form factor
+          else cr.cf[b] = hat_mod(B, b, qr);                                        // (B/b) mod q_r
+        }
+      }
+    }
+    std::vector<uint32_t> PB;
+    for (uint32_t j = 0; j < P.K; j++) PB.push_back(P.L + 1 + j);
+    for (uint32_t b = 0; b < P.K; b++) {
+      const uint64_t q = P.primes[PB[b]];
+      dpost[b] = pair(mulm(inv_mod(P.N % q, q), inv_mod(hat_mod(PB, b, q), q), q), q);
+    }
+    for (uint32_t r = 0; r <= l; r++) {
+      ConvRowDev& cr = dtab[r];
+      cr = ConvRowDev{};
+      cr.src_row0 = 0;
+      cr.nb = (int)P.K;
+      for (uint32_t b = 0; b < P.K; b++) cr.cf[b] = hat_mod(PB, b, P.primes[r]);
+    }
+    auto up = [&](const void* h, size_t bytes) {
+      void* d = c->dalloc(bytes);
+      HCUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
+      c->owned.push_back(d);
+      return d;
+    };
+    lc.modup_post = (double2*)up(upost.data(), upost.size() * sizeof(double2));
+    lc.modup_tab = (ConvRowDev*)up(utab.data(), utab.size() * sizeof(ConvRowDev));
+    lc.moddown_post = (double2*)up(dpost.data(), dpost.size() * sizeof(double2));
+    lc.moddown_tab = (ConvRowDev*)up(dtab.data(), dtab.size() * sizeof(ConvRowDev));
+    HCUDA(cudaStreamSynchronize(c->stream));
+  }
   lc.pmod = c->upload_u64(pm);
   lc.pmods = c->upload_u64(pms);
   lc.pinv = c->upload_u64(pi);
@@ -256,102 +316,58 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
   return c->lconst.emplace((int)l, lc).first->second;
 }
 
-// D14 tables: digit >= 0: ModUp digit at level l; digit = -1: ModDown P -> Q_l
-static const ConvEntry& conv_entry(helrm_ctx* c, uint32_t l, int digit) {
-  auto key = std::make_pair((int)l, digit);
-  auto it = c->conv.find(key);
-  if (it != c->conv.end()) return it->second;
+// D15 for G polynomials at once, all digits: in_g = in + g in_stride ([l+1][N],
+// NTT form) -> out [G][dnum][l+1+K][N] (NTT form).  One INTT of the G (l+1)
+// limbs into y-form, one fused conversion + NTT over every output limb (the
+// digit's own limbs go through INTT/NTT unchanged: a bit-exact copy).
+static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int G, uint32_t l, uint64_t* out) {
   const Params& P = c->P;
-  std::vector<uint32_t> src, tgt;
-  std::vector<int16_t> rows;
-  if (digit >= 0) {
-    uint32_t lo = digit * P.alpha, hi = std::min((uint32_t)(digit + 1) * P.alpha, l + 1);
-    for (uint32_t i = lo; i < hi; i++) src.push_back(i);
-    for (uint32_t r = 0; r < l + 1 + P.K; r++) {
-      if (r >= lo && r < hi) continue;
-      tgt.push_back(P.qp_chain(l, r));
-      rows.push_back((int16_t)r);
-    }
-  } else {
-    for (uint32_t j = 0; j < P.K; j++) src.push_back(P.L + 1 + j);
-    for (uint32_t r = 0; r <= l; r++) {
-      tgt.push_back(r);
-      rows.push_back((int16_t)r);
-    }
-  }
-  need(src.size() <= (size_t)kMaxDigitPrimes && tgt.size() <= (size_t)kMaxLimbs, HELRM_ERR_CONFIG, "too many primes");
-  ConvDev h{};
-  h.nb = (int)src.size();
-  h.nt = (int)tgt.size();
-  for (size_t b = 0; b < src.size(); b++) {
-    uint64_t qb = P.primes[src[b]], hat = 1;
-    for (size_t b2 = 0; b2 < src.size(); b2++)
-      if (b2 != b) hat = mulm(hat, P.primes[src[b2]] % qb, qb);
-    h.bpr[b] = (uint8_t)src[b];
-    h.binv[b] = inv_mod(hat, qb);
-    h.binvs[b] = shoup_pre(h.binv[b], qb);
-  }
-  for (size_t t = 0; t < tgt.size(); t++) {
-    uint64_t qt = P.primes[tgt[t]];
-    h.tpr[t] = (uint8_t)tgt[t];
-    for (size_t b = 0; b < src.size(); b++) {
-      uint64_t hat = 1;
-      for (size_t b2 = 0; b2 < src.size(); b2++)
-        if (b2 != b) hat = mulm(hat, P.primes[src[b2]] % qt, qt);
-      h.bmod[t][b] = hat;
-    }
-  }
-  ConvEntry e;
-  e.d = (ConvDev*)c->dalloc(sizeof(ConvDev));
-  HCUDA(cudaMemcpyAsync(e.d, &h, sizeof(ConvDev), cudaMemcpyHostToDevice, c->stream));
-  HCUDA(cudaStreamSynchronize(c->stream));
-  c->owned.push_back(e.d);
-  e.nb = h.nb;
-  e.nt = h.nt;
-  e.rows = rows;
-  return c->conv.emplace(key, e).first->second;
+  const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, dn = P.dnum(l);
+  const LevelConst& lc = level_const(c, l);
+  DBuf y(c, G * nq * N);
+  // INTT straight into y-form (times [(Q_k/q_i)^-1]_{q_i}), one conversion
+  // launch over (g, digit) writing every output row, one NTT over all of them
+  launch_ntt_inv(c->dc(), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post);
+  launch_conv_rows(c->dc(), lc.modup_tab, (int)dn, (int)nl, y.p, nq * N, out, dn * nl * N, nl * N, G, P.map_qp(l));
+  ntt_fwd(c, out, out, G * dn * nl, P.map_qp(l));
 }
 
-// D15: in [l+1][N] NTT -> out [l+1+K][N] NTT
+// D16 for G polynomials: y_g = y + g ys ([l+1+K][N]) -> out_g = out + g os ([l+1][N])
+static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uint32_t l, uint64_t* out, size_t os) {
+  const Params& P = c->P;
+  const size_t N = P.N, nq = l + 1;
+  const LevelConst& lc = level_const(c, l);
+  DBuf yp(c, G * P.K * N), t(c, G * nq * N);
+  launch_ntt_inv(c->dc(), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
+                 lc.moddown_post);
+  launch_conv_rows(c->dc(), lc.moddown_tab, 1, (int)nq, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
+  ntt_fwd(c, t.p, t.p, G * nq, P.map_q(l));
+  launch_sub_scale(c->dc(), y, ys, t.p, nq * N, out, os, G, P.map_q(l), lc.pinv, lc.pinvs);
+}
+
 static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t* out) {
   const Params& P = c->P;
-  const size_t N = P.N;
-  const uint32_t lo = k * P.alpha, hi = std::min((uint32_t)(k + 1) * P.alpha, l + 1), nb = hi - lo;
-  const uint32_t nl = l + 1 + P.K;
-  need(lo <= l, HELRM_ERR_LEVEL, "digit beyond level");
-  DBuf x(c, nb * N);
-  ntt_inv(c, in + lo * N, x.p, nb, P.map_range(lo, nb));
-  const ConvEntry& ce = conv_entry(c, l, k);
-  launch_conv(c->dc(), ce.d, ce.nb, ce.nt, ce.rows.data(), x.p, out);
-  LimbMap m = P.map_qp(l);
-  ntt_fwd(c, out, out, lo, sub_map(m, 0, lo));
-  ntt_fwd(c, out + hi * N, out + hi * N, nl - hi, sub_map(m, hi, nl - hi));
-  HCUDA(cudaMemcpyAsync(out + lo * N, in + lo * N, nb * N * 8, cudaMemcpyDeviceToDevice, c->stream));
+  const size_t nl = l + 1 + P.K;
+  DBuf all(c, (size_t)P.dnum(l) * nl * P.N);
+  modup_batch(c, in, 0, 1, l, all.p);
+  HCUDA(cudaMemcpyAsync(out, all.p + (size_t)k * nl * P.N, nl * P.N * 8, cudaMemcpyDeviceToDevice, c->stream));
 }
 
-// D16: y [l+1+K][N] -> out [l+1][N]
 static void moddown(helrm_ctx* c, const uint64_t* y, uint32_t l, uint64_t* out) {
-  const Params& P = c->P;
-  const size_t N = P.N;
-  DBuf yp(c, P.K * N), t(c, (l + 1) * N);
-  ntt_inv(c, y + (l + 1) * N, yp.p, P.K, P.map_range(P.L + 1, P.K));
-  const ConvEntry& ce = conv_entry(c, l, -1);
-  launch_conv(c->dc(), ce.d, ce.nb, ce.nt, ce.rows.data(), yp.p, t.p);
-  ntt_fwd(c, t.p, t.p, l + 1, P.map_q(l));
-  const LevelConst& lc = level_const(c, l);
-  launch_sub_scale(c->dc(), y, t.p, out, P.map_q(l), lc.pinv, lc.pinvs);
+  const size_t nl = l + 1 + c->P.K;
+  moddown_batch(c, y, nl * c->P.N, 1, l, out, (l + 1) * c->P.N);
 }
 
-// D17 on one polynomial x [l+1][N] -> out [l][N]
-static void rescale_poly(helrm_ctx* c, const uint64_t* x, uint32_t l, uint64_t* out) {
+// D17 on a ciphertext [2][l+1][N] -> out [2][l][N]
+static void rescale_ct(helrm_ctx* c, const uint64_t* x, uint32_t l, uint64_t* out) {
   const Params& P = c->P;
   const size_t N = P.N;
-  DBuf xl(c, N), r(c, l * N);
-  ntt_inv(c, x + l * N, xl.p, 1, P.map_range(l, 1));
-  launch_rescale_prep(c->dc(), xl.p, P.primes[l], r.p, P.map_q(l - 1));
-  ntt_fwd(c, r.p, r.p, l, P.map_q(l - 1));
+  DBuf xl(c, 2 * N), r(c, 2 * l * N);
+  ntt_inv(c, x + l * N, xl.p, 2, P.map_range(l, 1), (l + 1) * N, N);
+  launch_rescale_prep(c->dc(), xl.p, N, P.primes[l], r.p, l * N, 2, P.map_q(l - 1));
+  ntt_fwd(c, r.p, r.p, 2 * l, P.map_q(l - 1));
   const LevelConst& lc = level_const(c, l);
-  launch_sub_scale(c->dc(), x, r.p, out, P.map_q(l - 1), lc.qlinv, lc.qlinvs);
+  launch_sub_scale(c->dc(), x, (l + 1) * N, r.p, l * N, out, l * N, 2, P.map_q(l - 1), lc.qlinv, lc.qlinvs);
 }
 
 static uint32_t rot_of_galois(helrm_ctx* c, uint64_t g) {
@@ -373,33 +389,36 @@ static const uint64_t* key_for(const helrm_rotkeys* rk, uint64_t g) {
   return it->second;
 }
 
-// KS_g over precomputed digits D [dnum][l+1+K][N]; with c0 != null computes the
-// lazy rotation (P phi(c0) + KS0, KS1).
-static void kip(helrm_ctx* c, const uint64_t* D, uint32_t l, const helrm_rotkeys* rk, uint64_t g, const uint64_t* c0,
-                uint64_t* out0, uint64_t* out1, bool accumulate) {
+// KS_g over precomputed digits D [dnum][l+1+K][N] (D18), fused with the
+// automorphism; add0/add_mul/add_rows as in KipArgs.
+static void kip(helrm_ctx* c, const uint64_t* D, uint32_t l, const helrm_rotkeys* rk, uint64_t g, const uint64_t* add0,
+                int add_rows, const uint64_t* add_mul, uint64_t* out0, uint64_t* out1, bool accumulate) {
   const Params& P = c->P;
   KipArgs a{};
   a.digits = D;
+  a.digit_stride = (size_t)(l + 1 + P.K) * P.N;
   a.dnum = (int)P.dnum(l);
   a.key = key_for(rk, g);
   a.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * P.N;
   a.key_half_stride = (size_t)(P.L + 1 + P.K) * P.N;
-  a.c0 = c0;
-  a.p_mod = c0 ? level_const(c, l).pmod : nullptr;
+  a.add0 = add0;
+  a.add_rows = add_rows;
+  a.add_mul = add_mul;
   a.rot = rot_of_galois(c, g);
   a.out0 = out0;
   a.out1 = out1;
   a.accumulate = accumulate ? 1 : 0;
-  a.level = l;
   launch_kip(c->dc(), a, P.map_qp(l));
 }
 
-static void modup_all(helrm_ctx* c, const uint64_t* c1, uint32_t l, uint64_t* D) {
-  const size_t nlN = (size_t)(l + 1 + c->P.K) * c->P.N;
-  for (uint32_t k = 0; k < c->P.dnum(l); k++) modup(c, c1, l, (int)k, D + k * nlN);
+// lazy rotation (P phi(c0) + KS0, KS1) over Q_l P from digits of c1
+static void rotate_lazy(helrm_ctx* c, const helrm_ct* in, const uint64_t* D, const helrm_rotkeys* rk, uint64_t g,
+                        uint64_t* out0, uint64_t* out1) {
+  const uint32_t l = in->level;
+  kip(c, D, l, rk, g, ct_c0(in), (int)l + 1, level_const(c, l).pmod, out0, out1, false);
 }
 
-// Rotate(ct, k) from digits D of ct.c1 (hoisted): out = ModDown(P phi(c0) + KS0), ModDown(KS1)
+// Rotate(ct, k) from digits D of ct.c1 (hoisted): ModDown of both lazy halves
 static void rotate_from_digits(helrm_ctx* c, const helrm_ct* in, const uint64_t* D, const helrm_rotkeys* rk, int64_t k,
                                helrm_ct* out) {
   const Params& P = c->P;
@@ -410,10 +429,9 @@ static void rotate_from_digits(helrm_ctx* c, const helrm_ct* in, const uint64_t*
     HCUDA(cudaMemcpyAsync(out->d, in->d, (size_t)2 * (l + 1) * N * 8, cudaMemcpyDeviceToDevice, c->stream));
     return;
   }
-  DBuf t0(c, nl * N), t1(c, nl * N);
-  kip(c, D, l, rk, g, ct_c0(in), t0.p, t1.p, false);
-  moddown(c, t0.p, l, ct_c0(out));
-  moddown(c, t1.p, l, ct_c1(out));
+  DBuf t(c, 2 * nl * N);
+  rotate_lazy(c, in, D, rk, g, t.p, t.p + nl * N);
+  moddown_batch(c, t.p, nl * N, 2, l, out->d, (l + 1) * N);
 }
 
 static void rotate(helrm_ctx* c, const helrm_ct* in, const helrm_rotkeys* rk, int64_t k, helrm_ct* out) {
@@ -423,14 +441,15 @@ static void rotate(helrm_ctx* c, const helrm_ct* in, const helrm_rotkeys* rk, in
     return;
   }
   DBuf D(c, (size_t)c->P.dnum(l) * (l + 1 + c->P.K) * c->P.N);
-  modup_all(c, ct_c1(in), l, D.p);
+  modup_batch(c, ct_c1(in), 0, 1, l, D.p);
   rotate_from_digits(c, in, D.p, rk, k, out);
 }
 
 static void ct_add_inplace(helrm_ctx* c, helrm_ct* acc, const helrm_ct* x) {
   LimbMap m = c->P.map_q(acc->level);
-  launch_binary(c->dc(), 0, ct_c0(acc), ct_c0(x), ct_c0(acc), m);
-  launch_binary(c->dc(), 0, ct_c1(acc), ct_c1(x), ct_c1(acc), m);
+  m.n = 2 * (acc->level + 1);
+  for (int i = acc->level + 1; i < m.n; i++) m.pr[i] = m.pr[i - acc->level - 1];
+  launch_binary(c->dc(), 0, acc->d, x->d, acc->d, m);
 }
 
 // ============================================================================
@@ -1247,84 +1266,131 @@ static void rot_sum(helrm_ctx* c, helrm_ct* ct, int64_t mbar, const helrm_rotkey
   helrm_ct_destroy(tmp);
 }
 
+static LimbMap map_twice(const LimbMap& m) {
+  LimbMap r = m;
+  r.n = 2 * m.n;
+  for (int i = 0; i < m.n; i++) r.pr[m.n + i] = m.pr[i];
+  return r;
+}
+
+// host-side MAC term list for every non-empty (o, i); uploaded once per call
+struct MacList {
+  std::vector<MacTerm> terms;
+  std::vector<int2> ranges;
+  std::vector<std::pair<int64_t, int64_t>> oi;   // (o, i) of each output pair
+};
+
+// D20: the double-hoisted BSGS lookup of one query (C input cts -> O outputs)
 static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
                           helrm_ct** out) {
   const Params& P = c->P;
   const uint32_t l = pl->level;
-  const size_t N = P.N, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
+  const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
   const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
   const LevelConst& lc = level_const(c, l);
-  // L1 + L2: digits and baby steps per input ct
-  std::vector<std::map<int, std::pair<uint64_t*, uint64_t*>>> ab(pl->C);
-  std::vector<std::unique_ptr<DBuf>> keep;
+  // L1 (hoist #1): digits of every input c1;  L2: lazy baby steps over Q_l P
+  std::vector<std::map<int, uint64_t*>> ab(pl->C);
+  size_t n_baby = 0;
+  for (auto& bl : pl->babies) n_baby += bl.size();
+  DBuf D(c, pl->C * dn * nlN), babies(c, std::max<size_t>(1, n_baby) * 2 * nlN);
+  size_t bi = 0;
   for (int64_t ci = 0; ci < pl->C; ci++) {
     const helrm_ct* ct = in[ci];
-    auto D = std::make_unique<DBuf>(c, dn * nlN);
-    modup_all(c, ct_c1(ct), l, D->p);
+    uint64_t* Dc = D.p + ci * dn * nlN;
+    modup_batch(c, ct_c1(ct), 0, 1, l, Dc);
+    KipMulti km{};
+    km.digits = Dc;
+    km.digit_stride = nlN;
+    km.dnum = (int)dn;
+    km.c0 = ct_c0(ct);
+    km.p_mod = lc.pmod;
+    km.level = l;
+    km.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+    km.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+    km.out_half = nlN;
     for (int j : pl->babies[ci]) {
-      auto buf = std::make_unique<DBuf>(c, 2 * nlN);
-      uint64_t* a = buf->p;
-      uint64_t* b = buf->p + nlN;
+      uint64_t* a = babies.p + bi++ * 2 * nlN;
       if (j == 0) {  // (P c0, P c1): Q limbs scaled by [P]_q, P limbs 0
         HCUDA(cudaMemsetAsync(a, 0, 2 * nlN * 8, c->stream));
         launch_scalar_mul(c->dc(), ct_c0(ct), a, mq, lc.pmod, lc.pmods);
-        launch_scalar_mul(c->dc(), ct_c1(ct), b, mq, lc.pmod, lc.pmods);
+        launch_scalar_mul(c->dc(), ct_c1(ct), a + nlN, mq, lc.pmod, lc.pmods);
       } else {
-        kip(c, D->p, l, rk, galois_of_rot(c, j), ct_c0(ct), a, b, false);
+        need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
+        const uint64_t g = galois_of_rot(c, j);
+        km.rot[km.n] = rot_of_galois(c, g);
+        km.key[km.n] = key_for(rk, g);
+        km.out[km.n] = a;
+        km.max_rot = std::max(km.max_rot, km.rot[km.n]);
+        km.n++;
       }
-      ab[ci][j] = {a, b};
-      keep.push_back(std::move(buf));
+      ab[ci][j] = a;
     }
-    keep.push_back(std::move(D));
+    if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
-  // host list of MAC terms for every (o, i); one upload
-  std::vector<MacTerm> terms;
-  std::vector<std::vector<std::pair<size_t, size_t>>> ranges(pl->O);
+  // L3: every inner sum (A, B)_{o,i} in one launch
+  MacList ml;
   for (int64_t o = 0; o < pl->O; o++)
-    for (auto& ent : pl->entries[o]) {
-      size_t s0 = terms.size();
+    for (size_t i = 0; i < pl->entries[o].size(); i++) {
+      const auto& ent = pl->entries[o][i];
+      if (ent.empty()) continue;
+      const int s0 = (int)ml.terms.size();
       for (const Entry& e : ent) {
-        auto& x = ab[e.c].at(e.j);
-        terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nlN, x.first, x.second});
+        uint64_t* x = ab[e.c].at(e.j);
+        ml.terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nlN, x, x + nlN});
       }
-      ranges[o].push_back({s0, terms.size() - s0});
+      ml.ranges.push_back(make_int2(s0, (int)ent.size()));
+      ml.oi.push_back({o, (int64_t)i});
     }
-  MacTerm* dterms = (MacTerm*)c->dalloc(std::max<size_t>(1, terms.size()) * sizeof(MacTerm));
-  HCUDA(cudaMemcpyAsync(dterms, terms.data(), terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice, c->stream));
-  DBuf AB(c, 2 * nlN), Bp(c, (l + 1) * N), D2(c, dn * nlN), O(c, 2 * nlN);
+  const int n_out = (int)ml.ranges.size();
+  DBuf dterms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), dranges(c, n_out + 1);
+  HCUDA(cudaMemcpyAsync(dterms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
+                        c->stream));
+  HCUDA(cudaMemcpyAsync(dranges.p, ml.ranges.data(), n_out * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+  DBuf AB(c, (size_t)n_out * 2 * nlN);
+  launch_diag_mac(c->dc(), (const MacTerm*)dterms.p, (const int2*)dranges.p, n_out, (int)ml.terms.size(), AB.p,
+                  2 * nlN, mqp);
+  // L4 (hoist #2) per output block: batched ModDown of every rotating B,
+  // batched ModUp of the results, then one fused (phi(A) + KS) per giant
+  DBuf O(c, 2 * nlN);
   for (int64_t o = 0; o < pl->O; o++) {
     HCUDA(cudaMemsetAsync(O.p, 0, 2 * nlN * 8, c->stream));
-    for (size_t i = 0; i < pl->entries[o].size(); i++) {
-      auto [s0, cnt] = ranges[o][i];
-      if (cnt == 0) continue;
-      // L3
-      launch_diag_mac(c->dc(), dterms + s0, (int)cnt, AB.p, AB.p + nlN, mqp);
-      const int64_t gi = pl->giants[o][i];
+    std::vector<int> rot_idx;
+    for (int z = 0; z < n_out; z++) {
+      if (ml.oi[z].first != o) continue;
+      const int64_t gi = pl->giants[o][ml.oi[z].second];
       if (gi % (int64_t)P.n == 0) {
-        launch_binary(c->dc(), 0, O.p, AB.p, O.p, mqp);
-        launch_binary(c->dc(), 0, O.p + nlN, AB.p + nlN, O.p + nlN, mqp);
+        launch_binary(c->dc(), 0, O.p, AB.p + (size_t)z * 2 * nlN, O.p, map_twice(mqp));
       } else {
-        // L4: B' = ModDown(B); (G0, G1) = KS(B'); O0 += phi(A) + G0; O1 += G1
-        moddown(c, AB.p + nlN, l, Bp.p);
-        modup_all(c, Bp.p, l, D2.p);
-        kip(c, D2.p, l, rk, galois_of_rot(c, gi), nullptr, O.p, O.p + nlN, true);
-        launch_automorph(c->dc(), AB.p, O.p, mqp, (uint32_t)gi, 1);
+        rot_idx.push_back(z);
       }
     }
-    // L6 + L7 + L8
-    helrm_ct* r = new_ct(c, l, in[0]->scale * (double)P.primes[l]);
-    moddown(c, O.p, l, ct_c0(r));
-    moddown(c, O.p + nlN, l, ct_c1(r));
+    // batches = maximal runs of consecutive pairs (one run unless a zero giant sits in the middle)
+    for (size_t r0 = 0; r0 < rot_idx.size();) {
+      size_t r1 = r0 + 1;
+      while (r1 < rot_idx.size() && rot_idx[r1] == rot_idx[r1 - 1] + 1) r1++;
+      const int z0 = rot_idx[r0], G = (int)(r1 - r0);
+      DBuf Bp(c, (size_t)G * nq * N), D2(c, (size_t)G * dn * nlN);
+      moddown_batch(c, AB.p + (size_t)z0 * 2 * nlN + nlN, 2 * nlN, G, l, Bp.p, nq * N);
+      modup_batch(c, Bp.p, nq * N, G, l, D2.p);
+      for (int k = 0; k < G; k++) {
+        const int z = z0 + k;
+        const int64_t gi = pl->giants[o][ml.oi[z].second];
+        kip(c, D2.p + (size_t)k * dn * nlN, l, rk, galois_of_rot(c, gi), AB.p + (size_t)z * 2 * nlN, (int)nl,
+            nullptr, O.p, O.p + nlN, true);
+      }
+      r0 = r1;
+    }
+    // L6 ModDown both halves (scale Delta q_l), L7 rescale, L8 RotSum
+    DBuf r(c, 2 * nq * N);
+    moddown_batch(c, O.p, nlN, 2, l, r.p, nq * N);
     helrm_ct* s = new_ct(c, l - 1, in[0]->scale);
-    rescale_poly(c, ct_c0(r), l, ct_c0(s));
-    rescale_poly(c, ct_c1(r), l, ct_c1(s));
-    helrm_ct_destroy(r);
+    rescale_ct(c, r.p, l, s->d);
     rot_sum(c, s, pl->mbar, rk);
     out[o] = s;
   }
-  c->dfree(dterms);
 }
 
+// D22: single-hoisted cross-check mode (full rotations in Q_l)
 static void lookup_single(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
                           helrm_ct** out) {
   const Params& P = c->P;
@@ -1335,48 +1401,54 @@ static void lookup_single(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
   for (int64_t ci = 0; ci < pl->C; ci++) {
     const helrm_ct* ct = in[ci];
     DBuf D(c, (size_t)P.dnum(l) * (l + 1 + P.K) * N);
-    modup_all(c, ct_c1(ct), l, D.p);
+    modup_batch(c, ct_c1(ct), 0, 1, l, D.p);
     for (int j : pl->babies[ci]) {
       helrm_ct* r = new_ct(c, l, ct->scale);
       rotate_from_digits(c, ct, D.p, rk, j, r);
       rots[ci][j] = r;
     }
   }
-  std::vector<MacTerm> terms;
-  std::vector<std::vector<std::pair<size_t, size_t>>> ranges(pl->O);
+  MacList ml;
   for (int64_t o = 0; o < pl->O; o++)
-    for (auto& ent : pl->entries[o]) {
-      size_t s0 = terms.size();
+    for (size_t i = 0; i < pl->entries[o].size(); i++) {
+      const auto& ent = pl->entries[o][i];
+      if (ent.empty()) continue;
+      const int s0 = (int)ml.terms.size();
       for (const Entry& e : ent) {
         helrm_ct* x = rots[e.c].at(e.j);
-        terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nqN, ct_c0(x), ct_c1(x)});
+        ml.terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nqN, ct_c0(x), ct_c1(x)});
       }
-      ranges[o].push_back({s0, terms.size() - s0});
+      ml.ranges.push_back(make_int2(s0, (int)ent.size()));
+      ml.oi.push_back({o, (int64_t)i});
     }
-  MacTerm* dterms = (MacTerm*)c->dalloc(std::max<size_t>(1, terms.size()) * sizeof(MacTerm));
-  HCUDA(cudaMemcpyAsync(dterms, terms.data(), terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice, c->stream));
-  helrm_ct* AB = new_ct(c, l, in[0]->scale);
+  const int n_out = (int)ml.ranges.size();
+  DBuf dterms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), dranges(c, n_out + 1);
+  HCUDA(cudaMemcpyAsync(dterms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
+                        c->stream));
+  HCUDA(cudaMemcpyAsync(dranges.p, ml.ranges.data(), n_out * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+  std::vector<helrm_ct*> AB(n_out);
+  for (int z = 0; z < n_out; z++) AB[z] = new_ct(c, l, in[0]->scale);
+  // outputs are written pairwise into separately allocated cts: one launch per pair
+  for (int z = 0; z < n_out; z++)
+    launch_diag_mac(c->dc(), (const MacTerm*)dterms.p, (const int2*)dranges.p + z, 1, ml.ranges[z].y, AB[z]->d,
+                    2 * nqN, mq);
   helrm_ct* R = new_ct(c, l, in[0]->scale);
   for (int64_t o = 0; o < pl->O; o++) {
     helrm_ct* acc = new_ct(c, l, in[0]->scale * (double)P.primes[l]);
     HCUDA(cudaMemsetAsync(acc->d, 0, 2 * nqN * 8, c->stream));
-    for (size_t i = 0; i < pl->entries[o].size(); i++) {
-      auto [s0, cnt] = ranges[o][i];
-      if (cnt == 0) continue;
-      launch_diag_mac(c->dc(), dterms + s0, (int)cnt, ct_c0(AB), ct_c1(AB), mq);
-      rotate(c, AB, rk, pl->giants[o][i], R);
+    for (int z = 0; z < n_out; z++) {
+      if (ml.oi[z].first != o) continue;
+      rotate(c, AB[z], rk, pl->giants[o][ml.oi[z].second], R);
       ct_add_inplace(c, acc, R);
     }
     helrm_ct* s = new_ct(c, l - 1, in[0]->scale);
-    rescale_poly(c, ct_c0(acc), l, ct_c0(s));
-    rescale_poly(c, ct_c1(acc), l, ct_c1(s));
+    rescale_ct(c, acc->d, l, s->d);
     helrm_ct_destroy(acc);
     rot_sum(c, s, pl->mbar, rk);
     out[o] = s;
   }
-  helrm_ct_destroy(AB);
   helrm_ct_destroy(R);
-  c->dfree(dterms);
+  for (auto* x : AB) helrm_ct_destroy(x);
   for (auto& m : rots)
     for (auto& kv : m) helrm_ct_destroy(kv.second);
 }
@@ -1442,8 +1514,7 @@ helrm_status helrm_rescale(helrm_ctx* c, const helrm_ct* in, helrm_ct** out) {
     need(c && in && out, HELRM_ERR_ARG, "null argument");
     need(in->level >= 1, HELRM_ERR_LEVEL, "rescale at level 0");
     helrm_ct* r = new_ct(c, in->level - 1, in->scale / (double)c->P.primes[in->level]);
-    rescale_poly(c, ct_c0(in), in->level, ct_c0(r));
-    rescale_poly(c, ct_c1(in), in->level, ct_c1(r));
+    rescale_ct(c, in->d, in->level, r->d);
     *out = r;
   });
 }
@@ -1465,7 +1536,7 @@ helrm_status helrm_rotate_hoisted(helrm_ctx* c, const helrm_rotkeys* rk, const h
     const uint32_t l = in->level;
     for (size_t i = 0; i < n_ring; i++) need(ring[i] && ring[i]->level == l, HELRM_ERR_LEVEL, "ring ct level");
     DBuf D(c, (size_t)c->P.dnum(l) * (l + 1 + c->P.K) * c->P.N);
-    modup_all(c, ct_c1(in), l, D.p);
+    modup_batch(c, ct_c1(in), 0, 1, l, D.p);
     for (size_t i = 0; i < n_amounts; i++) rotate_from_digits(c, in, D.p, rk, amounts[i], ring[i % n_ring]);
   });
 }

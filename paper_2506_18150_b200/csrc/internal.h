@@ -49,13 +49,10 @@ struct LimbMap {
   uint8_t pr[kMaxLimbs];
 };
 
-// Fast base conversion tables (D14), device resident.
-struct ConvDev {
-  int nb, nt;
-  uint8_t bpr[kMaxDigitPrimes];           // chain index of each source prime
-  uint8_t tpr[kMaxLimbs];                 // chain index of each target prime
-  uint64_t binv[kMaxDigitPrimes], binvs[kMaxDigitPrimes];   // [(B/b)^-1]_b
-  uint64_t bmod[kMaxLimbs][kMaxDigitPrimes];                // (B/b) mod t
+// one output row of a fused base conversion: out = sum_b y_{row0+b} cf[b] mod q_out
+struct ConvRowDev {
+  int src_row0, nb;
+  uint64_t cf[kMaxDigitPrimes];
 };
 
 struct Params {
@@ -137,10 +134,22 @@ struct ProfScope {
   ~ProfScope();
 };
 
-void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total_limbs,
-                    const LimbMap& map);
-void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total_limbs,
-                    const LimbMap& map);
+// NTT over n_total limbs: limb y = (poly y / map.n, limb y % map.n) lives at
+// src + (y / map.n) * src_stride + (y % map.n) * N (same for dst; stride 0 =
+// contiguous polys of map.n limbs).  src == dst allowed.
+void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
+                    const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0);
+// post (optional, per limb of map): final factor (w, w/q) replacing N^-1
+void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
+                    const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0,
+                    const double2* post = nullptr);
+// D14 base conversion from y-form sources (coefficients times [(B/b)^-1]_b,
+// folded into the INTT): for polynomial g and conversion k, every output row
+// r of the table: out_gk[r] = sum_b y_g[row0 + b] cf_kr[b] mod q_r
+// (coefficient form; an NTT follows).  z = g ncv + k.
+void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows, const uint64_t* y, size_t y_stride,
+                      uint64_t* out, size_t out_stride_g, size_t out_stride_k, int G, const LimbMap& out_map);
+size_t ntt_scratch_words(int log_n);
 
 void launch_reduce_signed(const DevCtx& c, const int64_t* m, uint64_t* out, const LimbMap& map);
 void launch_sample_uniform_ntt(const DevCtx& c, uint64_t* out, const LimbMap& map, uint64_t seed, uint64_t purpose,
@@ -152,35 +161,55 @@ void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const 
                        const uint64_t* sp);
 void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
                       int accumulate);
-void launch_conv(const DevCtx& c, const ConvDev* cv, int nb, int nt, const int16_t* rows, const uint64_t* in,
-                 uint64_t* out);
-void launch_sub_scale(const DevCtx& c, const uint64_t* y, const uint64_t* t, uint64_t* out, const LimbMap& map,
-                      const uint64_t* s, const uint64_t* sp);
-void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, uint64_t ql, uint64_t* out, const LimbMap& map);
-size_t ntt_scratch_words(int log_n);
+void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
+                      size_t os, int G, const LimbMap& map, const uint64_t* s, const uint64_t* sp);
+void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,
+                         const LimbMap& map);
 
 struct KipArgs {
-  const uint64_t* digits;     // [dnum][nl][N] (Q_l P, NTT slot order)
+  const uint64_t* digits;     // digit k of the switched polynomial at digits + k digit_stride ([nl][N], NTT slot order)
+  size_t digit_stride;
   int dnum;
   const uint64_t* key;        // key for g: [digit][2][L+1+K][N]
   size_t key_digit_stride;    // words between digits of the key
   size_t key_half_stride;     // words between b and a of a digit
-  const uint64_t* c0;         // optional: add P.phi(c0) on Q limbs ([level+1][N]), may be null
-  const uint64_t* p_mod;      // [level+1] P mod q_l (device), used with c0
+  const uint64_t* add0;       // optional: out0 += mul_l phi(add0)[l] for l < add_rows
+  int add_rows;
+  const uint64_t* add_mul;    // [add_rows] per-limb multiplier (device) or null for 1
   uint32_t rot;               // slot rotation amount (phi_{5^rot})
   uint64_t* out0;             // [nl][N]
   uint64_t* out1;
   int accumulate;             // out += result (else out = result)
-  uint32_t level;
 };
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map);
+
+// all babies of one ciphertext (k_kip_multi)
+constexpr int kMaxBabies = 128;
+struct KipMulti {
+  const uint64_t* digits;     // digit k at digits + k digit_stride ([nl][N])
+  size_t digit_stride;
+  int dnum;
+  const uint64_t* c0;         // [level+1][N]
+  const uint64_t* p_mod;      // [level+1] P mod q_l
+  uint32_t level;
+  size_t key_digit_stride, key_half_stride;
+  size_t out_half;            // words from a_j to b_j
+  int n;                      // number of babies
+  uint32_t max_rot;
+  uint32_t rot[kMaxBabies];
+  const uint64_t* key[kMaxBabies];
+  uint64_t* out[kMaxBabies];
+};
+void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map);
 
 struct MacTerm {
   const uint64_t* u;          // plaintext [nl][N]
   const uint64_t* x0;         // [nl][N]
   const uint64_t* x1;
 };
-void launch_diag_mac(const DevCtx& c, const MacTerm* terms_dev, int n_terms, uint64_t* out0, uint64_t* out1,
-                     const LimbMap& map);
+// n_out output pairs; pair z uses terms [ranges[z].x, +ranges[z].y) and is
+// written to out + z out_stride (A) and + nl N (B)
+void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int2* ranges, int n_out, int n_terms_total,
+                     uint64_t* out, size_t out_stride, const LimbMap& map);
 
 }  // namespace helrm

@@ -86,28 +86,33 @@ __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double 
 template <int SLOG, int MODE>
 __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                       const PrimeDev* __restrict__ primes,
-                                                      const __grid_constant__ LimbMap map, size_t limb0, int log_n,
+                                                      const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
-  __shared__ double sm[MODE == 0 ? kTileElems : 16 * kBlkPad];
+  constexpr bool P1 = MODE == 0;
+  __shared__ double sm[P1 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
   const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
   const double q = P.qd, qi = P.qinv;
-  const uint64_t* s = src + limb * N;
-  uint64_t* d = dst + limb * N;
+  const size_t gl = limb0 + limb, goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
+  const uint64_t* s = src + (P1 ? goff : limb * N);  // pass 1 reads the caller's limb
+  uint64_t* d = dst + (P1 ? limb * N : goff);        // pass 2 writes the caller's limb
   const int tid = threadIdx.x;
-  const int sub = MODE == 0 ? tid % SUBS : tid / TS;
-  const int t = MODE == 0 ? tid / SUBS : tid % TS;
-  const int gsub = MODE == 0 ? blockIdx.x * SUBS + sub : (int)grp[blockIdx.x * SUBS + sub];
-  const double2* __restrict__ twA = MODE == 0 ? P.tw1 : P.tw2 + (size_t)gsub * 256;
+  const int sub = P1 ? tid % SUBS : tid / TS;
+  const int t = P1 ? tid / SUBS : tid % TS;
+  const int gsub = P1 ? blockIdx.x * SUBS + sub : (int)grp[blockIdx.x * SUBS + sub];
+  const double2* __restrict__ twA = P1 ? P.tw1 : P.tw2 + (size_t)gsub * 256;
   double r[kEPT];
 #pragma unroll
   for (int k = 0; k < kEPT; k++) {
     const int e = t + TS * k;
-    if (MODE == 0) r[k] = u2d(s[(size_t)e * 256 + gsub]);
-    else r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
+    if (MODE == 0) {
+      r[k] = u2d(s[(size_t)e * 256 + gsub]);
+    } else {
+      r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
+    }
   }
   // phase A: stages 0..3 on layout e = t + TS k (twiddles independent of t)
 #pragma unroll
@@ -117,7 +122,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
     for (int k = 0; k < kEPT; k++) {
       if ((k & half) == 0) {
         // MODE 0: tw1[2^st + i]; MODE 1: tw2[B][2^st - 1 + i]
-        const double2 w = MODE == 0 ? twA[(1 << st) + (k >> (4 - st))] : twA[(1 << st) - 1 + (k >> (4 - st))];
+        const double2 w = P1 ? twA[(1 << st) + (k >> (4 - st))] : twA[(1 << st) - 1 + (k >> (4 - st))];
         ct_bfly(r[k], r[k + half], w, q);
       }
     }
@@ -130,16 +135,16 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const int e = t + TS * k;
-      if (MODE == 0) sm[e * SUBS + sub] = r[k];
+      if (P1) sm[e * SUBS + sub] = r[k];
       else sm[sub * kBlkPad + pidx(e)] = r[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const int e = kEPT * t + k;
-      r[k] = MODE == 0 ? sm[e * SUBS + sub] : sm[sub * kBlkPad + pidx(e)];
+      r[k] = P1 ? sm[e * SUBS + sub] : sm[sub * kBlkPad + pidx(e)];
     }
-    const double2* __restrict__ twB = MODE == 0 ? P.tw1 : twA + 15 + 15 * t;
+    const double2* __restrict__ twB = P1 ? P.tw1 : twA + 15 + 15 * t;
 #pragma unroll
     for (int st = 4; st < SLOG; st++) {
       const int half = S >> (st + 1);
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
         if ((k & half) == 0) {
           const int e = kEPT * t + k;
           double2 w;
-          if (MODE == 0) w = twB[(1 << st) + (e >> (SLOG - st))];
+          if (P1) w = twB[(1 << st) + (e >> (SLOG - st))];
           else w = twB[(1 << (st - 4)) - 1 + (k >> (SLOG - st))];
           ct_bfly(r[k], r[k + half], w, q);
         }
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
 #pragma unroll
     for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
   }
-  if (MODE == 0) {
+  if (P1) {
     // centred doubles into the (L2-resident) scratch, natural row positions
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
@@ -195,17 +200,19 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
 template <int SLOG, int MODE>
 __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                       const PrimeDev* __restrict__ primes,
-                                                      const __grid_constant__ LimbMap map, size_t limb0, int log_n,
+                                                      const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
-                                                      const uint8_t* __restrict__ einv) {
+                                                      const uint8_t* __restrict__ einv,
+                                                      const double2* __restrict__ post) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   __shared__ double sm[MODE == 0 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
   const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
   const double q = P.qd, qi = P.qinv;
-  const uint64_t* s = src + limb * N;
-  uint64_t* d = dst + limb * N;
+  const size_t gl = limb0 + limb, goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
+  const uint64_t* s = src + (MODE == 1 ? goff : limb * N);  // pass A gathers the caller's limb
+  uint64_t* d = dst + (MODE == 1 ? limb * N : goff);        // pass B writes the caller's limb
   const int tid = threadIdx.x;
   const int sub = MODE == 0 ? tid % SUBS : tid / TS;
   const int t = MODE == 0 ? tid / SUBS : tid % TS;
@@ -278,8 +285,10 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
     for (int k = 0; k < kEPT; k++) d[(size_t)gsub * 256 + t + TS * k] = (uint64_t)__double_as_longlong(r[k]);
   } else {
 #pragma unroll
+    // N^-1, or N^-1 times a per-limb factor (the y-form of a base conversion)
+    const double2 nm = post ? post[gl % map.n] : P.ninvd;
     for (int k = 0; k < kEPT; k++) {
-      const double v = mmul(r[k], P.ninvd.x, P.ninvd.y, q);
+      const double v = mmul(r[k], nm.x, nm.y, q);
       d[(size_t)(t + TS * k) * 256 + gsub] = d2u(v, q, qi, P.rc.q);
     }
   }
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
 
 // ---------------------------------------------------------------- launchers
 static size_t chunk_limbs(int N) {
-  size_t ch = ((size_t)64 << 16) / (size_t)N;  // 32 MiB of scratch per chunk
+  size_t ch = ((size_t)128 << 16) / (size_t)N;  // 64 MiB of scratch per chunk (L2 is 126 MB)
   return ch > 65535 ? 65535 : ch;
 }
 
@@ -295,76 +304,74 @@ size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)
 
 template <int SLOG>
 static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
-                      const LimbMap& map, size_t off) {
+                      const LimbMap& map, size_t off, size_t ss, size_t ds) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
-    k_ntt_fwd<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, c.log_n,
+    k_ntt_fwd<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
                                                                   c.ntt_grp, c.ntt_einv);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
-    k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, c.log_n, c.ntt_grp,
-                                                               c.ntt_einv);
+    k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
+                                                               c.ntt_grp, c.ntt_einv);
   }
   *c.launches += 2;
 }
 
 template <int SLOG>
 static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
-                      const LimbMap& map, size_t off) {
+                      const LimbMap& map, size_t off, size_t ss, size_t ds, const double2* post) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
-    k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, c.log_n, c.ntt_grp,
-                                                               c.ntt_einv);
+    k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
+                                                               c.ntt_grp, c.ntt_einv, nullptr);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
-    k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, c.log_n,
-                                                                  c.ntt_grp, c.ntt_einv);
+    k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
+                                                                  c.ntt_grp, c.ntt_einv, post);
   }
   *c.launches += 2;
 }
 
-void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map) {
+template <bool FWD>
+static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
+                    const LimbMap& map, size_t ss, size_t ds, const double2* post = nullptr) {
+  if (ss == 0) ss = (size_t)map.n * c.N;
+  if (ds == 0) ds = (size_t)map.n * c.N;
   const size_t ch = chunk_limbs(c.N);
   for (size_t off = 0; off < n_total; off += ch) {
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);
-    const uint64_t* s = src + off * c.N;
-    uint64_t* d = dst + off * c.N;
+#define HELRM_NTT_CASE(LG, SL)                                                  \
+  case LG:                                                                      \
+    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds);         \
+    else inv_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, post);        \
+    break;
     switch (c.log_n) {
-      case 12: fwd_chunk<4>(c, s, d, scratch, cnt, map, off); break;
-      case 13: fwd_chunk<5>(c, s, d, scratch, cnt, map, off); break;
-      case 14: fwd_chunk<6>(c, s, d, scratch, cnt, map, off); break;
-      case 15: fwd_chunk<7>(c, s, d, scratch, cnt, map, off); break;
-      case 16: fwd_chunk<8>(c, s, d, scratch, cnt, map, off); break;
+      HELRM_NTT_CASE(12, 4)
+      HELRM_NTT_CASE(13, 5)
+      HELRM_NTT_CASE(14, 6)
+      HELRM_NTT_CASE(15, 7)
+      HELRM_NTT_CASE(16, 8)
       default: throw Error(HELRM_ERR_CONFIG, "NTT supports 12 <= log N <= 16");
     }
+#undef HELRM_NTT_CASE
   }
   HCUDA(cudaGetLastError());
 }
 
+void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
+                    const LimbMap& map, size_t ss, size_t ds) {
+  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds);
+}
+
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map) {
-  const size_t ch = chunk_limbs(c.N);
-  for (size_t off = 0; off < n_total; off += ch) {
-    const unsigned cnt = (unsigned)std::min(ch, n_total - off);
-    const uint64_t* s = src + off * c.N;
-    uint64_t* d = dst + off * c.N;
-    switch (c.log_n) {
-      case 12: inv_chunk<4>(c, s, d, scratch, cnt, map, off); break;
-      case 13: inv_chunk<5>(c, s, d, scratch, cnt, map, off); break;
-      case 14: inv_chunk<6>(c, s, d, scratch, cnt, map, off); break;
-      case 15: inv_chunk<7>(c, s, d, scratch, cnt, map, off); break;
-      case 16: inv_chunk<8>(c, s, d, scratch, cnt, map, off); break;
-      default: throw Error(HELRM_ERR_CONFIG, "NTT supports 12 <= log N <= 16");
-    }
-  }
-  HCUDA(cudaGetLastError());
+                    const LimbMap& map, size_t ss, size_t ds, const double2* post) {
+  ntt_any<false>(c, src, dst, scratch, n_total, map, ss, ds, post);
 }
 
 }  // namespace helrm

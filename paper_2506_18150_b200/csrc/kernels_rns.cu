@@ -1,7 +1,6 @@
 // kernels_rns.cu -- element-wise RNS kernels of the lookup (sm_100a):
 // samplers (D9/D10), signed reduction, modular add/sub/mul, Galois
-// automorphisms as slot-order shifts (D8), fast base conversion (D14, the
-// core of ModUp D15 / ModDown D16), the ModDown / rescale finishing steps
+// automorphisms as slot-order shifts (D8), the ModDown / rescale finishing steps
 // (D16/D17), the key inner product with fused automorphism (D18), and the
 // plaintext-diagonal multiply-accumulate of the BSGS inner sums (D20 L3).
 //
@@ -117,85 +116,99 @@ __global__ void k_automorph(const uint64_t* __restrict__ a, uint64_t* __restrict
   out[o] = accumulate ? add_mod(out[o], v, primes[map.pr[l]].rc.q) : v;
 }
 
-// D14 Conv_{B->T}: out[row[t]][i] = (sum_b [x_b (B/b)^-1]_b ((B/b) mod t)) mod t.
-struct ConvRows {
-  int16_t row[kMaxLimbs];
-};
-__global__ void k_conv(const ConvDev* __restrict__ cv, const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
-                       const PrimeDev* __restrict__ primes, uint32_t N, const __grid_constant__ ConvRows rows, int t_per_block) {
+// D14 from y-form sources: out_gk[r][i] = sum_b y_g[row0 + b][i] cf_kr[b] mod q_r for
+// every row r (the table also reproduces a digit's own rows); the CTA stages
+// its conversion's table in shared memory, each thread loads its nb sources
+// once and produces all rows.  grid (N/256, G ncv).
+__global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict__ tab, int ncv, int rows,
+                                                   const uint64_t* __restrict__ y, size_t y_stride,
+                                                   uint64_t* __restrict__ out, size_t osg, size_t osk,
+                                                   const PrimeDev* __restrict__ primes,
+                                                   const __grid_constant__ LimbMap map, uint32_t N) {
+  __shared__ ConvRowDev st[kMaxLimbs];
+  __shared__ RedConst rcs[kMaxLimbs];
+  const int g = blockIdx.y / ncv, k = blockIdx.y % ncv;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+    st[r] = tab[(size_t)k * rows + r];
+    rcs[r] = primes[map.pr[r]].rc;
+  }
+  __syncthreads();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
-  const int nb = cv->nb;
-  uint64_t y[kMaxDigitPrimes];
+  const int nb = st[0].nb;
+  const uint64_t* src = y + (size_t)g * y_stride + (size_t)st[0].src_row0 * N + i;
+  uint64_t v[kMaxDigitPrimes];
 #pragma unroll
-  for (int b = 0; b < kMaxDigitPrimes; b++) {
-    if (b < nb) {
-      const uint64_t qb = primes[cv->bpr[b]].rc.q;
-      y[b] = shoup(in[(size_t)b * N + i], cv->binv[b], cv->binvs[b], qb);
-    }
-  }
-  const int t0 = blockIdx.y * t_per_block;
-  const int t1 = min(cv->nt, t0 + t_per_block);
-  for (int t = t0; t < t1; t++) {
-    const RedConst rc = primes[cv->tpr[t]].rc;
+  for (int b = 0; b < kMaxDigitPrimes; b++) v[b] = b < nb ? src[(size_t)b * N] : 0;
+  uint64_t* o = out + (size_t)g * osg + (size_t)k * osk + i;
+  for (int r = 0; r < rows; r++) {
     U128 acc{0, 0};
 #pragma unroll
     for (int b = 0; b < kMaxDigitPrimes; b++)
-      if (b < nb) mac128(acc, y[b], cv->bmod[t][b]);
-    out[(size_t)rows.row[t] * N + i] = reduce128(acc.hi, acc.lo, rc);
+      if (b < nb) mac128(acc, v[b], st[r].cf[b]);
+    o[(size_t)r * N] = reduce128(acc.hi, acc.lo, rcs[r]);
   }
 }
 
-// out[l] = (y[l] - t[l]) * s[l] mod q_l  (ModDown / rescale finish)
-__global__ void k_sub_scale(const uint64_t* __restrict__ y, const uint64_t* __restrict__ t, uint64_t* __restrict__ out,
-                            const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N,
-                            const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp) {
+// out[g][l] = (y[g][l] - t[g][l]) * s[l] mod q_l  (ModDown / rescale finish), z = g
+__global__ void k_sub_scale(const uint64_t* __restrict__ y, size_t ys, const uint64_t* __restrict__ t, size_t ts,
+                            uint64_t* __restrict__ out, size_t os, const PrimeDev* __restrict__ primes,
+                            const __grid_constant__ LimbMap map, uint32_t N, const uint64_t* __restrict__ s,
+                            const uint64_t* __restrict__ sp) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int l = blockIdx.y;
+  const int l = blockIdx.y, g = blockIdx.z;
   if (i >= N) return;
   const uint64_t q = primes[map.pr[l]].rc.q;
   const size_t o = (size_t)l * N + i;
-  out[o] = shoup(sub_mod(y[o], t[o], q), s[l], sp[l], q);
+  out[g * os + o] = shoup(sub_mod(y[g * ys + o], t[g * ts + o], q), s[l], sp[l], q);
 }
 
-// D17: r = ((x + h) mod q_l) - h, then r mod q_i for the remaining limbs
-__global__ void k_rescale_prep(const uint64_t* __restrict__ xl, uint64_t ql, uint64_t* __restrict__ out,
-                               const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N) {
+// D17: r = ((x + h) mod q_l) - h, then r mod q_i for the remaining limbs; z = polynomial
+__global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint64_t ql, uint64_t* __restrict__ out,
+                               size_t os, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map,
+                               uint32_t N) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
   const uint64_t h = (ql - 1) / 2;
-  const uint64_t v = xl[i];
+  const uint64_t v = xl[blockIdx.z * xs + i];
   const uint64_t q = primes[map.pr[l]].rc.q;
   uint64_t r;
   if (v <= h) {
-    r = v % q;                       // r = v >= 0
+    r = v % q;                          // r = v >= 0
   } else {
     const uint64_t mag = (ql - v) % q;  // r = v - ql < 0
     r = mag ? q - mag : 0;
   }
-  out[(size_t)l * N + i] = r;
+  out[blockIdx.z * os + (size_t)l * N + i] = r;
 }
 
 // D18 key inner product with the automorphism fused into the loads:
-//   out0[l][p] (+)= [c0] P phi(c0)[l][p] + sum_k phi(D_k)[l][p] b_k[l][p]
+//   out0[l][p] (+)= [l < add_rows] mul_l phi(add0)[l][p] + sum_k phi(D_k)[l][p] b_k[l][p]
 //   out1[l][p] (+)= sum_k phi(D_k)[l][p] a_k[l][p]
-__global__ void k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N) {
+// (add0 = c0 with mul = [P]_q for a lazy rotation; add0 = A with mul = 1 for
+// the giant step's phi(A) + KS(B'), D20 L4)
+__global__ void k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
+                      const __grid_constant__ LimbMap map, uint32_t N) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (p >= N) return;
-  const int nl = map.n;
   const uint32_t chain = map.pr[l];
   const RedConst rc = primes[chain].rc;
   const uint32_t sp = rot_src(p, a.rot, N / 2);
   U128 acc0{0, 0}, acc1{0, 0};
+  const uint64_t* kb = a.key + (size_t)chain * N + p;
+  const uint64_t* dg = a.digits + (size_t)l * N + sp;
   for (int k = 0; k < a.dnum; k++) {
-    const uint64_t d = a.digits[((size_t)k * nl + l) * N + sp];
-    const uint64_t* kb = a.key + (size_t)k * a.key_digit_stride + (size_t)chain * N;
-    mac128(acc0, d, kb[p]);
-    mac128(acc1, d, kb[a.key_half_stride + p]);
+    const uint64_t d = dg[(size_t)k * a.digit_stride];
+    mac128(acc0, d, kb[(size_t)k * a.key_digit_stride]);
+    mac128(acc1, d, kb[(size_t)k * a.key_digit_stride + a.key_half_stride]);
   }
-  if (a.c0 != nullptr && l <= (int)a.level) mac128(acc0, a.c0[(size_t)l * N + sp], a.p_mod[l]);
+  if (a.add0 != nullptr && l < a.add_rows) {
+    const uint64_t v = a.add0[(size_t)l * N + sp];
+    if (a.add_mul) mac128(acc0, v, a.add_mul[l]);
+    else mac128(acc0, v, 1);
+  }
   uint64_t r0 = reduce128(acc0.hi, acc0.lo, rc), r1 = reduce128(acc1.hi, acc1.lo, rc);
   const size_t o = (size_t)l * N + p;
   if (a.accumulate) {
@@ -206,24 +219,122 @@ __global__ void k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restr
   a.out1[o] = r1;
 }
 
-// D20 L3: (A, B)[l][p] = sum_t u_t[l][p] (x0_t, x1_t)[l][p]
-__global__ void k_diag_mac(const MacTerm* __restrict__ terms, int n_terms, uint64_t* __restrict__ out0,
-                           uint64_t* __restrict__ out1, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map,
-                           uint32_t N) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+// D20 L2, all baby steps of one input ciphertext in one pass: for each
+// baby j (rotation r_j, key K_j), over Q_l P,
+//   a_j[l][p] = [l <= level] [P]_{q_l} phi_j(c0)[l][p] + sum_k phi_j(D_k)[l][p] b_{j,k}[l][p]
+//   b_j[l][p] = sum_k phi_j(D_k)[l][p] a_{j,k}[l][p]
+// The CTA stages its 256-position tile of D_k and c0 plus a halo of max r_j
+// positions (cyclic inside the half) in shared memory once, then streams the
+// keys: the digits are read from HBM once for all babies instead of once per
+// baby.
+__global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMulti a, const PrimeDev* __restrict__ primes,
+                                                   const __grid_constant__ LimbMap map, uint32_t N) {
+  extern __shared__ uint64_t sh[];
   const int l = blockIdx.y;
-  if (p >= N) return;
+  const uint32_t n = N / 2, tile = blockDim.x;
+  const uint32_t p0 = blockIdx.x * tile, half = p0 >= n ? n : 0;
+  const uint32_t span = tile + a.max_rot;
+  const uint32_t chain = map.pr[l];
+  const RedConst rc = primes[chain].rc;
+  const bool has_c0 = l <= (int)a.level;
+  // stage D_k (and c0) tiles + halo
+  for (uint32_t e = threadIdx.x; e < span; e += tile) {
+    uint32_t j = p0 - half + e;
+    j = j >= n ? j - n : j;
+    const size_t src = (size_t)l * N + half + j;
+    for (int k = 0; k < a.dnum; k++) sh[k * span + e] = a.digits[(size_t)k * a.digit_stride + src];
+    if (has_c0) sh[a.dnum * span + e] = a.c0[src];
+  }
+  __syncthreads();
+  const uint32_t p = p0 + threadIdx.x;
+  const uint64_t pm = has_c0 ? a.p_mod[l] : 0;
+  // two babies per round: 2 x 2 dnum independent key loads in flight
+  for (int j0 = 0; j0 < a.n; j0 += 2) {
+    const int nj = a.n - j0 >= 2 ? 2 : 1;
+    uint64_t kv[2][2][8];
+#pragma unroll
+    for (int jj = 0; jj < 2; jj++) {
+      if (jj < nj) {
+        const uint64_t* kb = a.key[j0 + jj] + (size_t)chain * N + p;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          if (k < a.dnum) {
+            kv[jj][0][k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
+            kv[jj][1][k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 2; jj++) {
+      if (jj < nj) {
+        const int j = j0 + jj;
+        const uint32_t e = threadIdx.x + a.rot[j];
+        U128 acc0{0, 0}, acc1{0, 0};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          if (k < a.dnum) {
+            const uint64_t dv = sh[k * span + e];
+            mac128(acc0, dv, kv[jj][0][k]);
+            mac128(acc1, dv, kv[jj][1][k]);
+          }
+        }
+        if (has_c0) mac128(acc0, sh[a.dnum * span + e], pm);
+        uint64_t* o = a.out[j] + (size_t)l * N + p;
+        o[0] = reduce128(acc0.hi, acc0.lo, rc);
+        o[a.out_half] = reduce128(acc1.hi, acc1.lo, rc);
+      }
+    }
+  }
+}
+
+// D20 L3, batched over output pairs z: (A, B)_z[l][p] = sum_t u_t[l][p] (x0_t, x1_t)[l][p]
+// for the terms [range[z].x, range[z].x + range[z].y); (A, B)_z at out + z * out_stride.
+__global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ terms, const int2* __restrict__ ranges,
+                                                  uint64_t* __restrict__ out, size_t out_stride, size_t half,
+                                                  const PrimeDev* __restrict__ primes,
+                                                  const __grid_constant__ LimbMap map, uint32_t N) {
+  // grid: (tile, output pair, limb) -- limb outermost, so the baby pairs of a
+  // limb (2 n1 limbs) stay L2-resident while every giant of that limb runs
+  __shared__ MacTerm tm[kMaxBabies];
+  const int2 rg = ranges[blockIdx.y];
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.z;
   const RedConst rc = primes[map.pr[l]].rc;
   const size_t o = (size_t)l * N + p;
   U128 acc0{0, 0}, acc1{0, 0};
-  for (int t = 0; t < n_terms; t++) {
-    const MacTerm m = terms[t];
-    const uint64_t u = m.u[o];
-    mac128(acc0, u, m.x0[o]);
-    mac128(acc1, u, m.x1[o]);
+  for (int c0 = 0; c0 < rg.y; c0 += kMaxBabies) {   // term list staged in chunks
+    const int nt = min(kMaxBabies, rg.y - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) tm[t] = terms[rg.x + c0 + t];
+    __syncthreads();
+    if (p >= N) continue;
+    int t = 0;
+    // 4 terms per round: 12 independent loads in flight per thread
+    for (; t + 4 <= nt; t += 4) {
+      uint64_t u[4], a[4], b[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        u[k] = __ldcs(tm[t + k].u + o);   // plaintexts stream once: evict-first
+        a[k] = tm[t + k].x0[o];
+        b[k] = tm[t + k].x1[o];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        mac128(acc0, u[k], a[k]);
+        mac128(acc1, u[k], b[k]);
+      }
+    }
+    for (; t < nt; t++) {
+      const uint64_t u = __ldcs(tm[t].u + o);
+      mac128(acc0, u, tm[t].x0[o]);
+      mac128(acc1, u, tm[t].x1[o]);
+    }
   }
-  out0[o] = reduce128(acc0.hi, acc0.lo, rc);
-  out1[o] = reduce128(acc1.hi, acc1.lo, rc);
+  if (p >= N) return;
+  uint64_t* dst = out + (size_t)blockIdx.y * out_stride;
+  dst[o] = reduce128(acc0.hi, acc0.lo, rc);
+  dst[half + o] = reduce128(acc1.hi, acc1.lo, rc);
 }
 
 // ---------------- launchers ----------------
@@ -275,43 +386,54 @@ void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const L
   HCUDA(cudaGetLastError());
 }
 
-void launch_conv(const DevCtx& c, const ConvDev* cv, int nb, int nt, const int16_t* rows, const uint64_t* in,
-                 uint64_t* out) {
-  ProfScope ps_(c, "conv", 8.0 * c.N * (nt + nb));
-  ConvRows r{};
-  for (int t = 0; t < nt; t++) r.row[t] = rows[t];
-  const int tpb = 4;
-  k_conv<<<dim3((c.N + kT - 1) / kT, (nt + tpb - 1) / tpb), kT, 0, c.stream>>>(cv, in, out, c.primes, c.N, r, tpb);
+void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows, const uint64_t* y, size_t y_stride,
+                      uint64_t* out, size_t out_stride_g, size_t out_stride_k, int G, const LimbMap& out_map) {
+  ProfScope ps_(c, "conv", 8.0 * c.N * (double)G * ncv * (rows + 4));
+  k_conv_rows<<<dim3(c.N / 256, G * ncv), 256, 0, c.stream>>>(tab, ncv, rows, y, y_stride, out, out_stride_g,
+                                                              out_stride_k, c.primes, out_map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
-void launch_sub_scale(const DevCtx& c, const uint64_t* y, const uint64_t* t, uint64_t* out, const LimbMap& map,
-                      const uint64_t* s, const uint64_t* sp) {
-  ProfScope ps_(c, "sub_scale", 24.0 * c.N * map.n);
-  k_sub_scale<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(y, t, out, c.primes, map, c.N, s, sp);
+void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
+                      size_t os, int G, const LimbMap& map, const uint64_t* s, const uint64_t* sp) {
+  ProfScope ps_(c, "sub_scale", 24.0 * c.N * map.n * G);
+  k_sub_scale<<<dim3((c.N + kT - 1) / kT, map.n, G), kT, 0, c.stream>>>(y, ys, t, ts, out, os, c.primes, map, c.N, s,
+                                                                        sp);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
-void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, uint64_t ql, uint64_t* out, const LimbMap& map) {
-  ProfScope ps_(c, "rescale_prep", 8.0 * c.N * (1 + map.n));
-  k_rescale_prep<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(xl, ql, out, c.primes, map, c.N);
+void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,
+                         const LimbMap& map) {
+  ProfScope ps_(c, "rescale_prep", 8.0 * c.N * (1 + map.n) * G);
+  k_rescale_prep<<<dim3((c.N + kT - 1) / kT, map.n, G), kT, 0, c.stream>>>(xl, xs, ql, out, os, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
-  ProfScope ps_(c, "kip", 8.0 * c.N * (3.0 * a.dnum * map.n + (a.c0 ? a.level + 1 : 0) + (a.accumulate ? 4 : 2) * map.n));
+  ProfScope ps_(c, "kip", 8.0 * c.N * (3.0 * a.dnum * map.n + (a.add0 ? a.add_rows : 0) + (a.accumulate ? 4 : 2) * map.n));
   k_kip<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
-void launch_diag_mac(const DevCtx& c, const MacTerm* terms, int n_terms, uint64_t* out0, uint64_t* out1,
-                     const LimbMap& map) {
-  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (3.0 * n_terms + 2));
-  k_diag_mac<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(terms, n_terms, out0, out1, c.primes, map, c.N);
+void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
+  ProfScope ps_(c, "kip_multi", 8.0 * c.N * (a.dnum * map.n + (a.level + 1) +
+                                             (double)a.n * (2.0 * a.dnum * map.n + 2 * map.n)));
+  const uint32_t tile = 256;
+  const size_t smem = (size_t)(a.dnum + 1) * (tile + a.max_rot) * 8;
+  k_kip_multi<<<dim3(c.N / tile, map.n), tile, smem, c.stream>>>(a, c.primes, map, c.N);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+}
+
+void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int2* ranges, int n_out, int n_terms_total,
+                     uint64_t* out, size_t out_stride, const LimbMap& map) {
+  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (3.0 * n_terms_total + 2.0 * n_out));
+  k_diag_mac<<<dim3((c.N + kT - 1) / kT, n_out, map.n), kT, 0, c.stream>>>(terms, ranges, out, out_stride,
+                                                                           (size_t)map.n * c.N, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
