@@ -478,6 +478,8 @@ helrm_status helrm_params_create(const helrm_params_desc* d, helrm_params** out)
     auto p = find_primes(pg, P.N, q);
     need(q.size() + p.size() <= (size_t)kMaxLimbs, HELRM_ERR_CONFIG, "too many primes");
     need(p.size() <= (size_t)kMaxDigitPrimes, HELRM_ERR_CONFIG, "at most 8 special primes");
+    for (uint64_t x : q) need(x < (1ull << 50), HELRM_ERR_CONFIG, "primes must be below 2^50");
+    for (uint64_t x : p) need(x < (1ull << 50), HELRM_ERR_CONFIG, "primes must be below 2^50");
     P.L = (uint32_t)q.size() - 1;
     P.K = (uint32_t)p.size();
     P.alpha = P.K;
@@ -793,6 +795,7 @@ helrm_status helrm_rotkeys_gen(helrm_ctx* c, const helrm_sk* sk, const uint64_t*
         launch_scalar_mul(c->dc(), phis.p + lo * N, t.p, dm, lc.pmod + lo, lc.pmods + lo);
         launch_binary(c->dc(), 0, b + lo * N, t.p, b + lo * N, dm);
       }
+      launch_split(c->dc(), key, rk->words_per_key, 1);   // keys live in split form (streaming MACs)
     }
     HCUDA(cudaStreamSynchronize(c->stream));
     *out = rk;
@@ -835,7 +838,10 @@ helrm_status helrm_rotkeys_export(helrm_ctx* c, const helrm_rotkeys* r, uint64_t
   return guard([&] {
     need(c && r && coeff && n_words >= r->words_per_key, HELRM_ERR_ARG, "bad argument");
     const Params& P = c->P;
-    export_ntt(c, key_for(r, g), 2 * P.dnum(P.L), P.map_range(0, P.L + 1 + P.K), coeff);
+    DBuf tmp(c, r->words_per_key);
+    HCUDA(cudaMemcpyAsync(tmp.p, key_for(r, g), r->words_per_key * 8, cudaMemcpyDeviceToDevice, c->stream));
+    launch_split(c->dc(), tmp.p, r->words_per_key, 0);
+    export_ntt(c, tmp.p, 2 * P.dnum(P.L), P.map_range(0, P.L + 1 + P.K), coeff);
   });
 }
 
@@ -1206,6 +1212,7 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
         launch_reduce_signed(c->dc(), (const int64_t*)(dcoef.p + k * N), dst, m);
       }
       ntt_fwd(c, pl->diag + (size_t)u0 * pl->nl * N, pl->diag + (size_t)u0 * pl->nl * N, (size_t)cnt * pl->nl, m);
+      launch_split(c->dc(), pl->diag + (size_t)u0 * pl->nl * N, (size_t)cnt * pl->nl * N, 1);  // stored split
     }
     HCUDA(cudaStreamSynchronize(c->stream));
     *out = pl;
@@ -1273,12 +1280,64 @@ static LimbMap map_twice(const LimbMap& m) {
   return r;
 }
 
-// host-side MAC term list for every non-empty (o, i); uploaded once per call
+// host-side L3 work list: output pair z per non-empty (o, i) (in o, i order),
+// giants packed kGiantPack at a time, one term per baby pair used by the pack
 struct MacList {
   std::vector<MacTerm> terms;
-  std::vector<int2> ranges;
+  std::vector<int4> groups;
   std::vector<std::pair<int64_t, int64_t>> oi;   // (o, i) of each output pair
+  double n_u = 0, n_x = 0;
 };
+
+}  // extern "C" (templates below)
+
+template <class XF>
+static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr) {
+  MacList ml;
+  for (int64_t o = 0; o < pl->O; o++) {
+    std::vector<int64_t> gi;
+    for (size_t i = 0; i < pl->entries[o].size(); i++)
+      if (!pl->entries[o][i].empty()) gi.push_back((int64_t)i);
+    for (size_t g0 = 0; g0 < gi.size(); g0 += kGiantPack) {
+      const int ng = (int)std::min<size_t>(kGiantPack, gi.size() - g0);
+      const int z0 = (int)ml.oi.size();
+      std::map<std::pair<int, int>, MacTerm> tm;
+      for (int g = 0; g < ng; g++) {
+        ml.oi.push_back({o, gi[g0 + g]});
+        for (const Entry& e : pl->entries[o][gi[g0 + g]]) {
+          auto it = tm.find({e.c, e.j});
+          if (it == tm.end()) {
+            MacTerm t{};
+            auto x = xptr(e.c, e.j);
+            t.x0 = x.first;
+            t.x1 = x.second;
+            it = tm.emplace(std::make_pair(e.c, e.j), t).first;
+          }
+          it->second.u[g] = pl->diag + (size_t)e.uid * diag_stride;
+          ml.n_u += 1;
+        }
+      }
+      ml.groups.push_back(make_int4((int)ml.terms.size(), (int)tm.size(), z0, ng));
+      for (auto& kv : tm) ml.terms.push_back(kv.second);
+      ml.n_x += (double)tm.size();
+    }
+  }
+  return ml;
+}
+
+extern "C" {
+
+// upload the list and run the batched MAC into out (pair z at out + z out_stride)
+static void run_macs(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_stride, const LimbMap& map,
+                     bool x_split) {
+  DBuf dterms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), dgroups(c, 2 * ml.groups.size() + 1);
+  HCUDA(cudaMemcpyAsync(dterms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
+                        c->stream));
+  HCUDA(cudaMemcpyAsync(dgroups.p, ml.groups.data(), ml.groups.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                        c->stream));
+  launch_diag_mac(c->dc(), (const MacTerm*)dterms.p, (const int4*)dgroups.p, (int)ml.groups.size(), ml.n_u, ml.n_x,
+                  (int)ml.oi.size(), out, out_stride, map, x_split);
+}
 
 // D20: the double-hoisted BSGS lookup of one query (C input cts -> O outputs)
 static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
@@ -1312,8 +1371,8 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
       uint64_t* a = babies.p + bi++ * 2 * nlN;
       if (j == 0) {  // (P c0, P c1): Q limbs scaled by [P]_q, P limbs 0
         HCUDA(cudaMemsetAsync(a, 0, 2 * nlN * 8, c->stream));
-        launch_scalar_mul(c->dc(), ct_c0(ct), a, mq, lc.pmod, lc.pmods);
-        launch_scalar_mul(c->dc(), ct_c1(ct), a + nlN, mq, lc.pmod, lc.pmods);
+        launch_scalar_mul(c->dc(), ct_c0(ct), a, mq, lc.pmod, lc.pmods, 1);   // baby pairs are split
+        launch_scalar_mul(c->dc(), ct_c1(ct), a + nlN, mq, lc.pmod, lc.pmods, 1);
       } else {
         need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
         const uint64_t g = galois_of_rot(c, j);
@@ -1328,27 +1387,13 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
     if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
   // L3: every inner sum (A, B)_{o,i} in one launch
-  MacList ml;
-  for (int64_t o = 0; o < pl->O; o++)
-    for (size_t i = 0; i < pl->entries[o].size(); i++) {
-      const auto& ent = pl->entries[o][i];
-      if (ent.empty()) continue;
-      const int s0 = (int)ml.terms.size();
-      for (const Entry& e : ent) {
-        uint64_t* x = ab[e.c].at(e.j);
-        ml.terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nlN, x, x + nlN});
-      }
-      ml.ranges.push_back(make_int2(s0, (int)ent.size()));
-      ml.oi.push_back({o, (int64_t)i});
-    }
-  const int n_out = (int)ml.ranges.size();
-  DBuf dterms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), dranges(c, n_out + 1);
-  HCUDA(cudaMemcpyAsync(dterms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
-                        c->stream));
-  HCUDA(cudaMemcpyAsync(dranges.p, ml.ranges.data(), n_out * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+  const MacList ml = build_macs(pl, nlN, [&](int ci, int j) {
+    uint64_t* a = ab[ci].at(j);
+    return std::make_pair((const uint64_t*)a, (const uint64_t*)(a + nlN));
+  });
+  const int n_out = (int)ml.oi.size();
   DBuf AB(c, (size_t)n_out * 2 * nlN);
-  launch_diag_mac(c->dc(), (const MacTerm*)dterms.p, (const int2*)dranges.p, n_out, (int)ml.terms.size(), AB.p,
-                  2 * nlN, mqp);
+  run_macs(c, ml, AB.p, 2 * nlN, mqp, true);
   // L4 (hoist #2) per output block: batched ModDown of every rotating B,
   // batched ModUp of the results, then one fused (phi(A) + KS) per giant
   DBuf O(c, 2 * nlN);
@@ -1408,37 +1453,22 @@ static void lookup_single(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
       rots[ci][j] = r;
     }
   }
-  MacList ml;
-  for (int64_t o = 0; o < pl->O; o++)
-    for (size_t i = 0; i < pl->entries[o].size(); i++) {
-      const auto& ent = pl->entries[o][i];
-      if (ent.empty()) continue;
-      const int s0 = (int)ml.terms.size();
-      for (const Entry& e : ent) {
-        helrm_ct* x = rots[e.c].at(e.j);
-        ml.terms.push_back(MacTerm{pl->diag + (size_t)e.uid * nqN, ct_c0(x), ct_c1(x)});
-      }
-      ml.ranges.push_back(make_int2(s0, (int)ent.size()));
-      ml.oi.push_back({o, (int64_t)i});
-    }
-  const int n_out = (int)ml.ranges.size();
-  DBuf dterms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), dranges(c, n_out + 1);
-  HCUDA(cudaMemcpyAsync(dterms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
-                        c->stream));
-  HCUDA(cudaMemcpyAsync(dranges.p, ml.ranges.data(), n_out * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
-  std::vector<helrm_ct*> AB(n_out);
-  for (int z = 0; z < n_out; z++) AB[z] = new_ct(c, l, in[0]->scale);
-  // outputs are written pairwise into separately allocated cts: one launch per pair
-  for (int z = 0; z < n_out; z++)
-    launch_diag_mac(c->dc(), (const MacTerm*)dterms.p, (const int2*)dranges.p + z, 1, ml.ranges[z].y, AB[z]->d,
-                    2 * nqN, mq);
+  const MacList ml = build_macs(pl, nqN, [&](int ci, int j) {
+    helrm_ct* x = rots[ci].at(j);
+    return std::make_pair((const uint64_t*)ct_c0(x), (const uint64_t*)ct_c1(x));
+  });
+  const int n_out = (int)ml.oi.size();
+  DBuf ABbuf(c, (size_t)n_out * 2 * nqN);
+  run_macs(c, ml, ABbuf.p, 2 * nqN, mq, false);
+  std::vector<helrm_ct> AB(n_out);
+  for (int z = 0; z < n_out; z++) AB[z] = helrm_ct{c, l, in[0]->scale, ABbuf.p + (size_t)z * 2 * nqN};
   helrm_ct* R = new_ct(c, l, in[0]->scale);
   for (int64_t o = 0; o < pl->O; o++) {
     helrm_ct* acc = new_ct(c, l, in[0]->scale * (double)P.primes[l]);
     HCUDA(cudaMemsetAsync(acc->d, 0, 2 * nqN * 8, c->stream));
     for (int z = 0; z < n_out; z++) {
       if (ml.oi[z].first != o) continue;
-      rotate(c, AB[z], rk, pl->giants[o][ml.oi[z].second], R);
+      rotate(c, &AB[z], rk, pl->giants[o][ml.oi[z].second], R);
       ct_add_inplace(c, acc, R);
     }
     helrm_ct* s = new_ct(c, l - 1, in[0]->scale);
@@ -1448,7 +1478,6 @@ static void lookup_single(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
     out[o] = s;
   }
   helrm_ct_destroy(R);
-  for (auto* x : AB) helrm_ct_destroy(x);
   for (auto& m : rots)
     for (auto& kv : m) helrm_ct_destroy(kv.second);
 }

@@ -158,7 +158,9 @@ void launch_sample_small(const DevCtx& c, int64_t* out, uint64_t base, int kind,
 // op 0: a + b, 1: a - b, 2: a * b, 3: -a
 void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, const LimbMap& map);
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
-                       const uint64_t* sp);
+                       const uint64_t* sp, int split_out = 0);
+// in place: dir 1 -> split form, dir 0 -> canonical
+void launch_split(const DevCtx& c, uint64_t* x, size_t n, int dir);
 void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
                       int accumulate);
 void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
@@ -170,7 +172,7 @@ struct KipArgs {
   const uint64_t* digits;     // digit k of the switched polynomial at digits + k digit_stride ([nl][N], NTT slot order)
   size_t digit_stride;
   int dnum;
-  const uint64_t* key;        // key for g: [digit][2][L+1+K][N]
+  const uint64_t* key;        // key for g: [digit][2][L+1+K][N], split form
   size_t key_digit_stride;    // words between digits of the key
   size_t key_half_stride;     // words between b and a of a digit
   const uint64_t* add0;       // optional: out0 += mul_l phi(add0)[l] for l < add_rows
@@ -202,14 +204,18 @@ struct KipMulti {
 };
 void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map);
 
+// D20 L3 work list.  Giants are packed kGiantPack at a time: a term is one
+// baby pair x = (x0, x1) with the plaintext u of each giant of the pack that
+// uses it (null if none), so every baby value is loaded once per pack.
+constexpr int kGiantPack = 4;
 struct MacTerm {
-  const uint64_t* u;          // plaintext [nl][N]
   const uint64_t* x0;         // [nl][N]
   const uint64_t* x1;
+  const uint64_t* u[kGiantPack];  // plaintext [nl][N] (split form) or null
 };
-// n_out output pairs; pair z uses terms [ranges[z].x, +ranges[z].y) and is
-// written to out + z out_stride (A) and + nl N (B)
-void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int2* ranges, int n_out, int n_terms_total,
-                     uint64_t* out, size_t out_stride, const LimbMap& map);
+// group z: terms [g.x, g.x + g.y), output pairs g.z .. g.z + g.w - 1, each
+// written to out + pair out_stride (A) and + nl N (B).  x split iff x_split.
+void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
+                     double n_x_total, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map, bool x_split);
 
 }  // namespace helrm

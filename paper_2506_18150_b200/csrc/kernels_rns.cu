@@ -95,13 +95,20 @@ __global__ void k_binary(int op, const uint64_t* __restrict__ a, const uint64_t*
 // out[l] = a[l] * s[l] (shoup constants per limb)
 __global__ void k_scalar_mul(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
                              const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N,
-                             const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp) {
+                             const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp, int split_out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
   const uint64_t q = primes[map.pr[l]].rc.q;
   const size_t o = (size_t)l * N + i;
-  out[o] = shoup(a[o], s[l], sp[l], q);
+  const uint64_t v = shoup(a[o], s[l], sp[l], q);
+  out[o] = split_out ? to_split(v) : v;
+}
+
+// in-place conversion to (dir 1) / from (dir 0) the split form
+__global__ void k_split(uint64_t* __restrict__ x, size_t n, int dir) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    x[i] = dir ? to_split(x[i]) : from_split(x[i]);
 }
 
 // out[l][p] = a[l][rot_src(p)]  (+ out if accumulate)
@@ -196,20 +203,31 @@ __global__ void k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restr
   const uint32_t chain = map.pr[l];
   const RedConst rc = primes[chain].rc;
   const uint32_t sp = rot_src(p, a.rot, N / 2);
-  U128 acc0{0, 0}, acc1{0, 0};
-  const uint64_t* kb = a.key + (size_t)chain * N + p;
+  Acc3 acc0, acc1;
+  const uint64_t* kb = a.key + (size_t)chain * N + p;   // split-form key
   const uint64_t* dg = a.digits + (size_t)l * N + sp;
-  for (int k = 0; k < a.dnum; k++) {
-    const uint64_t d = dg[(size_t)k * a.digit_stride];
-    mac128(acc0, d, kb[(size_t)k * a.key_digit_stride]);
-    mac128(acc1, d, kb[(size_t)k * a.key_digit_stride + a.key_half_stride]);
+  uint64_t dv[8], kv0[8], kv1[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    if (k < a.dnum) {
+      dv[k] = dg[(size_t)k * a.digit_stride];
+      kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
+      kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    if (k < a.dnum) {
+      const uint64_t d = to_split(dv[k]);
+      mac_split(acc0, d, kv0[k]);
+      mac_split(acc1, d, kv1[k]);
+    }
   }
   if (a.add0 != nullptr && l < a.add_rows) {
     const uint64_t v = a.add0[(size_t)l * N + sp];
-    if (a.add_mul) mac128(acc0, v, a.add_mul[l]);
-    else mac128(acc0, v, 1);
+    mac_split(acc0, to_split(v), to_split(a.add_mul ? a.add_mul[l] : 1));
   }
-  uint64_t r0 = reduce128(acc0.hi, acc0.lo, rc), r1 = reduce128(acc1.hi, acc1.lo, rc);
+  uint64_t r0 = acc3_reduce(acc0, rc), r1 = acc3_reduce(acc1, rc);
   const size_t o = (size_t)l * N + p;
   if (a.accumulate) {
     r0 = add_mod(r0, a.out0[o], rc.q);
@@ -242,12 +260,12 @@ __global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMu
     uint32_t j = p0 - half + e;
     j = j >= n ? j - n : j;
     const size_t src = (size_t)l * N + half + j;
-    for (int k = 0; k < a.dnum; k++) sh[k * span + e] = a.digits[(size_t)k * a.digit_stride + src];
-    if (has_c0) sh[a.dnum * span + e] = a.c0[src];
+    for (int k = 0; k < a.dnum; k++) sh[k * span + e] = to_split(a.digits[(size_t)k * a.digit_stride + src]);
+    if (has_c0) sh[a.dnum * span + e] = to_split(a.c0[src]);
   }
   __syncthreads();
   const uint32_t p = p0 + threadIdx.x;
-  const uint64_t pm = has_c0 ? a.p_mod[l] : 0;
+  const uint64_t pm = has_c0 ? to_split(a.p_mod[l]) : 0;
   // two babies per round: 2 x 2 dnum independent key loads in flight
   for (int j0 = 0; j0 < a.n; j0 += 2) {
     const int nj = a.n - j0 >= 2 ? 2 : 1;
@@ -270,71 +288,86 @@ __global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMu
       if (jj < nj) {
         const int j = j0 + jj;
         const uint32_t e = threadIdx.x + a.rot[j];
-        U128 acc0{0, 0}, acc1{0, 0};
+        Acc3 acc0, acc1;
 #pragma unroll
         for (int k = 0; k < 8; k++) {
           if (k < a.dnum) {
             const uint64_t dv = sh[k * span + e];
-            mac128(acc0, dv, kv[jj][0][k]);
-            mac128(acc1, dv, kv[jj][1][k]);
+            mac_split(acc0, dv, kv[jj][0][k]);
+            mac_split(acc1, dv, kv[jj][1][k]);
           }
         }
-        if (has_c0) mac128(acc0, sh[a.dnum * span + e], pm);
-        uint64_t* o = a.out[j] + (size_t)l * N + p;
-        o[0] = reduce128(acc0.hi, acc0.lo, rc);
-        o[a.out_half] = reduce128(acc1.hi, acc1.lo, rc);
+        if (has_c0) mac_split(acc0, sh[a.dnum * span + e], pm);
+        uint64_t* o = a.out[j] + (size_t)l * N + p;   // baby pairs are stored split
+        o[0] = to_split(acc3_reduce(acc0, rc));
+        o[a.out_half] = to_split(acc3_reduce(acc1, rc));
       }
     }
   }
 }
 
-// D20 L3, batched over output pairs z: (A, B)_z[l][p] = sum_t u_t[l][p] (x0_t, x1_t)[l][p]
-// for the terms [range[z].x, range[z].x + range[z].y); (A, B)_z at out + z * out_stride.
-__global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ terms, const int2* __restrict__ ranges,
+// D20 L3: (A, B)_z[l][p] = sum_t u_{z,t}[l][p] (x0_t, x1_t)[l][p] for the
+// giants z of a pack.  grid: (tile, pack, limb) -- limb outermost so the
+// baby pairs of a limb stay L2-resident; each baby value is loaded once per
+// pack of kGiantPack giants.
+template <bool XSPLIT>
+__global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ terms, const int4* __restrict__ groups,
                                                   uint64_t* __restrict__ out, size_t out_stride, size_t half,
                                                   const PrimeDev* __restrict__ primes,
                                                   const __grid_constant__ LimbMap map, uint32_t N) {
-  // grid: (tile, output pair, limb) -- limb outermost, so the baby pairs of a
-  // limb (2 n1 limbs) stay L2-resident while every giant of that limb runs
-  __shared__ MacTerm tm[kMaxBabies];
-  const int2 rg = ranges[blockIdx.y];
+  constexpr int G = kGiantPack;
+  constexpr int kChunk = 64;
+  __shared__ MacTerm tm[kChunk];
+  const int4 gr = groups[blockIdx.y];
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.z;
   const RedConst rc = primes[map.pr[l]].rc;
   const size_t o = (size_t)l * N + p;
-  U128 acc0{0, 0}, acc1{0, 0};
-  for (int c0 = 0; c0 < rg.y; c0 += kMaxBabies) {   // term list staged in chunks
-    const int nt = min(kMaxBabies, rg.y - c0);
+  Acc3 acc0[G], acc1[G];
+  for (int c0 = 0; c0 < gr.y; c0 += kChunk) {   // term list staged in chunks
+    const int nt = min(kChunk, gr.y - c0);
     __syncthreads();
-    for (int t = threadIdx.x; t < nt; t += blockDim.x) tm[t] = terms[rg.x + c0 + t];
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) tm[t] = terms[gr.x + c0 + t];
     __syncthreads();
     if (p >= N) continue;
-    int t = 0;
-    // 4 terms per round: 12 independent loads in flight per thread
-    for (; t + 4 <= nt; t += 4) {
-      uint64_t u[4], a[4], b[4];
+    // two terms per round: 2 x (2 + G) independent loads in flight
+    for (int t = 0; t < nt; t += 2) {
+      const int nr = nt - t >= 2 ? 2 : 1;
+      uint64_t x0[2], x1[2], u[2][G];
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        u[k] = __ldcs(tm[t + k].u + o);   // plaintexts stream once: evict-first
-        a[k] = tm[t + k].x0[o];
-        b[k] = tm[t + k].x1[o];
+      for (int r = 0; r < 2; r++) {
+        if (r < nr) {
+          const MacTerm& m = tm[t + r];
+          x0[r] = m.x0[o];
+          x1[r] = m.x1[o];
+#pragma unroll
+          for (int g = 0; g < G; g++) u[r][g] = m.u[g] ? __ldcs(m.u[g] + o) : 0;  // plaintexts stream once
+        } else {
+          x0[r] = x1[r] = 0;
+#pragma unroll
+          for (int g = 0; g < G; g++) u[r][g] = 0;
+        }
       }
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        mac128(acc0, u[k], a[k]);
-        mac128(acc1, u[k], b[k]);
+      for (int r = 0; r < 2; r++) {
+        const uint64_t a = XSPLIT ? x0[r] : to_split(x0[r]), b = XSPLIT ? x1[r] : to_split(x1[r]);
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+          mac_split(acc0[g], u[r][g], a);
+          mac_split(acc1[g], u[r][g], b);
+        }
       }
-    }
-    for (; t < nt; t++) {
-      const uint64_t u = __ldcs(tm[t].u + o);
-      mac128(acc0, u, tm[t].x0[o]);
-      mac128(acc1, u, tm[t].x1[o]);
     }
   }
   if (p >= N) return;
-  uint64_t* dst = out + (size_t)blockIdx.y * out_stride;
-  dst[o] = reduce128(acc0.hi, acc0.lo, rc);
-  dst[half + o] = reduce128(acc1.hi, acc1.lo, rc);
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    if (g < gr.w) {
+      uint64_t* dst = out + (size_t)(gr.z + g) * out_stride;
+      dst[o] = acc3_reduce(acc0[g], rc);
+      dst[half + o] = acc3_reduce(acc1[g], rc);
+    }
+  }
 }
 
 // ---------------- launchers ----------------
@@ -371,9 +404,16 @@ void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b
 }
 
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
-                       const uint64_t* sp) {
+                       const uint64_t* sp, int split_out) {
   ProfScope ps_(c, "scalar_mul", 16.0 * c.N * map.n);
-  k_scalar_mul<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp);
+  k_scalar_mul<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp, split_out);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+}
+
+void launch_split(const DevCtx& c, uint64_t* x, size_t n, int dir) {
+  ProfScope ps_(c, "split", 16.0 * n);
+  k_split<<<148 * 8, 256, 0, c.stream>>>(x, n, dir);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -429,11 +469,12 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
   HCUDA(cudaGetLastError());
 }
 
-void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int2* ranges, int n_out, int n_terms_total,
-                     uint64_t* out, size_t out_stride, const LimbMap& map) {
-  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (3.0 * n_terms_total + 2.0 * n_out));
-  k_diag_mac<<<dim3((c.N + kT - 1) / kT, n_out, map.n), kT, 0, c.stream>>>(terms, ranges, out, out_stride,
-                                                                           (size_t)map.n * c.N, c.primes, map, c.N);
+void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
+                     double n_x_total, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map, bool x_split) {
+  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + 2.0 * n_x_total + 2.0 * n_out));
+  auto kern = x_split ? k_diag_mac<true> : k_diag_mac<false>;
+  kern<<<dim3((c.N + kT - 1) / kT, n_groups, map.n), kT, 0, c.stream>>>(terms, groups, out, out_stride,
+                                                                        (size_t)map.n * c.N, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
