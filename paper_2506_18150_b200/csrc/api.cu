@@ -276,9 +276,12 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
         cr.src_row0 = (int)lo;
         cr.nb = (int)B.size();
         const uint64_t qr = P.primes[P.qp_chain(l, r)];
+        cr.q = (double)qr;
+        cr.qinv = 1.0 / (double)qr;
         for (size_t b = 0; b < B.size(); b++) {
-          if (r >= lo && r < hi) cr.cf[b] = (r - lo == b) ? hat_mod(B, b, qr) : 0;  // undo the y-form factor
-          else cr.cf[b] = hat_mod(B, b, qr);                                        // (B/b) mod q_r
+          const uint64_t w = (r >= lo && r < hi) ? ((r - lo == b) ? hat_mod(B, b, qr) : 0)  // undo the y-form factor
+                                                 : hat_mod(B, b, qr);                         // (B/b) mod q_r
+          cr.cf[b] = make_double2((double)w, (double)w / (double)qr);
         }
       }
     }
@@ -293,7 +296,13 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
       cr = ConvRowDev{};
       cr.src_row0 = 0;
       cr.nb = (int)P.K;
-      for (uint32_t b = 0; b < P.K; b++) cr.cf[b] = hat_mod(PB, b, P.primes[r]);
+      const uint64_t qr = P.primes[r];
+      cr.q = (double)qr;
+      cr.qinv = 1.0 / (double)qr;
+      for (uint32_t b = 0; b < P.K; b++) {
+        const uint64_t w = hat_mod(PB, b, qr);
+        cr.cf[b] = make_double2((double)w, (double)w / (double)qr);
+      }
     }
     auto up = [&](const void* h, size_t bytes) {
       void* d = c->dalloc(bytes);
@@ -328,8 +337,9 @@ static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int 
   // INTT straight into y-form (times [(Q_k/q_i)^-1]_{q_i}), one conversion
   // launch over (g, digit) writing every output row, one NTT over all of them
   launch_ntt_inv(c->dc(), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post);
-  launch_conv_rows(c->dc(), lc.modup_tab, (int)dn, (int)nl, y.p, nq * N, out, dn * nl * N, nl * N, G, P.map_qp(l));
-  ntt_fwd(c, out, out, G * dn * nl, P.map_qp(l));
+  launch_conv_rows(c->dc(), lc.modup_tab, (int)dn, (int)nl, (int)P.alpha, y.p, nq * N, out, dn * nl * N, nl * N, G,
+                   P.map_qp(l));
+  launch_ntt_fwd(c->dc(), out, out, c->scratch, G * dn * nl, P.map_qp(l), 0, 0, true);
 }
 
 // D16 for G polynomials: y_g = y + g ys ([l+1+K][N]) -> out_g = out + g os ([l+1][N])
@@ -340,8 +350,8 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   DBuf yp(c, G * P.K * N), t(c, G * nq * N);
   launch_ntt_inv(c->dc(), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
                  lc.moddown_post);
-  launch_conv_rows(c->dc(), lc.moddown_tab, 1, (int)nq, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
-  ntt_fwd(c, t.p, t.p, G * nq, P.map_q(l));
+  launch_conv_rows(c->dc(), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
+  launch_ntt_fwd(c->dc(), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true);
   launch_sub_scale(c->dc(), y, ys, t.p, nq * N, out, os, G, P.map_q(l), lc.pinv, lc.pinvs);
 }
 
@@ -562,7 +572,7 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
         for (uint32_t t = 0; t < 16; t++)
           for (uint32_t st = 4; st < 8; st++)
             for (uint32_t ii = 0; ii < (1u << (st - 4)); ii++)
-              put(t2, B * 256 + 15 + 15 * t + (1u << (st - 4)) - 1 + ii,
+              put(t2, B * 256 + 15 + 16 * ((1u << (st - 4)) - 1 + ii) + t,
                   (1ull << (s1 + st)) + (B << st) + t * (1ull << (st - 4)) + ii);
       }
     }

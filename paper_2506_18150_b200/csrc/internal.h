@@ -49,10 +49,12 @@ struct LimbMap {
   uint8_t pr[kMaxLimbs];
 };
 
-// one output row of a fused base conversion: out = sum_b y_{row0+b} cf[b] mod q_out
+// one output row of a base conversion: out = sum_b y_{row0+b} cf[b] mod q_out,
+// evaluated on the FP64 pipe: cf as (w, w / q_out) pairs
 struct ConvRowDev {
   int src_row0, nb;
-  uint64_t cf[kMaxDigitPrimes];
+  double q, qinv;
+  double2 cf[kMaxDigitPrimes];
 };
 
 struct Params {
@@ -137,18 +139,21 @@ struct ProfScope {
 // NTT over n_total limbs: limb y = (poly y / map.n, limb y % map.n) lives at
 // src + (y / map.n) * src_stride + (y % map.n) * N (same for dst; stride 0 =
 // contiguous polys of map.n limbs).  src == dst allowed.
+// din: the source limbs hold centred integer-valued doubles (k_conv_rows output)
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0);
+                    const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0, bool din = false);
 // post (optional, per limb of map): final factor (w, w/q) replacing N^-1
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0,
                     const double2* post = nullptr);
 // D14 base conversion from y-form sources (coefficients times [(B/b)^-1]_b,
 // folded into the INTT): for polynomial g and conversion k, every output row
-// r of the table: out_gk[r] = sum_b y_g[row0 + b] cf_kr[b] mod q_r
-// (coefficient form; an NTT follows).  z = g ncv + k.
-void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows, const uint64_t* y, size_t y_stride,
-                      uint64_t* out, size_t out_stride_g, size_t out_stride_k, int G, const LimbMap& out_map);
+// r of the table: out_gk[r] = sum_b y_g[row0 + b] cf_kr[b] mod q_r, written
+// as centred integer-valued doubles (coefficient form; a din NTT follows).
+// z = g ncv + k.
+void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows, int nb_max, const uint64_t* y,
+                      size_t y_stride, uint64_t* out, size_t out_stride_g, size_t out_stride_k, int G,
+                      const LimbMap& out_map);
 size_t ntt_scratch_words(int log_n);
 
 void launch_reduce_signed(const DevCtx& c, const int64_t* m, uint64_t* out, const LimbMap& map);

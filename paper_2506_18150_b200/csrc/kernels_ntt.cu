@@ -82,7 +82,7 @@ __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double 
 // threads per sub-transform.
 //   MODE 0 (pass 1): sub-transform = column (stride 256); twiddles tw1[2^st + i].
 //   MODE 1 (pass 2): sub-transform = 256-block B; twiddles tw2[B][...]:
-//     [0, 15): phase A, 2^st - 1 + i_loc;  [15 + 15 t, ...): thread t's phase B.
+//     [0, 15): phase A, 2^st - 1 + i_loc;  15 + 16 j + t: thread t's phase-B twiddle j.
 template <int SLOG, int MODE>
 __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                       const PrimeDev* __restrict__ primes,
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
-  constexpr bool P1 = MODE == 0;
+  constexpr bool P1 = MODE != 1;  // MODE 2 = pass 1 whose input limbs are centred doubles (conversion output)
   __shared__ double sm[P1 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
 #pragma unroll
   for (int k = 0; k < kEPT; k++) {
     const int e = t + TS * k;
-    if (MODE == 0) {
+    if (MODE == 2) {
+      r[k] = __longlong_as_double((long long)s[(size_t)e * 256 + gsub]);
+    } else if (MODE == 0) {
       r[k] = u2d(s[(size_t)e * 256 + gsub]);
     } else {
       r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
       const int e = kEPT * t + k;
       r[k] = P1 ? sm[e * SUBS + sub] : sm[sub * kBlkPad + pidx(e)];
     }
-    const double2* __restrict__ twB = P1 ? P.tw1 : twA + 15 + 15 * t;
+    const double2* __restrict__ twB = P1 ? P.tw1 : twA + 15 + t;  // phase-B twiddle j of thread t at 15 + 16 j + t
 #pragma unroll
     for (int st = 4; st < SLOG; st++) {
       const int half = S >> (st + 1);
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
           const int e = kEPT * t + k;
           double2 w;
           if (P1) w = twB[(1 << st) + (e >> (SLOG - st))];
-          else w = twB[(1 << (st - 4)) - 1 + (k >> (SLOG - st))];
+          else w = twB[((1 << (st - 4)) - 1 + (k >> (SLOG - st))) * 16];
           ct_bfly(r[k], r[k + half], w, q);
         }
       }
@@ -182,14 +184,14 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
     __syncthreads();
     // permuted store: block of rank g = 16 cta + i lives at slot positions
     // (g / stride) n + (g % stride) + stride tp; for a given tp the 16 blocks are adjacent
-    const int n = N >> 1, stride = N >> 9;
+    const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
 #pragma unroll 4
     for (int idx = tid; idx < kTileElems; idx += kThreads) {
       const int i = idx % 16, tp = idx / 16;
       const int g = blockIdx.x * 16 + i;
       const int B = grp[g];
       const int e = einv[B * 256 + tp];
-      d[(g / stride) * n + (g % stride) + stride * tp] = smu[i * kBlkPad + pidx(e)];
+      d[(size_t)(g >> lgs) * n + (g & (stride - 1)) + (tp << lgs)] = smu[i * kBlkPad + pidx(e)];
     }
   }
 }
@@ -220,14 +222,14 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
   const double2* __restrict__ twA = MODE == 0 ? P.itw1 : P.itw2 + (size_t)gsub * 256;
   double r[kEPT];
   if (MODE == 1) {
-    const int n = N >> 1, stride = N >> 9;
+    const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
 #pragma unroll 4
     for (int idx = tid; idx < kTileElems; idx += kThreads) {
       const int i = idx % 16, tp = idx / 16;
       const int g = blockIdx.x * 16 + i;
       const int B = grp[g];
       const int e = einv[B * 256 + tp];
-      sm[i * kBlkPad + pidx(e)] = u2d(s[(g / stride) * n + (g % stride) + stride * tp]);
+      sm[i * kBlkPad + pidx(e)] = u2d(s[(size_t)(g >> lgs) * n + (g & (stride - 1)) + (tp << lgs)]);
     }
     __syncthreads();
 #pragma unroll
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
     }
   }
   if (SLOG > 4) {
-    const double2* __restrict__ twB = MODE == 0 ? P.itw1 : twA + 15 + 15 * t;
+    const double2* __restrict__ twB = MODE == 0 ? P.itw1 : twA + 15 + t;  // phase-B twiddle j of thread t at 15 + 16 j + t
 #pragma unroll
     for (int st = SLOG - 1; st >= 4; st--) {
       const int half = S >> (st + 1);
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
           const int e = kEPT * t + k;
           double2 w;
           if (MODE == 0) w = twB[(1 << st) + (e >> (SLOG - st))];
-          else w = twB[(1 << (st - 4)) - 1 + (k >> (SLOG - st))];
+          else w = twB[((1 << (st - 4)) - 1 + (k >> (SLOG - st))) * 16];
           gs_bfly(r[k], r[k + half], w, q, qi);
         }
       }
@@ -304,13 +306,14 @@ size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)
 
 template <int SLOG>
 static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
-                      const LimbMap& map, size_t off, size_t ss, size_t ds) {
+                      const LimbMap& map, size_t off, size_t ss, size_t ds, bool din) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
-    k_ntt_fwd<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
-                                                                  c.ntt_grp, c.ntt_einv);
+    auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
+    k1<<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
+                                                 c.ntt_einv);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
@@ -340,7 +343,7 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
 
 template <bool FWD>
 static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, const double2* post = nullptr) {
+                    const LimbMap& map, size_t ss, size_t ds, const double2* post = nullptr, bool din = false) {
   if (ss == 0) ss = (size_t)map.n * c.N;
   if (ds == 0) ds = (size_t)map.n * c.N;
   const size_t ch = chunk_limbs(c.N);
@@ -348,7 +351,7 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);
 #define HELRM_NTT_CASE(LG, SL)                                                  \
   case LG:                                                                      \
-    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds);         \
+    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din);    \
     else inv_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, post);        \
     break;
     switch (c.log_n) {
@@ -365,8 +368,8 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
 }
 
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds) {
-  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds);
+                    const LimbMap& map, size_t ss, size_t ds, bool din) {
+  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din);
 }
 
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,

@@ -127,33 +127,49 @@ __global__ void k_automorph(const uint64_t* __restrict__ a, uint64_t* __restrict
 // every row r (the table also reproduces a digit's own rows); the CTA stages
 // its conversion's table in shared memory, each thread loads its nb sources
 // once and produces all rows.  grid (N/256, G ncv).
+// FP64 helpers shared with the NTT butterflies: exact Y W mod q for
+// |Y W / q| < 2^51 via an FMA-split product and a rounded quotient.
+namespace {
+constexpr double kMagicC = 6755399441055744.0;  // 1.5 * 2^52
+__device__ __forceinline__ double c_u2d(uint64_t x) {
+  return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
+}
+__device__ __forceinline__ double c_mmul(double y, double w, double wq, double q) {
+  const double h = y * w;
+  const double k = __fma_rn(y, wq, kMagicC) - kMagicC;
+  const double l = __fma_rn(y, w, -h);
+  return __fma_rn(-k, q, h) + l;
+}
+__device__ __forceinline__ double c_cred(double x, double q, double qi) {
+  const double k = __fma_rn(x, qi, kMagicC) - kMagicC;
+  return __fma_rn(-k, q, x);
+}
+}  // namespace
+
+template <int NB>
 __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict__ tab, int ncv, int rows,
                                                    const uint64_t* __restrict__ y, size_t y_stride,
-                                                   uint64_t* __restrict__ out, size_t osg, size_t osk,
-                                                   const PrimeDev* __restrict__ primes,
-                                                   const __grid_constant__ LimbMap map, uint32_t N) {
+                                                   uint64_t* __restrict__ out, size_t osg, size_t osk, uint32_t N) {
   __shared__ ConvRowDev st[kMaxLimbs];
-  __shared__ RedConst rcs[kMaxLimbs];
   const int g = blockIdx.y / ncv, k = blockIdx.y % ncv;
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) {
-    st[r] = tab[(size_t)k * rows + r];
-    rcs[r] = primes[map.pr[r]].rc;
-  }
+  const ConvRowDev* tk = tab + (size_t)k * rows;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) st[r] = tk[r];
   __syncthreads();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int nb = st[0].nb;
   const uint64_t* src = y + (size_t)g * y_stride + (size_t)st[0].src_row0 * N + i;
-  uint64_t v[kMaxDigitPrimes];
+  double v[NB];
 #pragma unroll
-  for (int b = 0; b < kMaxDigitPrimes; b++) v[b] = b < nb ? src[(size_t)b * N] : 0;
+  for (int b = 0; b < NB; b++) v[b] = b < nb ? c_u2d(src[(size_t)b * N]) : 0.0;  // missing sources = 0
   uint64_t* o = out + (size_t)g * osg + (size_t)k * osk + i;
+#pragma unroll 2
   for (int r = 0; r < rows; r++) {
-    U128 acc{0, 0};
+    const double q = st[r].q, qi = st[r].qinv;
+    double acc = 0.0;
 #pragma unroll
-    for (int b = 0; b < kMaxDigitPrimes; b++)
-      if (b < nb) mac128(acc, v[b], st[r].cf[b]);
-    o[(size_t)r * N] = reduce128(acc.hi, acc.lo, rcs[r]);
+    for (int b = 0; b < NB; b++) acc += c_mmul(v[b], st[r].cf[b].x, st[r].cf[b].y, q);  // each in [-q/2, q/2]
+    o[(size_t)r * N] = (uint64_t)__double_as_longlong(c_cred(acc, q, qi));
   }
 }
 
@@ -426,11 +442,15 @@ void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const L
   HCUDA(cudaGetLastError());
 }
 
-void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows, const uint64_t* y, size_t y_stride,
-                      uint64_t* out, size_t out_stride_g, size_t out_stride_k, int G, const LimbMap& out_map) {
+void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows, int nb_max, const uint64_t* y,
+                      size_t y_stride, uint64_t* out, size_t out_stride_g, size_t out_stride_k, int G,
+                      const LimbMap& out_map) {
   ProfScope ps_(c, "conv", 8.0 * c.N * (double)G * ncv * (rows + 4));
-  k_conv_rows<<<dim3(c.N / 256, G * ncv), 256, 0, c.stream>>>(tab, ncv, rows, y, y_stride, out, out_stride_g,
-                                                              out_stride_k, c.primes, out_map, c.N);
+  auto kern = nb_max <= 1 ? k_conv_rows<1> : nb_max <= 2 ? k_conv_rows<2> : nb_max <= 4 ? k_conv_rows<4>
+                                                                                     : k_conv_rows<8>;
+  (void)out_map;
+  kern<<<dim3(c.N / 256, G * ncv), 256, 0, c.stream>>>(tab, ncv, rows, y, y_stride, out, out_stride_g, out_stride_k,
+                                                       c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
