@@ -16,6 +16,8 @@ Shapes and distributions (BASELINE.json `configs`):
                    level 19.  One 50257x768 table compressed base 256 into
                    2 sub-tables 256x768, entries N(0, 0.02^2); 128 token ids
                    U[0, 50257); layout L2 (token stride 1024 in and out).
+  llm_small        the same layout on the Tiny ring (N=2^12): 64 tokens of a
+                   1000x48 table, base 32, stride 128 (4 in / 4 out cts).
   microbench       N=2^16, Criteo's primes; 1024 ciphertexts of uniform limbs
                    (drawn by the D9 PRNG, purpose 9 -- see microbench_seed).
 
@@ -42,7 +44,7 @@ CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431,
                 495595, 10, 822, 1375]
 CRITEO_VOCAB_SEED = 230
 
-CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "llm", "microbench")
+CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "llm", "llm_small", "microbench")
 
 
 def subtable_rows(k: int, p: int) -> int:
@@ -107,6 +109,9 @@ _CONFIGS = {
     "criteo": Config("criteo", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
     "criteo_b64": Config("criteo_b64", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=64),
     "llm": Config("llm", 16, [(50, 20)], [(50, 4)], 40, 19, 1),
+    # LLM-L2 layout scaled to the Tiny ring so the oracle runs it live: 64 tokens
+    # of a 1000 x 48 table (base 32, 2 digits), stride 128 -> 4 in / 4 out cts
+    "llm_small": Config("llm_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
     "microbench": Config("microbench", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=1024),
 }
 
@@ -147,8 +152,8 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
         tables = [Table(k, 16, 64, rng.normal(0.0, 0.05, size=(subtable_rows(k, 64), 16))) for k in CRITEO_VOCAB]
         idx = np.array([[_zipf_index(rng, k) for k in CRITEO_VOCAB] for _ in range(B)], dtype=np.int64)
         return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))
-    if name == "llm":
-        V, d, p, m, stride = 50257, 768, 256, 128, 1024
+    if name in ("llm", "llm_small"):
+        V, d, p, m, stride = (50257, 768, 256, 128, 1024) if name == "llm" else (1000, 48, 32, 64, 128)
         w = rng.normal(0.0, 0.02, size=(subtable_rows(V, p), d))
         tables = [Table(V, d, p, w, in_off=stride * t, out_off=stride * t, weight_id=0) for t in range(m)]
         idx = rng.integers(0, V, size=(B, m)).astype(np.int64)

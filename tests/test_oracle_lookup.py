@@ -223,3 +223,27 @@ def test_per_digit_partial_lookups_sum_encrypted():
         total += core.decrypt_decode(run.P, run.sk, lk.lookup(run.P, run.plan, run.u_ntt, run.rk, [ct])[0])
     y = lk.gather(run.lay, w.indices[0])
     assert np.abs(total[: run.lay.M] - y).max() < 2e-3
+
+
+def test_llm_full_size_plan_counts():
+    """LLM-L2 at full size (n = 2^15): 1279 distinct diagonals shared by the 4
+    blocks (t0 = -767), n1 = 64, n2 = 20, 82 rotation amounts (63 babies + 20
+    giants; giant 12 is amount 1, also a baby)."""
+    w = synth.make_workload("llm")
+    lay = lk.layout(w)
+    n = 1 << 15
+    plan = lk.make_plan(lay, n, 19)
+    assert (plan.C, plan.O, len(plan.u_slots), plan.n1, plan.n2) == (4, 4, 1279, 64, [20] * 4)
+    assert plan.t0 == [n - 767] * 4 and plan.n_diag == 4 * 1279
+    amts = plan.rotation_amounts(types.SimpleNamespace(n=n))
+    assert len(amts) == 82 and (n - 767 + 64 * 12) % n == 1
+
+
+def test_llm_small_lookup_decrypts_to_gather():
+    """LLM-L2 layout (4 input / 4 output cts, shared diagonals, mbar = n, no
+    RotSum) on the Tiny ring: every output block decrypts to the gather."""
+    w = synth.make_workload("llm_small")
+    run = lk.run_config(w)
+    assert (run.plan.C, run.plan.O, len(run.plan.u_slots), run.plan.n1) == (4, 4, 111, 16)
+    z = np.concatenate([core.decrypt_decode(run.P, run.sk, o) for o in run.outs[0]])
+    assert np.abs(z[: run.lay.M] - lk.gather(run.lay, w.indices[0])).max() < 1e-3
