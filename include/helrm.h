@@ -213,6 +213,22 @@ helrm_status helrm_ct_alloc(helrm_ctx* c, uint32_t level, double scale, helrm_ct
  * (purpose 9, a = ct, b = poly, c = limb), written in NTT form. */
 helrm_status helrm_ct_random(helrm_ctx* c, uint64_t seed, uint32_t ct_index, uint32_t level, helrm_ct** out);
 
+/* ---- multi-GPU: one process per GPU ----------------- */
+/* Contiguous split of n_items over world ranks: [lo, hi) for `rank`. */
+helrm_status helrm_dist_range(int64_t n_items, int world, int rank, int64_t* lo, int64_t* hi);
+/* NCCL unique id (128 bytes) to broadcast through torch.distributed. */
+helrm_status helrm_comm_unique_id(uint8_t* id);
+/* Create the context's communicator (NCCL is loaded at run time). */
+helrm_status helrm_comm_init(helrm_ctx* c, const uint8_t* id, int rank, int world);
+/* helrm_lookup with the giant steps split over the ranks: rank 0's inputs are
+ * broadcast (every rank passes buffers at the plan's level, e.g. from
+ * helrm_ct_alloc), each rank computes the partial Q_l P accumulators of its
+ * giant range, ncclAllReduce(uint64, sum) + a mod-q kernel combine them, and
+ * every rank finishes (ModDown, rescale, RotSum).  Bit-identical to
+ * helrm_lookup for every world size (only exact modular sums are split). */
+helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                               size_t batch, helrm_ct** out);
+
 const char* helrm_last_error(void);
 const char* helrm_version(void);
 

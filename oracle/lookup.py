@@ -360,13 +360,29 @@ def rot_sum(P: Params, ct: Ciphertext, mbar: int, rk) -> Ciphertext:
 def lookup(P: Params, plan: Plan, u_ntt: List[np.ndarray], rk, cts: List[Ciphertext]) -> List[Ciphertext]:
     if len(cts) != plan.C:
         raise ValueError("HELRM_ERR_LAYOUT")
-    l = plan.level
     for ct in cts:
-        if ct.level != l:
+        if ct.level != plan.level:
             raise ValueError("HELRM_ERR_LEVEL")
     if plan.mode == MODE_SINGLE:
         return _lookup_single(P, plan, u_ntt, rk, cts)
+    O = lookup_partial(P, plan, u_ntt, rk, cts, 0, None)
+    return lookup_finish(P, plan, rk, O, cts[0].scale)
+
+
+def giant_pairs(plan: Plan) -> List[Tuple[int, int]]:
+    """The non-empty (o, i) giant pairs in (o, i) order -- the unit D23 splits."""
+    return [(o, i) for o in range(plan.O) for i, ent in enumerate(plan.entries[o]) if ent]
+
+
+def lookup_partial(P: Params, plan: Plan, u_ntt, rk, cts: List[Ciphertext], z_lo: int, z_hi: Optional[int]):
+    """D20 L1-L4 restricted to the giant pairs z in [z_lo, z_hi) of
+    giant_pairs(plan): returns the Q_l P accumulators (O0, O1) per output
+    block.  Over all pairs this is the lookup up to L5; the partial results of
+    a split sum exactly to it (D23)."""
+    l = plan.level
     qp = P.qp(l)
+    pairs = giant_pairs(plan)
+    mine = set(pairs[z_lo:z_hi] if z_hi is not None else pairs[z_lo:])
     # L1: D^c_k = ModUp_k(c1^c)
     D = [[core.modup(P, ct.c1, l, k) for k in range(P.dnum(l))] for ct in cts]
     # L2: baby steps (a, b)^c_j over Q_l P, lazy (no ModDown)
@@ -384,7 +400,7 @@ def lookup(P: Params, plan: Plan, u_ntt: List[np.ndarray], rk, cts: List[Ciphert
         O0 = np.zeros((len(qp), P.N), dtype=np.uint64)
         O1 = np.zeros_like(O0)
         for i, ent in enumerate(plan.entries[o]):
-            if not ent:
+            if not ent or (o, i) not in mine:
                 continue
             # L3: (A, B)_{o,i} = sum_c sum_j u_{o,c,i,j} (.) (a, b)^c_j
             A = np.zeros_like(O0)
@@ -404,14 +420,22 @@ def lookup(P: Params, plan: Plan, u_ntt: List[np.ndarray], rk, cts: List[Ciphert
                 G0, G1 = core.keyswitch(P, Bp, g, rk, l)
                 O0 = core.vadd(O0, core.vadd(core.automorph_ntt(A, g, P.N), G0, qp), qp)
                 O1 = core.vadd(O1, G1, qp)
-        # L6: ModDown both halves; scale Delta q_l
-        ct = Ciphertext(core.moddown(P, O0, l), core.moddown(P, O1, l), l, Fraction(cts[0].scale) * P.q[l])
-        # L7: rescale -> level l-1, scale Delta;  L8: RotSum when mbar < n
+        outs.append((O0, O1))
+    return outs
+
+
+def lookup_finish(P: Params, plan: Plan, rk, O, scale) -> List[Ciphertext]:
+    """D20 L6-L8 per output block: ModDown both halves (scale Delta q_l),
+    rescale (scale Delta), RotSum when mbar < n."""
+    l = plan.level
+    res = []
+    for (O0, O1) in O:
+        ct = Ciphertext(core.moddown(P, O0, l), core.moddown(P, O1, l), l, Fraction(scale) * P.q[l])
         ct = core.rescale(P, ct)
         if plan.mbar < P.n:
             ct = rot_sum(P, ct, plan.mbar, rk)
-        outs.append(ct)
-    return outs
+        res.append(ct)
+    return res
 
 
 def _lookup_single(P: Params, plan: Plan, u_ntt, rk, cts):

@@ -91,6 +91,8 @@ struct helrm_ctx {
 
   Profiler prof;
   std::string prof_json;
+  ncclComm_t comm = nullptr;      // helrm_comm_init
+  int rank = 0, world = 1;
 
   DevCtx dc() { return DevCtx{dprimes, dslotpos, dgrp, deinv, P.log_n, P.N, stream, &launches, &prof}; }
 
@@ -656,6 +658,7 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
 void helrm_ctx_destroy(helrm_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
+  if (c->comm) nccl().commDestroy(c->comm);
   for (void* p : c->owned) cudaFreeAsync(p, c->stream);
   cudaStreamSynchronize(c->stream);
   delete c;
@@ -1302,12 +1305,17 @@ struct MacList {
 }  // extern "C" (templates below)
 
 template <class XF>
-static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr) {
+static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int64_t z_lo = 0,
+                          int64_t z_hi = INT64_MAX) {
   MacList ml;
+  int64_t zg = 0;   // global index of the non-empty (o, i) pairs
   for (int64_t o = 0; o < pl->O; o++) {
     std::vector<int64_t> gi;
     for (size_t i = 0; i < pl->entries[o].size(); i++)
-      if (!pl->entries[o][i].empty()) gi.push_back((int64_t)i);
+      if (!pl->entries[o][i].empty()) {
+        if (zg >= z_lo && zg < z_hi) gi.push_back((int64_t)i);
+        zg++;
+      }
     for (size_t g0 = 0; g0 < gi.size(); g0 += kGiantPack) {
       const int ng = (int)std::min<size_t>(kGiantPack, gi.size() - g0);
       const int z0 = (int)ml.oi.size();
@@ -1349,9 +1357,12 @@ static void run_macs(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_
                   (int)ml.oi.size(), out, out_stride, map, x_split);
 }
 
-// D20: the double-hoisted BSGS lookup of one query (C input cts -> O outputs)
-static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
-                          helrm_ct** out) {
+// D20 L1-L4 for the giant pairs z in [z_lo, z_hi) of the non-empty (o, i)
+// enumeration: accumulates into O [pl->O][2][l+1+K][N] (zeroed by the caller).
+// With z over everything this is the whole lookup up to L5; split over ranks
+// the partial O's sum exactly to the full one (D23).
+static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk,
+                               const helrm_ct* const* in, int64_t z_lo, int64_t z_hi, uint64_t* Oall) {
   const Params& P = c->P;
   const uint32_t l = pl->level;
   const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
@@ -1400,15 +1411,17 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
   const MacList ml = build_macs(pl, nlN, [&](int ci, int j) {
     uint64_t* a = ab[ci].at(j);
     return std::make_pair((const uint64_t*)a, (const uint64_t*)(a + nlN));
-  });
+  }, z_lo, z_hi);
   const int n_out = (int)ml.oi.size();
+  if (n_out == 0) return;
   DBuf AB(c, (size_t)n_out * 2 * nlN);
   run_macs(c, ml, AB.p, 2 * nlN, mqp, true);
   // L4 (hoist #2) per output block: batched ModDown of every rotating B,
   // batched ModUp of the results, then one fused (phi(A) + KS) per giant
-  DBuf O(c, 2 * nlN);
   for (int64_t o = 0; o < pl->O; o++) {
-    HCUDA(cudaMemsetAsync(O.p, 0, 2 * nlN * 8, c->stream));
+    struct {
+      uint64_t* p;
+    } O{Oall + (size_t)o * 2 * nlN};
     std::vector<int> rot_idx;
     for (int z = 0; z < n_out; z++) {
       if (ml.oi[z].first != o) continue;
@@ -1435,14 +1448,41 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
       }
       r0 = r1;
     }
-    // L6 ModDown both halves (scale Delta q_l), L7 rescale, L8 RotSum
+  }
+}
+
+// D20 L6-L8 per output block: ModDown both halves (scale Delta q_l),
+// rescale (scale Delta), RotSum when mbar < n
+static void lookup_finish(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* Oall,
+                          double scale, helrm_ct** out) {
+  const Params& P = c->P;
+  const uint32_t l = pl->level;
+  const size_t N = P.N, nq = l + 1, nlN = (size_t)(l + 1 + P.K) * N;
+  for (int64_t o = 0; o < pl->O; o++) {
     DBuf r(c, 2 * nq * N);
-    moddown_batch(c, O.p, nlN, 2, l, r.p, nq * N);
-    helrm_ct* s = new_ct(c, l - 1, in[0]->scale);
+    moddown_batch(c, Oall + (size_t)o * 2 * nlN, nlN, 2, l, r.p, nq * N);
+    helrm_ct* s = new_ct(c, l - 1, scale);
     rescale_ct(c, r.p, l, s->d);
     rot_sum(c, s, pl->mbar, rk);
     out[o] = s;
   }
+}
+
+static int64_t count_pairs(const helrm_plan* pl) {
+  int64_t n = 0;
+  for (auto& eo : pl->entries)
+    for (auto& e : eo) n += !e.empty();
+  return n;
+}
+
+// D20: the double-hoisted BSGS lookup of one query (C input cts -> O outputs)
+static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                          helrm_ct** out) {
+  const size_t nlN = (size_t)(pl->level + 1 + c->P.K) * c->P.N;
+  DBuf O(c, (size_t)pl->O * 2 * nlN);
+  HCUDA(cudaMemsetAsync(O.p, 0, (size_t)pl->O * 2 * nlN * 8, c->stream));
+  lookup_double_part(c, pl, rk, in, 0, INT64_MAX, O.p);
+  lookup_finish(c, pl, rk, O.p, in[0]->scale, out);
 }
 
 // D22: single-hoisted cross-check mode (full rotations in Q_l)
@@ -1590,6 +1630,76 @@ helrm_status helrm_ct_random(helrm_ctx* c, uint64_t seed, uint32_t ct_index, uin
     for (int poly = 0; poly < 2; poly++)
       launch_sample_uniform_ntt(c->dc(), ct->d + (size_t)poly * (level + 1) * c->P.N, m, seed, 9, ct_index, poly, m);
     *out = ct;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU (D23): giant-range partition + uint64 all-reduce
+// ---------------------------------------------------------------------------
+helrm_status helrm_dist_range(int64_t n_items, int world, int rank, int64_t* lo, int64_t* hi) {
+  return guard([&] {
+    need(lo && hi && world >= 1 && rank >= 0 && rank < world && n_items >= 0, HELRM_ERR_ARG, "bad argument");
+    // contiguous, as even as possible: the first (n mod world) ranks get one more
+    const int64_t q = n_items / world, r = n_items % world;
+    *lo = rank * q + std::min<int64_t>(rank, r);
+    *hi = *lo + q + (rank < r ? 1 : 0);
+  });
+}
+
+helrm_status helrm_comm_unique_id(uint8_t* id) {
+  return guard([&] {
+    need(id, HELRM_ERR_ARG, "null argument");
+    ncclUniqueId u;
+    HNCCL(nccl().getUniqueId(&u));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+  });
+}
+
+helrm_status helrm_comm_init(helrm_ctx* c, const uint8_t* id, int rank, int world) {
+  return guard([&] {
+    need(c && id && world >= 1 && rank >= 0 && rank < world, HELRM_ERR_ARG, "bad argument");
+    HCUDA(cudaSetDevice(c->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    if (c->comm) nccl().commDestroy(c->comm);
+    c->comm = nullptr;
+    HNCCL(nccl().commInitRank(&c->comm, world, u, rank));
+    c->rank = rank;
+    c->world = world;
+  });
+}
+
+helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                               size_t batch, helrm_ct** out) {
+  if (out)
+    for (size_t i = 0; i < batch * (p ? p->O : 0); i++) out[i] = nullptr;
+  return guard([&] {
+    need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
+    need(p->mode == HELRM_MODE_DOUBLE, HELRM_ERR_ARG, "the distributed lookup runs the double-hoisted mode");
+    for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
+    const Params& P = c->P;
+    const size_t nlN = (size_t)(p->level + 1 + P.K) * P.N;
+    int64_t lo = 0, hi = INT64_MAX;
+    (void)helrm_dist_range(count_pairs(p), c->world, c->rank, &lo, &hi);
+    for (size_t q = 0; q < batch; q++) {
+      const helrm_ct* const* cin = in + q * p->C;
+      for (int64_t ci = 0; ci < p->C; ci++) {
+        need(cin[ci] != nullptr && cin[ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's");
+        if (c->world > 1)   // the query lives on rank 0: broadcast it (in place on every rank's buffer)
+          HNCCL(nccl().broadcast(cin[ci]->d, cin[ci]->d, (size_t)2 * (p->level + 1) * P.N, ncclUint64, 0, c->comm,
+                                 c->stream));
+      }
+      DBuf O(c, (size_t)p->O * 2 * nlN);
+      HCUDA(cudaMemsetAsync(O.p, 0, (size_t)p->O * 2 * nlN * 8, c->stream));
+      lookup_double_part(c, p, rk, cin, lo, hi, O.p);
+      if (c->world > 1) {
+        // L5: exact sum of the partial accumulators (each < q, so < world q < 2^64), then mod q
+        HNCCL(nccl().allReduce(O.p, O.p, (size_t)p->O * 2 * nlN, ncclUint64, ncclSum, c->comm, c->stream));
+        for (int64_t h = 0; h < 2 * p->O; h++) launch_modred(c->dc(), O.p + (size_t)h * nlN, P.map_qp(p->level));
+      }
+      lookup_finish(c, p, rk, O.p, cin[0]->scale, out + q * p->O);
+    }
   });
 }
 

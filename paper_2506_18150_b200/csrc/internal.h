@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "arith.cuh"
 #include "../../include/helrm.h"
 
@@ -83,6 +85,25 @@ struct Params {
     return m;
   }
 };
+
+// NCCL, resolved at run time (nccl_dl.cpp)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl();
+#define HNCCL(x)                                                                                       \
+  do {                                                                                                 \
+    ncclResult_t r_ = (x);                                                                             \
+    if (r_ != ncclSuccess)                                                                             \
+      throw ::helrm::Error(HELRM_ERR_NCCL, std::string(#x) + ": " + ::helrm::nccl().getErrorString(r_)); \
+  } while (0)
 
 // host math (host_math.cpp)
 bool is_prime_u64(uint64_t n);
@@ -170,6 +191,8 @@ void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const L
                       int accumulate);
 void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
                       size_t os, int G, const LimbMap& map, const uint64_t* s, const uint64_t* sp);
+// out[l] = in[l] mod q_l for in < 2^64 (after a uint64 sum all-reduce)
+void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map);
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,
                          const LimbMap& map);
 

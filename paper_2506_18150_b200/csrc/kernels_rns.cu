@@ -386,6 +386,19 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   }
 }
 
+// D20 L5: after ncclAllReduce(uint64, sum) of partial Q_l P accumulators
+// (each < q, at most 2^13 ranks -> no wrap), reduce every word mod its prime
+__global__ void k_modred(uint64_t* __restrict__ x, const PrimeDev* __restrict__ primes,
+                         const __grid_constant__ LimbMap map, uint32_t N) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  if (i >= N) return;
+  const RedConst rc = primes[map.pr[l]].rc;
+  const size_t o = (size_t)l * N + i;
+  const uint64_t v = x[o];
+  x[o] = v - mulhi64(v, rc.mu) * rc.q >= rc.q ? v - mulhi64(v, rc.mu) * rc.q - rc.q : v - mulhi64(v, rc.mu) * rc.q;
+}
+
 // ---------------- launchers ----------------
 static dim3 grid_for(uint32_t N, int limbs) { return dim3((N + kT - 1) / kT, limbs); }
 
@@ -460,6 +473,13 @@ void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint6
   ProfScope ps_(c, "sub_scale", 24.0 * c.N * map.n * G);
   k_sub_scale<<<dim3((c.N + kT - 1) / kT, map.n, G), kT, 0, c.stream>>>(y, ys, t, ts, out, os, c.primes, map, c.N, s,
                                                                         sp);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+}
+
+void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map) {
+  ProfScope ps_(c, "modred", 16.0 * c.N * map.n);
+  k_modred<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(x, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }

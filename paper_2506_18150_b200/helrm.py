@@ -97,6 +97,10 @@ _SIGS = {
     "helrm_rescale": [_vp, _vp, _pp],
     "helrm_rotate": [_vp, _vp, _vp, _i64, _pp],
     "helrm_rotate_hoisted": [_vp, _vp, _vp, _i64p, _sz, _pp, _sz],
+    "helrm_dist_range": [_i64, ctypes.c_int, ctypes.c_int, _i64p, _i64p],
+    "helrm_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
+    "helrm_comm_init": [_vp, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int],
+    "helrm_lookup_dist": [_vp, _vp, _vp, _pp, _sz, _pp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_L, _name)
@@ -120,7 +124,8 @@ _L.helrm_rotkeys_bytes.restype = _sz
 EXPORTED = sorted(list(_SIGS) + ["helrm_params_destroy", "helrm_ctx_destroy", "helrm_sk_destroy", "helrm_pk_destroy",
                                  "helrm_rotkeys_destroy", "helrm_tables_destroy", "helrm_ct_destroy",
                                  "helrm_plan_destroy", "helrm_last_error", "helrm_version", "helrm_ctx_launches",
-                                 "helrm_rotkeys_bytes", "helrm_ctx_profile", "helrm_ctx_profile_json"])
+                                 "helrm_rotkeys_bytes", "helrm_ctx_profile", "helrm_ctx_profile_json", "helrm_dist_range",
+                                 "helrm_comm_unique_id", "helrm_comm_init", "helrm_lookup_dist"])
 
 
 def _check(code: int):
@@ -451,3 +456,30 @@ def rotate_hoisted(ctx: Context, rk: RotKeys, ct: Ciphertext, amounts: Sequence[
     a = np.ascontiguousarray(np.array(list(amounts), dtype=np.int64))
     r = (ctypes.c_void_p * len(ring))(*[c.h for c in ring])
     _check(_L.helrm_rotate_hoisted(ctx.h, rk.h, ct.h, a.ctypes.data_as(_i64p), a.size, r, len(ring)))
+
+
+# ---------------------------------------------------------------- multi-GPU
+def dist_range(n_items: int, world: int, rank: int):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(_L.helrm_dist_range(n_items, world, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_L.helrm_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init(ctx: Context, uid: bytes, rank: int, world: int):
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(_L.helrm_comm_init(ctx.h, buf, rank, world))
+
+
+def lookup_dist(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Ciphertext], batch: int = 1) -> List[Ciphertext]:
+    info = plan.info()
+    assert len(cts) == batch * info.n_in_cts
+    ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
+    outs = (ctypes.c_void_p * (batch * info.n_out_cts))()
+    _check(_L.helrm_lookup_dist(ctx.h, plan.h, rk.h, ins, batch, outs))
+    return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]

@@ -320,3 +320,27 @@ def test_llm_full_size_plan_and_decryption(torch_mod):
     y = lk.gather(lay, w.indices[0])
     z = np.concatenate([E.h.decrypt_decode(E.ctx, sk, o) for o in outs[0]])
     assert np.abs(z[: lay.M] - y).max() < 1e-3
+
+
+@gpu
+@pytest.mark.parametrize("name", ["uci", "llm_small"])
+def test_lookup_dist_single_rank_matches_lookup(name, torch_mod):
+    """helrm_lookup_dist on a 1-rank NCCL communicator (the only GPU a gpurun
+    box has) runs the partitioned code path (broadcast, partial accumulators,
+    finish) and must equal helrm_lookup bit for bit; the 2-rank split itself
+    is covered on CPU by tests/test_dist_cpu.py."""
+    E = env(name, torch_mod)
+    h, cfg = E.h, E.cfg
+    w = synth.make_workload(name)
+    plan, sk, outs = _gpu_lookup(E, w)
+    h.comm_init(E.ctx, h.comm_unique_id(), 0, 1)
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N), cfg.seed)
+    info = plan.info()
+    x = h.encode_query(T, w.indices[0], w.dense[0], info.n_in_cts * cfg.n_slots)
+    cts = [h.encrypt(E.ctx, pk, x[c * cfg.n_slots:(c + 1) * cfg.n_slots], cfg.level,
+                     (cfg.seed << 20) | c) for c in range(info.n_in_cts)]
+    got = h.lookup_dist(E.ctx, plan, rk, cts)
+    for a, b in zip(got, outs[0]):
+        assert np.array_equal(h.ct_export(E.ctx, a), h.ct_export(E.ctx, b))
