@@ -35,6 +35,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
@@ -313,6 +314,8 @@ def run_gpu(args, world, rank, local):
            "path": "helrm_ct_import (pinned host, coefficient form) -> helrm_lookup -> helrm_ct_export"}
 
     secondary = {}
+    if world > 1 or args.dist:
+        secondary["dist_b1"] = dist_b1(args, ctx, helrm, torch, stream, plan, rk, cts, world, rank)
     if not args.skip_micro:
         secondary = micro(args, ctx, helrm, torch, stream, sk, cfg, world)
 
@@ -328,6 +331,34 @@ def helrm_ct_export_into(helrm, ctx, ct, host: np.ndarray):
     import ctypes
     helrm._check(helrm._L.helrm_ct_export(ctx.h, ct.h, host.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                          host.size))
+
+
+def dist_b1(args, ctx, helrm, torch, stream, plan, rk, cts, world, rank):
+    """One query split over all ranks (giant-range partition, NCCL uint64
+    all-reduce + mod q; helrm_lookup_dist): device time per lookup, max over
+    ranks.  Rank 0's query is broadcast into every rank's buffer."""
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(helrm.comm_unique_id()), dtype=torch.uint8).cuda())
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast(uid, 0)
+    helrm.comm_init(ctx, bytes(uid.cpu().numpy().tobytes()), rank, world)
+    for _ in range(args.warmup):
+        for o in helrm.lookup_dist(ctx, plan, rk, [cts[0]]):
+            o.close()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        for o in helrm.lookup_dist(ctx, plan, rk, [cts[0]]):
+            o.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+    return {"ms_per_lookup": round(ms, 4), "lookups_per_s": round(1e3 / ms, 3), "world": world,
+            "partition": "giant range per rank, NCCL allreduce(uint64, sum) + mod-q kernel"}
 
 
 def micro(args, ctx, helrm, torch, stream, sk, cfg, world):
@@ -397,6 +428,7 @@ def main():
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--micro-cts", type=int, default=1024)
     ap.add_argument("--rot-cts", type=int, default=8)
+    ap.add_argument("--dist", action="store_true", help="also time the partitioned batch-1 lookup at world size 1")
     ap.add_argument("--ncu-step", action="store_true", help="profile one lookup in a cudaProfiler range and exit")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
