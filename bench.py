@@ -68,7 +68,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -317,7 +317,7 @@ def run_gpu(args, world, rank, local):
     if world > 1 or args.dist:
         secondary["dist_b1"] = dist_b1(args, ctx, helrm, torch, stream, plan, rk, cts, world, rank)
     if not args.skip_micro:
-        secondary = micro(args, ctx, helrm, torch, stream, sk, cfg, world)
+        secondary.update(micro(args, ctx, helrm, torch, stream, sk, cfg, world))
 
     return {
         "value": value, "ms": ms / args.steps, "launches": launches, "clocks": clk.summary(),

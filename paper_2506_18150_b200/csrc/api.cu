@@ -67,7 +67,8 @@ struct LevelConst {
   // fused base conversions (D14 inside the NTT): INTT post-factors
   // N^-1 [(B/b)^-1]_b (y-form) and per-output-row coefficient tables
   double2* modup_post = nullptr;   // [l+1]
-  ConvRowDev* modup_tab = nullptr; // [dnum(l)][l+1+K]
+  ConvRowDev* modup_tab = nullptr; // [dnum(l)][modup_rows]: the rows outside digit k
+  int modup_rows = 0;
   double2* moddown_post = nullptr; // [K]
   ConvRowDev* moddown_tab = nullptr; // [l+1]
 };
@@ -85,6 +86,7 @@ struct helrm_ctx {
   uint64_t* dcdt = nullptr;
   uint64_t* scratch = nullptr;
   std::map<int, LevelConst> lconst;
+  std::map<std::pair<int, int>, uint32_t*> modup_lidx;   // (level, G) -> NTT limb table of modup_batch
   std::vector<void*> owned;       // device allocations freed at destroy
   uint64_t launches = 0;
   std::vector<uint32_t> dlog5;    // dlog5[g] for odd g < 2N (0xffffffff if not a power of 5)
@@ -262,7 +264,12 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
     };
     auto pair = [&](uint64_t w, uint64_t q) { return make_double2((double)w, (double)w / (double)q); };
     std::vector<double2> upost(l + 1), dpost(P.K);
-    std::vector<ConvRowDev> utab((size_t)dn * nl), dtab(l + 1);
+    // rows outside digit k (the digit's own limbs are copied, not converted)
+    uint32_t min_dig = P.alpha;
+    for (uint32_t k = 0; k < dn; k++) min_dig = std::min(min_dig, std::min((k + 1) * P.alpha, l + 1) - k * P.alpha);
+    const uint32_t urows = nl - min_dig;
+    lc.modup_rows = (int)urows;
+    std::vector<ConvRowDev> utab((size_t)dn * urows), dtab(l + 1);
     for (uint32_t k = 0; k < dn; k++) {
       std::vector<uint32_t> B;
       const uint32_t lo = k * P.alpha, hi = std::min((k + 1) * P.alpha, l + 1);
@@ -272,19 +279,30 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
         const uint64_t binv = inv_mod(hat_mod(B, b, q), q);
         upost[B[b]] = pair(mulm(inv_mod(P.N % q, q), binv, q), q);
       }
+      uint32_t j = 0;
       for (uint32_t r = 0; r < nl; r++) {
-        ConvRowDev& cr = utab[(size_t)k * nl + r];
+        if (r >= lo && r < hi) continue;
+        ConvRowDev& cr = utab[(size_t)k * urows + j++];
         cr = ConvRowDev{};
         cr.src_row0 = (int)lo;
         cr.nb = (int)B.size();
+        cr.out_row = (int)r;
         const uint64_t qr = P.primes[P.qp_chain(l, r)];
         cr.q = (double)qr;
         cr.qinv = 1.0 / (double)qr;
         for (size_t b = 0; b < B.size(); b++) {
-          const uint64_t w = (r >= lo && r < hi) ? ((r - lo == b) ? hat_mod(B, b, qr) : 0)  // undo the y-form factor
-                                                 : hat_mod(B, b, qr);                         // (B/b) mod q_r
+          const uint64_t w = hat_mod(B, b, qr);   // (B/b) mod q_r
           cr.cf[b] = make_double2((double)w, (double)w / (double)qr);
         }
+      }
+      for (; j < urows; j++) {   // padding rows (a digit with fewer primes than alpha has more outside rows)
+        ConvRowDev& cr = utab[(size_t)k * urows + j];
+        cr = ConvRowDev{};
+        cr.src_row0 = (int)lo;
+        cr.nb = (int)B.size();
+        cr.out_row = -1;
+        cr.q = 1.0;
+        cr.qinv = 1.0;
       }
     }
     std::vector<uint32_t> PB;
@@ -298,6 +316,7 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
       cr = ConvRowDev{};
       cr.src_row0 = 0;
       cr.nb = (int)P.K;
+      cr.out_row = (int)r;
       const uint64_t qr = P.primes[r];
       cr.q = (double)qr;
       cr.qinv = 1.0 / (double)qr;
@@ -331,17 +350,51 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
 // NTT form) -> out [G][dnum][l+1+K][N] (NTT form).  One INTT of the G (l+1)
 // limbs into y-form, one fused conversion + NTT over every output limb (the
 // digit's own limbs go through INTT/NTT unchanged: a bit-exact copy).
+// NTT limb table of modup_batch: every (g, k, r) with r outside digit k, as
+// layout limb (g dnum + k)(l+1+K) + r of out (cached per (level, G))
+static const uint32_t* modup_lidx(helrm_ctx* c, uint32_t l, int G, size_t* count) {
+  const Params& P = c->P;
+  const uint32_t nl = l + 1 + P.K, dn = P.dnum(l);
+  std::vector<uint32_t> v;
+  for (int g = 0; g < G; g++)
+    for (uint32_t k = 0; k < dn; k++) {
+      const uint32_t lo = k * P.alpha, hi = std::min((k + 1) * P.alpha, l + 1);
+      for (uint32_t r = 0; r < nl; r++)
+        if (r < lo || r >= hi) v.push_back(((uint32_t)g * dn + k) * nl + r);
+    }
+  *count = v.size();
+  auto key = std::make_pair((int)l, G);
+  auto it = c->modup_lidx.find(key);
+  if (it != c->modup_lidx.end()) return it->second;
+  uint32_t* d = (uint32_t*)c->dalloc(v.size() * 4);
+  HCUDA(cudaMemcpyAsync(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  HCUDA(cudaStreamSynchronize(c->stream));
+  c->owned.push_back(d);
+  c->modup_lidx.emplace(key, d);
+  return d;
+}
+
 static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int G, uint32_t l, uint64_t* out) {
   const Params& P = c->P;
   const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, dn = P.dnum(l);
   const LevelConst& lc = level_const(c, l);
+  if (in_stride == 0) in_stride = nq * N;
+  size_t n_conv = 0;
+  const uint32_t* lidx = modup_lidx(c, l, G, &n_conv);
   DBuf y(c, G * nq * N);
-  // INTT straight into y-form (times [(Q_k/q_i)^-1]_{q_i}), one conversion
-  // launch over (g, digit) writing every output row, one NTT over all of them
+  // D15 step 1: INTT straight into y-form (times [(Q_k/q_i)^-1]_{q_i});
+  // step 2: one conversion launch over (g, digit) writing the rows outside
+  // the digit; step 3: one NTT over exactly those limbs.  The digit's own
+  // limbs are copied unchanged (NTT form).
   launch_ntt_inv(c->dc(), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post);
-  launch_conv_rows(c->dc(), lc.modup_tab, (int)dn, (int)nl, (int)P.alpha, y.p, nq * N, out, dn * nl * N, nl * N, G,
-                   P.map_qp(l));
-  launch_ntt_fwd(c->dc(), out, out, c->scratch, G * dn * nl, P.map_qp(l), 0, 0, true);
+  launch_conv_rows(c->dc(), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
+                   nl * N, G, P.map_qp(l));
+  launch_ntt_fwd(c->dc(), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
+  for (size_t k = 0; k < dn; k++) {
+    const size_t lo = k * P.alpha, hi = std::min<size_t>((k + 1) * P.alpha, l + 1);
+    HCUDA(cudaMemcpy2DAsync(out + k * nl * N + lo * N, dn * nl * N * 8, in + lo * N, in_stride * 8, (hi - lo) * N * 8,
+                            G, cudaMemcpyDeviceToDevice, c->stream));
+  }
 }
 
 // D16 for G polynomials: y_g = y + g ys ([l+1+K][N]) -> out_g = out + g os ([l+1][N])
@@ -495,6 +548,7 @@ helrm_status helrm_params_create(const helrm_params_desc* d, helrm_params** out)
     P.L = (uint32_t)q.size() - 1;
     P.K = (uint32_t)p.size();
     P.alpha = P.K;
+    need(P.dnum(P.L) <= 7, HELRM_ERR_CONFIG, "dnum = ceil((L+1)/K) must be <= 7 (key-switch kernels)");
     P.log_scale = d->log_scale;
     need(d->log_scale >= 1 && d->log_scale < 62, HELRM_ERR_CONFIG, "bad log_scale");
     P.primes = q;
@@ -808,7 +862,7 @@ helrm_status helrm_rotkeys_gen(helrm_ctx* c, const helrm_sk* sk, const uint64_t*
         launch_scalar_mul(c->dc(), phis.p + lo * N, t.p, dm, lc.pmod + lo, lc.pmods + lo);
         launch_binary(c->dc(), 0, b + lo * N, t.p, b + lo * N, dm);
       }
-      launch_split(c->dc(), key, rk->words_per_key, 1);   // keys live in split form (streaming MACs)
+      launch_dform(c->dc(), key, rk->words_per_key, m, 1);   // keys live in D-form (FP64 MACs)
     }
     HCUDA(cudaStreamSynchronize(c->stream));
     *out = rk;
@@ -853,7 +907,7 @@ helrm_status helrm_rotkeys_export(helrm_ctx* c, const helrm_rotkeys* r, uint64_t
     const Params& P = c->P;
     DBuf tmp(c, r->words_per_key);
     HCUDA(cudaMemcpyAsync(tmp.p, key_for(r, g), r->words_per_key * 8, cudaMemcpyDeviceToDevice, c->stream));
-    launch_split(c->dc(), tmp.p, r->words_per_key, 0);
+    launch_dform(c->dc(), tmp.p, r->words_per_key, P.map_range(0, P.L + 1 + P.K), 0);
     export_ntt(c, tmp.p, 2 * P.dnum(P.L), P.map_range(0, P.L + 1 + P.K), coeff);
   });
 }
@@ -1225,7 +1279,7 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
         launch_reduce_signed(c->dc(), (const int64_t*)(dcoef.p + k * N), dst, m);
       }
       ntt_fwd(c, pl->diag + (size_t)u0 * pl->nl * N, pl->diag + (size_t)u0 * pl->nl * N, (size_t)cnt * pl->nl, m);
-      launch_split(c->dc(), pl->diag + (size_t)u0 * pl->nl * N, (size_t)cnt * pl->nl * N, 1);  // stored split
+      launch_dform(c->dc(), pl->diag + (size_t)u0 * pl->nl * N, (size_t)cnt * pl->nl * N, m, 1);  // stored in D-form
     }
     HCUDA(cudaStreamSynchronize(c->stream));
     *out = pl;
@@ -1299,7 +1353,7 @@ struct MacList {
   std::vector<MacTerm> terms;
   std::vector<int4> groups;
   std::vector<std::pair<int64_t, int64_t>> oi;   // (o, i) of each output pair
-  double n_u = 0, n_x = 0;
+  double n_u = 0, n_x = 0;   // plaintext limb-sets read, distinct baby pairs read
 };
 
 }  // extern "C" (templates below)
@@ -1308,6 +1362,7 @@ template <class XF>
 static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int64_t z_lo = 0,
                           int64_t z_hi = INT64_MAX) {
   MacList ml;
+  std::set<std::pair<int, int>> xs;   // distinct (c, j) baby pairs
   int64_t zg = 0;   // global index of the non-empty (o, i) pairs
   for (int64_t o = 0; o < pl->O; o++) {
     std::vector<int64_t> gi;
@@ -1336,10 +1391,13 @@ static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int
         }
       }
       ml.groups.push_back(make_int4((int)ml.terms.size(), (int)tm.size(), z0, ng));
-      for (auto& kv : tm) ml.terms.push_back(kv.second);
-      ml.n_x += (double)tm.size();
+      for (auto& kv : tm) {
+        ml.terms.push_back(kv.second);
+        xs.insert(kv.first);
+      }
     }
   }
+  ml.n_x = (double)xs.size();
   return ml;
 }
 
@@ -1347,14 +1405,14 @@ extern "C" {
 
 // upload the list and run the batched MAC into out (pair z at out + z out_stride)
 static void run_macs(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_stride, const LimbMap& map,
-                     bool x_split) {
+                     bool x_dform) {
   DBuf dterms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), dgroups(c, 2 * ml.groups.size() + 1);
   HCUDA(cudaMemcpyAsync(dterms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
                         c->stream));
   HCUDA(cudaMemcpyAsync(dgroups.p, ml.groups.data(), ml.groups.size() * sizeof(int4), cudaMemcpyHostToDevice,
                         c->stream));
   launch_diag_mac(c->dc(), (const MacTerm*)dterms.p, (const int4*)dgroups.p, (int)ml.groups.size(), ml.n_u, ml.n_x,
-                  (int)ml.oi.size(), out, out_stride, map, x_split);
+                  (int)ml.oi.size(), out, out_stride, map, x_dform);
 }
 
 // D20 L1-L4 for the giant pairs z in [z_lo, z_hi) of the non-empty (o, i)
@@ -1392,7 +1450,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
       uint64_t* a = babies.p + bi++ * 2 * nlN;
       if (j == 0) {  // (P c0, P c1): Q limbs scaled by [P]_q, P limbs 0
         HCUDA(cudaMemsetAsync(a, 0, 2 * nlN * 8, c->stream));
-        launch_scalar_mul(c->dc(), ct_c0(ct), a, mq, lc.pmod, lc.pmods, 1);   // baby pairs are split
+        launch_scalar_mul(c->dc(), ct_c0(ct), a, mq, lc.pmod, lc.pmods, 1);   // baby pairs are in D-form
         launch_scalar_mul(c->dc(), ct_c1(ct), a + nlN, mq, lc.pmod, lc.pmods, 1);
       } else {
         need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");

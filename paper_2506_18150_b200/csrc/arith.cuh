@@ -72,40 +72,6 @@ HD uint64_t reduce128(uint64_t hi, uint64_t lo, const RedConst& c) {
 
 HD uint64_t mul_mod(uint64_t a, uint64_t b, const RedConst& c) { return reduce128(mulhi64(a, b), a * b, c); }
 
-// ---- "split" residues for streaming multiply-accumulates (q < 2^50) ----
-// x = x1 2^25 + x0 with x0, x1 < 2^25 is stored as (x1 << 32) | x0, so a
-// product of two residues is four 32x32 -> 64-bit IMAD.WIDE with 64-bit
-// accumulators c0 += x0 y0, c1 += x0 y1 + x1 y0, c2 += x1 y1 (each term
-// < 2^51: 8192 products fit), reduced once: x = c0 + c1 2^25 + c2 2^50.
-// Rotation keys, plaintext diagonals and the baby-step pairs live in this
-// form on the device.
-HD uint64_t to_split(uint64_t x) { return ((x >> 25) << 32) | (x & 0x1FFFFFFull); }
-HD uint64_t from_split(uint64_t s) { return ((s >> 32) << 25) | (s & 0xFFFFFFFFull); }
-
-struct Acc3 {
-  uint64_t c0 = 0, c1 = 0, c2 = 0;
-};
-
-HD void mac_split(Acc3& a, uint64_t xs, uint64_t ys) {
-  const uint32_t x0 = (uint32_t)xs, x1 = (uint32_t)(xs >> 32), y0 = (uint32_t)ys, y1 = (uint32_t)(ys >> 32);
-  a.c0 += (uint64_t)x0 * y0;
-  a.c1 += (uint64_t)x0 * y1;
-  a.c1 += (uint64_t)x1 * y0;
-  a.c2 += (uint64_t)x1 * y1;
-}
-
-// (c0 + c1 2^25 + c2 2^50) mod q
-HD uint64_t acc3_reduce(const Acc3& a, const RedConst& rc) {
-  uint64_t lo = a.c0, hi = 0;
-  uint64_t t = a.c1 << 25;
-  lo += t;
-  hi += (lo < t) + (a.c1 >> 39);
-  t = a.c2 << 50;
-  lo += t;
-  hi += (lo < t) + (a.c2 >> 14);
-  return reduce128(hi, lo, rc);
-}
-
 // counter-based SplitMix64 (D9): word(seed, stream, k) = SM((seed ^ SM(stream)) + (k+1) gamma)
 HD uint64_t sm_mix(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

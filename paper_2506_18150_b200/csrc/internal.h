@@ -51,10 +51,11 @@ struct LimbMap {
   uint8_t pr[kMaxLimbs];
 };
 
-// one output row of a base conversion: out = sum_b y_{row0+b} cf[b] mod q_out,
-// evaluated on the FP64 pipe: cf as (w, w / q_out) pairs
+// one output row of a base conversion: out[out_row] = sum_b y_{row0+b} cf[b]
+// mod q_out (out_row < 0: padding, nothing written), evaluated on the FP64
+// pipe: cf as (w, w / q_out) pairs
 struct ConvRowDev {
-  int src_row0, nb;
+  int src_row0, nb, out_row;
   double q, qinv;
   double2 cf[kMaxDigitPrimes];
 };
@@ -161,12 +162,14 @@ struct ProfScope {
 // src + (y / map.n) * src_stride + (y % map.n) * N (same for dst; stride 0 =
 // contiguous polys of map.n limbs).  src == dst allowed.
 // din: the source limbs hold centred integer-valued doubles (k_conv_rows output)
+// lidx (optional device table): launch limb v is layout limb lidx[v]
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0, bool din = false);
+                    const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0, bool din = false,
+                    const uint32_t* lidx = nullptr);
 // post (optional, per limb of map): final factor (w, w/q) replacing N^-1
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0,
-                    const double2* post = nullptr);
+                    const double2* post = nullptr, const uint32_t* lidx = nullptr);
 // D14 base conversion from y-form sources (coefficients times [(B/b)^-1]_b,
 // folded into the INTT): for polynomial g and conversion k, every output row
 // r of the table: out_gk[r] = sum_b y_g[row0 + b] cf_kr[b] mod q_r, written
@@ -184,9 +187,10 @@ void launch_sample_small(const DevCtx& c, int64_t* out, uint64_t base, int kind,
 // op 0: a + b, 1: a - b, 2: a * b, 3: -a
 void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, const LimbMap& map);
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
-                       const uint64_t* sp, int split_out = 0);
-// in place: dir 1 -> split form, dir 0 -> canonical
-void launch_split(const DevCtx& c, uint64_t* x, size_t n, int dir);
+                       const uint64_t* sp, int dform_out = 0);
+// in place: dir 1 -> D-form (fmath.cuh), dir 0 -> canonical; word i is in limb
+// (i / N) mod map.n of a repeating [map.n][N] layout
+void launch_dform(const DevCtx& c, uint64_t* x, size_t n, const LimbMap& map, int dir);
 void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
                       int accumulate);
 void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
@@ -200,7 +204,7 @@ struct KipArgs {
   const uint64_t* digits;     // digit k of the switched polynomial at digits + k digit_stride ([nl][N], NTT slot order)
   size_t digit_stride;
   int dnum;
-  const uint64_t* key;        // key for g: [digit][2][L+1+K][N], split form
+  const uint64_t* key;        // key for g: [digit][2][L+1+K][N], D-form
   size_t key_digit_stride;    // words between digits of the key
   size_t key_half_stride;     // words between b and a of a digit
   const uint64_t* add0;       // optional: out0 += mul_l phi(add0)[l] for l < add_rows
@@ -239,11 +243,13 @@ constexpr int kGiantPack = 4;
 struct MacTerm {
   const uint64_t* x0;         // [nl][N]
   const uint64_t* x1;
-  const uint64_t* u[kGiantPack];  // plaintext [nl][N] (split form) or null
+  const uint64_t* u[kGiantPack];  // plaintext [nl][N] (D-form) or null
 };
 // group z: terms [g.x, g.x + g.y), output pairs g.z .. g.z + g.w - 1, each
-// written to out + pair out_stride (A) and + nl N (B).  x split iff x_split.
+// written to out + pair out_stride (A) and + nl N (B).  u in D-form; x in
+// D-form iff x_dform (else canonical).
 void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
-                     double n_x_total, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map, bool x_split);
+                     double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
+                     bool x_dform);
 
 }  // namespace helrm

@@ -22,14 +22,21 @@
 // buffer of <= 32 MiB per chunk of limbs, which stays L2-resident: HBM sees
 // one read and one write per coefficient per transform.
 //
-// Butterfly arithmetic runs on the FP64 pipe (q < 2^51): residues are exact
-// integer-valued doubles, the product Y W = h + l is split exactly with an
-// FMA, the quotient k = rint(Y W / q) comes from one FMA against the
+// Butterfly arithmetic runs on the FP64 pipe (fmath.cuh, q < 2^51): residues
+// are exact integer-valued doubles, the product Y W = h + l is split exactly
+// with an FMA, the quotient k = rint(Y W / q) comes from one FMA against the
 // precomputed W/q (round-to-nearest via the 1.5 2^52 shift), and
 // r = (h - k q) + l is exact; values stay in (-2q, 2q) by centred
 // reductions.  Measured on B200: ~2.7x the modmul throughput of 64-bit
 // integer Shoup (profiles/r01_peak_int.txt).
+//
+// Limb selection: limb v of a launch is limb lidx[v] of the layout when a
+// device table is given (ModUp skips the digit's own limbs this way), else v.
+// (A prime-major variant whose pass-2 CTAs loop over several limbs of one
+// prime to reuse their twiddles measured slower on B200 -- 2 CTAs/SM instead
+// of 4 -- and was dropped, profiles/r01_ab_ntt.txt.)
 #include "internal.h"
+#include "fmath.cuh"
 
 namespace helrm {
 
@@ -38,33 +45,14 @@ constexpr int kEPT = 16;                     // elements per thread
 constexpr int kTileElems = 4096;             // elements per CTA
 constexpr int kThreads = kTileElems / kEPT;  // 256
 constexpr int kBlkPad = 256 + 16;            // pass-2 smem block stride (1 pad word per 16)
-constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-constexpr double kTwo52 = 4503599627370496.0;
+
+using fm::cred;
+using fm::d2u;
+using fm::mmul;
+using fm::u2d;
 
 __device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
 
-__device__ __forceinline__ double u2d(uint64_t x) {  // x < 2^52
-  return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - kTwo52;
-}
-__device__ __forceinline__ double rnd(double x) { return (x + kMagic) - kMagic; }  // |x| < 2^51
-// centred reduction: |x| < 2^51 q-multiples -> [-q/2, q/2]
-__device__ __forceinline__ double cred(double x, double q, double qi) {
-  const double k = __fma_rn(x, qi, kMagic) - kMagic;
-  return __fma_rn(-k, q, x);
-}
-// Y W mod q, exact, in [-q/2 - 1, q/2 + 1] (|Y| < 2^51)
-__device__ __forceinline__ double mmul(double y, double w, double wq, double q) {
-  const double h = y * w;
-  const double k = __fma_rn(y, wq, kMagic) - kMagic;
-  const double l = __fma_rn(y, w, -h);
-  return __fma_rn(-k, q, h) + l;
-}
-// canonical uint64 in [0, q) from an integer-valued double with |x| <= q
-__device__ __forceinline__ uint64_t d2u(double x, double q, double qi, uint64_t qint) {
-  x = cred(x, q, qi);
-  const long long v = (long long)(__double_as_longlong(x + kMagic) & 0xFFFFFFFFFFFFFull) - (1ll << 51);
-  return (uint64_t)(v < 0 ? v + (long long)qint : v);
-}
 __device__ __forceinline__ void ct_bfly(double& x, double& y, double2 w, double q) {
   const double r = mmul(y, w.x, w.y, q);
   const double a = x;
@@ -88,15 +76,17 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
-                                                      const uint8_t* __restrict__ einv) {
+                                                      const uint8_t* __restrict__ einv,
+                                                      const uint32_t* __restrict__ lidx) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   constexpr bool P1 = MODE != 1;  // MODE 2 = pass 1 whose input limbs are centred doubles (conversion output)
   __shared__ double sm[P1 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
-  const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
+  const size_t gl = lidx ? lidx[limb0 + limb] : limb0 + limb;
+  const PrimeDev& P = primes[map.pr[gl % map.n]];
   const double q = P.qd, qi = P.qinv;
-  const size_t gl = limb0 + limb, goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
+  const size_t goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
   const uint64_t* s = src + (P1 ? goff : limb * N);  // pass 1 reads the caller's limb
   uint64_t* d = dst + (P1 ? limb * N : goff);        // pass 2 writes the caller's limb
   const int tid = threadIdx.x;
@@ -205,14 +195,16 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv,
-                                                      const double2* __restrict__ post) {
+                                                      const double2* __restrict__ post,
+                                                      const uint32_t* __restrict__ lidx) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   __shared__ double sm[MODE == 0 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
-  const PrimeDev& P = primes[map.pr[(limb0 + limb) % map.n]];
+  const size_t gl = lidx ? lidx[limb0 + limb] : limb0 + limb;
+  const PrimeDev& P = primes[map.pr[gl % map.n]];
   const double q = P.qd, qi = P.qinv;
-  const size_t gl = limb0 + limb, goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
+  const size_t goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
   const uint64_t* s = src + (MODE == 1 ? goff : limb * N);  // pass A gathers the caller's limb
   uint64_t* d = dst + (MODE == 1 ? limb * N : goff);        // pass B writes the caller's limb
   const int tid = threadIdx.x;
@@ -306,44 +298,45 @@ size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)
 
 template <int SLOG>
 static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
-                      const LimbMap& map, size_t off, size_t ss, size_t ds, bool din) {
+                      const LimbMap& map, size_t off, size_t ss, size_t ds, bool din, const uint32_t* lidx) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
     auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
     k1<<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
-                                                 c.ntt_einv);
+                                                 c.ntt_einv, lidx);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
     k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv);
+                                                               c.ntt_grp, c.ntt_einv, lidx);
   }
   *c.launches += 2;
 }
 
 template <int SLOG>
 static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
-                      const LimbMap& map, size_t off, size_t ss, size_t ds, const double2* post) {
+                      const LimbMap& map, size_t off, size_t ss, size_t ds, const double2* post,
+                      const uint32_t* lidx) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
     k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, nullptr);
+                                                               c.ntt_grp, c.ntt_einv, nullptr, lidx);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
     k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                                  c.ntt_grp, c.ntt_einv, post);
+                                                                  c.ntt_grp, c.ntt_einv, post, lidx);
   }
   *c.launches += 2;
 }
 
 template <bool FWD>
 static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, const double2* post = nullptr, bool din = false) {
+                    const LimbMap& map, size_t ss, size_t ds, const double2* post, bool din, const uint32_t* lidx) {
   if (ss == 0) ss = (size_t)map.n * c.N;
   if (ds == 0) ds = (size_t)map.n * c.N;
   const size_t ch = chunk_limbs(c.N);
@@ -351,8 +344,8 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);
 #define HELRM_NTT_CASE(LG, SL)                                                  \
   case LG:                                                                      \
-    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din);    \
-    else inv_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, post);        \
+    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din, lidx);    \
+    else inv_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, post, lidx);        \
     break;
     switch (c.log_n) {
       HELRM_NTT_CASE(12, 4)
@@ -368,13 +361,13 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
 }
 
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, bool din) {
-  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din);
+                    const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx) {
+  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din, lidx);
 }
 
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, const double2* post) {
-  ntt_any<false>(c, src, dst, scratch, n_total, map, ss, ds, post);
+                    const LimbMap& map, size_t ss, size_t ds, const double2* post, const uint32_t* lidx) {
+  ntt_any<false>(c, src, dst, scratch, n_total, map, ss, ds, post, false, lidx);
 }
 
 }  // namespace helrm

@@ -7,6 +7,7 @@
 // Layout: polynomials are [limb][N] uint64, NTT form in slot order; one
 // thread per coefficient, blockIdx.y = limb, coalesced 8-byte accesses.
 #include "internal.h"
+#include "fmath.cuh"
 
 namespace helrm {
 
@@ -95,20 +96,24 @@ __global__ void k_binary(int op, const uint64_t* __restrict__ a, const uint64_t*
 // out[l] = a[l] * s[l] (shoup constants per limb)
 __global__ void k_scalar_mul(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
                              const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N,
-                             const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp, int split_out) {
+                             const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp, int dform_out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
   const uint64_t q = primes[map.pr[l]].rc.q;
   const size_t o = (size_t)l * N + i;
   const uint64_t v = shoup(a[o], s[l], sp[l], q);
-  out[o] = split_out ? to_split(v) : v;
+  out[o] = dform_out ? fm::d2bits(fm::u2c(v, (double)q)) : v;
 }
 
-// in-place conversion to (dir 1) / from (dir 0) the split form
-__global__ void k_split(uint64_t* __restrict__ x, size_t n, int dir) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    x[i] = dir ? to_split(x[i]) : from_split(x[i]);
+// in-place conversion to (dir 1) / from (dir 0) D-form; word i belongs to limb
+// (i / N) mod map.n of a repeating [map.n][N] layout
+__global__ void k_dform(uint64_t* __restrict__ x, size_t n, uint32_t log_n, const PrimeDev* __restrict__ primes,
+                        const __grid_constant__ LimbMap map, int dir) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const PrimeDev& P = primes[map.pr[(i >> log_n) % map.n]];
+    x[i] = dir ? fm::d2bits(fm::u2c(x[i], P.qd)) : fm::c2u(fm::bits2d(x[i]), P.rc.q);
+  }
 }
 
 // out[l][p] = a[l][rot_src(p)]  (+ out if accumulate)
@@ -127,24 +132,6 @@ __global__ void k_automorph(const uint64_t* __restrict__ a, uint64_t* __restrict
 // every row r (the table also reproduces a digit's own rows); the CTA stages
 // its conversion's table in shared memory, each thread loads its nb sources
 // once and produces all rows.  grid (N/256, G ncv).
-// FP64 helpers shared with the NTT butterflies: exact Y W mod q for
-// |Y W / q| < 2^51 via an FMA-split product and a rounded quotient.
-namespace {
-constexpr double kMagicC = 6755399441055744.0;  // 1.5 * 2^52
-__device__ __forceinline__ double c_u2d(uint64_t x) {
-  return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
-}
-__device__ __forceinline__ double c_mmul(double y, double w, double wq, double q) {
-  const double h = y * w;
-  const double k = __fma_rn(y, wq, kMagicC) - kMagicC;
-  const double l = __fma_rn(y, w, -h);
-  return __fma_rn(-k, q, h) + l;
-}
-__device__ __forceinline__ double c_cred(double x, double q, double qi) {
-  const double k = __fma_rn(x, qi, kMagicC) - kMagicC;
-  return __fma_rn(-k, q, x);
-}
-}  // namespace
 
 template <int NB>
 __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict__ tab, int ncv, int rows,
@@ -161,15 +148,16 @@ __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict_
   const uint64_t* src = y + (size_t)g * y_stride + (size_t)st[0].src_row0 * N + i;
   double v[NB];
 #pragma unroll
-  for (int b = 0; b < NB; b++) v[b] = b < nb ? c_u2d(src[(size_t)b * N]) : 0.0;  // missing sources = 0
+  for (int b = 0; b < NB; b++) v[b] = b < nb ? fm::u2d(src[(size_t)b * N]) : 0.0;  // missing sources = 0
   uint64_t* o = out + (size_t)g * osg + (size_t)k * osk + i;
 #pragma unroll 2
   for (int r = 0; r < rows; r++) {
+    if (st[r].out_row < 0) continue;
     const double q = st[r].q, qi = st[r].qinv;
     double acc = 0.0;
 #pragma unroll
-    for (int b = 0; b < NB; b++) acc += c_mmul(v[b], st[r].cf[b].x, st[r].cf[b].y, q);  // each in [-q/2, q/2]
-    o[(size_t)r * N] = (uint64_t)__double_as_longlong(c_cred(acc, q, qi));
+    for (int b = 0; b < NB; b++) acc += fm::mmul(v[b], st[r].cf[b].x, st[r].cf[b].y, q);  // each in [-q/2, q/2]
+    o[(size_t)st[r].out_row * N] = (uint64_t)__double_as_longlong(fm::cred(acc, q, qi));
   }
 }
 
@@ -210,44 +198,45 @@ __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint6
 //   out0[l][p] (+)= [l < add_rows] mul_l phi(add0)[l][p] + sum_k phi(D_k)[l][p] b_k[l][p]
 //   out1[l][p] (+)= sum_k phi(D_k)[l][p] a_k[l][p]
 // (add0 = c0 with mul = [P]_q for a lazy rotation; add0 = A with mul = 1 for
-// the giant step's phi(A) + KS(B'), D20 L4)
-__global__ void k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
-                      const __grid_constant__ LimbMap map, uint32_t N) {
+// the giant step's phi(A) + KS(B'), D20 L4).  Keys in D-form; the products
+// are exact FP64 MACs (fmath.cuh), dnum + 1 <= kFAccTerms terms.
+// DNUM is a template parameter so that all 3 DNUM loads of a thread are in
+// flight before the first product (a runtime bound made the compiler convert
+// each digit right after its load, serialising the memory latency).
+template <int DNUM>
+__global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
+                                             const __grid_constant__ LimbMap map, uint32_t N) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (p >= N) return;
   const uint32_t chain = map.pr[l];
-  const RedConst rc = primes[chain].rc;
+  const PrimeDev& P = primes[chain];
+  const double q = P.qd, qi = P.qinv;
   const uint32_t sp = rot_src(p, a.rot, N / 2);
-  Acc3 acc0, acc1;
-  const uint64_t* kb = a.key + (size_t)chain * N + p;   // split-form key
+  const uint64_t* kb = a.key + (size_t)chain * N + p;   // D-form key
   const uint64_t* dg = a.digits + (size_t)l * N + sp;
-  uint64_t dv[8], kv0[8], kv1[8];
+  uint64_t dv[DNUM], kv0[DNUM], kv1[DNUM];
+  const bool add = a.add0 != nullptr && l < a.add_rows;
+  const uint64_t av = add ? a.add0[(size_t)l * N + sp] : 0;
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
-    if (k < a.dnum) {
-      dv[k] = dg[(size_t)k * a.digit_stride];
-      kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
-      kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
-    }
+  for (int k = 0; k < DNUM; k++) {
+    dv[k] = dg[(size_t)k * a.digit_stride];
+    kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
+    kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
   }
+  fm::FAcc acc0, acc1;
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
-    if (k < a.dnum) {
-      const uint64_t d = to_split(dv[k]);
-      mac_split(acc0, d, kv0[k]);
-      mac_split(acc1, d, kv1[k]);
-    }
+  for (int k = 0; k < DNUM; k++) {
+    const double d = fm::u2d(dv[k]);
+    fm::fmac(acc0, d, fm::bits2d(kv0[k]));
+    fm::fmac(acc1, d, fm::bits2d(kv1[k]));
   }
-  if (a.add0 != nullptr && l < a.add_rows) {
-    const uint64_t v = a.add0[(size_t)l * N + sp];
-    mac_split(acc0, to_split(v), to_split(a.add_mul ? a.add_mul[l] : 1));
-  }
-  uint64_t r0 = acc3_reduce(acc0, rc), r1 = acc3_reduce(acc1, rc);
+  if (add) fm::fmac(acc0, fm::u2d(av), a.add_mul ? fm::u2c(a.add_mul[l], q) : 1.0);
+  uint64_t r0 = fm::c2u(fm::fred(acc0, q, qi), P.rc.q), r1 = fm::c2u(fm::fred(acc1, q, qi), P.rc.q);
   const size_t o = (size_t)l * N + p;
   if (a.accumulate) {
-    r0 = add_mod(r0, a.out0[o], rc.q);
-    r1 = add_mod(r1, a.out1[o], rc.q);
+    r0 = add_mod(r0, a.out0[o], P.rc.q);
+    r1 = add_mod(r1, a.out1[o], P.rc.q);
   }
   a.out0[o] = r0;
   a.out1[o] = r1;
@@ -258,75 +247,64 @@ __global__ void k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restr
 //   a_j[l][p] = [l <= level] [P]_{q_l} phi_j(c0)[l][p] + sum_k phi_j(D_k)[l][p] b_{j,k}[l][p]
 //   b_j[l][p] = sum_k phi_j(D_k)[l][p] a_{j,k}[l][p]
 // The CTA stages its 256-position tile of D_k and c0 plus a halo of max r_j
-// positions (cyclic inside the half) in shared memory once, then streams the
-// keys: the digits are read from HBM once for all babies instead of once per
-// baby.
-__global__ void __launch_bounds__(256) k_kip_multi(const __grid_constant__ KipMulti a, const PrimeDev* __restrict__ primes,
-                                                   const __grid_constant__ LimbMap map, uint32_t N) {
-  extern __shared__ uint64_t sh[];
+// positions (cyclic inside the half) in shared memory once (as doubles), then
+// streams the D-form keys: the digits are read from HBM once for all babies
+// instead of once per baby.  Baby pairs are written in D-form.
+template <int DNUM>
+__global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ KipMulti a,
+                                                      const PrimeDev* __restrict__ primes,
+                                                      const __grid_constant__ LimbMap map, uint32_t N) {
+  extern __shared__ double shd[];
   const int l = blockIdx.y;
   const uint32_t n = N / 2, tile = blockDim.x;
   const uint32_t p0 = blockIdx.x * tile, half = p0 >= n ? n : 0;
   const uint32_t span = tile + a.max_rot;
   const uint32_t chain = map.pr[l];
-  const RedConst rc = primes[chain].rc;
+  const PrimeDev& P = primes[chain];
+  const double q = P.qd, qi = P.qinv;
   const bool has_c0 = l <= (int)a.level;
   // stage D_k (and c0) tiles + halo
   for (uint32_t e = threadIdx.x; e < span; e += tile) {
     uint32_t j = p0 - half + e;
     j = j >= n ? j - n : j;
     const size_t src = (size_t)l * N + half + j;
-    for (int k = 0; k < a.dnum; k++) sh[k * span + e] = to_split(a.digits[(size_t)k * a.digit_stride + src]);
-    if (has_c0) sh[a.dnum * span + e] = to_split(a.c0[src]);
+#pragma unroll
+    for (int k = 0; k < DNUM; k++) shd[k * span + e] = fm::u2d(a.digits[(size_t)k * a.digit_stride + src]);
+    if (has_c0) shd[DNUM * span + e] = fm::u2d(a.c0[src]);
   }
   __syncthreads();
   const uint32_t p = p0 + threadIdx.x;
-  const uint64_t pm = has_c0 ? to_split(a.p_mod[l]) : 0;
-  // two babies per round: 2 x 2 dnum independent key loads in flight
-  for (int j0 = 0; j0 < a.n; j0 += 2) {
-    const int nj = a.n - j0 >= 2 ? 2 : 1;
-    uint64_t kv[2][2][8];
+  const double pm = has_c0 ? fm::u2c(a.p_mod[l], q) : 0.0;
+  for (int j = 0; j < a.n; j++) {
+    const uint64_t* kb = a.key[j] + (size_t)chain * N + p;
+    uint64_t kv0[DNUM], kv1[DNUM];
 #pragma unroll
-    for (int jj = 0; jj < 2; jj++) {
-      if (jj < nj) {
-        const uint64_t* kb = a.key[j0 + jj] + (size_t)chain * N + p;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          if (k < a.dnum) {
-            kv[jj][0][k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
-            kv[jj][1][k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
-          }
-        }
-      }
+    for (int k = 0; k < DNUM; k++) {
+      kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
+      kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
     }
+    const uint32_t e = threadIdx.x + a.rot[j];
+    fm::FAcc acc0, acc1;
 #pragma unroll
-    for (int jj = 0; jj < 2; jj++) {
-      if (jj < nj) {
-        const int j = j0 + jj;
-        const uint32_t e = threadIdx.x + a.rot[j];
-        Acc3 acc0, acc1;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          if (k < a.dnum) {
-            const uint64_t dv = sh[k * span + e];
-            mac_split(acc0, dv, kv[jj][0][k]);
-            mac_split(acc1, dv, kv[jj][1][k]);
-          }
-        }
-        if (has_c0) mac_split(acc0, sh[a.dnum * span + e], pm);
-        uint64_t* o = a.out[j] + (size_t)l * N + p;   // baby pairs are stored split
-        o[0] = to_split(acc3_reduce(acc0, rc));
-        o[a.out_half] = to_split(acc3_reduce(acc1, rc));
-      }
+    for (int k = 0; k < DNUM; k++) {
+      const double dv = shd[k * span + e];
+      fm::fmac(acc0, dv, fm::bits2d(kv0[k]));
+      fm::fmac(acc1, dv, fm::bits2d(kv1[k]));
     }
+    if (has_c0) fm::fmac(acc0, shd[DNUM * span + e], pm);
+    uint64_t* o = a.out[j] + (size_t)l * N + p;   // baby pairs are stored in D-form
+    o[0] = fm::d2bits(fm::fred(acc0, q, qi));
+    o[a.out_half] = fm::d2bits(fm::fred(acc1, q, qi));
   }
 }
 
 // D20 L3: (A, B)_z[l][p] = sum_t u_{z,t}[l][p] (x0_t, x1_t)[l][p] for the
 // giants z of a pack.  grid: (tile, pack, limb) -- limb outermost so the
 // baby pairs of a limb stay L2-resident; each baby value is loaded once per
-// pack of kGiantPack giants.
-template <bool XSPLIT>
+// pack of kGiantPack giants.  Plaintexts u in D-form; x in D-form (XD) or
+// canonical (single mode, centred on load).  Exact FP64 MACs, folded every
+// kFAccTerms products; the output pairs are canonical.
+template <bool XD>
 __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ terms, const int4* __restrict__ groups,
                                                   uint64_t* __restrict__ out, size_t out_stride, size_t half,
                                                   const PrimeDev* __restrict__ primes,
@@ -337,9 +315,11 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   const int4 gr = groups[blockIdx.y];
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.z;
-  const RedConst rc = primes[map.pr[l]].rc;
+  const PrimeDev& P = primes[map.pr[l]];
+  const double q = P.qd, qi = P.qinv;
   const size_t o = (size_t)l * N + p;
-  Acc3 acc0[G], acc1[G];
+  fm::FAcc acc0[G], acc1[G];
+  int cnt = 0;
   for (int c0 = 0; c0 < gr.y; c0 += kChunk) {   // term list staged in chunks
     const int nt = min(kChunk, gr.y - c0);
     __syncthreads();
@@ -364,13 +344,24 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
           for (int g = 0; g < G; g++) u[r][g] = 0;
         }
       }
-#pragma unroll
-      for (int r = 0; r < 2; r++) {
-        const uint64_t a = XSPLIT ? x0[r] : to_split(x0[r]), b = XSPLIT ? x1[r] : to_split(x1[r]);
+      if (cnt + 2 > fm::kFAccTerms) {
 #pragma unroll
         for (int g = 0; g < G; g++) {
-          mac_split(acc0[g], u[r][g], a);
-          mac_split(acc1[g], u[r][g], b);
+          fm::fold(acc0[g], q, qi);
+          fm::fold(acc1[g], q, qi);
+        }
+        cnt = 0;
+      }
+      cnt += 2;
+#pragma unroll
+      for (int r = 0; r < 2; r++) {
+        const double xa = XD ? fm::bits2d(x0[r]) : fm::u2c(x0[r], q);
+        const double xb = XD ? fm::bits2d(x1[r]) : fm::u2c(x1[r], q);
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+          const double ud = fm::bits2d(u[r][g]);
+          fm::fmac(acc0[g], ud, xa);
+          fm::fmac(acc1[g], ud, xb);
         }
       }
     }
@@ -380,8 +371,8 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   for (int g = 0; g < G; g++) {
     if (g < gr.w) {
       uint64_t* dst = out + (size_t)(gr.z + g) * out_stride;
-      dst[o] = acc3_reduce(acc0[g], rc);
-      dst[half + o] = acc3_reduce(acc1[g], rc);
+      dst[o] = fm::c2u(fm::fred(acc0[g], q, qi), P.rc.q);
+      dst[half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
     }
   }
 }
@@ -433,16 +424,16 @@ void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b
 }
 
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
-                       const uint64_t* sp, int split_out) {
+                       const uint64_t* sp, int dform_out) {
   ProfScope ps_(c, "scalar_mul", 16.0 * c.N * map.n);
-  k_scalar_mul<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp, split_out);
+  k_scalar_mul<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp, dform_out);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
-void launch_split(const DevCtx& c, uint64_t* x, size_t n, int dir) {
-  ProfScope ps_(c, "split", 16.0 * n);
-  k_split<<<148 * 8, 256, 0, c.stream>>>(x, n, dir);
+void launch_dform(const DevCtx& c, uint64_t* x, size_t n, const LimbMap& map, int dir) {
+  ProfScope ps_(c, "dform", 16.0 * n);
+  k_dform<<<148 * 8, 256, 0, c.stream>>>(x, n, c.log_n, c.primes, map, dir);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -494,7 +485,18 @@ void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_
 
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
   ProfScope ps_(c, "kip", 8.0 * c.N * (3.0 * a.dnum * map.n + (a.add0 ? a.add_rows : 0) + (a.accumulate ? 4 : 2) * map.n));
-  k_kip<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
+  decltype(&k_kip<1>) kern = nullptr;
+  switch (a.dnum) {
+    case 1: kern = k_kip<1>; break;
+    case 2: kern = k_kip<2>; break;
+    case 3: kern = k_kip<3>; break;
+    case 4: kern = k_kip<4>; break;
+    case 5: kern = k_kip<5>; break;
+    case 6: kern = k_kip<6>; break;
+    case 7: kern = k_kip<7>; break;
+    default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
+  }
+  kern<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -504,15 +506,28 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
                                              (double)a.n * (2.0 * a.dnum * map.n + 2 * map.n)));
   const uint32_t tile = 256;
   const size_t smem = (size_t)(a.dnum + 1) * (tile + a.max_rot) * 8;
-  k_kip_multi<<<dim3(c.N / tile, map.n), tile, smem, c.stream>>>(a, c.primes, map, c.N);
+  decltype(&k_kip_multi<1>) kern = nullptr;
+  switch (a.dnum) {
+    case 1: kern = k_kip_multi<1>; break;
+    case 2: kern = k_kip_multi<2>; break;
+    case 3: kern = k_kip_multi<3>; break;
+    case 4: kern = k_kip_multi<4>; break;
+    case 5: kern = k_kip_multi<5>; break;
+    case 6: kern = k_kip_multi<6>; break;
+    case 7: kern = k_kip_multi<7>; break;
+    default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
+  }
+  kern<<<dim3(c.N / tile, map.n), tile, smem, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
-                     double n_x_total, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map, bool x_split) {
-  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + 2.0 * n_x_total + 2.0 * n_out));
-  auto kern = x_split ? k_diag_mac<true> : k_diag_mac<false>;
+                     double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
+                     bool x_dform) {
+  // algorithmic bytes: every plaintext and every distinct baby pair once, the outputs once
+  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + 2.0 * n_x_distinct + 2.0 * n_out));
+  auto kern = x_dform ? k_diag_mac<true> : k_diag_mac<false>;
   kern<<<dim3((c.N + kT - 1) / kT, n_groups, map.n), kT, 0, c.stream>>>(terms, groups, out, out_stride,
                                                                         (size_t)map.n * c.N, c.primes, map, c.N);
   (*c.launches)++;

@@ -1,0 +1,12 @@
+#!/bin/bash
+# A/B timing of NTT kernel variants (env switches read by libhelrm at load time)
+for v in "HELRM_NTT_OLD=1" "HELRM_NTT_PRIME_MAJOR=0 HELRM_NTT_R=1" "HELRM_NTT_PRIME_MAJOR=1 HELRM_NTT_R=1" "HELRM_NTT_PRIME_MAJOR=1" "HELRM_NTT_PRIME_MAJOR=1 HELRM_NTT_R=4"; do
+  env $v python bench.py --steps 5 --warmup 3 --skip-cpu-baseline --rot-cts 2 > gpurun_out/ab_tmp.json 2>/dev/null
+  python - "$v" <<'PY'
+import json, sys
+d = json.load(open("gpurun_out/ab_tmp.json"))
+k = d["step"]["kernels"]
+f = lambda n: k.get(n, {}).get("ms_per_step", 0)
+print(f"{sys.argv[1]:45s} step {d['ms_per_step']:.3f} ms | p1 {f('ntt_fwd_p1'):.3f} p2 {f('ntt_fwd_p2'):.3f} pa {f('ntt_inv_pa'):.3f} pb {f('ntt_inv_pb'):.3f} | micro fwd {d['secondary']['ntt_fwd_GBps']} inv {d['secondary']['ntt_inv_GBps']} GB/s")
+PY
+done
