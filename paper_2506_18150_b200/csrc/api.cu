@@ -96,17 +96,40 @@ struct helrm_ctx {
   ncclComm_t comm = nullptr;      // helrm_comm_init
   int rank = 0, world = 1;
 
-  DevCtx dc() { return DevCtx{dprimes, dslotpos, dgrp, deinv, P.log_n, P.N, stream, &launches, &prof}; }
+  // side streams of the pipelined giant steps (lookup_double_part): NTT work
+  // (FP64-bound) on s_ntt at the highest priority, key switches (HBM-bound)
+  // on s_kip, so they overlap the diagonal MACs on the context stream
+  cudaStream_t s_ntt = nullptr, s_kip = nullptr;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  cudaEvent_t ev() {
+    if (evnext == evpool.size()) {
+      cudaEvent_t e;
+      HCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evpool.push_back(e);
+    }
+    return evpool[evnext++];
+  }
+  // s waits for everything enqueued on `on` so far
+  void join(cudaStream_t s, cudaStream_t on) {
+    cudaEvent_t e = ev();
+    HCUDA(cudaEventRecord(e, on));
+    HCUDA(cudaStreamWaitEvent(s, e, 0));
+  }
 
-  void* dalloc(size_t bytes) {
+  DevCtx dc(cudaStream_t s = nullptr) {
+    return DevCtx{dprimes, dslotpos, dgrp, deinv, P.log_n, P.N, s ? s : stream, &launches, &prof};
+  }
+
+  void* dalloc(size_t bytes, cudaStream_t s = nullptr) {
     void* p = nullptr;
     if (bytes == 0) bytes = 8;
-    cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+    cudaError_t e = cudaMallocAsync(&p, bytes, s ? s : stream);
     if (e != cudaSuccess) throw Error(HELRM_ERR_ALLOC, std::string("device allocation failed: ") + cudaGetErrorString(e));
     return p;
   }
-  void dfree(void* p) {
-    if (p) cudaFreeAsync(p, stream);
+  void dfree(void* p, cudaStream_t s = nullptr) {
+    if (p) cudaFreeAsync(p, s ? s : stream);
   }
   uint64_t* upload_u64(const std::vector<uint64_t>& v) {
     uint64_t* d = (uint64_t*)dalloc(v.size() * 8);
@@ -117,12 +140,14 @@ struct helrm_ctx {
   }
 };
 
-// RAII device buffer on the context stream
+// RAII device buffer, stream-ordered on the context stream (or on s)
 struct DBuf {
   helrm_ctx* c;
+  cudaStream_t s;
   uint64_t* p;
-  DBuf(helrm_ctx* c_, size_t words) : c(c_), p((uint64_t*)c_->dalloc(words * 8)) {}
-  ~DBuf() { c->dfree(p); }
+  DBuf(helrm_ctx* c_, size_t words, cudaStream_t s_ = nullptr)
+      : c(c_), s(s_), p((uint64_t*)c_->dalloc(words * 8, s_)) {}
+  ~DBuf() { c->dfree(p, s); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
 };
@@ -374,40 +399,44 @@ static const uint32_t* modup_lidx(helrm_ctx* c, uint32_t l, int G, size_t* count
   return d;
 }
 
-static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int G, uint32_t l, uint64_t* out) {
+static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int G, uint32_t l, uint64_t* out,
+                        cudaStream_t st = nullptr) {
   const Params& P = c->P;
   const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, dn = P.dnum(l);
   const LevelConst& lc = level_const(c, l);
   if (in_stride == 0) in_stride = nq * N;
   size_t n_conv = 0;
   const uint32_t* lidx = modup_lidx(c, l, G, &n_conv);
-  DBuf y(c, G * nq * N);
+  if (!st) st = c->stream;
+  DBuf y(c, G * nq * N, st);
   // D15 step 1: INTT straight into y-form (times [(Q_k/q_i)^-1]_{q_i});
   // step 2: one conversion launch over (g, digit) writing the rows outside
   // the digit; step 3: one NTT over exactly those limbs.  The digit's own
   // limbs are copied unchanged (NTT form).
-  launch_ntt_inv(c->dc(), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post);
-  launch_conv_rows(c->dc(), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
+  launch_ntt_inv(c->dc(st), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post);
+  launch_conv_rows(c->dc(st), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
                    nl * N, G, P.map_qp(l));
-  launch_ntt_fwd(c->dc(), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
+  launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
   for (size_t k = 0; k < dn; k++) {
     const size_t lo = k * P.alpha, hi = std::min<size_t>((k + 1) * P.alpha, l + 1);
     HCUDA(cudaMemcpy2DAsync(out + k * nl * N + lo * N, dn * nl * N * 8, in + lo * N, in_stride * 8, (hi - lo) * N * 8,
-                            G, cudaMemcpyDeviceToDevice, c->stream));
+                            G, cudaMemcpyDeviceToDevice, st));
   }
 }
 
 // D16 for G polynomials: y_g = y + g ys ([l+1+K][N]) -> out_g = out + g os ([l+1][N])
-static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uint32_t l, uint64_t* out, size_t os) {
+static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uint32_t l, uint64_t* out, size_t os,
+                          cudaStream_t st = nullptr) {
   const Params& P = c->P;
   const size_t N = P.N, nq = l + 1;
   const LevelConst& lc = level_const(c, l);
-  DBuf yp(c, G * P.K * N), t(c, G * nq * N);
-  launch_ntt_inv(c->dc(), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
+  if (!st) st = c->stream;
+  DBuf yp(c, G * P.K * N, st), t(c, G * nq * N, st);
+  launch_ntt_inv(c->dc(st), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
                  lc.moddown_post);
-  launch_conv_rows(c->dc(), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
-  launch_ntt_fwd(c->dc(), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true);
-  launch_sub_scale(c->dc(), y, ys, t.p, nq * N, out, os, G, P.map_q(l), lc.pinv, lc.pinvs);
+  launch_conv_rows(c->dc(st), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
+  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true);
+  launch_sub_scale(c->dc(st), y, ys, t.p, nq * N, out, os, G, P.map_q(l), lc.pinv, lc.pinvs);
 }
 
 static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t* out) {
@@ -457,7 +486,8 @@ static const uint64_t* key_for(const helrm_rotkeys* rk, uint64_t g) {
 // KS_g over precomputed digits D [dnum][l+1+K][N] (D18), fused with the
 // automorphism; add0/add_mul/add_rows as in KipArgs.
 static void kip(helrm_ctx* c, const uint64_t* D, uint32_t l, const helrm_rotkeys* rk, uint64_t g, const uint64_t* add0,
-                int add_rows, const uint64_t* add_mul, uint64_t* out0, uint64_t* out1, bool accumulate) {
+                int add_rows, const uint64_t* add_mul, uint64_t* out0, uint64_t* out1, bool accumulate,
+                cudaStream_t st = nullptr) {
   const Params& P = c->P;
   KipArgs a{};
   a.digits = D;
@@ -473,7 +503,7 @@ static void kip(helrm_ctx* c, const uint64_t* D, uint32_t l, const helrm_rotkeys
   a.out0 = out0;
   a.out1 = out1;
   a.accumulate = accumulate ? 1 : 0;
-  launch_kip(c->dc(), a, P.map_qp(l));
+  launch_kip(c->dc(st), a, P.map_qp(l));
 }
 
 // lazy rotation (P phi(c0) + KS0, KS1) over Q_l P from digits of c1
@@ -587,10 +617,25 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
     c->P = p->P;
     c->device = device;
     c->stream = (cudaStream_t)stream;
+    {
+      int lo_prio = 0, hi_prio = 0;
+      HCUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+      const char* e = getenv("HELRM_PRIO");
+      const int mode = e ? atoi(e) : 1;
+      HCUDA(cudaStreamCreateWithPriority(&c->s_ntt, cudaStreamNonBlocking, mode == 1 ? hi_prio : lo_prio));
+      HCUDA(cudaStreamCreateWithPriority(&c->s_kip, cudaStreamNonBlocking, mode == 2 ? hi_prio : lo_prio));
+    }
     cudaMemPool_t pool;
     HCUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     HCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    {
+      // stream-ordered reuse across the side streams must not add hidden
+      // dependencies (they would serialise the pipelined giant steps)
+      const char* e = getenv("HELRM_POOLDEP");
+      int dep = e ? atoi(e) : 0;
+      HCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &dep));
+    }
     const Params& P = c->P;
     const size_t N = P.N, np = P.primes.size();
     // NTT twiddles as (w, w/q) double pairs; per prime [tw1 256][tw2 N][itw1 256][itw2 N]
@@ -712,9 +757,14 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
 void helrm_ctx_destroy(helrm_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
+  if (c->s_ntt) cudaStreamSynchronize(c->s_ntt);
+  if (c->s_kip) cudaStreamSynchronize(c->s_kip);
   if (c->comm) nccl().commDestroy(c->comm);
   for (void* p : c->owned) cudaFreeAsync(p, c->stream);
   cudaStreamSynchronize(c->stream);
+  for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
+  if (c->s_ntt) cudaStreamDestroy(c->s_ntt);
+  if (c->s_kip) cudaStreamDestroy(c->s_kip);
   delete c;
 }
 
@@ -1354,6 +1404,7 @@ struct MacList {
   std::vector<int4> groups;
   std::vector<std::pair<int64_t, int64_t>> oi;   // (o, i) of each output pair
   double n_u = 0, n_x = 0;   // plaintext limb-sets read, distinct baby pairs read
+  std::vector<double> gu;    // plaintexts per group
 };
 
 }  // extern "C" (templates below)
@@ -1374,6 +1425,7 @@ static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int
     for (size_t g0 = 0; g0 < gi.size(); g0 += kGiantPack) {
       const int ng = (int)std::min<size_t>(kGiantPack, gi.size() - g0);
       const int z0 = (int)ml.oi.size();
+      double gu = 0;
       std::map<std::pair<int, int>, MacTerm> tm;
       for (int g = 0; g < ng; g++) {
         ml.oi.push_back({o, gi[g0 + g]});
@@ -1388,9 +1440,11 @@ static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int
           }
           it->second.u[g] = pl->diag + (size_t)e.uid * diag_stride;
           ml.n_u += 1;
+          gu += 1;
         }
       }
       ml.groups.push_back(make_int4((int)ml.terms.size(), (int)tm.size(), z0, ng));
+      ml.gu.push_back(gu);
       for (auto& kv : tm) {
         ml.terms.push_back(kv.second);
         xs.insert(kv.first);
@@ -1403,16 +1457,39 @@ static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int
 
 extern "C" {
 
-// upload the list and run the batched MAC into out (pair z at out + z out_stride)
-static void run_macs(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_stride, const LimbMap& map,
-                     bool x_dform) {
-  DBuf dterms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), dgroups(c, 2 * ml.groups.size() + 1);
-  HCUDA(cudaMemcpyAsync(dterms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
-                        c->stream));
-  HCUDA(cudaMemcpyAsync(dgroups.p, ml.groups.data(), ml.groups.size() * sizeof(int4), cudaMemcpyHostToDevice,
-                        c->stream));
-  launch_diag_mac(c->dc(), (const MacTerm*)dterms.p, (const int4*)dgroups.p, (int)ml.groups.size(), ml.n_u, ml.n_x,
-                  (int)ml.oi.size(), out, out_stride, map, x_dform);
+// the MAC work list on the device (uploaded once per lookup)
+struct MacDev {
+  DBuf terms, groups;
+  MacDev(helrm_ctx* c, const MacList& ml)
+      : terms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), groups(c, 2 * ml.groups.size() + 1) {
+    HCUDA(cudaMemcpyAsync(terms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
+                          c->stream));
+    HCUDA(cudaMemcpyAsync(groups.p, ml.groups.data(), ml.groups.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                          c->stream));
+  }
+};
+
+// run the batched MAC of groups [g0, g1) into out (pair z at out + z out_stride)
+static void run_macs(helrm_ctx* c, const MacList& ml, const MacDev& md, size_t g0, size_t g1, uint64_t* out,
+                     size_t out_stride, const LimbMap& map, bool x_dform) {
+  if (g1 <= g0) return;
+  double nu = 0;
+  int nout = 0;
+  for (size_t g = g0; g < g1; g++) {
+    nu += ml.gu[g];
+    nout += ml.groups[g].w;
+  }
+  // algorithmic bytes: plaintexts of the groups, each distinct baby pair once per lookup (charged to the
+  // first launch), the outputs
+  const double nx = g0 == 0 ? ml.n_x : 0.0;
+  launch_diag_mac(c->dc(), (const MacTerm*)md.terms.p, (const int4*)md.groups.p + g0, (int)(g1 - g0), nu, nx, nout,
+                  out, out_stride, map, x_dform);
+}
+
+static void run_macs_all(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_stride, const LimbMap& map,
+                         bool x_dform) {
+  MacDev md(c, ml);
+  run_macs(c, ml, md, 0, ml.groups.size(), out, out_stride, map, x_dform);
 }
 
 // D20 L1-L4 for the giant pairs z in [z_lo, z_hi) of the non-empty (o, i)
@@ -1426,6 +1503,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
   const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
   const LevelConst& lc = level_const(c, l);
+  c->evnext = 0;
   // L1 (hoist #1): digits of every input c1;  L2: lazy baby steps over Q_l P
   std::vector<std::map<int, uint64_t*>> ab(pl->C);
   size_t n_baby = 0;
@@ -1465,47 +1543,67 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     }
     if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
-  // L3: every inner sum (A, B)_{o,i} in one launch
+  // L3 + L4, pipelined over the MAC groups (packs of kGiantPack giants):
+  //   context stream: the inner sums (A, B) of group p          (HBM-bound)
+  //   s_ntt:          ModDown(B) + ModUp(B') of group p - 1      (FP64-bound, hoist #2)
+  //   s_kip:          phi(A) + KS(B') into O for group p - 2     (HBM-bound)
+  // Every (A, B) pair and digit set has its own buffer, so the three streams
+  // only meet at the events; O is only touched by s_kip.
   const MacList ml = build_macs(pl, nlN, [&](int ci, int j) {
     uint64_t* a = ab[ci].at(j);
     return std::make_pair((const uint64_t*)a, (const uint64_t*)(a + nlN));
   }, z_lo, z_hi);
   const int n_out = (int)ml.oi.size();
   if (n_out == 0) return;
-  DBuf AB(c, (size_t)n_out * 2 * nlN);
-  run_macs(c, ml, AB.p, 2 * nlN, mqp, true);
-  // L4 (hoist #2) per output block: batched ModDown of every rotating B,
-  // batched ModUp of the results, then one fused (phi(A) + KS) per giant
-  for (int64_t o = 0; o < pl->O; o++) {
-    struct {
-      uint64_t* p;
-    } O{Oall + (size_t)o * 2 * nlN};
-    std::vector<int> rot_idx;
-    for (int z = 0; z < n_out; z++) {
-      if (ml.oi[z].first != o) continue;
-      const int64_t gi = pl->giants[o][ml.oi[z].second];
-      if (gi % (int64_t)P.n == 0) {
-        launch_binary(c->dc(), 0, O.p, AB.p + (size_t)z * 2 * nlN, O.p, map_twice(mqp));
-      } else {
-        rot_idx.push_back(z);
-      }
-    }
-    // batches = maximal runs of consecutive pairs (one run unless a zero giant sits in the middle)
-    for (size_t r0 = 0; r0 < rot_idx.size();) {
+  DBuf AB(c, (size_t)n_out * 2 * nlN), Bp(c, (size_t)n_out * nq * N), D2(c, (size_t)n_out * dn * nlN);
+  MacDev md(c, ml);
+  static const bool pipe = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
+  cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream;
+  if (pipe) {
+    c->join(sn, c->stream);
+    c->join(sk, c->stream);   // O zeroed, babies ready
+  }
+  const LimbMap m2 = map_twice(mqp);
+  static const int mac_ch = getenv("HELRM_MACCH") ? atoi(getenv("HELRM_MACCH")) : 2;   // MAC groups per launch
+  static const int ntt_ch = getenv("HELRM_NTTCH") ? atoi(getenv("HELRM_NTTCH")) : 8;   // giants per ModDown/ModUp batch
+  for (size_t gp = 0; gp < ml.groups.size(); gp += mac_ch) {
+    const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
+    const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
+    run_macs(c, ml, md, gp, gq, AB.p, 2 * nlN, mqp, true);
+    if (pipe) c->join(sn, c->stream);
+    std::vector<int> rot;   // rotating pairs of the chunk (zero giants need no key switch)
+    for (int z = z0; z < z1; z++)
+      if (pl->giants[ml.oi[z].first][ml.oi[z].second] % (int64_t)P.n != 0) rot.push_back(z);
+    int zdone = z0;   // pairs [z0, zdone) handed to s_kip
+    for (size_t r0 = 0; r0 < rot.size();) {   // runs of consecutive rotating pairs, at most ntt_ch long
       size_t r1 = r0 + 1;
-      while (r1 < rot_idx.size() && rot_idx[r1] == rot_idx[r1 - 1] + 1) r1++;
-      const int z0 = rot_idx[r0], G = (int)(r1 - r0);
-      DBuf Bp(c, (size_t)G * nq * N), D2(c, (size_t)G * dn * nlN);
-      moddown_batch(c, AB.p + (size_t)z0 * 2 * nlN + nlN, 2 * nlN, G, l, Bp.p, nq * N);
-      modup_batch(c, Bp.p, nq * N, G, l, D2.p);
-      for (int k = 0; k < G; k++) {
-        const int z = z0 + k;
-        const int64_t gi = pl->giants[o][ml.oi[z].second];
-        kip(c, D2.p + (size_t)k * dn * nlN, l, rk, galois_of_rot(c, gi), AB.p + (size_t)z * 2 * nlN, (int)nl,
-            nullptr, O.p, O.p + nlN, true);
+      while (r1 < rot.size() && rot[r1] == rot[r1 - 1] + 1 && (int)(r1 - r0) < ntt_ch) r1++;
+      const int za = rot[r0], G = (int)(r1 - r0);
+      moddown_batch(c, AB.p + (size_t)za * 2 * nlN + nlN, 2 * nlN, G, l, Bp.p + (size_t)za * nq * N, nq * N, sn);
+      modup_batch(c, Bp.p + (size_t)za * nq * N, nq * N, G, l, D2.p + (size_t)za * dn * nlN, sn);
+      if (pipe) c->join(sk, sn);
+      const int zend = r1 < rot.size() ? rot[r1] : z1;
+      for (int z = zdone; z < zend; z++) {
+        uint64_t* O = Oall + (size_t)ml.oi[z].first * 2 * nlN;
+        const int64_t gi = pl->giants[ml.oi[z].first][ml.oi[z].second];
+        if (gi % (int64_t)P.n == 0)
+          launch_binary(c->dc(sk), 0, O, AB.p + (size_t)z * 2 * nlN, O, m2);
+        else
+          kip(c, D2.p + (size_t)z * dn * nlN, l, rk, galois_of_rot(c, gi), AB.p + (size_t)z * 2 * nlN, (int)nl,
+              nullptr, O, O + nlN, true, sk);
       }
+      zdone = zend;
       r0 = r1;
     }
+    if (pipe) c->join(sk, c->stream);
+    for (int z = zdone; z < z1; z++) {   // zero giants with no rotating pair after them
+      uint64_t* O = Oall + (size_t)ml.oi[z].first * 2 * nlN;
+      launch_binary(c->dc(sk), 0, O, AB.p + (size_t)z * 2 * nlN, O, m2);
+    }
+  }
+  if (pipe) {
+    c->join(c->stream, sn);
+    c->join(c->stream, sk);
   }
 }
 
@@ -1567,7 +1665,7 @@ static void lookup_single(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
   });
   const int n_out = (int)ml.oi.size();
   DBuf ABbuf(c, (size_t)n_out * 2 * nqN);
-  run_macs(c, ml, ABbuf.p, 2 * nqN, mq, false);
+  run_macs_all(c, ml, ABbuf.p, 2 * nqN, mq, false);
   std::vector<helrm_ct> AB(n_out);
   for (int z = 0; z < n_out; z++) AB[z] = helrm_ct{c, l, in[0]->scale, ABbuf.p + (size_t)z * 2 * nqN};
   helrm_ct* R = new_ct(c, l, in[0]->scale);
@@ -1598,6 +1696,7 @@ helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys
     need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
     for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
     for (size_t q = 0; q < batch; q++) {
+      c->evnext = 0;
       for (int64_t ci = 0; ci < p->C; ci++) {
         need(in[q * p->C + ci] != nullptr, HELRM_ERR_ARG, "null input ciphertext");
         need(in[q * p->C + ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's level");
