@@ -453,15 +453,16 @@ static void moddown(helrm_ctx* c, const uint64_t* y, uint32_t l, uint64_t* out) 
 }
 
 // D17 on a ciphertext [2][l+1][N] -> out [2][l][N]
-static void rescale_ct(helrm_ctx* c, const uint64_t* x, uint32_t l, uint64_t* out) {
+// (G contiguous ciphertexts [G][2][l+1][N] -> [G][2][l][N])
+static void rescale_ct(helrm_ctx* c, const uint64_t* x, uint32_t l, uint64_t* out, int G = 1) {
   const Params& P = c->P;
   const size_t N = P.N;
-  DBuf xl(c, 2 * N), r(c, 2 * l * N);
-  ntt_inv(c, x + l * N, xl.p, 2, P.map_range(l, 1), (l + 1) * N, N);
-  launch_rescale_prep(c->dc(), xl.p, N, P.primes[l], r.p, l * N, 2, P.map_q(l - 1));
-  ntt_fwd(c, r.p, r.p, 2 * l, P.map_q(l - 1));
+  DBuf xl(c, 2 * G * N), r(c, 2 * G * l * N);
+  ntt_inv(c, x + l * N, xl.p, 2 * G, P.map_range(l, 1), (l + 1) * N, N);
+  launch_rescale_prep(c->dc(), xl.p, N, P.primes[l], r.p, l * N, 2 * G, P.map_q(l - 1));
+  ntt_fwd(c, r.p, r.p, 2 * G * l, P.map_q(l - 1));
   const LevelConst& lc = level_const(c, l);
-  launch_sub_scale(c->dc(), x, (l + 1) * N, r.p, l * N, out, l * N, 2, P.map_q(l - 1), lc.qlinv, lc.qlinvs);
+  launch_sub_scale(c->dc(), x, (l + 1) * N, r.p, l * N, out, l * N, 2 * G, P.map_q(l - 1), lc.qlinv, lc.qlinvs);
 }
 
 static uint32_t rot_of_galois(helrm_ctx* c, uint64_t g) {
@@ -1471,7 +1472,7 @@ struct MacDev {
 
 // run the batched MAC of groups [g0, g1) into out (pair z at out + z out_stride)
 static void run_macs(helrm_ctx* c, const MacList& ml, const MacDev& md, size_t g0, size_t g1, uint64_t* out,
-                     size_t out_stride, const LimbMap& map, bool x_dform) {
+                     size_t out_stride, const LimbMap& map, bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0) {
   if (g1 <= g0) return;
   double nu = 0;
   int nout = 0;
@@ -1483,7 +1484,7 @@ static void run_macs(helrm_ctx* c, const MacList& ml, const MacDev& md, size_t g
   // first launch), the outputs
   const double nx = g0 == 0 ? ml.n_x : 0.0;
   launch_diag_mac(c->dc(), (const MacTerm*)md.terms.p, (const int4*)md.groups.p + g0, (int)(g1 - g0), nu, nx, nout,
-                  out, out_stride, map, x_dform);
+                  out, out_stride, map, x_dform, nq, xq, oq);
 }
 
 static void run_macs_all(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_stride, const LimbMap& map,
@@ -1492,44 +1493,65 @@ static void run_macs_all(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t 
   run_macs(c, ml, md, 0, ml.groups.size(), out, out_stride, map, x_dform);
 }
 
-// D20 L1-L4 for the giant pairs z in [z_lo, z_hi) of the non-empty (o, i)
-// enumeration: accumulates into O [pl->O][2][l+1+K][N] (zeroed by the caller).
-// With z over everything this is the whole lookup up to L5; split over ranks
-// the partial O's sum exactly to the full one (D23).
+// D20 L1-L4 for Qc queries (in[q C + c]) and the giant pairs z in [z_lo, z_hi)
+// of the non-empty (o, i) enumeration: accumulates into Oall [O][Qc][2][l+1+K][N]
+// (zeroed by the caller).  With z over everything this is the whole lookup up
+// to L5; split over ranks the partial O's sum exactly to the full one (D23).
+// The queries of a call share every key and plaintext read: the key switches
+// load each key value once and apply it to all queries (kip_multi stages up
+// to 4 queries' digit tiles per CTA), the diagonal MAC re-reads its plaintext
+// tiles from L2 for the second and later queries.
 static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk,
-                               const helrm_ct* const* in, int64_t z_lo, int64_t z_hi, uint64_t* Oall) {
+                               const helrm_ct* const* in, int Qc, int64_t z_lo, int64_t z_hi, uint64_t* Oall) {
   const Params& P = c->P;
   const uint32_t l = pl->level;
-  const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
+  const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, nqN = nq * N, dn = P.dnum(l);
+  const size_t C = pl->C;
   const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
   const LevelConst& lc = level_const(c, l);
   c->evnext = 0;
-  // L1 (hoist #1): digits of every input c1;  L2: lazy baby steps over Q_l P
-  std::vector<std::map<int, uint64_t*>> ab(pl->C);
+  // inputs: ct (q, ci) at X + (q C + ci) 2 nqN (gathered unless there is a single one)
+  std::unique_ptr<DBuf> Xb;
+  const uint64_t* X = in[0]->d;
+  if (Qc * C > 1) {
+    Xb.reset(new DBuf(c, (size_t)Qc * C * 2 * nqN));
+    for (size_t i = 0; i < (size_t)Qc * C; i++)
+      HCUDA(cudaMemcpyAsync(Xb->p + i * 2 * nqN, in[i]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
+    X = Xb->p;
+  }
+  const size_t xs = C * 2 * nqN;   // query stride of the inputs
+  // L1 (hoist #1): digits of every input c1 [ci][q][dn][nl][N];  L2: lazy baby steps over Q_l P,
+  // baby b of query q at babies + (b Qc + q) 2 nlN
+  std::vector<std::map<int, uint64_t*>> ab(C);
   size_t n_baby = 0;
   for (auto& bl : pl->babies) n_baby += bl.size();
-  DBuf D(c, pl->C * dn * nlN), babies(c, std::max<size_t>(1, n_baby) * 2 * nlN);
+  DBuf D(c, C * Qc * dn * nlN), babies(c, std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
   size_t bi = 0;
-  for (int64_t ci = 0; ci < pl->C; ci++) {
-    const helrm_ct* ct = in[ci];
-    uint64_t* Dc = D.p + ci * dn * nlN;
-    modup_batch(c, ct_c1(ct), 0, 1, l, Dc);
+  for (size_t ci = 0; ci < C; ci++) {
+    const uint64_t* c0 = X + ci * 2 * nqN;
+    uint64_t* Dc = D.p + ci * Qc * dn * nlN;
+    modup_batch(c, c0 + nqN, xs, Qc, l, Dc);
     KipMulti km{};
     km.digits = Dc;
     km.digit_stride = nlN;
     km.dnum = (int)dn;
-    km.c0 = ct_c0(ct);
+    km.c0 = c0;
     km.p_mod = lc.pmod;
     km.level = l;
     km.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
     km.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
     km.out_half = nlN;
+    km.nq = Qc;
+    km.qk = std::min(Qc, 4);
+    km.dq = dn * nlN;
+    km.cq = xs;
+    km.oq = 2 * nlN;
     for (int j : pl->babies[ci]) {
-      uint64_t* a = babies.p + bi++ * 2 * nlN;
+      uint64_t* a = babies.p + bi++ * Qc * 2 * nlN;
       if (j == 0) {  // (P c0, P c1): Q limbs scaled by [P]_q, P limbs 0
-        HCUDA(cudaMemsetAsync(a, 0, 2 * nlN * 8, c->stream));
-        launch_scalar_mul(c->dc(), ct_c0(ct), a, mq, lc.pmod, lc.pmods, 1);   // baby pairs are in D-form
-        launch_scalar_mul(c->dc(), ct_c1(ct), a + nlN, mq, lc.pmod, lc.pmods, 1);
+        HCUDA(cudaMemsetAsync(a, 0, (size_t)Qc * 2 * nlN * 8, c->stream));
+        launch_scalar_mul(c->dc(), c0, a, mq, lc.pmod, lc.pmods, 1, Qc, xs, 2 * nlN);   // baby pairs are in D-form
+        launch_scalar_mul(c->dc(), c0 + nqN, a + nlN, mq, lc.pmod, lc.pmods, 1, Qc, xs, 2 * nlN);
       } else {
         need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
         const uint64_t g = galois_of_rot(c, j);
@@ -1544,18 +1566,20 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
   // L3 + L4, pipelined over the MAC groups (packs of kGiantPack giants):
-  //   context stream: the inner sums (A, B) of group p          (HBM-bound)
-  //   s_ntt:          ModDown(B) + ModUp(B') of group p - 1      (FP64-bound, hoist #2)
-  //   s_kip:          phi(A) + KS(B') into O for group p - 2     (HBM-bound)
+  //   context stream: the inner sums (A, B) of a chunk of groups (HBM-bound)
+  //   s_ntt:          ModDown(B) + ModUp(B') of the previous one (FP64-bound, hoist #2)
+  //   s_kip:          phi(A) + KS(B') into O                     (HBM-bound)
   // Every (A, B) pair and digit set has its own buffer, so the three streams
-  // only meet at the events; O is only touched by s_kip.
+  // only meet at the events; O is only touched by s_kip.  Pair z of query q
+  // lives at AB + (z Qc + q) 2 nlN, so a run of pairs is one strided batch.
   const MacList ml = build_macs(pl, nlN, [&](int ci, int j) {
     uint64_t* a = ab[ci].at(j);
     return std::make_pair((const uint64_t*)a, (const uint64_t*)(a + nlN));
   }, z_lo, z_hi);
   const int n_out = (int)ml.oi.size();
   if (n_out == 0) return;
-  DBuf AB(c, (size_t)n_out * 2 * nlN), Bp(c, (size_t)n_out * nq * N), D2(c, (size_t)n_out * dn * nlN);
+  const size_t zq = (size_t)Qc;   // pairs per z
+  DBuf AB(c, (size_t)n_out * zq * 2 * nlN), Bp(c, (size_t)n_out * zq * nqN), D2(c, (size_t)n_out * zq * dn * nlN);
   MacDev md(c, ml);
   static const bool pipe = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
   cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream;
@@ -1564,12 +1588,18 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     c->join(sk, c->stream);   // O zeroed, babies ready
   }
   const LimbMap m2 = map_twice(mqp);
+  auto Oq = [&](int z) { return Oall + (size_t)ml.oi[z].first * zq * 2 * nlN; };
+  auto zero_giant = [&](int z) {   // O_o += (A, B)_z for every query
+    for (int q = 0; q < Qc; q++)
+      launch_binary(c->dc(sk), 0, Oq(z) + (size_t)q * 2 * nlN, AB.p + ((size_t)z * zq + q) * 2 * nlN,
+                    Oq(z) + (size_t)q * 2 * nlN, m2);
+  };
   static const int mac_ch = getenv("HELRM_MACCH") ? atoi(getenv("HELRM_MACCH")) : 2;   // MAC groups per launch
   static const int ntt_ch = getenv("HELRM_NTTCH") ? atoi(getenv("HELRM_NTTCH")) : 8;   // giants per ModDown/ModUp batch
   for (size_t gp = 0; gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
     const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
-    run_macs(c, ml, md, gp, gq, AB.p, 2 * nlN, mqp, true);
+    run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN);
     if (pipe) c->join(sn, c->stream);
     std::vector<int> rot;   // rotating pairs of the chunk (zero giants need no key switch)
     for (int z = z0; z < z1; z++)
@@ -1578,28 +1608,41 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     for (size_t r0 = 0; r0 < rot.size();) {   // runs of consecutive rotating pairs, at most ntt_ch long
       size_t r1 = r0 + 1;
       while (r1 < rot.size() && rot[r1] == rot[r1 - 1] + 1 && (int)(r1 - r0) < ntt_ch) r1++;
-      const int za = rot[r0], G = (int)(r1 - r0);
-      moddown_batch(c, AB.p + (size_t)za * 2 * nlN + nlN, 2 * nlN, G, l, Bp.p + (size_t)za * nq * N, nq * N, sn);
-      modup_batch(c, Bp.p + (size_t)za * nq * N, nq * N, G, l, D2.p + (size_t)za * dn * nlN, sn);
+      const size_t za = rot[r0], G = (r1 - r0) * zq;
+      moddown_batch(c, AB.p + za * zq * 2 * nlN + nlN, 2 * nlN, (int)G, l, Bp.p + za * zq * nqN, nqN, sn);
+      modup_batch(c, Bp.p + za * zq * nqN, nqN, (int)G, l, D2.p + za * zq * dn * nlN, sn);
       if (pipe) c->join(sk, sn);
       const int zend = r1 < rot.size() ? rot[r1] : z1;
       for (int z = zdone; z < zend; z++) {
-        uint64_t* O = Oall + (size_t)ml.oi[z].first * 2 * nlN;
         const int64_t gi = pl->giants[ml.oi[z].first][ml.oi[z].second];
-        if (gi % (int64_t)P.n == 0)
-          launch_binary(c->dc(sk), 0, O, AB.p + (size_t)z * 2 * nlN, O, m2);
-        else
-          kip(c, D2.p + (size_t)z * dn * nlN, l, rk, galois_of_rot(c, gi), AB.p + (size_t)z * 2 * nlN, (int)nl,
-              nullptr, O, O + nlN, true, sk);
+        if (gi % (int64_t)P.n == 0) {
+          zero_giant(z);
+        } else {
+          KipArgs a{};
+          a.digits = D2.p + (size_t)z * zq * dn * nlN;
+          a.digit_stride = nlN;
+          a.dnum = (int)dn;
+          a.key = key_for(rk, galois_of_rot(c, gi));
+          a.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+          a.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+          a.add0 = AB.p + (size_t)z * zq * 2 * nlN;
+          a.add_rows = (int)nl;
+          a.rot = rot_of_galois(c, galois_of_rot(c, gi));
+          a.out0 = Oq(z);
+          a.out1 = Oq(z) + nlN;
+          a.accumulate = 1;
+          a.nq = Qc;
+          a.dq = dn * nlN;
+          a.aq = 2 * nlN;
+          a.oq = 2 * nlN;
+          launch_kip(c->dc(sk), a, mqp);
+        }
       }
       zdone = zend;
       r0 = r1;
     }
     if (pipe) c->join(sk, c->stream);
-    for (int z = zdone; z < z1; z++) {   // zero giants with no rotating pair after them
-      uint64_t* O = Oall + (size_t)ml.oi[z].first * 2 * nlN;
-      launch_binary(c->dc(sk), 0, O, AB.p + (size_t)z * 2 * nlN, O, m2);
-    }
+    for (int z = zdone; z < z1; z++) zero_giant(z);   // zero giants with no rotating pair after them
   }
   if (pipe) {
     c->join(c->stream, sn);
@@ -1607,20 +1650,63 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   }
 }
 
-// D20 L6-L8 per output block: ModDown both halves (scale Delta q_l),
-// rescale (scale Delta), RotSum when mbar < n
-static void lookup_finish(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* Oall,
+// D21 RotSum on Qc contiguous ciphertexts S [Qc][2][l+1][N] at level l:
+// ct += Rotate(ct, mbar 2^r), each rotation batched over the queries (one
+// key read for all of them)
+static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t mbar, const helrm_rotkeys* rk) {
+  const Params& P = c->P;
+  const int64_t n = P.n;
+  if (mbar >= n) return;
+  const size_t N = P.N, nq = l + 1, nqN = nq * N, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
+  const LevelConst& lc = level_const(c, l);
+  DBuf D(c, (size_t)Qc * dn * nlN), T(c, (size_t)Qc * 2 * nlN), R(c, (size_t)Qc * 2 * nqN);
+  LimbMap m2 = map_twice(P.map_q(l));
+  for (int64_t r = mbar; r < n; r *= 2) {
+    const uint64_t g = galois_of_rot(c, r);
+    modup_batch(c, S + nqN, 2 * nqN, Qc, l, D.p);
+    KipArgs a{};
+    a.digits = D.p;
+    a.digit_stride = nlN;
+    a.dnum = (int)dn;
+    a.key = key_for(rk, g);
+    a.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+    a.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+    a.add0 = S;                       // lazy rotation: P phi(c0) + KS0, KS1
+    a.add_rows = (int)nq;
+    a.add_mul = lc.pmod;
+    a.rot = rot_of_galois(c, g);
+    a.out0 = T.p;
+    a.out1 = T.p + nlN;
+    a.accumulate = 0;
+    a.nq = Qc;
+    a.dq = dn * nlN;
+    a.aq = 2 * nqN;
+    a.oq = 2 * nlN;
+    launch_kip(c->dc(), a, P.map_qp(l));
+    moddown_batch(c, T.p, nlN, 2 * Qc, l, R.p, nqN);
+    for (int q = 0; q < Qc; q++)
+      launch_binary(c->dc(), 0, S + (size_t)q * 2 * nqN, R.p + (size_t)q * 2 * nqN, S + (size_t)q * 2 * nqN, m2);
+  }
+}
+
+// D20 L6-L8 per output block for Qc queries (Oall [O][Qc][2][l+1+K][N]):
+// ModDown both halves (scale Delta q_l), rescale (scale Delta), RotSum when
+// mbar < n; out[q O + o]
+static void lookup_finish(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* Oall, int Qc,
                           double scale, helrm_ct** out) {
   const Params& P = c->P;
   const uint32_t l = pl->level;
-  const size_t N = P.N, nq = l + 1, nlN = (size_t)(l + 1 + P.K) * N;
+  const size_t N = P.N, nq = l + 1, nlN = (size_t)(l + 1 + P.K) * N, oN = 2 * (size_t)l * N;
   for (int64_t o = 0; o < pl->O; o++) {
-    DBuf r(c, 2 * nq * N);
-    moddown_batch(c, Oall + (size_t)o * 2 * nlN, nlN, 2, l, r.p, nq * N);
-    helrm_ct* s = new_ct(c, l - 1, scale);
-    rescale_ct(c, r.p, l, s->d);
-    rot_sum(c, s, pl->mbar, rk);
-    out[o] = s;
+    DBuf r(c, (size_t)Qc * 2 * nq * N), S(c, (size_t)Qc * oN);
+    moddown_batch(c, Oall + (size_t)o * Qc * 2 * nlN, nlN, 2 * Qc, l, r.p, nq * N);
+    rescale_ct(c, r.p, l, S.p, Qc);
+    rot_sum_batch(c, S.p, Qc, l - 1, pl->mbar, rk);
+    for (int q = 0; q < Qc; q++) {
+      helrm_ct* s = new_ct(c, l - 1, scale);
+      HCUDA(cudaMemcpyAsync(s->d, S.p + (size_t)q * oN, oN * 8, cudaMemcpyDeviceToDevice, c->stream));
+      out[(size_t)q * pl->O + o] = s;
+    }
   }
 }
 
@@ -1631,14 +1717,37 @@ static int64_t count_pairs(const helrm_plan* pl) {
   return n;
 }
 
-// D20: the double-hoisted BSGS lookup of one query (C input cts -> O outputs)
+// device words one query of a batched double-hoisted lookup keeps live
+static size_t query_words(helrm_ctx* c, const helrm_plan* pl) {
+  const Params& P = c->P;
+  const size_t l = pl->level, N = P.N, nq = l + 1, nl = l + 1 + P.K, dn = P.dnum(l);
+  size_t nb = 0, pairs = (size_t)count_pairs(pl);
+  for (auto& b : pl->babies) nb += b.size();
+  return N * (pl->C * (2 * nq + dn * nl) + nb * 2 * nl + pairs * (2 * nl + nq + dn * nl) + pl->O * 2 * nl +
+              pl->O * 4 * nq);
+}
+
+// D20: the double-hoisted BSGS lookup of `batch` queries (C input cts -> O
+// outputs each), in chunks of queries that share every key and plaintext read
 static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
-                          helrm_ct** out) {
+                          size_t batch, helrm_ct** out) {
   const size_t nlN = (size_t)(pl->level + 1 + c->P.K) * c->P.N;
-  DBuf O(c, (size_t)pl->O * 2 * nlN);
-  HCUDA(cudaMemsetAsync(O.p, 0, (size_t)pl->O * 2 * nlN * 8, c->stream));
-  lookup_double_part(c, pl, rk, in, 0, INT64_MAX, O.p);
-  lookup_finish(c, pl, rk, O.p, in[0]->scale, out);
+  size_t qc = 1;
+  if (batch > 1) {
+    size_t fr = 0, tot = 0;
+    HCUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t budget = std::min<size_t>(fr / 2, (size_t)48 << 30);
+    qc = std::max<size_t>(1, std::min(batch, budget / (8 * query_words(c, pl))));
+    if (getenv("HELRM_QCHUNK")) qc = std::max(1, atoi(getenv("HELRM_QCHUNK")));
+    qc = std::min(qc, batch);
+  }
+  for (size_t q0 = 0; q0 < batch; q0 += qc) {
+    const int Qc = (int)std::min(qc, batch - q0);
+    DBuf O(c, (size_t)pl->O * Qc * 2 * nlN);
+    HCUDA(cudaMemsetAsync(O.p, 0, (size_t)pl->O * Qc * 2 * nlN * 8, c->stream));
+    lookup_double_part(c, pl, rk, in + q0 * pl->C, Qc, 0, INT64_MAX, O.p);
+    lookup_finish(c, pl, rk, O.p, Qc, in[q0 * pl->C]->scale, out + q0 * pl->O);
+  }
 }
 
 // D22: single-hoisted cross-check mode (full rotations in Q_l)
@@ -1701,11 +1810,9 @@ helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys
         need(in[q * p->C + ci] != nullptr, HELRM_ERR_ARG, "null input ciphertext");
         need(in[q * p->C + ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's level");
       }
-      if (p->mode == HELRM_MODE_DOUBLE)
-        lookup_double(c, p, rk, in + q * p->C, out + q * p->O);
-      else
-        lookup_single(c, p, rk, in + q * p->C, out + q * p->O);
+      if (p->mode != HELRM_MODE_DOUBLE) lookup_single(c, p, rk, in + q * p->C, out + q * p->O);
     }
+    if (p->mode == HELRM_MODE_DOUBLE) lookup_double(c, p, rk, in, batch, out);
   });
 }
 
@@ -1849,13 +1956,13 @@ helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_ro
       }
       DBuf O(c, (size_t)p->O * 2 * nlN);
       HCUDA(cudaMemsetAsync(O.p, 0, (size_t)p->O * 2 * nlN * 8, c->stream));
-      lookup_double_part(c, p, rk, cin, lo, hi, O.p);
+      lookup_double_part(c, p, rk, cin, 1, lo, hi, O.p);
       if (c->world > 1) {
         // L5: exact sum of the partial accumulators (each < q, so < world q < 2^64), then mod q
         HNCCL(nccl().allReduce(O.p, O.p, (size_t)p->O * 2 * nlN, ncclUint64, ncclSum, c->comm, c->stream));
         for (int64_t h = 0; h < 2 * p->O; h++) launch_modred(c->dc(), O.p + (size_t)h * nlN, P.map_qp(p->level));
       }
-      lookup_finish(c, p, rk, O.p, cin[0]->scale, out + q * p->O);
+      lookup_finish(c, p, rk, O.p, 1, cin[0]->scale, out + q * p->O);
     }
   });
 }

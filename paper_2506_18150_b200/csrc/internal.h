@@ -187,7 +187,8 @@ void launch_sample_small(const DevCtx& c, int64_t* out, uint64_t base, int kind,
 // op 0: a + b, 1: a - b, 2: a * b, 3: -a
 void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, const LimbMap& map);
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
-                       const uint64_t* sp, int dform_out = 0);
+                       const uint64_t* sp, int dform_out = 0, int G = 1, size_t a_stride = 0,
+                       size_t out_stride = 0);
 // in place: dir 1 -> D-form (fmath.cuh), dir 0 -> canonical; word i is in limb
 // (i / N) mod map.n of a repeating [map.n][N] layout
 void launch_dform(const DevCtx& c, uint64_t* x, size_t n, const LimbMap& map, int dir);
@@ -214,6 +215,10 @@ struct KipArgs {
   uint64_t* out0;             // [nl][N]
   uint64_t* out1;
   int accumulate;             // out += result (else out = result)
+  // queries sharing the key (batched lookups): query q uses digits + q dq,
+  // add0 + q aq and writes out0/out1 + q oq; the key is loaded once for all
+  int nq = 1;
+  size_t dq = 0, aq = 0, oq = 0;
 };
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map);
 
@@ -233,6 +238,10 @@ struct KipMulti {
   uint32_t rot[kMaxBabies];
   const uint64_t* key[kMaxBabies];
   uint64_t* out[kMaxBabies];
+  // queries sharing the keys: query q has digits + q dq, c0 + q cq and writes
+  // out[j] + q oq; a CTA stages qk queries' tiles and applies each key value to all
+  int nq = 1, qk = 1;
+  size_t dq = 0, cq = 0, oq = 0;
 };
 void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map);
 
@@ -248,8 +257,9 @@ struct MacTerm {
 // group z: terms [g.x, g.x + g.y), output pairs g.z .. g.z + g.w - 1, each
 // written to out + pair out_stride (A) and + nl N (B).  u in D-form; x in
 // D-form iff x_dform (else canonical).
+// nq queries: query q reads x + q xq and writes out + q oq (plaintexts shared).
 void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
                      double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
-                     bool x_dform);
+                     bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0);
 
 }  // namespace helrm

@@ -96,14 +96,15 @@ __global__ void k_binary(int op, const uint64_t* __restrict__ a, const uint64_t*
 // out[l] = a[l] * s[l] (shoup constants per limb)
 __global__ void k_scalar_mul(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
                              const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N,
-                             const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp, int dform_out) {
+                             const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp, int dform_out,
+                             size_t as, size_t os) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
   const uint64_t q = primes[map.pr[l]].rc.q;
   const size_t o = (size_t)l * N + i;
-  const uint64_t v = shoup(a[o], s[l], sp[l], q);
-  out[o] = dform_out ? fm::d2bits(fm::u2c(v, (double)q)) : v;
+  const uint64_t v = shoup(a[blockIdx.z * as + o], s[l], sp[l], q);
+  out[blockIdx.z * os + o] = dform_out ? fm::d2bits(fm::u2c(v, (double)q)) : v;
 }
 
 // in-place conversion to (dir 1) / from (dir 0) D-form; word i belongs to limb
@@ -215,31 +216,46 @@ __global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs a, 
   const uint32_t sp = rot_src(p, a.rot, N / 2);
   const uint64_t* kb = a.key + (size_t)chain * N + p;   // D-form key
   const uint64_t* dg = a.digits + (size_t)l * N + sp;
-  uint64_t dv[DNUM], kv0[DNUM], kv1[DNUM];
   const bool add = a.add0 != nullptr && l < a.add_rows;
-  const uint64_t av = add ? a.add0[(size_t)l * N + sp] : 0;
+  const double amul = add && a.add_mul ? fm::u2c(a.add_mul[l], q) : 1.0;
+  uint64_t dv[DNUM], kv0[DNUM], kv1[DNUM];
+  uint64_t av = add ? a.add0[(size_t)l * N + sp] : 0;
 #pragma unroll
   for (int k = 0; k < DNUM; k++) {
     dv[k] = dg[(size_t)k * a.digit_stride];
-    kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
-    kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
+    if (a.nq == 1) {
+      kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
+      kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
+    } else {
+      kv0[k] = kb[(size_t)k * a.key_digit_stride];
+      kv1[k] = kb[(size_t)k * a.key_digit_stride + a.key_half_stride];
+    }
   }
-  fm::FAcc acc0, acc1;
-#pragma unroll
-  for (int k = 0; k < DNUM; k++) {
-    const double d = fm::u2d(dv[k]);
-    fm::fmac(acc0, d, fm::bits2d(kv0[k]));
-    fm::fmac(acc1, d, fm::bits2d(kv1[k]));
-  }
-  if (add) fm::fmac(acc0, fm::u2d(av), a.add_mul ? fm::u2c(a.add_mul[l], q) : 1.0);
-  uint64_t r0 = fm::c2u(fm::fred(acc0, q, qi), P.rc.q), r1 = fm::c2u(fm::fred(acc1, q, qi), P.rc.q);
   const size_t o = (size_t)l * N + p;
-  if (a.accumulate) {
-    r0 = add_mod(r0, a.out0[o], P.rc.q);
-    r1 = add_mod(r1, a.out1[o], P.rc.q);
+  for (int qq = 0; qq < a.nq; qq++) {
+    if (qq > 0) {
+#pragma unroll
+      for (int k = 0; k < DNUM; k++) dv[k] = dg[(size_t)qq * a.dq + (size_t)k * a.digit_stride];
+      if (add) av = a.add0[(size_t)qq * a.aq + (size_t)l * N + sp];
+    }
+    fm::FAcc acc0, acc1;
+#pragma unroll
+    for (int k = 0; k < DNUM; k++) {
+      const double d = fm::u2d(dv[k]);
+      fm::fmac(acc0, d, fm::bits2d(kv0[k]));
+      fm::fmac(acc1, d, fm::bits2d(kv1[k]));
+    }
+    if (add) fm::fmac(acc0, fm::u2d(av), amul);
+    uint64_t r0 = fm::c2u(fm::fred(acc0, q, qi), P.rc.q), r1 = fm::c2u(fm::fred(acc1, q, qi), P.rc.q);
+    uint64_t* o0 = a.out0 + (size_t)qq * a.oq + o;
+    uint64_t* o1 = a.out1 + (size_t)qq * a.oq + o;
+    if (a.accumulate) {
+      r0 = add_mod(r0, *o0, P.rc.q);
+      r1 = add_mod(r1, *o1, P.rc.q);
+    }
+    *o0 = r0;
+    *o1 = r1;
   }
-  a.out0[o] = r0;
-  a.out1[o] = r1;
 }
 
 // D20 L2, all baby steps of one input ciphertext in one pass: for each
@@ -263,14 +279,21 @@ __global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ Ki
   const PrimeDev& P = primes[chain];
   const double q = P.qd, qi = P.qinv;
   const bool has_c0 = l <= (int)a.level;
-  // stage D_k (and c0) tiles + halo
-  for (uint32_t e = threadIdx.x; e < span; e += tile) {
-    uint32_t j = p0 - half + e;
-    j = j >= n ? j - n : j;
-    const size_t src = (size_t)l * N + half + j;
+  const int q0 = blockIdx.z * a.qk, nqc = min(a.qk, a.nq - q0);   // this CTA's queries
+  const int slab = (DNUM + 1) * span;                              // doubles per staged query
+  // stage D_k (and c0) tiles + halo of every query of the CTA
+  for (int qq = 0; qq < nqc; qq++) {
+    const uint64_t* dgq = a.digits + (size_t)(q0 + qq) * a.dq;
+    const uint64_t* c0q = a.c0 + (size_t)(q0 + qq) * a.cq;
+    double* sq = shd + qq * slab;
+    for (uint32_t e = threadIdx.x; e < span; e += tile) {
+      uint32_t j = p0 - half + e;
+      j = j >= n ? j - n : j;
+      const size_t src = (size_t)l * N + half + j;
 #pragma unroll
-    for (int k = 0; k < DNUM; k++) shd[k * span + e] = fm::u2d(a.digits[(size_t)k * a.digit_stride + src]);
-    if (has_c0) shd[DNUM * span + e] = fm::u2d(a.c0[src]);
+      for (int k = 0; k < DNUM; k++) sq[k * span + e] = fm::u2d(dgq[(size_t)k * a.digit_stride + src]);
+      if (has_c0) sq[DNUM * span + e] = fm::u2d(c0q[src]);
+    }
   }
   __syncthreads();
   const uint32_t p = p0 + threadIdx.x;
@@ -284,17 +307,20 @@ __global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ Ki
       kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
     }
     const uint32_t e = threadIdx.x + a.rot[j];
-    fm::FAcc acc0, acc1;
+    for (int qq = 0; qq < nqc; qq++) {
+      const double* sq = shd + qq * slab;
+      fm::FAcc acc0, acc1;
 #pragma unroll
-    for (int k = 0; k < DNUM; k++) {
-      const double dv = shd[k * span + e];
-      fm::fmac(acc0, dv, fm::bits2d(kv0[k]));
-      fm::fmac(acc1, dv, fm::bits2d(kv1[k]));
+      for (int k = 0; k < DNUM; k++) {
+        const double dv = sq[k * span + e];
+        fm::fmac(acc0, dv, fm::bits2d(kv0[k]));
+        fm::fmac(acc1, dv, fm::bits2d(kv1[k]));
+      }
+      if (has_c0) fm::fmac(acc0, sq[DNUM * span + e], pm);
+      uint64_t* o = a.out[j] + (size_t)(q0 + qq) * a.oq + (size_t)l * N + p;   // baby pairs are stored in D-form
+      o[0] = fm::d2bits(fm::fred(acc0, q, qi));
+      o[a.out_half] = fm::d2bits(fm::fred(acc1, q, qi));
     }
-    if (has_c0) fm::fmac(acc0, shd[DNUM * span + e], pm);
-    uint64_t* o = a.out[j] + (size_t)l * N + p;   // baby pairs are stored in D-form
-    o[0] = fm::d2bits(fm::fred(acc0, q, qi));
-    o[a.out_half] = fm::d2bits(fm::fred(acc1, q, qi));
   }
 }
 
@@ -308,7 +334,8 @@ template <bool XD>
 __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ terms, const int4* __restrict__ groups,
                                                   uint64_t* __restrict__ out, size_t out_stride, size_t half,
                                                   const PrimeDev* __restrict__ primes,
-                                                  const __grid_constant__ LimbMap map, uint32_t N) {
+                                                  const __grid_constant__ LimbMap map, uint32_t N, int nq, size_t xq,
+                                                  size_t oq) {
   constexpr int G = kGiantPack;
   constexpr int kChunk = 64;
   __shared__ MacTerm tm[kChunk];
@@ -317,7 +344,8 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   const int l = blockIdx.z;
   const PrimeDev& P = primes[map.pr[l]];
   const double q = P.qd, qi = P.qinv;
-  const size_t o = (size_t)l * N + p;
+  for (int qq = 0; qq < nq; qq++) {   // queries share the plaintexts (re-read from L2)
+  const size_t o = (size_t)l * N + p, ox = o + (size_t)qq * xq;
   fm::FAcc acc0[G], acc1[G];
   int cnt = 0;
   for (int c0 = 0; c0 < gr.y; c0 += kChunk) {   // term list staged in chunks
@@ -334,10 +362,15 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
       for (int r = 0; r < 2; r++) {
         if (r < nr) {
           const MacTerm& m = tm[t + r];
-          x0[r] = m.x0[o];
-          x1[r] = m.x1[o];
+          x0[r] = m.x0[ox];
+          x1[r] = m.x1[ox];
+          if (nq == 1) {
 #pragma unroll
-          for (int g = 0; g < G; g++) u[r][g] = m.u[g] ? __ldcs(m.u[g] + o) : 0;  // plaintexts stream once
+            for (int g = 0; g < G; g++) u[r][g] = m.u[g] ? __ldcs(m.u[g] + o) : 0;  // plaintexts stream once
+          } else {
+#pragma unroll
+            for (int g = 0; g < G; g++) u[r][g] = m.u[g] ? m.u[g][o] : 0;
+          }
         } else {
           x0[r] = x1[r] = 0;
 #pragma unroll
@@ -366,14 +399,16 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
       }
     }
   }
-  if (p >= N) return;
+  if (p < N) {
 #pragma unroll
-  for (int g = 0; g < G; g++) {
-    if (g < gr.w) {
-      uint64_t* dst = out + (size_t)(gr.z + g) * out_stride;
-      dst[o] = fm::c2u(fm::fred(acc0[g], q, qi), P.rc.q);
-      dst[half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
+    for (int g = 0; g < G; g++) {
+      if (g < gr.w) {
+        uint64_t* dst = out + (size_t)(gr.z + g) * out_stride + (size_t)qq * oq;
+        dst[o] = fm::c2u(fm::fred(acc0[g], q, qi), P.rc.q);
+        dst[half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
+      }
     }
+  }
   }
 }
 
@@ -424,9 +459,10 @@ void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b
 }
 
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
-                       const uint64_t* sp, int dform_out) {
-  ProfScope ps_(c, "scalar_mul", 16.0 * c.N * map.n);
-  k_scalar_mul<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp, dform_out);
+                       const uint64_t* sp, int dform_out, int G, size_t as, size_t os) {
+  ProfScope ps_(c, "scalar_mul", 16.0 * c.N * map.n * G);
+  k_scalar_mul<<<dim3((c.N + kT - 1) / kT, map.n, G), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp,
+                                                                          dform_out, as, os);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -484,7 +520,8 @@ void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_
 }
 
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
-  ProfScope ps_(c, "kip", 8.0 * c.N * (3.0 * a.dnum * map.n + (a.add0 ? a.add_rows : 0) + (a.accumulate ? 4 : 2) * map.n));
+  ProfScope ps_(c, "kip", 8.0 * c.N * (2.0 * a.dnum * map.n + a.nq * (a.dnum * map.n + (a.add0 ? a.add_rows : 0) +
+                                                                      (a.accumulate ? 4 : 2) * map.n)));
   decltype(&k_kip<1>) kern = nullptr;
   switch (a.dnum) {
     case 1: kern = k_kip<1>; break;
@@ -502,10 +539,11 @@ void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
 }
 
 void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
-  ProfScope ps_(c, "kip_multi", 8.0 * c.N * (a.dnum * map.n + (a.level + 1) +
-                                             (double)a.n * (2.0 * a.dnum * map.n + 2 * map.n)));
+  const double zq = (a.nq + a.qk - 1) / a.qk;   // key passes
+  ProfScope ps_(c, "kip_multi", 8.0 * c.N * (a.nq * (a.dnum * map.n + (a.level + 1.0) + a.n * 2.0 * map.n) +
+                                             zq * a.n * 2.0 * a.dnum * map.n));
   const uint32_t tile = 256;
-  const size_t smem = (size_t)(a.dnum + 1) * (tile + a.max_rot) * 8;
+  const size_t smem = (size_t)a.qk * (a.dnum + 1) * (tile + a.max_rot) * 8;
   decltype(&k_kip_multi<1>) kern = nullptr;
   switch (a.dnum) {
     case 1: kern = k_kip_multi<1>; break;
@@ -517,19 +555,21 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
     case 7: kern = k_kip_multi<7>; break;
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
-  kern<<<dim3(c.N / tile, map.n), tile, smem, c.stream>>>(a, c.primes, map, c.N);
+  if (smem > 48 * 1024) HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<dim3(c.N / tile, map.n, (unsigned)zq), tile, smem, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
                      double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
-                     bool x_dform) {
-  // algorithmic bytes: every plaintext and every distinct baby pair once, the outputs once
-  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + 2.0 * n_x_distinct + 2.0 * n_out));
+                     bool x_dform, int nq, size_t xq, size_t oq) {
+  // algorithmic bytes: every plaintext once, every distinct baby pair and output once per query
+  ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + nq * (2.0 * n_x_distinct + 2.0 * n_out)));
   auto kern = x_dform ? k_diag_mac<true> : k_diag_mac<false>;
   kern<<<dim3((c.N + kT - 1) / kT, n_groups, map.n), kT, 0, c.stream>>>(terms, groups, out, out_stride,
-                                                                        (size_t)map.n * c.N, c.primes, map, c.N);
+                                                                        (size_t)map.n * c.N, c.primes, map, c.N, nq,
+                                                                        xq, oq);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
