@@ -12,6 +12,10 @@
 // the host only schedules launches on the context stream.
 #include <omp.h>
 
+#include <chrono>
+
+#include <atomic>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -87,6 +91,33 @@ struct helrm_ctx {
   uint64_t* scratch = nullptr;
   std::map<int, LevelConst> lconst;
   std::map<std::pair<int, int>, uint32_t*> modup_lidx;   // (level, G) -> NTT limb table of modup_batch
+  // CUDA-graph replay of the double-hoisted lookup (one graph per plan, key
+  // set and query-chunk size): the ~400 launches, allocations and copies of a
+  // lookup are enqueued once at capture; a replay costs one graph launch.
+  struct LookupGraph {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t* X = nullptr;        // staged inputs [Qc][C][2][l+1][N]
+    uint64_t* S = nullptr;        // outputs [O][Qc][2][l][N]
+    void* pinned = nullptr;       // host copy of the MAC work list the graph re-uploads
+    size_t uses = 0;
+    uint64_t launches = 0;        // kernel launches inside the graph (added to the counter per replay)
+    bool failed = false;
+  };
+  std::map<std::tuple<uint64_t, uint64_t, int>, LookupGraph> graphs;   // (plan id, key-set id, Qc)
+  void drop_graphs(uint64_t id) {
+    for (auto it = graphs.begin(); it != graphs.end();) {
+      if (std::get<0>(it->first) == id || std::get<1>(it->first) == id) {
+        cudaStreamSynchronize(stream);
+        if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+        if (it->second.pinned) cudaFreeHost(it->second.pinned);
+        dfree(it->second.X);
+        dfree(it->second.S);
+        it = graphs.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
   std::vector<void*> owned;       // device allocations freed at destroy
   uint64_t launches = 0;
   std::vector<uint32_t> dlog5;    // dlog5[g] for odd g < 2N (0xffffffff if not a power of 5)
@@ -100,6 +131,7 @@ struct helrm_ctx {
   // (FP64-bound) on s_ntt at the highest priority, key switches (HBM-bound)
   // on s_kip, so they overlap the diagonal MACs on the context stream
   cudaStream_t s_ntt = nullptr, s_kip = nullptr;
+  cudaStream_t s_cap = nullptr;   // private stream the lookup graphs are captured on
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
   cudaEvent_t ev() {
@@ -112,6 +144,7 @@ struct helrm_ctx {
   }
   // s waits for everything enqueued on `on` so far
   void join(cudaStream_t s, cudaStream_t on) {
+    HostTimer ht_("join");
     cudaEvent_t e = ev();
     HCUDA(cudaEventRecord(e, on));
     HCUDA(cudaStreamWaitEvent(s, e, 0));
@@ -122,6 +155,7 @@ struct helrm_ctx {
   }
 
   void* dalloc(size_t bytes, cudaStream_t s = nullptr) {
+    HostTimer ht_("cudaMallocAsync");
     void* p = nullptr;
     if (bytes == 0) bytes = 8;
     cudaError_t e = cudaMallocAsync(&p, bytes, s ? s : stream);
@@ -129,6 +163,7 @@ struct helrm_ctx {
     return p;
   }
   void dfree(void* p, cudaStream_t s = nullptr) {
+    HostTimer ht_("cudaFreeAsync");
     if (p) cudaFreeAsync(p, s ? s : stream);
   }
   uint64_t* upload_u64(const std::vector<uint64_t>& v) {
@@ -161,10 +196,13 @@ struct helrm_pk {
   helrm_ctx* c;
   uint64_t* d;                    // [2][L+1][N]: b, a
 };
+static std::atomic<uint64_t> g_obj_id{1};   // identity of plans / key sets for the graph cache
+
 struct helrm_rotkeys {
   helrm_ctx* c;
   std::map<uint64_t, uint64_t*> keys;   // galois -> [dnum][2][L+1+K][N]
   size_t words_per_key = 0;
+  uint64_t id = g_obj_id++;
 };
 struct helrm_ct {
   helrm_ctx* c;
@@ -202,6 +240,7 @@ struct helrm_plan {
   int64_t n_unique = 0;
   uint32_t nl = 0;
   std::vector<int64_t> rotations;
+  uint64_t id = g_obj_id++;
 };
 
 // ============================================================================
@@ -218,7 +257,27 @@ cudaEvent_t Profiler::get() {
   HCUDA(cudaEventCreate(&e));
   return e;
 }
-ProfScope::ProfScope(const DevCtx& c_, const char* name, double bytes) : c(c_) {
+static const bool g_hostprof = getenv("HELRM_HOSTPROF") && atoi(getenv("HELRM_HOSTPROF")) != 0;
+static std::map<std::string, std::pair<uint64_t, double>> g_hostt;
+bool hostprof_on() { return g_hostprof; }
+void hostprof_add(const char* name, double us) {
+  auto& e = g_hostt[name];
+  e.first++;
+  e.second += us;
+}
+double hostprof_now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static void hostprof_dump(const char* tag) {
+  if (!g_hostprof) return;
+  fprintf(stderr, "[helrm hostprof] %s\n", tag);
+  for (auto& kv : g_hostt)
+    fprintf(stderr, "  %-24s %6llu calls %10.1f us\n", kv.first.c_str(), (unsigned long long)kv.second.first,
+            kv.second.second);
+  g_hostt.clear();
+}
+
+ProfScope::ProfScope(const DevCtx& c_, const char* name, double bytes) : c(c_), ht(name) {
   if (c.prof && c.prof->on) {
     Profiler::Rec r{name, c.prof->get(), c.prof->get(), bytes};
     HCUDA(cudaEventRecord(r.a, c.stream));
@@ -399,8 +458,10 @@ static const uint32_t* modup_lidx(helrm_ctx* c, uint32_t l, int G, size_t* count
   return d;
 }
 
+// copy_own = false: the digit's own limbs of out are left unwritten; the key
+// switch reads them from `in` (KipArgs::own)
 static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int G, uint32_t l, uint64_t* out,
-                        cudaStream_t st = nullptr) {
+                        cudaStream_t st = nullptr, bool copy_own = true) {
   const Params& P = c->P;
   const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, dn = P.dnum(l);
   const LevelConst& lc = level_const(c, l);
@@ -417,7 +478,8 @@ static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int 
   launch_conv_rows(c->dc(st), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
                    nl * N, G, P.map_qp(l));
   launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
-  for (size_t k = 0; k < dn; k++) {
+  HostTimer ht_("modup own-limb copies");
+  for (size_t k = 0; copy_own && k < dn; k++) {
     const size_t lo = k * P.alpha, hi = std::min<size_t>((k + 1) * P.alpha, l + 1);
     HCUDA(cudaMemcpy2DAsync(out + k * nl * N + lo * N, dn * nl * N * 8, in + lo * N, in_stride * 8, (hi - lo) * N * 8,
                             G, cudaMemcpyDeviceToDevice, st));
@@ -625,6 +687,7 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       const int mode = e ? atoi(e) : 1;
       HCUDA(cudaStreamCreateWithPriority(&c->s_ntt, cudaStreamNonBlocking, mode == 1 ? hi_prio : lo_prio));
       HCUDA(cudaStreamCreateWithPriority(&c->s_kip, cudaStreamNonBlocking, mode == 2 ? hi_prio : lo_prio));
+      HCUDA(cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
     }
     cudaMemPool_t pool;
     HCUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -760,12 +823,20 @@ void helrm_ctx_destroy(helrm_ctx* c) {
   cudaStreamSynchronize(c->stream);
   if (c->s_ntt) cudaStreamSynchronize(c->s_ntt);
   if (c->s_kip) cudaStreamSynchronize(c->s_kip);
+  for (auto& kv : c->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.pinned) cudaFreeHost(kv.second.pinned);
+    c->dfree(kv.second.X);
+    c->dfree(kv.second.S);
+  }
+  c->graphs.clear();
   if (c->comm) nccl().commDestroy(c->comm);
   for (void* p : c->owned) cudaFreeAsync(p, c->stream);
   cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
   if (c->s_ntt) cudaStreamDestroy(c->s_ntt);
   if (c->s_kip) cudaStreamDestroy(c->s_kip);
+  if (c->s_cap) cudaStreamDestroy(c->s_cap);
   delete c;
 }
 
@@ -799,9 +870,16 @@ const char* helrm_ctx_profile_json(helrm_ctx* c) {
     double ms = 0, bytes = 0;
   };
   std::map<std::string, Agg> agg;
+  static const bool trace = getenv("HELRM_TRACE") && atoi(getenv("HELRM_TRACE")) != 0;
   for (auto& r : c->prof.recs) {
     float ms = 0;
     cudaEventElapsedTime(&ms, r.a, r.b);
+    if (trace && !c->prof.recs.empty()) {   // timeline: start / end relative to the first record
+      float t0 = 0, t1 = 0;
+      cudaEventElapsedTime(&t0, c->prof.recs[0].a, r.a);
+      cudaEventElapsedTime(&t1, c->prof.recs[0].a, r.b);
+      fprintf(stderr, "[trace] %-14s %10.3f %10.3f\n", r.name, t0, t1);
+    }
     auto& a = agg[r.name];
     a.n++;
     a.ms += ms;
@@ -924,6 +1002,7 @@ helrm_status helrm_rotkeys_gen(helrm_ctx* c, const helrm_sk* sk, const uint64_t*
 
 void helrm_rotkeys_destroy(helrm_rotkeys* r) {
   if (!r) return;
+  r->c->drop_graphs(r->id);
   for (auto& kv : r->keys) r->c->dfree(kv.second);
   delete r;
 }
@@ -1340,6 +1419,7 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
 }
 
 void helrm_plan_destroy(helrm_plan* p) {
+  if (p && p->c) p->c->drop_graphs(p->id);
   if (!p) return;
   p->c->dfree(p->diag);
   delete p;
@@ -1459,14 +1539,26 @@ static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int
 extern "C" {
 
 // the MAC work list on the device (uploaded once per lookup)
+// (pinned != null: the list is staged in pinned host memory owned by the
+// caller, at least mac_list_bytes() -- a copy from pinned memory can be
+// captured into a CUDA graph)
 struct MacDev {
   DBuf terms, groups;
-  MacDev(helrm_ctx* c, const MacList& ml)
+  MacDev(helrm_ctx* c, const MacList& ml, void** pinned = nullptr)
       : terms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), groups(c, 2 * ml.groups.size() + 1) {
-    HCUDA(cudaMemcpyAsync(terms.p, ml.terms.data(), ml.terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice,
-                          c->stream));
-    HCUDA(cudaMemcpyAsync(groups.p, ml.groups.data(), ml.groups.size() * sizeof(int4), cudaMemcpyHostToDevice,
-                          c->stream));
+    const size_t tb = ml.terms.size() * sizeof(MacTerm), gb = ml.groups.size() * sizeof(int4);
+    const void* ht = ml.terms.data();
+    const void* hg = ml.groups.data();
+    if (pinned) {   // allocated by the caller before the capture (mac_list_bytes)
+      need(*pinned != nullptr, HELRM_ERR_ARG, "pinned MAC staging buffer missing");
+      std::memcpy(*pinned, ht, tb);
+      std::memcpy((char*)*pinned + tb, hg, gb);
+      ht = *pinned;
+      hg = (const char*)*pinned + tb;
+    }
+    HostTimer ht_("MacDev upload");
+    HCUDA(cudaMemcpyAsync(terms.p, ht, tb, cudaMemcpyHostToDevice, c->stream));
+    HCUDA(cudaMemcpyAsync(groups.p, hg, gb, cudaMemcpyHostToDevice, c->stream));
   }
 };
 
@@ -1501,8 +1593,8 @@ static void run_macs_all(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t 
 // load each key value once and apply it to all queries (kip_multi stages up
 // to 4 queries' digit tiles per CTA), the diagonal MAC re-reads its plaintext
 // tiles from L2 for the second and later queries.
-static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk,
-                               const helrm_ct* const* in, int Qc, int64_t z_lo, int64_t z_hi, uint64_t* Oall) {
+static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* X,
+                               int Qc, int64_t z_lo, int64_t z_hi, uint64_t* Oall, void** pinned = nullptr) {
   const Params& P = c->P;
   const uint32_t l = pl->level;
   const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, nqN = nq * N, dn = P.dnum(l);
@@ -1510,15 +1602,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
   const LevelConst& lc = level_const(c, l);
   c->evnext = 0;
-  // inputs: ct (q, ci) at X + (q C + ci) 2 nqN (gathered unless there is a single one)
-  std::unique_ptr<DBuf> Xb;
-  const uint64_t* X = in[0]->d;
-  if (Qc * C > 1) {
-    Xb.reset(new DBuf(c, (size_t)Qc * C * 2 * nqN));
-    for (size_t i = 0; i < (size_t)Qc * C; i++)
-      HCUDA(cudaMemcpyAsync(Xb->p + i * 2 * nqN, in[i]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
-    X = Xb->p;
-  }
+  // inputs: ct (q, ci) at X + (q C + ci) 2 nqN (staged by the caller)
   const size_t xs = C * 2 * nqN;   // query stride of the inputs
   // L1 (hoist #1): digits of every input c1 [ci][q][dn][nl][N];  L2: lazy baby steps over Q_l P,
   // baby b of query q at babies + (b Qc + q) 2 nlN
@@ -1530,8 +1614,11 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   for (size_t ci = 0; ci < C; ci++) {
     const uint64_t* c0 = X + ci * 2 * nqN;
     uint64_t* Dc = D.p + ci * Qc * dn * nlN;
-    modup_batch(c, c0 + nqN, xs, Qc, l, Dc);
+    modup_batch(c, c0 + nqN, xs, Qc, l, Dc, nullptr, false);
     KipMulti km{};
+    km.own = c0 + nqN;
+    km.ownq = xs;
+    km.alpha = (int)P.alpha;
     km.digits = Dc;
     km.digit_stride = nlN;
     km.dnum = (int)dn;
@@ -1580,7 +1667,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   if (n_out == 0) return;
   const size_t zq = (size_t)Qc;   // pairs per z
   DBuf AB(c, (size_t)n_out * zq * 2 * nlN), Bp(c, (size_t)n_out * zq * nqN), D2(c, (size_t)n_out * zq * dn * nlN);
-  MacDev md(c, ml);
+  MacDev md(c, ml, pinned);
   static const bool pipe = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
   cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream;
   if (pipe) {
@@ -1610,7 +1697,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
       while (r1 < rot.size() && rot[r1] == rot[r1 - 1] + 1 && (int)(r1 - r0) < ntt_ch) r1++;
       const size_t za = rot[r0], G = (r1 - r0) * zq;
       moddown_batch(c, AB.p + za * zq * 2 * nlN + nlN, 2 * nlN, (int)G, l, Bp.p + za * zq * nqN, nqN, sn);
-      modup_batch(c, Bp.p + za * zq * nqN, nqN, (int)G, l, D2.p + za * zq * dn * nlN, sn);
+      modup_batch(c, Bp.p + za * zq * nqN, nqN, (int)G, l, D2.p + za * zq * dn * nlN, sn, false);
       if (pipe) c->join(sk, sn);
       const int zend = r1 < rot.size() ? rot[r1] : z1;
       for (int z = zdone; z < zend; z++) {
@@ -1635,6 +1722,10 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
           a.dq = dn * nlN;
           a.aq = 2 * nlN;
           a.oq = 2 * nlN;
+          a.own = Bp.p + (size_t)z * zq * nqN;
+          a.ownq = nqN;
+          a.alpha = (int)P.alpha;
+          a.level = (int)l;
           launch_kip(c->dc(sk), a, mqp);
         }
       }
@@ -1663,8 +1754,12 @@ static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t
   LimbMap m2 = map_twice(P.map_q(l));
   for (int64_t r = mbar; r < n; r *= 2) {
     const uint64_t g = galois_of_rot(c, r);
-    modup_batch(c, S + nqN, 2 * nqN, Qc, l, D.p);
+    modup_batch(c, S + nqN, 2 * nqN, Qc, l, D.p, nullptr, false);
     KipArgs a{};
+    a.own = S + nqN;
+    a.ownq = 2 * nqN;
+    a.alpha = (int)P.alpha;
+    a.level = (int)l;
     a.digits = D.p;
     a.digit_stride = nlN;
     a.dnum = (int)dn;
@@ -1691,23 +1786,47 @@ static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t
 
 // D20 L6-L8 per output block for Qc queries (Oall [O][Qc][2][l+1+K][N]):
 // ModDown both halves (scale Delta q_l), rescale (scale Delta), RotSum when
-// mbar < n; out[q O + o]
+// mbar < n; results into S [O][Qc][2][l][N]
 static void lookup_finish(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* Oall, int Qc,
-                          double scale, helrm_ct** out) {
+                          uint64_t* S) {
   const Params& P = c->P;
   const uint32_t l = pl->level;
   const size_t N = P.N, nq = l + 1, nlN = (size_t)(l + 1 + P.K) * N, oN = 2 * (size_t)l * N;
   for (int64_t o = 0; o < pl->O; o++) {
-    DBuf r(c, (size_t)Qc * 2 * nq * N), S(c, (size_t)Qc * oN);
+    DBuf r(c, (size_t)Qc * 2 * nq * N);
+    uint64_t* So = S + (size_t)o * Qc * oN;
     moddown_batch(c, Oall + (size_t)o * Qc * 2 * nlN, nlN, 2 * Qc, l, r.p, nq * N);
-    rescale_ct(c, r.p, l, S.p, Qc);
-    rot_sum_batch(c, S.p, Qc, l - 1, pl->mbar, rk);
+    rescale_ct(c, r.p, l, So, Qc);
+    rot_sum_batch(c, So, Qc, l - 1, pl->mbar, rk);
+  }
+}
+
+// the whole double-hoisted lookup of Qc staged queries X -> S (no host
+// synchronisation inside: this is what a CUDA graph captures)
+static void lookup_chunk(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* X, int Qc,
+                         uint64_t* S, void** pinned) {
+  const size_t nlN = (size_t)(pl->level + 1 + c->P.K) * c->P.N;
+  DBuf O(c, (size_t)pl->O * Qc * 2 * nlN);
+  HCUDA(cudaMemsetAsync(O.p, 0, (size_t)pl->O * Qc * 2 * nlN * 8, c->stream));
+  lookup_double_part(c, pl, rk, X, Qc, 0, INT64_MAX, O.p, pinned);
+  lookup_finish(c, pl, rk, O.p, Qc, S);
+}
+
+static void stage_inputs(helrm_ctx* c, const helrm_ct* const* in, size_t n, size_t words, uint64_t* X) {
+  for (size_t i = 0; i < n; i++)
+    HCUDA(cudaMemcpyAsync(X + i * words, in[i]->d, words * 8, cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// output ciphertexts of a chunk: out[q O + o] <- S [o][q]
+static void emit_outputs(helrm_ctx* c, const helrm_plan* pl, const uint64_t* S, int Qc, double scale,
+                         helrm_ct** out) {
+  const size_t oN = 2 * (size_t)pl->level * c->P.N;
+  for (int64_t o = 0; o < pl->O; o++)
     for (int q = 0; q < Qc; q++) {
-      helrm_ct* s = new_ct(c, l - 1, scale);
-      HCUDA(cudaMemcpyAsync(s->d, S.p + (size_t)q * oN, oN * 8, cudaMemcpyDeviceToDevice, c->stream));
+      helrm_ct* s = new_ct(c, pl->level - 1, scale);
+      HCUDA(cudaMemcpyAsync(s->d, S + ((size_t)o * Qc + q) * oN, oN * 8, cudaMemcpyDeviceToDevice, c->stream));
       out[(size_t)q * pl->O + o] = s;
     }
-  }
 }
 
 static int64_t count_pairs(const helrm_plan* pl) {
@@ -1728,10 +1847,13 @@ static size_t query_words(helrm_ctx* c, const helrm_plan* pl) {
 }
 
 // D20: the double-hoisted BSGS lookup of `batch` queries (C input cts -> O
-// outputs each), in chunks of queries that share every key and plaintext read
+// outputs each), in chunks of queries that share every key and plaintext
+// read.  Chunks of <= 2 queries replay a captured CUDA graph from the second
+// call on (the first call runs eagerly and creates every cached constant).
 static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
                           size_t batch, helrm_ct** out) {
-  const size_t nlN = (size_t)(pl->level + 1 + c->P.K) * c->P.N;
+  const Params& P = c->P;
+  const size_t nqN = (size_t)(pl->level + 1) * P.N, oN = 2 * (size_t)pl->level * P.N;
   size_t qc = 1;
   if (batch > 1) {
     size_t fr = 0, tot = 0;
@@ -1741,12 +1863,68 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
     if (getenv("HELRM_QCHUNK")) qc = std::max(1, atoi(getenv("HELRM_QCHUNK")));
     qc = std::min(qc, batch);
   }
+  static const bool graphs = getenv("HELRM_GRAPH") ? atoi(getenv("HELRM_GRAPH")) != 0 : true;
   for (size_t q0 = 0; q0 < batch; q0 += qc) {
     const int Qc = (int)std::min(qc, batch - q0);
-    DBuf O(c, (size_t)pl->O * Qc * 2 * nlN);
-    HCUDA(cudaMemsetAsync(O.p, 0, (size_t)pl->O * Qc * 2 * nlN * 8, c->stream));
-    lookup_double_part(c, pl, rk, in + q0 * pl->C, Qc, 0, INT64_MAX, O.p);
-    lookup_finish(c, pl, rk, O.p, Qc, in[q0 * pl->C]->scale, out + q0 * pl->O);
+    const size_t nin = (size_t)Qc * pl->C;
+    const double scale = in[q0 * pl->C]->scale;
+    if (!graphs || c->prof.on || Qc > 2) {
+      DBuf X(c, nin * 2 * nqN), S(c, (size_t)pl->O * Qc * oN);
+      stage_inputs(c, in + q0 * pl->C, nin, 2 * nqN, X.p);
+      lookup_chunk(c, pl, rk, X.p, Qc, S.p, nullptr);
+      emit_outputs(c, pl, S.p, Qc, scale, out + q0 * pl->O);
+      continue;
+    }
+    helrm_ctx::LookupGraph& G = c->graphs[std::make_tuple(pl->id, rk->id, Qc)];
+    if (!G.X) {
+      G.X = (uint64_t*)c->dalloc(nin * 2 * nqN * 8);
+      G.S = (uint64_t*)c->dalloc((size_t)pl->O * Qc * oN * 8);
+      // MAC work list bound: every term carries >= 1 plaintext, every group >= 1 pair
+      HCUDA(cudaMallocHost(&G.pinned, (size_t)pl->n_diag * sizeof(MacTerm) + count_pairs(pl) * sizeof(int4) + 64));
+    }
+    stage_inputs(c, in + q0 * pl->C, nin, 2 * nqN, G.X);
+    if (G.exec) {
+      HCUDA(cudaGraphLaunch(G.exec, c->stream));
+      c->launches += G.launches;
+    } else if (G.uses == 0 || G.failed) {
+      lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
+    } else {
+      // capture on the private stream (the context stream may be the legacy
+      // default stream, which cannot be captured), ordered after the staging
+      cudaGraph_t graph = nullptr;
+      cudaStream_t user = c->stream;
+      c->join(c->s_cap, user);
+      c->stream = c->s_cap;
+      const uint64_t l0 = c->launches;
+      cudaError_t e = cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        try {
+          lookup_chunk(c, pl, rk, G.X, Qc, G.S, &G.pinned);
+        } catch (...) {
+          cudaStreamEndCapture(c->s_cap, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          graph = nullptr;
+          cudaGetLastError();
+          e = cudaErrorStreamCaptureInvalidated;
+        }
+      }
+      if (e == cudaSuccess) e = cudaStreamEndCapture(c->s_cap, &graph);
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&G.exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      c->stream = user;
+      if (e != cudaSuccess) {   // not capturable here: run eagerly from now on
+        cudaGetLastError();
+        G.exec = nullptr;
+        G.failed = true;
+        c->launches = l0;
+        lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
+      } else {
+        G.launches = c->launches - l0;
+        HCUDA(cudaGraphLaunch(G.exec, c->stream));
+      }
+    }
+    G.uses++;
+    emit_outputs(c, pl, G.S, Qc, scale, out + q0 * pl->O);
   }
 }
 
@@ -1812,7 +1990,11 @@ helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys
       }
       if (p->mode != HELRM_MODE_DOUBLE) lookup_single(c, p, rk, in + q * p->C, out + q * p->O);
     }
-    if (p->mode == HELRM_MODE_DOUBLE) lookup_double(c, p, rk, in, batch, out);
+    if (p->mode == HELRM_MODE_DOUBLE) {
+      HostTimer ht_("helrm_lookup(total)");
+      lookup_double(c, p, rk, in, batch, out);
+    }
+    hostprof_dump("helrm_lookup");
   });
 }
 
@@ -1954,15 +2136,18 @@ helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_ro
           HNCCL(nccl().broadcast(cin[ci]->d, cin[ci]->d, (size_t)2 * (p->level + 1) * P.N, ncclUint64, 0, c->comm,
                                  c->stream));
       }
-      DBuf O(c, (size_t)p->O * 2 * nlN);
+      DBuf O(c, (size_t)p->O * 2 * nlN), X(c, (size_t)p->C * 2 * (p->level + 1) * P.N),
+          S(c, (size_t)p->O * 2 * p->level * P.N);
       HCUDA(cudaMemsetAsync(O.p, 0, (size_t)p->O * 2 * nlN * 8, c->stream));
-      lookup_double_part(c, p, rk, cin, 1, lo, hi, O.p);
+      stage_inputs(c, cin, p->C, 2 * (p->level + 1) * P.N, X.p);
+      lookup_double_part(c, p, rk, X.p, 1, lo, hi, O.p);
       if (c->world > 1) {
         // L5: exact sum of the partial accumulators (each < q, so < world q < 2^64), then mod q
         HNCCL(nccl().allReduce(O.p, O.p, (size_t)p->O * 2 * nlN, ncclUint64, ncclSum, c->comm, c->stream));
         for (int64_t h = 0; h < 2 * p->O; h++) launch_modred(c->dc(), O.p + (size_t)h * nlN, P.map_qp(p->level));
       }
-      lookup_finish(c, p, rk, O.p, 1, cin[0]->scale, out + q * p->O);
+      lookup_finish(c, p, rk, O.p, 1, S.p);
+      emit_outputs(c, p, S.p, 1, cin[0]->scale, out + q * p->O);
     }
   });
 }

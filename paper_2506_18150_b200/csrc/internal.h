@@ -150,10 +150,24 @@ struct DevCtx {
   Profiler* prof;
 };
 
+// host-side time per call site (HELRM_HOSTPROF=1; diagnostics of launch overhead)
+bool hostprof_on();
+void hostprof_add(const char* name, double us);
+double hostprof_now_us();
+struct HostTimer {
+  const char* name;
+  double t0;
+  explicit HostTimer(const char* n) : name(n), t0(hostprof_on() ? hostprof_now_us() : 0) {}
+  ~HostTimer() {
+    if (hostprof_on()) hostprof_add(name, hostprof_now_us() - t0);
+  }
+};
+
 // RAII: records a start event now and a stop event at scope exit
 struct ProfScope {
   const DevCtx& c;
   int idx = -1;
+  HostTimer ht;
   ProfScope(const DevCtx& c_, const char* name, double bytes = 0);
   ~ProfScope();
 };
@@ -219,6 +233,11 @@ struct KipArgs {
   // add0 + q aq and writes out0/out1 + q oq; the key is loaded once for all
   int nq = 1;
   size_t dq = 0, aq = 0, oq = 0;
+  // digit k's own limbs (rows k alpha .. of Q_l) are read from the switched
+  // polynomial itself (NTT form) when own != null: own + q ownq + row N
+  const uint64_t* own = nullptr;
+  size_t ownq = 0;
+  int alpha = 1, level = 0;
 };
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map);
 
@@ -242,6 +261,9 @@ struct KipMulti {
   // out[j] + q oq; a CTA stages qk queries' tiles and applies each key value to all
   int nq = 1, qk = 1;
   size_t dq = 0, cq = 0, oq = 0;
+  const uint64_t* own = nullptr;   // as KipArgs::own (the c1 of each query)
+  size_t ownq = 0;
+  int alpha = 1;
 };
 void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map);
 

@@ -204,8 +204,8 @@ __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint6
 // DNUM is a template parameter so that all 3 DNUM loads of a thread are in
 // flight before the first product (a runtime bound made the compiler convert
 // each digit right after its load, serialising the memory latency).
-template <int DNUM>
-__global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
+template <int DNUM, int QR>
+__global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
                                              const __grid_constant__ LimbMap map, uint32_t N) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
@@ -216,13 +216,13 @@ __global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs a, 
   const uint32_t sp = rot_src(p, a.rot, N / 2);
   const uint64_t* kb = a.key + (size_t)chain * N + p;   // D-form key
   const uint64_t* dg = a.digits + (size_t)l * N + sp;
+  const int kown = (a.own && l <= a.level) ? l / a.alpha : -1;   // digit whose own limb this row is
+  const uint64_t* og = a.own ? a.own + (size_t)l * N + sp : nullptr;
   const bool add = a.add0 != nullptr && l < a.add_rows;
   const double amul = add && a.add_mul ? fm::u2c(a.add_mul[l], q) : 1.0;
-  uint64_t dv[DNUM], kv0[DNUM], kv1[DNUM];
-  uint64_t av = add ? a.add0[(size_t)l * N + sp] : 0;
+  uint64_t kv0[DNUM], kv1[DNUM];
 #pragma unroll
   for (int k = 0; k < DNUM; k++) {
-    dv[k] = dg[(size_t)k * a.digit_stride];
     if (a.nq == 1) {
       kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
       kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
@@ -232,29 +232,42 @@ __global__ void __launch_bounds__(256) k_kip(const __grid_constant__ KipArgs a, 
     }
   }
   const size_t o = (size_t)l * N + p;
-  for (int qq = 0; qq < a.nq; qq++) {
-    if (qq > 0) {
+  // QR queries per round: QR (DNUM + 1) loads in flight against the key held in registers
+  for (int q0 = 0; q0 < a.nq; q0 += QR) {
+    const int nr = a.nq - q0 >= QR ? QR : a.nq - q0;
+    uint64_t dv[QR][DNUM], av[QR];
 #pragma unroll
-      for (int k = 0; k < DNUM; k++) dv[k] = dg[(size_t)qq * a.dq + (size_t)k * a.digit_stride];
-      if (add) av = a.add0[(size_t)qq * a.aq + (size_t)l * N + sp];
-    }
-    fm::FAcc acc0, acc1;
+    for (int r = 0; r < QR; r++) {
+      if (r < nr) {
+        const uint64_t* dq = dg + (size_t)(q0 + r) * a.dq;
 #pragma unroll
-    for (int k = 0; k < DNUM; k++) {
-      const double d = fm::u2d(dv[k]);
-      fm::fmac(acc0, d, fm::bits2d(kv0[k]));
-      fm::fmac(acc1, d, fm::bits2d(kv1[k]));
+        for (int k = 0; k < DNUM; k++)
+          dv[r][k] = k == kown ? og[(size_t)(q0 + r) * a.ownq] : dq[(size_t)k * a.digit_stride];
+        av[r] = add ? a.add0[(size_t)(q0 + r) * a.aq + (size_t)l * N + sp] : 0;
+      }
     }
-    if (add) fm::fmac(acc0, fm::u2d(av), amul);
-    uint64_t r0 = fm::c2u(fm::fred(acc0, q, qi), P.rc.q), r1 = fm::c2u(fm::fred(acc1, q, qi), P.rc.q);
-    uint64_t* o0 = a.out0 + (size_t)qq * a.oq + o;
-    uint64_t* o1 = a.out1 + (size_t)qq * a.oq + o;
-    if (a.accumulate) {
-      r0 = add_mod(r0, *o0, P.rc.q);
-      r1 = add_mod(r1, *o1, P.rc.q);
+#pragma unroll
+    for (int r = 0; r < QR; r++) {
+      if (r < nr) {
+        fm::FAcc acc0, acc1;
+#pragma unroll
+        for (int k = 0; k < DNUM; k++) {
+          const double d = fm::u2d(dv[r][k]);
+          fm::fmac(acc0, d, fm::bits2d(kv0[k]));
+          fm::fmac(acc1, d, fm::bits2d(kv1[k]));
+        }
+        if (add) fm::fmac(acc0, fm::u2d(av[r]), amul);
+        uint64_t r0 = fm::c2u(fm::fred(acc0, q, qi), P.rc.q), r1 = fm::c2u(fm::fred(acc1, q, qi), P.rc.q);
+        uint64_t* o0 = a.out0 + (size_t)(q0 + r) * a.oq + o;
+        uint64_t* o1 = a.out1 + (size_t)(q0 + r) * a.oq + o;
+        if (a.accumulate) {
+          r0 = add_mod(r0, *o0, P.rc.q);
+          r1 = add_mod(r1, *o1, P.rc.q);
+        }
+        *o0 = r0;
+        *o1 = r1;
+      }
     }
-    *o0 = r0;
-    *o1 = r1;
   }
 }
 
@@ -282,16 +295,19 @@ __global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ Ki
   const int q0 = blockIdx.z * a.qk, nqc = min(a.qk, a.nq - q0);   // this CTA's queries
   const int slab = (DNUM + 1) * span;                              // doubles per staged query
   // stage D_k (and c0) tiles + halo of every query of the CTA
+  const int kown = (a.own && has_c0) ? l / a.alpha : -1;   // digit whose own limb this row is
   for (int qq = 0; qq < nqc; qq++) {
     const uint64_t* dgq = a.digits + (size_t)(q0 + qq) * a.dq;
     const uint64_t* c0q = a.c0 + (size_t)(q0 + qq) * a.cq;
+    const uint64_t* owq = a.own ? a.own + (size_t)(q0 + qq) * a.ownq : nullptr;
     double* sq = shd + qq * slab;
     for (uint32_t e = threadIdx.x; e < span; e += tile) {
       uint32_t j = p0 - half + e;
       j = j >= n ? j - n : j;
       const size_t src = (size_t)l * N + half + j;
 #pragma unroll
-      for (int k = 0; k < DNUM; k++) sq[k * span + e] = fm::u2d(dgq[(size_t)k * a.digit_stride + src]);
+      for (int k = 0; k < DNUM; k++)
+        sq[k * span + e] = fm::u2d(k == kown ? owq[src] : dgq[(size_t)k * a.digit_stride + src]);
       if (has_c0) sq[DNUM * span + e] = fm::u2d(c0q[src]);
     }
   }
@@ -412,6 +428,78 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   }
 }
 
+// D20 L3 for a batch of queries: thread (position p of a 16-position tile,
+// query qq of an 8-query chunk, component) accumulates the kGiantPack
+// giants of its group; a term's 4 plaintext values are shared by the 16
+// threads of a position (L1 hits), each baby value is read by one thread.
+// Query chunk fastest in the grid, so a plaintext tile is reused from L2 by
+// the next chunk: plaintexts stream from HBM about once per launch.
+template <bool XD>
+__global__ void __launch_bounds__(256) k_diag_mac_q(const MacTerm* __restrict__ terms, const int4* __restrict__ groups,
+                                                    uint64_t* __restrict__ out, size_t out_stride, size_t half,
+                                                    const PrimeDev* __restrict__ primes,
+                                                    const __grid_constant__ LimbMap map, uint32_t N, int nq, size_t xq,
+                                                    size_t oq, int nqc) {
+  constexpr int G = kGiantPack;
+  constexpr int kChunk = 64;
+  __shared__ MacTerm tm[kChunk];
+  const int tid = threadIdx.x;
+  const int pl = tid & 15, qq = (tid >> 4) & 7, comp = tid >> 7;
+  const int qc = blockIdx.x % nqc, tile = blockIdx.x / nqc;
+  const int qy = qc * 8 + qq;
+  const bool act = qy < nq;
+  const uint32_t p = tile * 16 + pl;
+  const int4 gr = groups[blockIdx.y];
+  const int l = blockIdx.z;
+  const PrimeDev& P = primes[map.pr[l]];
+  const double q = P.qd, qi = P.qinv;
+  const size_t o = (size_t)l * N + p, ox = o + (size_t)(act ? qy : 0) * xq;
+  fm::FAcc acc[G];
+  int cnt = 0;
+  for (int c0 = 0; c0 < gr.y; c0 += kChunk) {
+    const int nt = min(kChunk, gr.y - c0);
+    __syncthreads();
+    for (int t = tid; t < nt; t += blockDim.x) tm[t] = terms[gr.x + c0 + t];
+    __syncthreads();
+    if (!act) continue;
+    for (int t = 0; t < nt; t += 2) {
+      const int nr = nt - t >= 2 ? 2 : 1;
+      uint64_t xv[2], uv[2][G];
+#pragma unroll
+      for (int r = 0; r < 2; r++) {
+        if (r < nr) {
+          const MacTerm& m = tm[t + r];
+          xv[r] = (comp ? m.x1 : m.x0)[ox];
+#pragma unroll
+          for (int g = 0; g < G; g++) uv[r][g] = m.u[g] ? m.u[g][o] : 0;
+        } else {
+          xv[r] = 0;
+#pragma unroll
+          for (int g = 0; g < G; g++) uv[r][g] = 0;
+        }
+      }
+      if (cnt + 2 > fm::kFAccTerms) {
+#pragma unroll
+        for (int g = 0; g < G; g++) fm::fold(acc[g], q, qi);
+        cnt = 0;
+      }
+      cnt += 2;
+#pragma unroll
+      for (int r = 0; r < 2; r++) {
+        const double x = XD ? fm::bits2d(xv[r]) : fm::u2c(xv[r], q);
+#pragma unroll
+        for (int g = 0; g < G; g++) fm::fmac(acc[g], fm::bits2d(uv[r][g]), x);
+      }
+    }
+  }
+  if (!act) return;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+    if (g < gr.w)
+      out[(size_t)(gr.z + g) * out_stride + (size_t)qy * oq + (comp ? half : 0) + o] =
+          fm::c2u(fm::fred(acc[g], q, qi), P.rc.q);
+}
+
 // D20 L5: after ncclAllReduce(uint64, sum) of partial Q_l P accumulators
 // (each < q, at most 2^13 ranks -> no wrap), reduce every word mod its prime
 __global__ void k_modred(uint64_t* __restrict__ x, const PrimeDev* __restrict__ primes,
@@ -522,15 +610,16 @@ void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
   ProfScope ps_(c, "kip", 8.0 * c.N * (2.0 * a.dnum * map.n + a.nq * (a.dnum * map.n + (a.add0 ? a.add_rows : 0) +
                                                                       (a.accumulate ? 4 : 2) * map.n)));
-  decltype(&k_kip<1>) kern = nullptr;
+  decltype(&k_kip<1, 1>) kern = nullptr;
+  const bool b = a.nq > 1;
   switch (a.dnum) {
-    case 1: kern = k_kip<1>; break;
-    case 2: kern = k_kip<2>; break;
-    case 3: kern = k_kip<3>; break;
-    case 4: kern = k_kip<4>; break;
-    case 5: kern = k_kip<5>; break;
-    case 6: kern = k_kip<6>; break;
-    case 7: kern = k_kip<7>; break;
+    case 1: kern = b ? k_kip<1, 2> : k_kip<1, 1>; break;
+    case 2: kern = b ? k_kip<2, 2> : k_kip<2, 1>; break;
+    case 3: kern = b ? k_kip<3, 2> : k_kip<3, 1>; break;
+    case 4: kern = b ? k_kip<4, 2> : k_kip<4, 1>; break;
+    case 5: kern = b ? k_kip<5, 2> : k_kip<5, 1>; break;
+    case 6: kern = b ? k_kip<6, 2> : k_kip<6, 1>; break;
+    case 7: kern = b ? k_kip<7, 2> : k_kip<7, 1>; break;
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
   kern<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
@@ -566,10 +655,18 @@ void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, 
                      bool x_dform, int nq, size_t xq, size_t oq) {
   // algorithmic bytes: every plaintext once, every distinct baby pair and output once per query
   ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + nq * (2.0 * n_x_distinct + 2.0 * n_out)));
-  auto kern = x_dform ? k_diag_mac<true> : k_diag_mac<false>;
-  kern<<<dim3((c.N + kT - 1) / kT, n_groups, map.n), kT, 0, c.stream>>>(terms, groups, out, out_stride,
-                                                                        (size_t)map.n * c.N, c.primes, map, c.N, nq,
-                                                                        xq, oq);
+  if (nq > 1) {
+    const int nqc = (nq + 7) / 8;
+    auto kq = x_dform ? k_diag_mac_q<true> : k_diag_mac_q<false>;
+    kq<<<dim3(nqc * (c.N / 16), n_groups, map.n), 256, 0, c.stream>>>(terms, groups, out, out_stride,
+                                                                       (size_t)map.n * c.N, c.primes, map, c.N, nq,
+                                                                       xq, oq, nqc);
+  } else {
+    auto kern = x_dform ? k_diag_mac<true> : k_diag_mac<false>;
+    kern<<<dim3((c.N + kT - 1) / kT, n_groups, map.n), kT, 0, c.stream>>>(terms, groups, out, out_stride,
+                                                                          (size_t)map.n * c.N, c.primes, map, c.N, 1,
+                                                                          0, 0);
+  }
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
