@@ -87,6 +87,7 @@ struct helrm_ctx {
   uint32_t* dslotpos = nullptr;
   uint32_t* dgrp = nullptr;
   uint8_t* deinv = nullptr;
+  uint16_t* dperm = nullptr;
   uint64_t* dcdt = nullptr;
   uint64_t* scratch = nullptr;
   std::map<int, LevelConst> lconst;
@@ -151,7 +152,7 @@ struct helrm_ctx {
   }
 
   DevCtx dc(cudaStream_t s = nullptr) {
-    return DevCtx{dprimes, dslotpos, dgrp, deinv, P.log_n, P.N, s ? s : stream, &launches, &prof};
+    return DevCtx{dprimes, dslotpos, dgrp, deinv, dperm, P.log_n, P.N, s ? s : stream, &launches, &prof};
   }
 
   void* dalloc(size_t bytes, cudaStream_t s = nullptr) {
@@ -800,6 +801,16 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       c->deinv = (uint8_t*)c->dalloc(N);
       c->owned.push_back(c->deinv);
       HCUDA(cudaMemcpyAsync(c->deinv, einv.data(), N, cudaMemcpyHostToDevice, c->stream));
+      // coalesced form for the pass-2 / pass-A CTAs: one uint16 smem offset per (tp, i)
+      std::vector<uint16_t> perm(N);
+      for (uint32_t x = 0; x < N / 4096; x++)
+        for (uint32_t idx = 0; idx < 4096; idx++) {
+          const uint32_t i = idx % 16, tp = idx / 16, B = grp[16 * x + i], e = einv[B * 256 + tp];
+          perm[x * 4096 + idx] = (uint16_t)(i * (256 + 16) + e + (e >> 4));   // kBlkPad, pidx (kernels_ntt.cu)
+        }
+      c->dperm = (uint16_t*)c->dalloc(N * 2);
+      c->owned.push_back(c->dperm);
+      HCUDA(cudaMemcpyAsync(c->dperm, perm.data(), N * 2, cudaMemcpyHostToDevice, c->stream));
       HCUDA(cudaStreamSynchronize(c->stream));
     }
     c->dcdt = c->upload_u64(gauss_cdt_table());

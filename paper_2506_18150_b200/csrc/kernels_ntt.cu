@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv,
+                                                      const uint16_t* __restrict__ perm,
                                                       const uint32_t* __restrict__ lidx) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   constexpr bool P1 = MODE != 1;  // MODE 2 = pass 1 whose input limbs are centred doubles (conversion output)
@@ -177,14 +178,11 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
     // permuted store: block of rank g = 16 cta + i lives at slot positions
     // (g / stride) n + (g % stride) + stride tp; for a given tp the 16 blocks are adjacent
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
+    const uint16_t* pm = perm + (size_t)blockIdx.x * kTileElems;
+    const int i = tid % 16, g = blockIdx.x * 16 + i;   // idx % 16 == tid % 16
+    uint64_t* dg = d + (size_t)(g >> lgs) * n + (g & (stride - 1));
 #pragma unroll 4
-    for (int idx = tid; idx < kTileElems; idx += kThreads) {
-      const int i = idx % 16, tp = idx / 16;
-      const int g = blockIdx.x * 16 + i;
-      const int B = grp[g];
-      const int e = einv[B * 256 + tp];
-      d[(size_t)(g >> lgs) * n + (g & (stride - 1)) + (tp << lgs)] = smu[i * kBlkPad + pidx(e)];
-    }
+    for (int idx = tid; idx < kTileElems; idx += kThreads) dg[(size_t)(idx / 16) << lgs] = smu[pm[idx]];
   }
 }
 
@@ -197,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv,
+                                                      const uint16_t* __restrict__ perm,
                                                       const double2* __restrict__ post,
                                                       const uint32_t* __restrict__ lidx) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
@@ -217,14 +216,11 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
   double r[kEPT];
   if (MODE == 1) {
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
+    const uint16_t* pm = perm + (size_t)blockIdx.x * kTileElems;
+    const int i = tid % 16, g = blockIdx.x * 16 + i;
+    const uint64_t* sg = s + (size_t)(g >> lgs) * n + (g & (stride - 1));
 #pragma unroll 4
-    for (int idx = tid; idx < kTileElems; idx += kThreads) {
-      const int i = idx % 16, tp = idx / 16;
-      const int g = blockIdx.x * 16 + i;
-      const int B = grp[g];
-      const int e = einv[B * 256 + tp];
-      sm[i * kBlkPad + pidx(e)] = u2d(s[(size_t)(g >> lgs) * n + (g & (stride - 1)) + (tp << lgs)]);
-    }
+    for (int idx = tid; idx < kTileElems; idx += kThreads) sm[pm[idx]] = u2d(sg[(size_t)(idx / 16) << lgs]);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kEPT; k++) r[k] = sm[sub * kBlkPad + pidx(kEPT * t + k)];
@@ -310,12 +306,12 @@ static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
     auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
     k1<<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
-                                                 c.ntt_einv, lidx);
+                                                 c.ntt_einv, c.ntt_perm, lidx);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
     k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, lidx);
+                                                               c.ntt_grp, c.ntt_einv, c.ntt_perm, lidx);
   }
   *c.launches += 2;
 }
@@ -329,12 +325,12 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
   {
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
     k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, nullptr, lidx);
+                                                               c.ntt_grp, c.ntt_einv, c.ntt_perm, nullptr, lidx);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
     k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                                  c.ntt_grp, c.ntt_einv, post, lidx);
+                                                                  c.ntt_grp, c.ntt_einv, c.ntt_perm, post, lidx);
   }
   *c.launches += 2;
 }
