@@ -200,6 +200,77 @@ def _oracle_parts(P, core, l, qp, c0, c1, g, rk):
     return t
 
 
+# ------------------------------------------------------------------ roofline
+def fp64_peak():
+    """FP64 FMA rate of the B200 from its unit counts and clock:
+    148 SMs x 64 FP64 FMA lanes per clock x sm_max_mhz (MEASURED_PEAKS.json)."""
+    try:
+        with open(PEAKS_PATH) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+        src = "148 SMs x 64 FP64 lanes x sm_max_mhz (MEASURED_PEAKS.json)"
+    except Exception:
+        mhz, src = 1965.0, "148 SMs x 64 FP64 lanes x 1965 MHz (B200 boost clock)"
+    return 148 * 64 * mhz * 1e6, src
+
+
+NTT_FP64_OPS_PER_BFLY = 8   # exact FP64 modular butterfly: 6 (product split + quotient) + 2 (add, sub)
+
+
+def ncu_traffic():
+    """dram bytes (read + write) per launch of the NTT passes, from the
+    committed ncu --set full capture of `bench.py --ncu-step`
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def roofline_from_stats(stats, steps, cfg):
+    """Dominant kernel = the forward NTT (passes 1 + 2, ~35% of the step):
+    FP64-pipe bound, so achieved butterflies/s against the FP64 FMA rate / 8.
+    The HBM-bound kernels (diagonal MAC, key switches) are listed with their
+    algorithmic GB/s against the measured HBM copy bandwidth."""
+    N, logN = cfg.N, int(round(math.log2(cfg.N)))
+    p1, p2 = stats.get("ntt_fwd_p1"), stats.get("ntt_fwd_p2")
+    peak_fp64, src = fp64_peak()
+    peak_bfly = peak_fp64 / NTT_FP64_OPS_PER_BFLY / 1e9
+    hbm, hsrc = hbm_peak()
+    out = {"bound": "alu", "kernel": "ntt_fwd (passes 1+2, FP64 pipe)", "achieved": None, "peak": round(peak_bfly, 1),
+           "unit": "Gbutterfly/s", "frac": None, "traffic": None,
+           "peak_source": f"{src} / {NTT_FP64_OPS_PER_BFLY} FP64 ops per exact butterfly"}
+    if p1 and p2:
+        limbs = p1["bytes"] / (8.0 * N)                 # limb transforms in the profiled steps
+        ms = p1["ms"] + p2["ms"]
+        bfly = limbs * (N // 2) * logN
+        ach = bfly / (ms / 1e3) / 1e9
+        tot = sum(v["ms"] for v in stats.values())
+        tr = ncu_traffic()
+        out.update({"achieved": round(ach, 1), "frac": round(ach / peak_bfly, 4),
+                    "launches_per_step": (p1["count"] + p2["count"]) // steps,
+                    "limb_transforms_per_step": round(limbs / steps, 1),
+                    "avg_transform_us": round(ms * 1e3 / limbs, 4),
+                    "share_of_step": round(ms / tot, 3),
+                    "algorithmic_bytes_per_limb": 16 * N,
+                    "traffic": tr.get("ntt_fwd_bytes_per_limb"),
+                    "traffic_unit": "dram bytes per limb transform (ncu, profiles/ncu_traffic.json)"})
+    hk = {}
+    for k in ("diag_mac", "kip_multi", "kip"):
+        v = stats.get(k)
+        if v:
+            gbs = v["bytes"] / (v["ms"] / 1e3) / 1e9
+            hk[k] = {"achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
+                     "ms_per_step": round(v["ms"] / steps, 4), "traffic": tr_get(k)}
+    out["hbm_kernels"] = hk
+    out["hbm_peak_source"] = hsrc
+    return out
+
+
+def tr_get(k):
+    return ncu_traffic().get(k + "_bytes_per_launch")
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_gpu(args, world, rank, local):
     import torch
@@ -268,15 +339,8 @@ def run_gpu(args, world, rank, local):
         step(i)
     stats = ctx.profile_stats()
     ctx.profile(False)
-    top = max(stats.items(), key=lambda kv: kv[1]["ms"])
-    peak, peak_src = hbm_peak()
+    roofline = roofline_from_stats(stats, args.steps, cfg)
     total_kernel_ms = sum(v["ms"] for v in stats.values())
-    achieved = top[1]["bytes"] / (top[1]["ms"] / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-                "share_of_step": round(top[1]["ms"] / total_kernel_ms, 3),
-                "bytes_per_launch": round(top[1]["bytes"] / top[1]["count"]),
-                "avg_launch_us": round(top[1]["ms"] * 1e3 / top[1]["count"], 2)}
     step_bytes = sum(v["bytes"] for v in stats.values()) / args.steps
     kernels = {k: {"count": v["count"] // args.steps, "ms_per_step": round(v["ms"] / args.steps, 4),
                    "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in
@@ -320,6 +384,8 @@ def run_gpu(args, world, rank, local):
         secondary["dist_b1"] = dist_b1(args, ctx, helrm, torch, stream, plan, rk, cts, world, rank)
     if not args.skip_micro:
         secondary.update(micro(args, ctx, helrm, torch, stream, sk, cfg, world))
+    if not args.skip_llm:
+        secondary["llm_128_tokens"] = llm_lookup(args, helrm, torch, stream, world, dev)
 
     return {
         "value": value, "ms": ms / args.steps, "launches": launches, "clocks": clk.summary(),
@@ -388,6 +454,55 @@ def batch_lookup(args, ctx, helrm, torch, stream, plan, rk, cts, world, B=64):
             "inputs": f"{len(cts)} encrypted queries cycled"}
 
 
+def llm_lookup(args, helrm, torch, stream, world, dev):
+    """BASELINE.json configs[3]: LLM-style batched token embedding -- 128
+    tokens of the 50257 x 768 table (base 256, 2 digits), layout L2 (4 input /
+    4 output ciphertexts, 1279 distinct pre-rotated diagonals shared by the 4
+    blocks), N = 2^16, 20 + 4 primes.  Own context; device time per 128-token
+    lookup, max over ranks; token-lookups/s = 128 / t."""
+    import synth
+    w = synth.make_workload("llm")
+    cfg = w.config
+    P = helrm.params_from_config(cfg)
+    ctx = helrm.Context(P, dev, stream.cuda_stream)
+    t0 = time.time()
+    T = helrm.tables_create(P, w.tables, w.n_dense)
+    plan = helrm.plan_create(ctx, T, cfg.level)
+    info = plan.info()
+    sk = helrm.sk_gen(ctx, cfg.seed)
+    pk = helrm.pk_gen(ctx, sk, cfg.seed)
+    rk = helrm.rotkeys_gen(ctx, sk, plan.galois(cfg.N), cfg.seed)
+    x = helrm.encode_query(T, w.indices[0], w.dense[0], info.n_in_cts * cfg.n_slots)
+    cts = [helrm.encrypt(ctx, pk, x[c * cfg.n_slots:(c + 1) * cfg.n_slots], cfg.level, (cfg.seed << 20) | c)
+           for c in range(info.n_in_cts)]
+    ctx.sync()
+    setup = time.time() - t0
+    for _ in range(3):
+        for o in helrm.lookup(ctx, plan, rk, cts):
+            o.close()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record(stream)
+    for _ in range(reps):
+        for o in helrm.lookup(ctx, plan, rk, cts):
+            o.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / reps
+    tokens = w.indices.shape[1]
+    res = {"tokens_per_lookup": tokens, "ms_per_lookup": round(ms, 3),
+           "token_lookups_per_s": round(world * tokens * 1e3 / ms, 1), "in_cts": info.n_in_cts,
+           "out_cts": info.n_out_cts, "unique_diagonals": info.n_unique, "n1": info.n1,
+           "rotation_keys": info.n_rotations, "setup_s": round(setup, 1),
+           "diag_GiB": round(info.diag_bytes / 2**30, 2), "keys_GiB": round(rk.nbytes() / 2**30, 2)}
+    for h in (rk, pk, sk, plan, T):
+        h.close()
+    ctx.close()
+    return res
+
+
 def micro(args, ctx, helrm, torch, stream, sk, cfg, world):
     """configs[4]: NTT GB/s over 1024 cts x 2 x 24 limbs; hoisted rotations/s."""
     N, L = cfg.N, cfg.level
@@ -453,6 +568,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-micro", action="store_true")
     ap.add_argument("--skip-batch", action="store_true", help="skip the Criteo batch-64 measurement")
+    ap.add_argument("--skip-llm", action="store_true", help="skip the LLM-style 128-token measurement")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--micro-cts", type=int, default=1024)
     ap.add_argument("--rot-cts", type=int, default=8)
