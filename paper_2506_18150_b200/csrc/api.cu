@@ -87,7 +87,7 @@ struct helrm_ctx {
   uint32_t* dslotpos = nullptr;
   uint32_t* dgrp = nullptr;
   uint8_t* deinv = nullptr;
-  uint16_t* dperm = nullptr;
+  uint8_t* dtpos = nullptr;
   uint64_t* dcdt = nullptr;
   uint64_t* scratch = nullptr;
   std::map<int, LevelConst> lconst;
@@ -152,7 +152,7 @@ struct helrm_ctx {
   }
 
   DevCtx dc(cudaStream_t s = nullptr) {
-    return DevCtx{dprimes, dslotpos, dgrp, deinv, dperm, P.log_n, P.N, s ? s : stream, &launches, &prof};
+    return DevCtx{dprimes, dslotpos, dgrp, deinv, dtpos, P.log_n, P.N, s ? s : stream, &launches, &prof};
   }
 
   void* dalloc(size_t bytes, cudaStream_t s = nullptr) {
@@ -801,16 +801,20 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       c->deinv = (uint8_t*)c->dalloc(N);
       c->owned.push_back(c->deinv);
       HCUDA(cudaMemcpyAsync(c->deinv, einv.data(), N, cudaMemcpyHostToDevice, c->stream));
-      // coalesced form for the pass-2 / pass-A CTAs: one uint16 smem offset per (tp, i)
-      std::vector<uint16_t> perm(N);
-      for (uint32_t x = 0; x < N / 4096; x++)
-        for (uint32_t idx = 0; idx < 4096; idx++) {
-          const uint32_t i = idx % 16, tp = idx / 16, B = grp[16 * x + i], e = einv[B * 256 + tp];
-          perm[x * 4096 + idx] = (uint16_t)(i * (256 + 16) + e + (e >> 4));   // kBlkPad, pidx (kernels_ntt.cu)
+      // rank of each element's slot position within its block (inverse of einv); the
+      // pass-2 / pass-A swizzle needs tp(16 t + k) mod 16 distinct over t for every k
+      std::vector<uint8_t> tpos(N);
+      for (uint32_t B = 0; B < nb; B++)
+        for (uint32_t tp = 0; tp < 256; tp++) tpos[B * 256 + einv[B * 256 + tp]] = (uint8_t)tp;
+      for (uint32_t B = 0; B < nb; B++)
+        for (uint32_t k = 0; k < 16; k++) {
+          uint32_t seen = 0;
+          for (uint32_t t = 0; t < 16; t++) seen |= 1u << (tpos[B * 256 + 16 * t + k] & 15);
+          need(seen == 0xffffu, HELRM_ERR_CONFIG, "slot-order swizzle invariant");
         }
-      c->dperm = (uint16_t*)c->dalloc(N * 2);
-      c->owned.push_back(c->dperm);
-      HCUDA(cudaMemcpyAsync(c->dperm, perm.data(), N * 2, cudaMemcpyHostToDevice, c->stream));
+      c->dtpos = (uint8_t*)c->dalloc(N);
+      c->owned.push_back(c->dtpos);
+      HCUDA(cudaMemcpyAsync(c->dtpos, tpos.data(), N, cudaMemcpyHostToDevice, c->stream));
       HCUDA(cudaStreamSynchronize(c->stream));
     }
     c->dcdt = c->upload_u64(gauss_cdt_table());
@@ -1679,7 +1683,9 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   const size_t zq = (size_t)Qc;   // pairs per z
   DBuf AB(c, (size_t)n_out * zq * 2 * nlN), Bp(c, (size_t)n_out * zq * nqN), D2(c, (size_t)n_out * zq * dn * nlN);
   MacDev md(c, ml, pinned);
-  static const bool pipe = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
+  // (serialised while the per-kernel profiler is on, so each kernel's events time it alone)
+  static const bool pipe_env = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
+  const bool pipe = pipe_env && !c->prof.on;
   cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream;
   if (pipe) {
     c->join(sn, c->stream);

@@ -144,8 +144,7 @@ struct DevCtx {
   const uint32_t* slotpos;    // [N] slot position of bitrev index r
   const uint32_t* ntt_grp;    // [N/256] 256-blocks ordered by (half, slot residue): 16 per pass-2 CTA
   const uint8_t* ntt_einv;    // [N] per block: element index of its tp-th smallest slot position
-  const uint16_t* ntt_perm;   // [N/4096][4096] pass-2 CTA x, idx = 16 tp + i: smem offset of the element
-                              // of block grp[16x + i] with the tp-th smallest slot position
+  const uint8_t* ntt_tpos;    // [N] per block: rank of element e's slot position within the block
   uint32_t log_n, N;
   cudaStream_t stream;
   uint64_t* launches;         // host counter

@@ -74,12 +74,12 @@ __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double 
 //   MODE 1 (pass 2): sub-transform = 256-block B; twiddles tw2[B][...]:
 //     [0, 15): phase A, 2^st - 1 + i_loc;  15 + 16 j + t: thread t's phase-B twiddle j.
 template <int SLOG, int MODE>
-__global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+__global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv,
-                                                      const uint16_t* __restrict__ perm,
+                                                      const uint8_t* __restrict__ tpos,
                                                       const uint32_t* __restrict__ lidx) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   constexpr bool P1 = MODE != 1;  // MODE 2 = pass 1 whose input limbs are centred doubles (conversion output)
@@ -170,19 +170,32 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
       d[(size_t)e * 256 + gsub] = (uint64_t)__double_as_longlong(r[k]);
     }
   } else {
+    // slot-order store through shared memory: element e of block `sub` has
+    // rank tp(e) among its block's slot positions; it goes to
+    // smem[tp 16 + (sub ^ (tp & 15))].  tp(16 t + k) mod 16 is distinct over
+    // the 16 threads t of a block for every k (checked for every block at
+    // context creation), so the swizzled scatter and the row-wise read are
+    // both bank-conflict free.
+    const uint4 tv = *reinterpret_cast<const uint4*>(tpos + (size_t)gsub * 256 + kEPT * t);
+    const uint32_t tw4[4] = {tv.x, tv.y, tv.z, tv.w};
     __syncthreads();
     uint64_t* smu = reinterpret_cast<uint64_t*>(sm);
 #pragma unroll
-    for (int k = 0; k < kEPT; k++) smu[sub * kBlkPad + pidx(kEPT * t + k)] = d2u(r[k], q, qi, P.rc.q);
+    for (int k = 0; k < kEPT; k++) {
+      const int tp = (tw4[k >> 2] >> (8 * (k & 3))) & 0xff;
+      smu[tp * 16 + (sub ^ (tp & 15))] = d2u(r[k], q, qi, P.rc.q);
+    }
     __syncthreads();
-    // permuted store: block of rank g = 16 cta + i lives at slot positions
-    // (g / stride) n + (g % stride) + stride tp; for a given tp the 16 blocks are adjacent
+    // block of rank g = 16 cta + i lives at slot positions (g / stride) n +
+    // (g % stride) + stride tp; for a given tp the 16 blocks are adjacent
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
-    const uint16_t* pm = perm + (size_t)blockIdx.x * kTileElems;
     const int i = tid % 16, g = blockIdx.x * 16 + i;   // idx % 16 == tid % 16
     uint64_t* dg = d + (size_t)(g >> lgs) * n + (g & (stride - 1));
 #pragma unroll 4
-    for (int idx = tid; idx < kTileElems; idx += kThreads) dg[(size_t)(idx / 16) << lgs] = smu[pm[idx]];
+    for (int idx = tid; idx < kTileElems; idx += kThreads) {
+      const int tp = idx / 16;
+      dg[(size_t)tp << lgs] = smu[tp * 16 + (i ^ (tp & 15))];
+    }
   }
 }
 
@@ -190,12 +203,12 @@ __global__ void __launch_bounds__(kThreads) k_ntt_fwd(const uint64_t* __restrict
 //   MODE 1 (pass A): blocks gathered from slot order, the last 8 stages;
 //   MODE 0 (pass B): columns, the first s1 stages, times N^-1, natural order.
 template <int SLOG, int MODE>
-__global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+__global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv,
-                                                      const uint16_t* __restrict__ perm,
+                                                      const uint8_t* __restrict__ tpos,
                                                       const double2* __restrict__ post,
                                                       const uint32_t* __restrict__ lidx) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
@@ -216,14 +229,21 @@ __global__ void __launch_bounds__(kThreads) k_ntt_inv(const uint64_t* __restrict
   double r[kEPT];
   if (MODE == 1) {
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
-    const uint16_t* pm = perm + (size_t)blockIdx.x * kTileElems;
     const int i = tid % 16, g = blockIdx.x * 16 + i;
     const uint64_t* sg = s + (size_t)(g >> lgs) * n + (g & (stride - 1));
 #pragma unroll 4
-    for (int idx = tid; idx < kTileElems; idx += kThreads) sm[pm[idx]] = u2d(sg[(size_t)(idx / 16) << lgs]);
+    for (int idx = tid; idx < kTileElems; idx += kThreads) {   // swizzled gather, as the forward store
+      const int tp = idx / 16;
+      sm[tp * 16 + (i ^ (tp & 15))] = u2d(sg[(size_t)tp << lgs]);
+    }
+    const uint4 tv = *reinterpret_cast<const uint4*>(tpos + (size_t)gsub * 256 + kEPT * t);
+    const uint32_t tw4[4] = {tv.x, tv.y, tv.z, tv.w};
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kEPT; k++) r[k] = sm[sub * kBlkPad + pidx(kEPT * t + k)];
+    for (int k = 0; k < kEPT; k++) {
+      const int tp = (tw4[k >> 2] >> (8 * (k & 3))) & 0xff;
+      r[k] = sm[tp * 16 + (sub ^ (tp & 15))];
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
@@ -306,12 +326,12 @@ static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
     auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
     k1<<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
-                                                 c.ntt_einv, c.ntt_perm, lidx);
+                                                 c.ntt_einv, c.ntt_tpos, lidx);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
     k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, c.ntt_perm, lidx);
+                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, lidx);
   }
   *c.launches += 2;
 }
@@ -325,12 +345,12 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
   {
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
     k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, c.ntt_perm, nullptr, lidx);
+                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, nullptr, lidx);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
     k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                                  c.ntt_grp, c.ntt_einv, c.ntt_perm, post, lidx);
+                                                                  c.ntt_grp, c.ntt_einv, c.ntt_tpos, post, lidx);
   }
   *c.launches += 2;
 }
