@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
   // QR queries per round: QR (DNUM + 1) loads in flight against the key held in registers
   for (int q0 = 0; q0 < a.nq; q0 += QR) {
     const int nr = a.nq - q0 >= QR ? QR : a.nq - q0;
-    uint64_t dv[QR][DNUM], av[QR];
+    uint64_t dv[QR][DNUM], av[QR], pv0[QR], pv1[QR];
 #pragma unroll
     for (int r = 0; r < QR; r++) {
       if (r < nr) {
@@ -244,6 +244,9 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
         for (int k = 0; k < DNUM; k++)
           dv[r][k] = k == kown ? og[(size_t)(q0 + r) * a.ownq] : dq[(size_t)k * a.digit_stride];
         av[r] = add ? a.add0[(size_t)(q0 + r) * a.aq + (size_t)l * N + sp] : 0;
+        // the accumulated outputs are fetched with the operands (one memory round trip per thread)
+        pv0[r] = a.accumulate ? a.out0[(size_t)(q0 + r) * a.oq + o] : 0;
+        pv1[r] = a.accumulate ? a.out1[(size_t)(q0 + r) * a.oq + o] : 0;
       }
     }
 #pragma unroll
@@ -261,8 +264,8 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
         uint64_t* o0 = a.out0 + (size_t)(q0 + r) * a.oq + o;
         uint64_t* o1 = a.out1 + (size_t)(q0 + r) * a.oq + o;
         if (a.accumulate) {
-          r0 = add_mod(r0, *o0, P.rc.q);
-          r1 = add_mod(r1, *o1, P.rc.q);
+          r0 = add_mod(r0, pv0[r], P.rc.q);
+          r1 = add_mod(r1, pv1[r], P.rc.q);
         }
         *o0 = r0;
         *o1 = r1;
