@@ -131,7 +131,7 @@ struct helrm_ctx {
   // side streams of the pipelined giant steps (lookup_double_part): NTT work
   // (FP64-bound) on s_ntt at the highest priority, key switches (HBM-bound)
   // on s_kip, so they overlap the diagonal MACs on the context stream
-  cudaStream_t s_ntt = nullptr, s_kip = nullptr;
+  cudaStream_t s_ntt = nullptr, s_kip = nullptr, s_mac = nullptr;
   cudaStream_t s_cap = nullptr;   // private stream the lookup graphs are captured on
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
@@ -151,8 +151,9 @@ struct helrm_ctx {
     HCUDA(cudaStreamWaitEvent(s, e, 0));
   }
 
-  DevCtx dc(cudaStream_t s = nullptr) {
-    return DevCtx{dprimes, dslotpos, dgrp, deinv, dtpos, P.log_n, P.N, s ? s : stream, &launches, &prof};
+  int persist = 0;                // persistent CTAs per SM for the HBM-bound kernels (0 = full grids)
+  DevCtx dc(cudaStream_t s = nullptr, int pers = 0) {
+    return DevCtx{dprimes, dslotpos, dgrp, deinv, dtpos, P.log_n, P.N, s ? s : stream, pers, &launches, &prof};
   }
 
   void* dalloc(size_t bytes, cudaStream_t s = nullptr) {
@@ -488,8 +489,9 @@ static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int 
 }
 
 // D16 for G polynomials: y_g = y + g ys ([l+1+K][N]) -> out_g = out + g os ([l+1][N])
+// (accumulate: out += ModDown(y); the finishing (y - t) P^-1 runs in the NTT's pass-2 epilogue)
 static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uint32_t l, uint64_t* out, size_t os,
-                          cudaStream_t st = nullptr) {
+                          cudaStream_t st = nullptr, bool accumulate = false) {
   const Params& P = c->P;
   const size_t N = P.N, nq = l + 1;
   const LevelConst& lc = level_const(c, l);
@@ -498,8 +500,15 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   launch_ntt_inv(c->dc(st), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
                  lc.moddown_post);
   launch_conv_rows(c->dc(st), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
-  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true);
-  launch_sub_scale(c->dc(st), y, ys, t.p, nq * N, out, os, G, P.map_q(l), lc.pinv, lc.pinvs);
+  NttEpi epi;
+  epi.y = y;
+  epi.ys = ys;
+  epi.out = out;
+  epi.os = os;
+  epi.s = lc.pinv;
+  epi.sp = lc.pinvs;
+  epi.accumulate = accumulate ? 1 : 0;
+  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true, nullptr, &epi);
 }
 
 static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t* out) {
@@ -523,9 +532,15 @@ static void rescale_ct(helrm_ctx* c, const uint64_t* x, uint32_t l, uint64_t* ou
   DBuf xl(c, 2 * G * N), r(c, 2 * G * l * N);
   ntt_inv(c, x + l * N, xl.p, 2 * G, P.map_range(l, 1), (l + 1) * N, N);
   launch_rescale_prep(c->dc(), xl.p, N, P.primes[l], r.p, l * N, 2 * G, P.map_q(l - 1));
-  ntt_fwd(c, r.p, r.p, 2 * G * l, P.map_q(l - 1));
   const LevelConst& lc = level_const(c, l);
-  launch_sub_scale(c->dc(), x, (l + 1) * N, r.p, l * N, out, l * N, 2 * G, P.map_q(l - 1), lc.qlinv, lc.qlinvs);
+  NttEpi epi;   // x_i' = (x_i - NTT(r)_i) q_l^-1, fused into the NTT's pass 2
+  epi.y = x;
+  epi.ys = (l + 1) * N;
+  epi.out = out;
+  epi.os = l * N;
+  epi.s = lc.qlinv;
+  epi.sp = lc.qlinvs;
+  launch_ntt_fwd(c->dc(), r.p, r.p, c->scratch, 2 * G * l, P.map_q(l - 1), 0, 0, false, nullptr, &epi);
 }
 
 static uint32_t rot_of_galois(helrm_ctx* c, uint64_t g) {
@@ -684,10 +699,15 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
     {
       int lo_prio = 0, hi_prio = 0;
       HCUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+      // HELRM_PRIO 1: NTT stream high priority; 3: MAC / key-switch streams high (persistent HBM
+      // kernels get their SM slots first, the NTT fills the rest); 0: all equal
       const char* e = getenv("HELRM_PRIO");
       const int mode = e ? atoi(e) : 1;
       HCUDA(cudaStreamCreateWithPriority(&c->s_ntt, cudaStreamNonBlocking, mode == 1 ? hi_prio : lo_prio));
-      HCUDA(cudaStreamCreateWithPriority(&c->s_kip, cudaStreamNonBlocking, mode == 2 ? hi_prio : lo_prio));
+      HCUDA(cudaStreamCreateWithPriority(&c->s_kip, cudaStreamNonBlocking, mode == 3 ? hi_prio : lo_prio));
+      HCUDA(cudaStreamCreateWithPriority(&c->s_mac, cudaStreamNonBlocking, mode == 3 ? hi_prio : lo_prio));
+      const char* pe = getenv("HELRM_PERSIST");
+      c->persist = pe ? atoi(pe) : 0;
       HCUDA(cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
     }
     cudaMemPool_t pool;
@@ -838,6 +858,7 @@ void helrm_ctx_destroy(helrm_ctx* c) {
   cudaStreamSynchronize(c->stream);
   if (c->s_ntt) cudaStreamSynchronize(c->s_ntt);
   if (c->s_kip) cudaStreamSynchronize(c->s_kip);
+  if (c->s_mac) cudaStreamSynchronize(c->s_mac);
   for (auto& kv : c->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (kv.second.pinned) cudaFreeHost(kv.second.pinned);
@@ -852,6 +873,7 @@ void helrm_ctx_destroy(helrm_ctx* c) {
   if (c->s_ntt) cudaStreamDestroy(c->s_ntt);
   if (c->s_kip) cudaStreamDestroy(c->s_kip);
   if (c->s_cap) cudaStreamDestroy(c->s_cap);
+  if (c->s_mac) cudaStreamDestroy(c->s_mac);
   delete c;
 }
 
@@ -1579,7 +1601,8 @@ struct MacDev {
 
 // run the batched MAC of groups [g0, g1) into out (pair z at out + z out_stride)
 static void run_macs(helrm_ctx* c, const MacList& ml, const MacDev& md, size_t g0, size_t g1, uint64_t* out,
-                     size_t out_stride, const LimbMap& map, bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0) {
+                     size_t out_stride, const LimbMap& map, bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0,
+                     cudaStream_t st = nullptr, int pers = 0) {
   if (g1 <= g0) return;
   double nu = 0;
   int nout = 0;
@@ -1590,8 +1613,8 @@ static void run_macs(helrm_ctx* c, const MacList& ml, const MacDev& md, size_t g
   // algorithmic bytes: plaintexts of the groups, each distinct baby pair once per lookup (charged to the
   // first launch), the outputs
   const double nx = g0 == 0 ? ml.n_x : 0.0;
-  launch_diag_mac(c->dc(), (const MacTerm*)md.terms.p, (const int4*)md.groups.p + g0, (int)(g1 - g0), nu, nx, nout,
-                  out, out_stride, map, x_dform, nq, xq, oq);
+  launch_diag_mac(c->dc(st, pers), (const MacTerm*)md.terms.p, (const int4*)md.groups.p + g0, (int)(g1 - g0), nu,
+                  nx, nout, out, out_stride, map, x_dform, nq, xq, oq);
 }
 
 static void run_macs_all(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_stride, const LimbMap& map,
@@ -1686,10 +1709,12 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   // (serialised while the per-kernel profiler is on, so each kernel's events time it alone)
   static const bool pipe_env = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
   const bool pipe = pipe_env && !c->prof.on;
-  cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream;
+  cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream, sm = pipe ? c->s_mac : c->stream;
+  const int pers = pipe ? c->persist : 0;
   if (pipe) {
     c->join(sn, c->stream);
     c->join(sk, c->stream);   // O zeroed, babies ready
+    c->join(sm, c->stream);
   }
   const LimbMap m2 = map_twice(mqp);
   auto Oq = [&](int z) { return Oall + (size_t)ml.oi[z].first * zq * 2 * nlN; };
@@ -1703,8 +1728,8 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   for (size_t gp = 0; gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
     const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
-    run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN);
-    if (pipe) c->join(sn, c->stream);
+    run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
+    if (pipe) c->join(sn, sm);
     std::vector<int> rot;   // rotating pairs of the chunk (zero giants need no key switch)
     for (int z = z0; z < z1; z++)
       if (pl->giants[ml.oi[z].first][ml.oi[z].second] % (int64_t)P.n != 0) rot.push_back(z);
@@ -1743,18 +1768,19 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
           a.ownq = nqN;
           a.alpha = (int)P.alpha;
           a.level = (int)l;
-          launch_kip(c->dc(sk), a, mqp);
+          launch_kip(c->dc(sk, pers), a, mqp);
         }
       }
       zdone = zend;
       r0 = r1;
     }
-    if (pipe) c->join(sk, c->stream);
+    if (pipe) c->join(sk, sm);
     for (int z = zdone; z < z1; z++) zero_giant(z);   // zero giants with no rotating pair after them
   }
   if (pipe) {
     c->join(c->stream, sn);
     c->join(c->stream, sk);
+    c->join(c->stream, sm);
   }
 }
 
@@ -1767,8 +1793,7 @@ static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t
   if (mbar >= n) return;
   const size_t N = P.N, nq = l + 1, nqN = nq * N, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
   const LevelConst& lc = level_const(c, l);
-  DBuf D(c, (size_t)Qc * dn * nlN), T(c, (size_t)Qc * 2 * nlN), R(c, (size_t)Qc * 2 * nqN);
-  LimbMap m2 = map_twice(P.map_q(l));
+  DBuf D(c, (size_t)Qc * dn * nlN), T(c, (size_t)Qc * 2 * nlN);
   for (int64_t r = mbar; r < n; r *= 2) {
     const uint64_t g = galois_of_rot(c, r);
     modup_batch(c, S + nqN, 2 * nqN, Qc, l, D.p, nullptr, false);
@@ -1795,9 +1820,7 @@ static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t
     a.aq = 2 * nqN;
     a.oq = 2 * nlN;
     launch_kip(c->dc(), a, P.map_qp(l));
-    moddown_batch(c, T.p, nlN, 2 * Qc, l, R.p, nqN);
-    for (int q = 0; q < Qc; q++)
-      launch_binary(c->dc(), 0, S + (size_t)q * 2 * nqN, R.p + (size_t)q * 2 * nqN, S + (size_t)q * 2 * nqN, m2);
+    moddown_batch(c, T.p, nlN, 2 * Qc, l, S, nqN, nullptr, true);   // S += Rotate(S)
   }
 }
 
@@ -1926,7 +1949,7 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
         }
       }
       if (e == cudaSuccess) e = cudaStreamEndCapture(c->s_cap, &graph);
-      if (e == cudaSuccess) e = cudaGraphInstantiate(&G.exec, graph, 0);
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&G.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
       if (graph) cudaGraphDestroy(graph);
       c->stream = user;
       if (e != cudaSuccess) {   // not capturable here: run eagerly from now on

@@ -147,6 +147,7 @@ struct DevCtx {
   const uint8_t* ntt_tpos;    // [N] per block: rank of element e's slot position within the block
   uint32_t log_n, N;
   cudaStream_t stream;
+  int persist;                // > 0: HBM-bound MAC / key-switch kernels run persistent, persist CTAs per SM
   uint64_t* launches;         // host counter
   Profiler* prof;
 };
@@ -173,6 +174,18 @@ struct ProfScope {
   ~ProfScope();
 };
 
+// Optional epilogue of the forward NTT (the last step of ModDown D16 and of
+// rescale D17): instead of storing t = NTT(.) the pass-2 kernel stores, for
+// limb l of poly g,  out[g][l] (+)= (y[g][l] - t[g][l]) * s[l]  mod q_l.
+struct NttEpi {
+  const uint64_t* y = nullptr;   // y + g ys + l N
+  size_t ys = 0;
+  uint64_t* out = nullptr;       // out + g os + l N
+  size_t os = 0;
+  const uint64_t* s = nullptr;   // per-limb factor and its Shoup companion
+  const uint64_t* sp = nullptr;
+  int accumulate = 0;            // out += instead of out =
+};
 // NTT over n_total limbs: limb y = (poly y / map.n, limb y % map.n) lives at
 // src + (y / map.n) * src_stride + (y % map.n) * N (same for dst; stride 0 =
 // contiguous polys of map.n limbs).  src == dst allowed.
@@ -180,7 +193,7 @@ struct ProfScope {
 // lidx (optional device table): launch limb v is layout limb lidx[v]
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0, bool din = false,
-                    const uint32_t* lidx = nullptr);
+                    const uint32_t* lidx = nullptr, const NttEpi* epi = nullptr);
 // post (optional, per limb of map): final factor (w, w/q) replacing N^-1
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0,

@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
                                                       const uint32_t* __restrict__ grp,
                                                       const uint8_t* __restrict__ einv,
                                                       const uint8_t* __restrict__ tpos,
-                                                      const uint32_t* __restrict__ lidx) {
+                                                      const uint32_t* __restrict__ lidx,
+                                                      const __grid_constant__ NttEpi epi) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   constexpr bool P1 = MODE != 1;  // MODE 2 = pass 1 whose input limbs are centred doubles (conversion output)
   __shared__ double sm[P1 ? kTileElems : 16 * kBlkPad];
@@ -190,11 +191,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
     // (g % stride) + stride tp; for a given tp the 16 blocks are adjacent
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
     const int i = tid % 16, g = blockIdx.x * 16 + i;   // idx % 16 == tid % 16
-    uint64_t* dg = d + (size_t)(g >> lgs) * n + (g & (stride - 1));
+    const size_t pbase = (size_t)(g >> lgs) * n + (g & (stride - 1));
+    if (epi.out == nullptr) {
+      uint64_t* dg = d + pbase;
 #pragma unroll 4
-    for (int idx = tid; idx < kTileElems; idx += kThreads) {
-      const int tp = idx / 16;
-      dg[(size_t)tp << lgs] = smu[tp * 16 + (i ^ (tp & 15))];
+      for (int idx = tid; idx < kTileElems; idx += kThreads) {
+        const int tp = idx / 16;
+        dg[(size_t)tp << lgs] = smu[tp * 16 + (i ^ (tp & 15))];
+      }
+    } else {   // fused ModDown / rescale finish: out (+)= (y - t) s mod q
+      const size_t pg = gl / map.n, lg = gl % map.n;
+      const uint64_t qq = P.rc.q, sv = epi.s[lg], svp = epi.sp[lg];
+      const uint64_t* yg = epi.y + pg * epi.ys + lg * (size_t)N + pbase;
+      uint64_t* og = epi.out + pg * epi.os + lg * (size_t)N + pbase;
+#pragma unroll 4
+      for (int idx = tid; idx < kTileElems; idx += kThreads) {
+        const int tp = idx / 16;
+        const size_t at = (size_t)tp << lgs;
+        uint64_t v = shoup(sub_mod(yg[at], smu[tp * 16 + (i ^ (tp & 15))], qq), sv, svp, qq);
+        if (epi.accumulate) v = add_mod(v, og[at], qq);
+        og[at] = v;
+      }
     }
   }
 }
@@ -319,19 +336,20 @@ size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)
 
 template <int SLOG>
 static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
-                      const LimbMap& map, size_t off, size_t ss, size_t ds, bool din, const uint32_t* lidx) {
+                      const LimbMap& map, size_t off, size_t ss, size_t ds, bool din, const uint32_t* lidx,
+                      const NttEpi& epi) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
     auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
     k1<<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
-                                                 c.ntt_einv, c.ntt_tpos, lidx);
+                                                 c.ntt_einv, c.ntt_tpos, lidx, epi);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
     k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, lidx);
+                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, lidx, epi);
   }
   *c.launches += 2;
 }
@@ -357,7 +375,8 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
 
 template <bool FWD>
 static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, const double2* post, bool din, const uint32_t* lidx) {
+                    const LimbMap& map, size_t ss, size_t ds, const double2* post, bool din, const uint32_t* lidx,
+                    const NttEpi& epi = NttEpi{}) {
   if (ss == 0) ss = (size_t)map.n * c.N;
   if (ds == 0) ds = (size_t)map.n * c.N;
   const size_t ch = chunk_limbs(c.N);
@@ -365,7 +384,7 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);
 #define HELRM_NTT_CASE(LG, SL)                                                  \
   case LG:                                                                      \
-    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din, lidx);    \
+    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din, lidx, epi);    \
     else inv_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, post, lidx);        \
     break;
     switch (c.log_n) {
@@ -382,8 +401,8 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
 }
 
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx) {
-  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din, lidx);
+                    const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi* epi) {
+  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din, lidx, epi ? *epi : NttEpi{});
 }
 
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,

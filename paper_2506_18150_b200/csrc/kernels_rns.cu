@@ -207,9 +207,11 @@ __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint6
 template <int DNUM, int QR>
 __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
                                              const __grid_constant__ LimbMap map, uint32_t N) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int l = blockIdx.y;
-  if (p >= N) return;
+  // work item w = (tile, limb); a grid smaller than the work loops (persistent CTAs)
+  const uint32_t tiles = N / blockDim.x, total = tiles * (uint32_t)map.n;
+  for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
+  const uint32_t p = (w % tiles) * blockDim.x + threadIdx.x;
+  const int l = (int)(w / tiles);
   const uint32_t chain = map.pr[l];
   const PrimeDev& P = primes[chain];
   const double q = P.qd, qi = P.qinv;
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
         *o1 = r1;
       }
     }
+  }
   }
 }
 
@@ -354,13 +357,18 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
                                                   uint64_t* __restrict__ out, size_t out_stride, size_t half,
                                                   const PrimeDev* __restrict__ primes,
                                                   const __grid_constant__ LimbMap map, uint32_t N, int nq, size_t xq,
-                                                  size_t oq) {
+                                                  size_t oq, int n_groups) {
   constexpr int G = kGiantPack;
   constexpr int kChunk = 64;
   __shared__ MacTerm tm[kChunk];
-  const int4 gr = groups[blockIdx.y];
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int l = blockIdx.z;
+  // work item w = (tile fastest, group, limb outermost -- the baby pairs of a
+  // limb stay L2-resident); a grid smaller than the work loops (persistent
+  // CTAs leave room on every SM for the concurrent NTT work)
+  const uint32_t tiles = N / blockDim.x, total = tiles * (uint32_t)n_groups * (uint32_t)map.n;
+  for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
+  const int4 gr = groups[(w / tiles) % n_groups];
+  const uint32_t p = (w % tiles) * blockDim.x + threadIdx.x;
+  const int l = (int)(w / (tiles * n_groups));
   const PrimeDev& P = primes[map.pr[l]];
   const double q = P.qd, qi = P.qinv;
   for (int qq = 0; qq < nq; qq++) {   // queries share the plaintexts (re-read from L2)
@@ -427,6 +435,7 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
         dst[half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
       }
     }
+  }
   }
   }
 }
@@ -625,7 +634,9 @@ void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
     case 7: kern = b ? k_kip<7, 2> : k_kip<7, 1>; break;
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
-  kern<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
+  const unsigned total = (c.N / kT) * map.n;
+  const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
+  kern<<<grid, kT, 0, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -666,9 +677,10 @@ void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, 
                                                                        xq, oq, nqc);
   } else {
     auto kern = x_dform ? k_diag_mac<true> : k_diag_mac<false>;
-    kern<<<dim3((c.N + kT - 1) / kT, n_groups, map.n), kT, 0, c.stream>>>(terms, groups, out, out_stride,
-                                                                          (size_t)map.n * c.N, c.primes, map, c.N, 1,
-                                                                          0, 0);
+    const unsigned total = (c.N / kT) * n_groups * map.n;
+    const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
+    kern<<<grid, kT, 0, c.stream>>>(terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map, c.N, 1, 0, 0,
+                                    n_groups);
   }
   (*c.launches)++;
   HCUDA(cudaGetLastError());
