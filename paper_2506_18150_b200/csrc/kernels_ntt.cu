@@ -324,6 +324,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
 }
 
 // ---------------------------------------------------------------- launchers
+// extra dynamic shared memory per NTT CTA (HELRM_NTT_SMEM bytes): caps NTT CTAs per SM so
+// that concurrent HBM-bound kernels of the pipeline find room on every SM (experiment knob)
+static size_t ntt_xsmem() {
+  static const size_t v = getenv("HELRM_NTT_SMEM") ? (size_t)atoi(getenv("HELRM_NTT_SMEM")) : 0;
+  return v;
+}
+template <class K>
+static void allow_xsmem(K k) {
+  if (ntt_xsmem()) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ntt_xsmem());
+}
+
 static size_t chunk_limbs(int N) {
   static const size_t env = getenv("HELRM_NTT_CHUNK") ? (size_t)atoi(getenv("HELRM_NTT_CHUNK")) : 0;
   // 256 MiB of scratch per chunk (512 limbs at N = 2^16): larger launches lose less to partial
@@ -343,12 +354,14 @@ static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
   {
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
     auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
-    k1<<<dim3(g1, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
+    allow_xsmem(k1);
+    k1<<<dim3(g1, cnt), kThreads, ntt_xsmem(), c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
                                                  c.ntt_einv, c.ntt_tpos, lidx, epi);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
-    k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
+    allow_xsmem(k_ntt_fwd<8, 1>);
+    k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, ntt_xsmem(), c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
                                                                c.ntt_grp, c.ntt_einv, c.ntt_tpos, lidx, epi);
   }
   *c.launches += 2;
@@ -362,12 +375,14 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
-    k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, 0, c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
+    allow_xsmem(k_ntt_inv<8, 1>);
+    k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, ntt_xsmem(), c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
                                                                c.ntt_grp, c.ntt_einv, c.ntt_tpos, nullptr, lidx);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
-    k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, 0, c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
+    allow_xsmem(k_ntt_inv<SLOG, 0>);
+    k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, ntt_xsmem(), c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
                                                                   c.ntt_grp, c.ntt_einv, c.ntt_tpos, post, lidx);
   }
   *c.launches += 2;
