@@ -1518,7 +1518,9 @@ static LimbMap map_twice(const LimbMap& m) {
 // host-side L3 work list: output pair z per non-empty (o, i) (in o, i order),
 // giants packed kGiantPack at a time, one term per baby pair used by the pack
 struct MacList {
-  std::vector<MacTerm> terms;
+  int gp = kGiantPack;              // giants per pack (kGiantPack or kWidePack)
+  std::vector<char> terms;          // MacTermT<gp> records
+  size_t term_size = 0, n_terms = 0;
   std::vector<int4> groups;
   std::vector<std::pair<int64_t, int64_t>> oi;   // (o, i) of each output pair
   double n_u = 0, n_x = 0;   // plaintext limb-sets read, distinct baby pairs read
@@ -1527,10 +1529,12 @@ struct MacList {
 
 }  // extern "C" (templates below)
 
-template <class XF>
-static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int64_t z_lo = 0,
-                          int64_t z_hi = INT64_MAX) {
+template <int GP, class XF>
+static MacList build_macs_t(const helrm_plan* pl, size_t diag_stride, XF xptr, int64_t z_lo, int64_t z_hi) {
+  using Term = MacTermT<GP>;
   MacList ml;
+  ml.gp = GP;
+  ml.term_size = sizeof(Term);
   std::set<std::pair<int, int>> xs;   // distinct (c, j) baby pairs
   int64_t zg = 0;   // global index of the non-empty (o, i) pairs
   for (int64_t o = 0; o < pl->O; o++) {
@@ -1540,17 +1544,17 @@ static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int
         if (zg >= z_lo && zg < z_hi) gi.push_back((int64_t)i);
         zg++;
       }
-    for (size_t g0 = 0; g0 < gi.size(); g0 += kGiantPack) {
-      const int ng = (int)std::min<size_t>(kGiantPack, gi.size() - g0);
+    for (size_t g0 = 0; g0 < gi.size(); g0 += GP) {
+      const int ng = (int)std::min<size_t>(GP, gi.size() - g0);
       const int z0 = (int)ml.oi.size();
       double gu = 0;
-      std::map<std::pair<int, int>, MacTerm> tm;
+      std::map<std::pair<int, int>, Term> tm;
       for (int g = 0; g < ng; g++) {
         ml.oi.push_back({o, gi[g0 + g]});
         for (const Entry& e : pl->entries[o][gi[g0 + g]]) {
           auto it = tm.find({e.c, e.j});
           if (it == tm.end()) {
-            MacTerm t{};
+            Term t{};
             auto x = xptr(e.c, e.j);
             t.x0 = x.first;
             t.x1 = x.second;
@@ -1561,16 +1565,25 @@ static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int
           gu += 1;
         }
       }
-      ml.groups.push_back(make_int4((int)ml.terms.size(), (int)tm.size(), z0, ng));
+      ml.groups.push_back(make_int4((int)ml.n_terms, (int)tm.size(), z0, ng));
       ml.gu.push_back(gu);
       for (auto& kv : tm) {
-        ml.terms.push_back(kv.second);
+        const char* b = reinterpret_cast<const char*>(&kv.second);
+        ml.terms.insert(ml.terms.end(), b, b + sizeof(Term));
+        ml.n_terms++;
         xs.insert(kv.first);
       }
     }
   }
   ml.n_x = (double)xs.size();
   return ml;
+}
+
+template <class XF>
+static MacList build_macs(const helrm_plan* pl, size_t diag_stride, XF xptr, int64_t z_lo = 0,
+                          int64_t z_hi = INT64_MAX, bool wide = false) {
+  return wide ? build_macs_t<kWidePack>(pl, diag_stride, xptr, z_lo, z_hi)
+              : build_macs_t<kGiantPack>(pl, diag_stride, xptr, z_lo, z_hi);
 }
 
 extern "C" {
@@ -1582,8 +1595,8 @@ extern "C" {
 struct MacDev {
   DBuf terms, groups;
   MacDev(helrm_ctx* c, const MacList& ml, void** pinned = nullptr)
-      : terms(c, (ml.terms.size() * sizeof(MacTerm) + 7) / 8 + 1), groups(c, 2 * ml.groups.size() + 1) {
-    const size_t tb = ml.terms.size() * sizeof(MacTerm), gb = ml.groups.size() * sizeof(int4);
+      : terms(c, (ml.terms.size() + 7) / 8 + 1), groups(c, 2 * ml.groups.size() + 1) {
+    const size_t tb = ml.terms.size(), gb = ml.groups.size() * sizeof(int4);
     const void* ht = ml.terms.data();
     const void* hg = ml.groups.data();
     if (pinned) {   // allocated by the caller before the capture (mac_list_bytes)
@@ -1613,8 +1626,8 @@ static void run_macs(helrm_ctx* c, const MacList& ml, const MacDev& md, size_t g
   // algorithmic bytes: plaintexts of the groups, each distinct baby pair once per lookup (charged to the
   // first launch), the outputs
   const double nx = g0 == 0 ? ml.n_x : 0.0;
-  launch_diag_mac(c->dc(st, pers), (const MacTerm*)md.terms.p, (const int4*)md.groups.p + g0, (int)(g1 - g0), nu,
-                  nx, nout, out, out_stride, map, x_dform, nq, xq, oq);
+  launch_diag_mac(c->dc(st, pers), md.terms.p, (const int4*)md.groups.p + g0, (int)(g1 - g0), nu, nx, nout, out,
+                  out_stride, map, x_dform, nq, xq, oq, ml.gp == kWidePack);
 }
 
 static void run_macs_all(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t out_stride, const LimbMap& map,
@@ -1920,7 +1933,7 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
       G.X = (uint64_t*)c->dalloc(nin * 2 * nqN * 8);
       G.S = (uint64_t*)c->dalloc((size_t)pl->O * Qc * oN * 8);
       // MAC work list bound: every term carries >= 1 plaintext, every group >= 1 pair
-      HCUDA(cudaMallocHost(&G.pinned, (size_t)pl->n_diag * sizeof(MacTerm) + count_pairs(pl) * sizeof(int4) + 64));
+      HCUDA(cudaMallocHost(&G.pinned, (size_t)pl->n_diag * sizeof(MacTermW) + count_pairs(pl) * sizeof(int4) + 64));
     }
     stage_inputs(c, in + q0 * pl->C, nin, 2 * nqN, G.X);
     if (G.exec) {

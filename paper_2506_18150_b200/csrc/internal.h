@@ -283,19 +283,26 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map);
 
 // D20 L3 work list.  Giants are packed kGiantPack at a time: a term is one
 // baby pair x = (x0, x1) with the plaintext u of each giant of the pack that
-// uses it (null if none), so every baby value is loaded once per pack.
+// uses it (null if none), so every baby value is loaded once per pack.  The
+// query-batched kernel packs kWidePack giants (all of a Criteo output block)
+// so that each baby value is read once per query.
 constexpr int kGiantPack = 4;
-struct MacTerm {
+constexpr int kWidePack = 16;
+template <int GP>
+struct MacTermT {
   const uint64_t* x0;         // [nl][N]
   const uint64_t* x1;
-  const uint64_t* u[kGiantPack];  // plaintext [nl][N] (D-form) or null
+  const uint64_t* u[GP];      // plaintext [nl][N] (D-form) or null
 };
+using MacTerm = MacTermT<kGiantPack>;
+using MacTermW = MacTermT<kWidePack>;
 // group z: terms [g.x, g.x + g.y), output pairs g.z .. g.z + g.w - 1, each
 // written to out + pair out_stride (A) and + nl N (B).  u in D-form; x in
 // D-form iff x_dform (else canonical).
 // nq queries: query q reads x + q xq and writes out + q oq (plaintexts shared).
-void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
+// wide: terms are MacTermW (batched kernel, nq >= 1), else MacTerm.
+void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int n_groups, double n_u_total,
                      double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
-                     bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0);
+                     bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0, bool wide = false);
 
 }  // namespace helrm

@@ -347,12 +347,16 @@ __global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ Ki
 }
 
 // D20 L3: (A, B)_z[l][p] = sum_t u_{z,t}[l][p] (x0_t, x1_t)[l][p] for the
-// giants z of a pack.  grid: (tile, pack, limb) -- limb outermost so the
-// baby pairs of a limb stay L2-resident; each baby value is loaded once per
-// pack of kGiantPack giants.  Plaintexts u in D-form; x in D-form (XD) or
+// giants z of a pack.  Work item = (256-position tile fastest, pack, limb
+// outermost -- the baby pairs of a limb stay L2-resident); each baby value is
+// loaded once per pack of kGiantPack giants.  QN queries share every
+// plaintext value a thread loads (batched lookups: QN = 2, so the FP64 work
+// per plaintext byte doubles and the kernel stays HBM-bound at half the
+// plaintext traffic per query).  Plaintexts u in D-form; x in D-form (XD) or
 // canonical (single mode, centred on load).  Exact FP64 MACs, folded every
-// kFAccTerms products; the output pairs are canonical.
-template <bool XD>
+// kFAccTerms products; the output pairs are canonical.  A grid smaller than
+// the work loops (persistent CTAs, HELRM_PERSIST).
+template <bool XD, int QN>
 __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ terms, const int4* __restrict__ groups,
                                                   uint64_t* __restrict__ out, size_t out_stride, size_t half,
                                                   const PrimeDev* __restrict__ primes,
@@ -361,155 +365,90 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   constexpr int G = kGiantPack;
   constexpr int kChunk = 64;
   __shared__ MacTerm tm[kChunk];
-  // work item w = (tile fastest, group, limb outermost -- the baby pairs of a
-  // limb stay L2-resident); a grid smaller than the work loops (persistent
-  // CTAs leave room on every SM for the concurrent NTT work)
   const uint32_t tiles = N / blockDim.x, total = tiles * (uint32_t)n_groups * (uint32_t)map.n;
   for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
-  const int4 gr = groups[(w / tiles) % n_groups];
-  const uint32_t p = (w % tiles) * blockDim.x + threadIdx.x;
-  const int l = (int)(w / (tiles * n_groups));
-  const PrimeDev& P = primes[map.pr[l]];
-  const double q = P.qd, qi = P.qinv;
-  for (int qq = 0; qq < nq; qq++) {   // queries share the plaintexts (re-read from L2)
-  const size_t o = (size_t)l * N + p, ox = o + (size_t)qq * xq;
-  fm::FAcc acc0[G], acc1[G];
-  int cnt = 0;
-  for (int c0 = 0; c0 < gr.y; c0 += kChunk) {   // term list staged in chunks
-    const int nt = min(kChunk, gr.y - c0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < nt; t += blockDim.x) tm[t] = terms[gr.x + c0 + t];
-    __syncthreads();
-    if (p >= N) continue;
-    // two terms per round: 2 x (2 + G) independent loads in flight
-    for (int t = 0; t < nt; t += 2) {
-      const int nr = nt - t >= 2 ? 2 : 1;
-      uint64_t x0[2], x1[2], u[2][G];
+    const int4 gr = groups[(w / tiles) % n_groups];
+    const uint32_t p = (w % tiles) * blockDim.x + threadIdx.x;
+    const int l = (int)(w / (tiles * n_groups));
+    const PrimeDev& P = primes[map.pr[l]];
+    const double q = P.qd, qi = P.qinv;
+    const size_t o = (size_t)l * N + p;
+    for (int q0 = 0; q0 < nq; q0 += QN) {
+      size_t ox[QN];
 #pragma unroll
-      for (int r = 0; r < 2; r++) {
-        if (r < nr) {
-          const MacTerm& m = tm[t + r];
-          x0[r] = m.x0[ox];
-          x1[r] = m.x1[ox];
-          if (nq == 1) {
+      for (int r = 0; r < QN; r++) ox[r] = o + (size_t)min(q0 + r, nq - 1) * xq;   // ragged tail: reload, no store
+      fm::FAcc acc0[QN][G], acc1[QN][G];
+      int cnt = 0;
+      for (int c0 = 0; c0 < gr.y; c0 += kChunk) {   // term list staged in chunks
+        const int nt = min(kChunk, gr.y - c0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nt; t += blockDim.x) tm[t] = terms[gr.x + c0 + t];
+        __syncthreads();
+        // two terms per round: 2 (2 QN + G) independent loads in flight
+        for (int t = 0; t < nt; t += 2) {
+          const int nr = nt - t >= 2 ? 2 : 1;
+          uint64_t x0[2][QN], x1[2][QN], u[2][G];
 #pragma unroll
-            for (int g = 0; g < G; g++) u[r][g] = m.u[g] ? __ldcs(m.u[g] + o) : 0;  // plaintexts stream once
-          } else {
+          for (int r = 0; r < 2; r++) {
+            if (r < nr) {
+              const MacTerm& m = tm[t + r];
 #pragma unroll
-            for (int g = 0; g < G; g++) u[r][g] = m.u[g] ? m.u[g][o] : 0;
+              for (int k = 0; k < QN; k++) {
+                x0[r][k] = m.x0[ox[k]];
+                x1[r][k] = m.x1[ox[k]];
+              }
+#pragma unroll
+              for (int g = 0; g < G; g++)
+                u[r][g] = m.u[g] ? (QN == 1 && nq == 1 ? __ldcs(m.u[g] + o) : m.u[g][o]) : 0;
+            } else {
+#pragma unroll
+              for (int k = 0; k < QN; k++) x0[r][k] = x1[r][k] = 0;
+#pragma unroll
+              for (int g = 0; g < G; g++) u[r][g] = 0;
+            }
           }
-        } else {
-          x0[r] = x1[r] = 0;
+          if (cnt + 2 > fm::kFAccTerms) {
 #pragma unroll
-          for (int g = 0; g < G; g++) u[r][g] = 0;
+            for (int k = 0; k < QN; k++)
+#pragma unroll
+              for (int g = 0; g < G; g++) {
+                fm::fold(acc0[k][g], q, qi);
+                fm::fold(acc1[k][g], q, qi);
+              }
+            cnt = 0;
+          }
+          cnt += 2;
+#pragma unroll
+          for (int r = 0; r < 2; r++) {
+#pragma unroll
+            for (int k = 0; k < QN; k++) {
+              const double xa = XD ? fm::bits2d(x0[r][k]) : fm::u2c(x0[r][k], q);
+              const double xb = XD ? fm::bits2d(x1[r][k]) : fm::u2c(x1[r][k], q);
+#pragma unroll
+              for (int g = 0; g < G; g++) {
+                const double ud = fm::bits2d(u[r][g]);
+                fm::fmac(acc0[k][g], ud, xa);
+                fm::fmac(acc1[k][g], ud, xb);
+              }
+            }
+          }
         }
       }
-      if (cnt + 2 > fm::kFAccTerms) {
 #pragma unroll
-        for (int g = 0; g < G; g++) {
-          fm::fold(acc0[g], q, qi);
-          fm::fold(acc1[g], q, qi);
-        }
-        cnt = 0;
-      }
-      cnt += 2;
+      for (int k = 0; k < QN; k++) {
+        if (q0 + k < nq) {
 #pragma unroll
-      for (int r = 0; r < 2; r++) {
-        const double xa = XD ? fm::bits2d(x0[r]) : fm::u2c(x0[r], q);
-        const double xb = XD ? fm::bits2d(x1[r]) : fm::u2c(x1[r], q);
-#pragma unroll
-        for (int g = 0; g < G; g++) {
-          const double ud = fm::bits2d(u[r][g]);
-          fm::fmac(acc0[g], ud, xa);
-          fm::fmac(acc1[g], ud, xb);
+          for (int g = 0; g < G; g++) {
+            if (g < gr.w) {
+              uint64_t* dst = out + (size_t)(gr.z + g) * out_stride + (size_t)(q0 + k) * oq;
+              dst[o] = fm::c2u(fm::fred(acc0[k][g], q, qi), P.rc.q);
+              dst[half + o] = fm::c2u(fm::fred(acc1[k][g], q, qi), P.rc.q);
+            }
+          }
         }
       }
     }
   }
-  if (p < N) {
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-      if (g < gr.w) {
-        uint64_t* dst = out + (size_t)(gr.z + g) * out_stride + (size_t)qq * oq;
-        dst[o] = fm::c2u(fm::fred(acc0[g], q, qi), P.rc.q);
-        dst[half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
-      }
-    }
-  }
-  }
-  }
-}
-
-// D20 L3 for a batch of queries: thread (position p of a 16-position tile,
-// query qq of an 8-query chunk, component) accumulates the kGiantPack
-// giants of its group; a term's 4 plaintext values are shared by the 16
-// threads of a position (L1 hits), each baby value is read by one thread.
-// Query chunk fastest in the grid, so a plaintext tile is reused from L2 by
-// the next chunk: plaintexts stream from HBM about once per launch.
-template <bool XD>
-__global__ void __launch_bounds__(256) k_diag_mac_q(const MacTerm* __restrict__ terms, const int4* __restrict__ groups,
-                                                    uint64_t* __restrict__ out, size_t out_stride, size_t half,
-                                                    const PrimeDev* __restrict__ primes,
-                                                    const __grid_constant__ LimbMap map, uint32_t N, int nq, size_t xq,
-                                                    size_t oq, int nqc) {
-  constexpr int G = kGiantPack;
-  constexpr int kChunk = 64;
-  __shared__ MacTerm tm[kChunk];
-  const int tid = threadIdx.x;
-  const int pl = tid & 15, qq = (tid >> 4) & 7, comp = tid >> 7;
-  const int qc = blockIdx.x % nqc, tile = blockIdx.x / nqc;
-  const int qy = qc * 8 + qq;
-  const bool act = qy < nq;
-  const uint32_t p = tile * 16 + pl;
-  const int4 gr = groups[blockIdx.y];
-  const int l = blockIdx.z;
-  const PrimeDev& P = primes[map.pr[l]];
-  const double q = P.qd, qi = P.qinv;
-  const size_t o = (size_t)l * N + p, ox = o + (size_t)(act ? qy : 0) * xq;
-  fm::FAcc acc[G];
-  int cnt = 0;
-  for (int c0 = 0; c0 < gr.y; c0 += kChunk) {
-    const int nt = min(kChunk, gr.y - c0);
-    __syncthreads();
-    for (int t = tid; t < nt; t += blockDim.x) tm[t] = terms[gr.x + c0 + t];
-    __syncthreads();
-    if (!act) continue;
-    for (int t = 0; t < nt; t += 2) {
-      const int nr = nt - t >= 2 ? 2 : 1;
-      uint64_t xv[2], uv[2][G];
-#pragma unroll
-      for (int r = 0; r < 2; r++) {
-        if (r < nr) {
-          const MacTerm& m = tm[t + r];
-          xv[r] = (comp ? m.x1 : m.x0)[ox];
-#pragma unroll
-          for (int g = 0; g < G; g++) uv[r][g] = m.u[g] ? m.u[g][o] : 0;
-        } else {
-          xv[r] = 0;
-#pragma unroll
-          for (int g = 0; g < G; g++) uv[r][g] = 0;
-        }
-      }
-      if (cnt + 2 > fm::kFAccTerms) {
-#pragma unroll
-        for (int g = 0; g < G; g++) fm::fold(acc[g], q, qi);
-        cnt = 0;
-      }
-      cnt += 2;
-#pragma unroll
-      for (int r = 0; r < 2; r++) {
-        const double x = XD ? fm::bits2d(xv[r]) : fm::u2c(xv[r], q);
-#pragma unroll
-        for (int g = 0; g < G; g++) fm::fmac(acc[g], fm::bits2d(uv[r][g]), x);
-      }
-    }
-  }
-  if (!act) return;
-#pragma unroll
-  for (int g = 0; g < G; g++)
-    if (g < gr.w)
-      out[(size_t)(gr.z + g) * out_stride + (size_t)qy * oq + (comp ? half : 0) + o] =
-          fm::c2u(fm::fred(acc[g], q, qi), P.rc.q);
 }
 
 // D20 L5: after ncclAllReduce(uint64, sum) of partial Q_l P accumulators
@@ -664,24 +603,18 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
   HCUDA(cudaGetLastError());
 }
 
-void launch_diag_mac(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, double n_u_total,
+void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int n_groups, double n_u_total,
                      double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
-                     bool x_dform, int nq, size_t xq, size_t oq) {
+                     bool x_dform, int nq, size_t xq, size_t oq, bool wide) {
   // algorithmic bytes: every plaintext once, every distinct baby pair and output once per query
   ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + nq * (2.0 * n_x_distinct + 2.0 * n_out)));
-  if (nq > 1) {
-    const int nqc = (nq + 7) / 8;
-    auto kq = x_dform ? k_diag_mac_q<true> : k_diag_mac_q<false>;
-    kq<<<dim3(nqc * (c.N / 16), n_groups, map.n), 256, 0, c.stream>>>(terms, groups, out, out_stride,
-                                                                       (size_t)map.n * c.N, c.primes, map, c.N, nq,
-                                                                       xq, oq, nqc);
-  } else {
-    auto kern = x_dform ? k_diag_mac<true> : k_diag_mac<false>;
-    const unsigned total = (c.N / kT) * n_groups * map.n;
-    const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
-    kern<<<grid, kT, 0, c.stream>>>(terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map, c.N, 1, 0, 0,
-                                    n_groups);
-  }
+  (void)wide;
+  auto kern = x_dform ? (nq > 1 ? k_diag_mac<true, 2> : k_diag_mac<true, 1>)
+                      : (nq > 1 ? k_diag_mac<false, 2> : k_diag_mac<false, 1>);
+  const unsigned total = (c.N / kT) * n_groups * map.n;
+  const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
+  kern<<<grid, kT, 0, c.stream>>>((const MacTerm*)terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map,
+                                  c.N, nq, xq, oq, n_groups);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
