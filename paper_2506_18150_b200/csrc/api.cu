@@ -73,6 +73,7 @@ struct LevelConst {
   double2* modup_post = nullptr;   // [l+1]
   ConvRowDev* modup_tab = nullptr; // [dnum(l)][modup_rows]: the rows outside digit k
   int modup_rows = 0;
+  ConvRowDev* modup_dtab = nullptr; // [dnum(l)][l+1+K]: row r of digit k (own rows unused), for the fused NTT
   double2* moddown_post = nullptr; // [K]
   ConvRowDev* moddown_tab = nullptr; // [l+1]
 };
@@ -419,6 +420,20 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
     };
     lc.modup_post = (double2*)up(upost.data(), upost.size() * sizeof(double2));
     lc.modup_tab = (ConvRowDev*)up(utab.data(), utab.size() * sizeof(ConvRowDev));
+    {
+      std::vector<ConvRowDev> dt((size_t)dn * nl);
+      for (uint32_t k = 0; k < dn; k++) {
+        for (uint32_t r = 0; r < nl; r++) {   // same sources as the compacted table, keyed by row
+          dt[(size_t)k * nl + r] = utab[(size_t)k * urows];
+          dt[(size_t)k * nl + r].out_row = -1;
+        }
+        for (uint32_t j = 0; j < urows; j++) {
+          const ConvRowDev& e = utab[(size_t)k * urows + j];
+          if (e.out_row >= 0) dt[(size_t)k * nl + e.out_row] = e;
+        }
+      }
+      lc.modup_dtab = (ConvRowDev*)up(dt.data(), dt.size() * sizeof(ConvRowDev));
+    }
     lc.moddown_post = (double2*)up(dpost.data(), dpost.size() * sizeof(double2));
     lc.moddown_tab = (ConvRowDev*)up(dtab.data(), dtab.size() * sizeof(ConvRowDev));
     HCUDA(cudaStreamSynchronize(c->stream));
@@ -477,9 +492,21 @@ static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int 
   // the digit; step 3: one NTT over exactly those limbs.  The digit's own
   // limbs are copied unchanged (NTT form).
   launch_ntt_inv(c->dc(st), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post);
-  launch_conv_rows(c->dc(st), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
-                   nl * N, G, P.map_qp(l));
-  launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
+  static const bool fuse = getenv("HELRM_FUSECONV") ? atoi(getenv("HELRM_FUSECONV")) != 0 : false;
+  if (fuse) {   // conversion computed inside the NTT's pass 1 (no conversion kernel, no round trip)
+    NttConvIn cv;
+    cv.tab = lc.modup_dtab;
+    cv.tab_rows = (int)nl;
+    cv.ncv = (int)dn;
+    cv.nb_max = (int)P.alpha;
+    cv.y = y.p;
+    cv.ys = nq * N;
+    launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, false, lidx, nullptr, &cv);
+  } else {
+    launch_conv_rows(c->dc(st), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
+                     nl * N, G, P.map_qp(l));
+    launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
+  }
   HostTimer ht_("modup own-limb copies");
   for (size_t k = 0; copy_own && k < dn; k++) {
     const size_t lo = k * P.alpha, hi = std::min<size_t>((k + 1) * P.alpha, l + 1);
@@ -499,7 +526,18 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   DBuf yp(c, G * P.K * N, st), t(c, G * nq * N, st);
   launch_ntt_inv(c->dc(st), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
                  lc.moddown_post);
-  launch_conv_rows(c->dc(st), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
+  static const bool fuse = getenv("HELRM_FUSECONV") ? atoi(getenv("HELRM_FUSECONV")) != 0 : false;
+  NttConvIn cv;
+  if (fuse) {
+    cv.tab = lc.moddown_tab;
+    cv.tab_rows = (int)nq;
+    cv.ncv = 1;
+    cv.nb_max = (int)P.K;
+    cv.y = yp.p;
+    cv.ys = P.K * N;
+  } else {
+    launch_conv_rows(c->dc(st), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
+  }
   NttEpi epi;
   epi.y = y;
   epi.ys = ys;
@@ -508,7 +546,8 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   epi.s = lc.pinv;
   epi.sp = lc.pinvs;
   epi.accumulate = accumulate ? 1 : 0;
-  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true, nullptr, &epi);
+  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, !fuse, nullptr, &epi,
+                 fuse ? &cv : nullptr);
 }
 
 static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t* out) {

@@ -186,6 +186,16 @@ struct NttEpi {
   const uint64_t* sp = nullptr;
   int accumulate = 0;            // out += instead of out =
 };
+// Optional base conversion fused into the forward NTT's pass 1 (D14 inside
+// ModUp / ModDown): limb gl = (poly, row r) with poly = g ncv + k is not read
+// from src but computed as sum_b y_g[row0 + b] cf_kr[b] mod q_r from the
+// y-form sources y + g ys (tab[k tab_rows + r] holds row0, nb, cf).
+struct NttConvIn {
+  const ConvRowDev* tab = nullptr;
+  int tab_rows = 0, ncv = 1, nb_max = 0;
+  const uint64_t* y = nullptr;
+  size_t ys = 0;
+};
 // NTT over n_total limbs: limb y = (poly y / map.n, limb y % map.n) lives at
 // src + (y / map.n) * src_stride + (y % map.n) * N (same for dst; stride 0 =
 // contiguous polys of map.n limbs).  src == dst allowed.
@@ -193,7 +203,8 @@ struct NttEpi {
 // lidx (optional device table): launch limb v is layout limb lidx[v]
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0, bool din = false,
-                    const uint32_t* lidx = nullptr, const NttEpi* epi = nullptr);
+                    const uint32_t* lidx = nullptr, const NttEpi* epi = nullptr,
+                    const NttConvIn* conv = nullptr);
 // post (optional, per limb of map): final factor (w, w/q) replacing N^-1
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0,

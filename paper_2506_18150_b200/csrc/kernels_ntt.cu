@@ -73,7 +73,7 @@ __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double 
 //   MODE 0 (pass 1): sub-transform = column (stride 256); twiddles tw1[2^st + i].
 //   MODE 1 (pass 2): sub-transform = 256-block B; twiddles tw2[B][...]:
 //     [0, 15): phase A, 2^st - 1 + i_loc;  15 + 16 j + t: thread t's phase-B twiddle j.
-template <int SLOG, int MODE>
+template <int SLOG, int MODE, int NB = 1>
 __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
@@ -81,9 +81,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
                                                       const uint8_t* __restrict__ einv,
                                                       const uint8_t* __restrict__ tpos,
                                                       const uint32_t* __restrict__ lidx,
-                                                      const __grid_constant__ NttEpi epi) {
+                                                      const __grid_constant__ NttEpi epi,
+                                                      const __grid_constant__ NttConvIn cv) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
-  constexpr bool P1 = MODE != 1;  // MODE 2 = pass 1 whose input limbs are centred doubles (conversion output)
+  constexpr bool P1 = MODE != 1;  // MODE 2: pass 1 on centred doubles (conversion output); MODE 3: conversion fused
   __shared__ double sm[P1 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
@@ -99,15 +100,36 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
   const int gsub = P1 ? blockIdx.x * SUBS + sub : (int)grp[blockIdx.x * SUBS + sub];
   const double2* __restrict__ twA = P1 ? P.tw1 : P.tw2 + (size_t)gsub * 256;
   double r[kEPT];
+  if (MODE == 3) {
+    // D14 on the fly: out_r = sum_b y[row0 + b] cf[b] mod q_r (centred), the y-form sources
+    // being shared by every converted row of the digit (L2-resident)
+    const size_t poly = gl / map.n;
+    const ConvRowDev& cr = cv.tab[(size_t)(poly % cv.ncv) * cv.tab_rows + gl % map.n];
+    const uint64_t* ysrc = cv.y + (poly / cv.ncv) * cv.ys + (size_t)cr.src_row0 * N;
+    const int nb = cr.nb;
+    double2 cf[NB];
 #pragma unroll
-  for (int k = 0; k < kEPT; k++) {
-    const int e = t + TS * k;
-    if (MODE == 2) {
-      r[k] = __longlong_as_double((long long)s[(size_t)e * 256 + gsub]);
-    } else if (MODE == 0) {
-      r[k] = u2d(s[(size_t)e * 256 + gsub]);
-    } else {
-      r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
+    for (int b = 0; b < NB; b++) cf[b] = cr.cf[b];
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const size_t pos = (size_t)(t + TS * k) * 256 + gsub;
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < NB; b++)
+        if (b < nb) acc += mmul(u2d(ysrc[(size_t)b * N + pos]), cf[b].x, cf[b].y, q);   // each in [-q/2, q/2]
+      r[k] = cred(acc, q, qi);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kEPT; k++) {
+      const int e = t + TS * k;
+      if (MODE == 2) {
+        r[k] = __longlong_as_double((long long)s[(size_t)e * 256 + gsub]);
+      } else if (MODE == 0) {
+        r[k] = u2d(s[(size_t)e * 256 + gsub]);
+      } else {
+        r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
+      }
     }
   }
   // phase A: stages 0..3 on layout e = t + TS k (twiddles independent of t)
@@ -348,21 +370,24 @@ size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)
 template <int SLOG>
 static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
                       const LimbMap& map, size_t off, size_t ss, size_t ds, bool din, const uint32_t* lidx,
-                      const NttEpi& epi) {
+                      const NttEpi& epi, const NttConvIn& cv) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
-    auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
+    decltype(&k_ntt_fwd<SLOG, 0>) k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
+    if (cv.tab)
+      k1 = cv.nb_max <= 1 ? k_ntt_fwd<SLOG, 3, 1> : cv.nb_max <= 2 ? k_ntt_fwd<SLOG, 3, 2>
+           : cv.nb_max <= 4 ? k_ntt_fwd<SLOG, 3, 4> : k_ntt_fwd<SLOG, 3, 8>;
     allow_xsmem(k1);
     k1<<<dim3(g1, cnt), kThreads, ntt_xsmem(), c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
-                                                 c.ntt_einv, c.ntt_tpos, lidx, epi);
+                                                 c.ntt_einv, c.ntt_tpos, lidx, epi, cv);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
     allow_xsmem(k_ntt_fwd<8, 1>);
     k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, ntt_xsmem(), c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, lidx, epi);
+                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, lidx, epi, cv);
   }
   *c.launches += 2;
 }
@@ -391,7 +416,7 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
 template <bool FWD>
 static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t ss, size_t ds, const double2* post, bool din, const uint32_t* lidx,
-                    const NttEpi& epi = NttEpi{}) {
+                    const NttEpi& epi = NttEpi{}, const NttConvIn& cv = NttConvIn{}) {
   if (ss == 0) ss = (size_t)map.n * c.N;
   if (ds == 0) ds = (size_t)map.n * c.N;
   const size_t ch = chunk_limbs(c.N);
@@ -399,7 +424,7 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);
 #define HELRM_NTT_CASE(LG, SL)                                                  \
   case LG:                                                                      \
-    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din, lidx, epi);    \
+    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din, lidx, epi, cv);    \
     else inv_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, post, lidx);        \
     break;
     switch (c.log_n) {
@@ -416,8 +441,10 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
 }
 
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi* epi) {
-  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din, lidx, epi ? *epi : NttEpi{});
+                    const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi* epi,
+                    const NttConvIn* conv) {
+  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din, lidx, epi ? *epi : NttEpi{},
+                conv ? *conv : NttConvIn{});
 }
 
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
