@@ -1701,7 +1701,53 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   for (auto& bl : pl->babies) n_baby += bl.size();
   DBuf D(c, C * Qc * dn * nlN), babies(c, std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
   size_t bi = 0;
-  for (size_t ci = 0; ci < C; ci++) {
+  bool same_babies = Qc == 1 && C > 1;
+  for (size_t ci = 1; same_babies && ci < C; ci++) same_babies = pl->babies[ci] == pl->babies[0];
+  if (same_babies) {
+    // one query, C input cts with the same baby steps (LLM layout L2): the cts take the
+    // query role -- one batched ModUp, one baby kernel reading every key once for all C
+    const size_t nb = pl->babies[0].size();
+    modup_batch(c, X + nqN, 2 * nqN, (int)C, l, D.p, nullptr, false);
+    KipMulti km{};
+    km.own = X + nqN;
+    km.ownq = 2 * nqN;
+    km.alpha = (int)P.alpha;
+    km.digits = D.p;
+    km.digit_stride = nlN;
+    km.dnum = (int)dn;
+    km.c0 = X;
+    km.p_mod = lc.pmod;
+    km.level = l;
+    km.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+    km.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+    km.out_half = nlN;
+    km.nq = (int)C;
+    km.qk = std::min((int)C, 4);
+    km.dq = dn * nlN;
+    km.cq = 2 * nqN;
+    km.oq = nb * 2 * nlN;
+    for (size_t jj = 0; jj < nb; jj++) {
+      const int j = pl->babies[0][jj];
+      uint64_t* a = babies.p + jj * 2 * nlN;   // baby (ci, j) at babies + (ci nb + jj) 2 nlN
+      for (size_t ci = 0; ci < C; ci++) ab[ci][j] = a + ci * nb * 2 * nlN;
+      if (j == 0) {
+        for (size_t ci = 0; ci < C; ci++)
+          HCUDA(cudaMemsetAsync(a + ci * nb * 2 * nlN, 0, 2 * nlN * 8, c->stream));
+        launch_scalar_mul(c->dc(), X, a, mq, lc.pmod, lc.pmods, 1, (int)C, 2 * nqN, nb * 2 * nlN);
+        launch_scalar_mul(c->dc(), X + nqN, a + nlN, mq, lc.pmod, lc.pmods, 1, (int)C, 2 * nqN, nb * 2 * nlN);
+      } else {
+        need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
+        const uint64_t g = galois_of_rot(c, j);
+        km.rot[km.n] = rot_of_galois(c, g);
+        km.key[km.n] = key_for(rk, g);
+        km.out[km.n] = a;
+        km.max_rot = std::max(km.max_rot, km.rot[km.n]);
+        km.n++;
+      }
+    }
+    if (km.n) launch_kip_multi(c->dc(), km, mqp);
+  }
+  for (size_t ci = 0; !same_babies && ci < C; ci++) {
     const uint64_t* c0 = X + ci * 2 * nqN;
     uint64_t* Dc = D.p + ci * Qc * dn * nlN;
     modup_batch(c, c0 + nqN, xs, Qc, l, Dc, nullptr, false);
@@ -1777,10 +1823,33 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   };
   static const int mac_ch = getenv("HELRM_MACCH") ? atoi(getenv("HELRM_MACCH")) : 2;   // MAC groups per launch
   static const int ntt_ch = getenv("HELRM_NTTCH") ? atoi(getenv("HELRM_NTTCH")) : 8;   // giants per ModDown/ModUp batch
+  // Output blocks that repeat block 0's work list with the baby pairs of their own input ct
+  // (LLM layout L2: the 4 blocks share all 1279 plaintexts) run as one MAC launch in which
+  // the blocks take the query role, so each plaintext value is loaded once per 2 blocks.
+  size_t g_blk = ml.groups.size();
+  bool periodic = same_babies && pl->O == (int64_t)C && pl->O > 1 && ml.groups.size() % pl->O == 0;
+  if (periodic) {
+    g_blk = ml.groups.size() / pl->O;
+    const size_t ts = ml.term_size, nbb = pl->babies[0].size();
+    const int zb = ml.groups[g_blk].z;
+    for (int64_t o = 1; periodic && o < pl->O; o++)
+      for (size_t g = 0; periodic && g < g_blk; g++) {
+        const int4 a = ml.groups[g], b = ml.groups[o * g_blk + g];
+        periodic = b.y == a.y && b.w == a.w && b.z == a.z + (int)o * zb;
+        for (int t = 0; periodic && t < a.y; t++) {
+          const MacTerm* ta = reinterpret_cast<const MacTerm*>(&ml.terms[(size_t)(a.x + t) * ts]);
+          const MacTerm* tb = reinterpret_cast<const MacTerm*>(&ml.terms[(size_t)(b.x + t) * ts]);
+          periodic = tb->x0 == ta->x0 + o * nbb * 2 * nlN && tb->x1 == ta->x1 + o * nbb * 2 * nlN;
+          for (int u = 0; periodic && u < kGiantPack; u++) periodic = tb->u[u] == ta->u[u];
+        }
+      }
+    if (periodic) run_macs(c, ml, md, 0, g_blk, AB.p, zq * 2 * nlN, mqp, true, (int)pl->O, nbb * 2 * nlN,
+                           (size_t)zb * 2 * nlN, sm, pers);
+  }
   for (size_t gp = 0; gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
     const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
-    run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
+    if (!periodic) run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
     if (pipe) c->join(sn, sm);
     std::vector<int> rot;   // rotating pairs of the chunk (zero giants need no key switch)
     for (int z = z0; z < z1; z++)
