@@ -1843,10 +1843,60 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
           for (int u = 0; periodic && u < kGiantPack; u++) periodic = tb->u[u] == ta->u[u];
         }
       }
+    for (int z = 0; periodic && z < zb; z++)
+      for (int64_t o = 1; periodic && o < pl->O; o++)
+        periodic = pl->giants[o][ml.oi[z + o * zb].second] == pl->giants[0][ml.oi[z].second];
     if (periodic) run_macs(c, ml, md, 0, g_blk, AB.p, zq * 2 * nlN, mqp, true, (int)pl->O, nbb * 2 * nlN,
                            (size_t)zb * 2 * nlN, sm, pers);
   }
-  for (size_t gp = 0; gp < ml.groups.size(); gp += mac_ch) {
+  if (periodic) {
+    // giant steps of every block, then one key switch per giant with the blocks as queries
+    const int zb = ml.groups[g_blk].z;
+    if (pipe) c->join(sn, sm);
+    std::vector<int> rot;
+    for (int z = 0; z < n_out; z++)
+      if (pl->giants[ml.oi[z].first][ml.oi[z].second] % (int64_t)P.n != 0) rot.push_back(z);
+    for (size_t r0 = 0; r0 < rot.size();) {
+      size_t r1 = r0 + 1;
+      while (r1 < rot.size() && rot[r1] == rot[r1 - 1] + 1 && (int)(r1 - r0) < ntt_ch) r1++;
+      const size_t za = rot[r0], G = r1 - r0;
+      moddown_batch(c, AB.p + za * 2 * nlN + nlN, 2 * nlN, (int)G, l, Bp.p + za * nqN, nqN, sn);
+      modup_batch(c, Bp.p + za * nqN, nqN, (int)G, l, D2.p + za * dn * nlN, sn, false);
+      r0 = r1;
+    }
+    if (pipe) c->join(sk, sn);
+    if (pipe) c->join(sk, sm);
+    for (int z = 0; z < zb; z++) {
+      const int64_t gi = pl->giants[0][ml.oi[z].second];
+      if (gi % (int64_t)P.n == 0) {
+        for (int64_t o = 0; o < pl->O; o++) zero_giant(z + (int)o * zb);
+        continue;
+      }
+      KipArgs a{};
+      a.digits = D2.p + (size_t)z * dn * nlN;
+      a.digit_stride = nlN;
+      a.dnum = (int)dn;
+      a.key = key_for(rk, galois_of_rot(c, gi));
+      a.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+      a.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+      a.add0 = AB.p + (size_t)z * 2 * nlN;
+      a.add_rows = (int)nl;
+      a.rot = rot_of_galois(c, galois_of_rot(c, gi));
+      a.out0 = Oall;
+      a.out1 = Oall + nlN;
+      a.accumulate = 1;
+      a.nq = (int)pl->O;
+      a.dq = (size_t)zb * dn * nlN;
+      a.aq = (size_t)zb * 2 * nlN;
+      a.oq = 2 * nlN;
+      a.own = Bp.p + (size_t)z * nqN;
+      a.ownq = (size_t)zb * nqN;
+      a.alpha = (int)P.alpha;
+      a.level = (int)l;
+      launch_kip(c->dc(sk, pers), a, mqp);
+    }
+  }
+  for (size_t gp = 0; !periodic && gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
     const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
     if (!periodic) run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
