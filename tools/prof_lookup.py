@@ -10,7 +10,8 @@ import synth  # noqa: E402
 from paper_2506_18150_b200 import helrm  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-w = synth.make_workload("criteo", batch=2)
+name = sys.argv[2] if len(sys.argv) > 2 else "criteo"
+w = synth.make_workload(name, batch=2)
 cfg = w.config
 P = helrm.params_from_config(cfg)
 stream = torch.cuda.Stream()
@@ -20,11 +21,14 @@ plan = helrm.plan_create(ctx, T, cfg.level)
 sk = helrm.sk_gen(ctx, cfg.seed)
 pk = helrm.pk_gen(ctx, sk, cfg.seed)
 rk = helrm.rotkeys_gen(ctx, sk, plan.galois(cfg.N), cfg.seed)
+info = plan.info()
+C = info.n_in_cts
 cts = []
 for q in range(2):
-    x = helrm.encode_query(T, w.indices[q], w.dense[q], cfg.n_slots)
-    cts.append(helrm.encrypt(ctx, pk, x, cfg.level, (cfg.seed << 20) | q))
-batch = [cts[i % 2] for i in range(B)]
+    x = helrm.encode_query(T, w.indices[q], w.dense[q], C * cfg.n_slots)
+    cts.append([helrm.encrypt(ctx, pk, x[c * cfg.n_slots:(c + 1) * cfg.n_slots], cfg.level, (cfg.seed << 20) | (q * C + c))
+                for c in range(C)])
+batch = [ct for i in range(B) for ct in cts[i % 2]]
 for _ in range(2):
     for o in helrm.lookup(ctx, plan, rk, batch, B):
         o.close()
