@@ -205,6 +205,10 @@ void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0, bool din = false,
                     const uint32_t* lidx = nullptr, const NttEpi* epi = nullptr,
                     const NttConvIn* conv = nullptr);
+// single-kernel forward NTT on 4-CTA clusters (kernels_ntt_cl.cu), N = 2^16;
+// false if it does not apply (the caller then runs the two-pass kernels)
+bool ntt_fwd_cluster(const DevCtx& c, const uint64_t* src, uint64_t* dst, size_t n_total, const LimbMap& map,
+                     size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi& epi);
 // post (optional, per limb of map): final factor (w, w/q) replacing N^-1
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0,

@@ -419,6 +419,7 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
                     const NttEpi& epi = NttEpi{}, const NttConvIn& cv = NttConvIn{}) {
   if (ss == 0) ss = (size_t)map.n * c.N;
   if (ds == 0) ds = (size_t)map.n * c.N;
+  if (FWD && !cv.tab && ntt_fwd_cluster(c, src, dst, n_total, map, ss, ds, din, lidx, epi)) return;
   const size_t ch = chunk_limbs(c.N);
   for (size_t off = 0; off < n_total; off += ch) {
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);

@@ -609,8 +609,11 @@ void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int
   // algorithmic bytes: every plaintext once, every distinct baby pair and output once per query
   ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + nq * (2.0 * n_x_distinct + 2.0 * n_out)));
   (void)wide;
-  auto kern = x_dform ? (nq > 1 ? k_diag_mac<true, 2> : k_diag_mac<true, 1>)
-                      : (nq > 1 ? k_diag_mac<false, 2> : k_diag_mac<false, 1>);
+  // QN queries per plaintext load: 4 when the batch is a multiple of 4 (the LLM's 4 output blocks)
+  static const int q4 = getenv("HELRM_MAC_Q4") ? atoi(getenv("HELRM_MAC_Q4")) : 1;
+  auto kern = x_dform ? (nq % 4 == 0 && q4 ? k_diag_mac<true, 4> : nq > 1 ? k_diag_mac<true, 2> : k_diag_mac<true, 1>)
+                      : (nq % 4 == 0 && q4 ? k_diag_mac<false, 4>
+                                           : nq > 1 ? k_diag_mac<false, 2> : k_diag_mac<false, 1>);
   const unsigned total = (c.N / kT) * n_groups * map.n;
   const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
   kern<<<grid, kT, 0, c.stream>>>((const MacTerm*)terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map,
