@@ -189,6 +189,19 @@ helrm_status helrm_plan_rotations(const helrm_plan* p, int64_t* amounts, size_t 
 helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
                           size_t batch, helrm_ct** out);
 
+/* Serving form of the lookup on host buffers (coefficient form, the
+ * helrm_ct_import / helrm_ct_export exchange format; pinned memory makes the
+ * copies asynchronous): in[q C + c] is input ct c of query q,
+ * [2][level+1][N] words at the plan's level with scale `scale`; out[q O + o]
+ * receives output ct o of query q, [2][level][N] words.  The queries run
+ * one after another through the same computation as helrm_lookup (batch 1,
+ * double-hoisted mode), pipelined so that the host->device copy of query
+ * q+1 and the device->host copy of query q-1 overlap the lookup of query q.
+ * Returns after every output has been written.  LAYOUT if a key is missing,
+ * ARG for the single-hoisted mode. */
+helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                               const uint64_t* const* in, double scale, size_t batch, uint64_t* const* out);
+
 /* ---- primitives (parity tests and kernel microbenchmarks) --------------- */
 /* In-place negacyclic NTT (coefficient -> slot-order NTT form) / inverse on
  * n_polys x n_limbs limbs of N words at `dev`; limb i of a polynomial uses

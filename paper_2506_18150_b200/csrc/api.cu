@@ -134,6 +134,8 @@ struct helrm_ctx {
   // on s_kip, so they overlap the diagonal MACs on the context stream
   cudaStream_t s_ntt = nullptr, s_kip = nullptr, s_mac = nullptr;
   cudaStream_t s_cap = nullptr;   // private stream the lookup graphs are captured on
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // copy streams of helrm_lookup_host
+  cudaEvent_t hev[8] = {};                          // its events (outside the pool the lookup recycles)
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
   cudaEvent_t ev() {
@@ -748,6 +750,8 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       const char* pe = getenv("HELRM_PERSIST");
       c->persist = pe ? atoi(pe) : 0;
       HCUDA(cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
+      HCUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+      HCUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
     }
     cudaMemPool_t pool;
     HCUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -909,10 +913,14 @@ void helrm_ctx_destroy(helrm_ctx* c) {
   for (void* p : c->owned) cudaFreeAsync(p, c->stream);
   cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->hev)
+    if (e) cudaEventDestroy(e);
   if (c->s_ntt) cudaStreamDestroy(c->s_ntt);
   if (c->s_kip) cudaStreamDestroy(c->s_kip);
   if (c->s_cap) cudaStreamDestroy(c->s_cap);
   if (c->s_mac) cudaStreamDestroy(c->s_mac);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   delete c;
 }
 
@@ -2047,6 +2055,67 @@ static int64_t count_pairs(const helrm_plan* pl) {
   return n;
 }
 
+// graph cache entry of (plan, key set, chunk size): persistent staged inputs
+// X [Qc][C][2][l+1][N] and outputs S [O][Qc][2][l][N]
+static helrm_ctx::LookupGraph& graph_entry(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, int Qc) {
+  helrm_ctx::LookupGraph& G = c->graphs[std::make_tuple(pl->id, rk->id, Qc)];
+  if (!G.X) {
+    const size_t nqN = (size_t)(pl->level + 1) * c->P.N, oN = 2 * (size_t)pl->level * c->P.N;
+    G.X = (uint64_t*)c->dalloc((size_t)Qc * pl->C * 2 * nqN * 8);
+    G.S = (uint64_t*)c->dalloc((size_t)pl->O * Qc * oN * 8);
+    // MAC work list bound: every term carries >= 1 plaintext, every group >= 1 pair
+    HCUDA(cudaMallocHost(&G.pinned, (size_t)pl->n_diag * sizeof(MacTermW) + count_pairs(pl) * sizeof(int4) + 64));
+  }
+  return G;
+}
+
+// G.X -> G.S on the context stream: eagerly on the first use (creates every
+// cached constant), captured into a CUDA graph on the second, replayed after
+static void run_graph_chunk(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, helrm_ctx::LookupGraph& G,
+                            int Qc) {
+  if (G.exec) {
+    HCUDA(cudaGraphLaunch(G.exec, c->stream));
+    c->launches += G.launches;
+  } else if (G.uses == 0 || G.failed) {
+    lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
+  } else {
+    // capture on the private stream (the context stream may be the legacy
+    // default stream, which cannot be captured), ordered after the staging
+    cudaGraph_t graph = nullptr;
+    cudaStream_t user = c->stream;
+    c->join(c->s_cap, user);
+    c->stream = c->s_cap;
+    const uint64_t l0 = c->launches;
+    cudaError_t e = cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      try {
+        lookup_chunk(c, pl, rk, G.X, Qc, G.S, &G.pinned);
+      } catch (...) {
+        cudaStreamEndCapture(c->s_cap, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        graph = nullptr;
+        cudaGetLastError();
+        e = cudaErrorStreamCaptureInvalidated;
+      }
+    }
+    if (e == cudaSuccess) e = cudaStreamEndCapture(c->s_cap, &graph);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&G.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+    if (graph) cudaGraphDestroy(graph);
+    c->stream = user;
+    if (e != cudaSuccess) {   // not capturable here: run eagerly from now on
+      cudaGetLastError();
+      G.exec = nullptr;
+      G.failed = true;
+      c->launches = l0;
+      lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
+    } else {
+      G.launches = c->launches - l0;
+      HCUDA(cudaGraphLaunch(G.exec, c->stream));
+    }
+  }
+  G.uses++;
+}
+
 // device words one query of a batched double-hoisted lookup keeps live
 static size_t query_words(helrm_ctx* c, const helrm_plan* pl) {
   const Params& P = c->P;
@@ -2086,55 +2155,9 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
       emit_outputs(c, pl, S.p, Qc, scale, out + q0 * pl->O);
       continue;
     }
-    helrm_ctx::LookupGraph& G = c->graphs[std::make_tuple(pl->id, rk->id, Qc)];
-    if (!G.X) {
-      G.X = (uint64_t*)c->dalloc(nin * 2 * nqN * 8);
-      G.S = (uint64_t*)c->dalloc((size_t)pl->O * Qc * oN * 8);
-      // MAC work list bound: every term carries >= 1 plaintext, every group >= 1 pair
-      HCUDA(cudaMallocHost(&G.pinned, (size_t)pl->n_diag * sizeof(MacTermW) + count_pairs(pl) * sizeof(int4) + 64));
-    }
+    helrm_ctx::LookupGraph& G = graph_entry(c, pl, rk, Qc);
     stage_inputs(c, in + q0 * pl->C, nin, 2 * nqN, G.X);
-    if (G.exec) {
-      HCUDA(cudaGraphLaunch(G.exec, c->stream));
-      c->launches += G.launches;
-    } else if (G.uses == 0 || G.failed) {
-      lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
-    } else {
-      // capture on the private stream (the context stream may be the legacy
-      // default stream, which cannot be captured), ordered after the staging
-      cudaGraph_t graph = nullptr;
-      cudaStream_t user = c->stream;
-      c->join(c->s_cap, user);
-      c->stream = c->s_cap;
-      const uint64_t l0 = c->launches;
-      cudaError_t e = cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal);
-      if (e == cudaSuccess) {
-        try {
-          lookup_chunk(c, pl, rk, G.X, Qc, G.S, &G.pinned);
-        } catch (...) {
-          cudaStreamEndCapture(c->s_cap, &graph);
-          if (graph) cudaGraphDestroy(graph);
-          graph = nullptr;
-          cudaGetLastError();
-          e = cudaErrorStreamCaptureInvalidated;
-        }
-      }
-      if (e == cudaSuccess) e = cudaStreamEndCapture(c->s_cap, &graph);
-      if (e == cudaSuccess) e = cudaGraphInstantiate(&G.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
-      if (graph) cudaGraphDestroy(graph);
-      c->stream = user;
-      if (e != cudaSuccess) {   // not capturable here: run eagerly from now on
-        cudaGetLastError();
-        G.exec = nullptr;
-        G.failed = true;
-        c->launches = l0;
-        lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
-      } else {
-        G.launches = c->launches - l0;
-        HCUDA(cudaGraphLaunch(G.exec, c->stream));
-      }
-    }
-    G.uses++;
+    run_graph_chunk(c, pl, rk, G, Qc);
     emit_outputs(c, pl, G.S, Qc, scale, out + q0 * pl->O);
   }
 }
@@ -2184,6 +2207,52 @@ static void lookup_single(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
   helrm_ct_destroy(R);
   for (auto& m : rots)
     for (auto& kv : m) helrm_ct_destroy(kv.second);
+}
+
+helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                               const uint64_t* const* in, double scale, size_t batch, uint64_t* const* out) {
+  return guard([&] {
+    need(c && p && rk && (in || batch == 0) && (out || batch == 0), HELRM_ERR_ARG, "null argument");
+    need(p->mode == HELRM_MODE_DOUBLE, HELRM_ERR_ARG, "helrm_lookup_host runs the double-hoisted mode");
+    for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
+    const Params& P = c->P;
+    const uint32_t l = p->level;
+    const size_t nqN = (size_t)(l + 1) * P.N, oN = 2 * (size_t)l * P.N, C = p->C, O = p->O;
+    helrm_ctx::LookupGraph& G = graph_entry(c, p, rk, 1);
+    (void)scale;   // the lookup's arithmetic does not depend on the input scale (D20: output scale Delta)
+    // double-buffered device staging: H[s] inputs (coefficient form), D[s] outputs
+    DBuf H0(c, C * 2 * nqN), H1(c, C * 2 * nqN), D0(c, O * oN), D1(c, O * oN);
+    uint64_t* H[2] = {H0.p, H1.p};
+    uint64_t* D[2] = {D0.p, D1.p};
+    if (!c->hev[0])
+      for (auto& e : c->hev) HCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* h2d = c->hev;
+    cudaEvent_t* used = c->hev + 2;
+    cudaEvent_t* exp_ = c->hev + 4;
+    cudaEvent_t* d2h = c->hev + 6;
+    c->join(c->s_h2d, c->stream);   // staging buffers allocated on the context stream
+    for (size_t q = 0; q < batch; q++) {
+      const int b = (int)(q & 1);
+      if (q >= 2) HCUDA(cudaStreamWaitEvent(c->s_h2d, used[b], 0));
+      for (size_t ci = 0; ci < C; ci++)
+        HCUDA(cudaMemcpyAsync(H[b] + ci * 2 * nqN, in[q * C + ci], 2 * nqN * 8, cudaMemcpyHostToDevice, c->s_h2d));
+      HCUDA(cudaEventRecord(h2d[b], c->s_h2d));
+      HCUDA(cudaStreamWaitEvent(c->stream, h2d[b], 0));
+      ntt_fwd(c, H[b], G.X, 2 * C * (l + 1), P.map_q(l));   // coefficient -> NTT form, into the graph's inputs
+      HCUDA(cudaEventRecord(used[b], c->stream));
+      run_graph_chunk(c, p, rk, G, 1);
+      if (q >= 2) HCUDA(cudaStreamWaitEvent(c->stream, d2h[b], 0));
+      ntt_inv(c, G.S, D[b], 2 * O * l, P.map_q(l - 1));    // outputs back to coefficient form
+      HCUDA(cudaEventRecord(exp_[b], c->stream));
+      HCUDA(cudaStreamWaitEvent(c->s_d2h, exp_[b], 0));
+      for (size_t o = 0; o < O; o++)
+        HCUDA(cudaMemcpyAsync(out[q * O + o], D[b] + o * oN, oN * 8, cudaMemcpyDeviceToHost, c->s_d2h));
+      HCUDA(cudaEventRecord(d2h[b], c->s_d2h));
+    }
+    c->join(c->stream, c->s_d2h);
+    c->join(c->stream, c->s_h2d);
+    HCUDA(cudaStreamSynchronize(c->stream));
+  });
 }
 
 helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,

@@ -90,6 +90,7 @@ _SIGS = {
     "helrm_plan_info": [_vp, ctypes.POINTER(PlanInfo)],
     "helrm_plan_rotations": [_vp, _i64p, _sz, ctypes.POINTER(_sz)],
     "helrm_lookup": [_vp, _vp, _vp, _pp, _sz, _pp],
+    "helrm_lookup_host": [_vp, _vp, _vp, _pp, ctypes.c_double, _sz, _pp],
     "helrm_ntt_fwd": [_vp, _vp, _u32, _u32, _sz],
     "helrm_ntt_inv": [_vp, _vp, _u32, _u32, _sz],
     "helrm_modup": [_vp, _vp, _u32, _u32, _vp],
@@ -421,6 +422,20 @@ def lookup(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Ciphertext], bat
     outs = (ctypes.c_void_p * (batch * info.n_out_cts))()
     _check(_L.helrm_lookup(ctx.h, plan.h, rk.h, ins, batch, outs))
     return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]
+
+
+def lookup_host(ctx: Context, plan: Plan, rk: RotKeys, inputs: Sequence, scale: float, batch: int,
+                outputs: Sequence) -> None:
+    """helrm_lookup_host: `inputs` = batch x C host arrays (coefficient form
+    [2][level+1][N] uint64, pinned for asynchronous copies), `outputs` =
+    batch x O host arrays [2][level][N] filled in place."""
+    info = plan.info()
+    assert len(inputs) == batch * info.n_in_cts and len(outputs) == batch * info.n_out_cts
+    for a in list(inputs) + list(outputs):
+        assert a.dtype == np.uint64 and a.flags["C_CONTIGUOUS"]
+    ins = (ctypes.c_void_p * len(inputs))(*[a.ctypes.data for a in inputs])
+    outs = (ctypes.c_void_p * len(outputs))(*[a.ctypes.data for a in outputs])
+    _check(_L.helrm_lookup_host(ctx.h, plan.h, rk.h, ins, float(scale), batch, outs))
 
 
 # ---------------------------------------------------------------- primitives

@@ -412,3 +412,28 @@ def test_criteo_batched_equals_single(torch_mod):
     for q in range(3):
         single = h.lookup(E.ctx, plan, rk, [cts[q]])[0]
         assert np.array_equal(h.ct_export(E.ctx, outs[q]), h.ct_export(E.ctx, single)), q
+
+
+@gpu
+@pytest.mark.parametrize("name", ["uci", "llm_small"])
+def test_lookup_host_matches_lookup(name, torch_mod):
+    """helrm_lookup_host (host coefficient-form buffers, copies pipelined
+    against the lookups, CUDA-graph replay from the second query) equals
+    ct_import -> helrm_lookup -> ct_export bit for bit, for 3 queries."""
+    E = env(name, torch_mod)
+    w = synth.make_workload(name, batch=3)
+    h, cfg = E.h, w.config
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    plan = h.plan_create(E.ctx, T, cfg.level)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N), cfg.seed)
+    info = plan.info()
+    cts = _encrypt_batch(E, w, T, pk, info)
+    ins = [np.ascontiguousarray(h.ct_export(E.ctx, ct).reshape(-1)) for ct in cts]
+    outs = [np.zeros(2 * cfg.level * cfg.N, dtype=np.uint64) for _ in range(3 * info.n_out_cts)]
+    h.lookup_host(E.ctx, plan, rk, ins, 2.0 ** cfg.log_scale, 3, outs)
+    for q in range(3):
+        want = h.lookup(E.ctx, plan, rk, cts[q * info.n_in_cts:(q + 1) * info.n_in_cts])
+        for o in range(info.n_out_cts):
+            assert np.array_equal(outs[q * info.n_out_cts + o], h.ct_export(E.ctx, want[o]).reshape(-1)), (q, o)
