@@ -1707,7 +1707,10 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   std::vector<std::map<int, uint64_t*>> ab(C);
   size_t n_baby = 0;
   for (auto& bl : pl->babies) n_baby += bl.size();
-  DBuf D(c, C * Qc * dn * nlN), babies(c, std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
+  DBuf D(c, C * Qc * dn * nlN);
+  const bool fused_pre = (getenv("HELRM_FUSED_BM") ? atoi(getenv("HELRM_FUSED_BM")) != 0 : false) && Qc == 1 &&
+                         C == 1 && pl->babies[0].size() <= 48;
+  DBuf babies(c, fused_pre ? 1 : std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
   size_t bi = 0;
   bool same_babies = Qc == 1 && C > 1;
   for (size_t ci = 1; same_babies && ci < C; ci++) same_babies = pl->babies[ci] == pl->babies[0];
@@ -1755,6 +1758,10 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     }
     if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
+  // batch 1, one input ct: baby steps and inner sums fused in one kernel (no baby pairs in HBM)
+  static const bool fuse_env = getenv("HELRM_FUSED_BM") ? atoi(getenv("HELRM_FUSED_BM")) != 0 : false;
+  const bool fused = fuse_env && Qc == 1 && C == 1 && pl->babies[0].size() <= 48;
+  KipMulti kmf{};
   for (size_t ci = 0; !same_babies && ci < C; ci++) {
     const uint64_t* c0 = X + ci * 2 * nqN;
     uint64_t* Dc = D.p + ci * Qc * dn * nlN;
@@ -1777,6 +1784,22 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     km.dq = dn * nlN;
     km.cq = xs;
     km.oq = 2 * nlN;
+    if (fused) {   // keys only: k_baby_mac computes the pairs into shared memory
+      for (size_t jj = 0; jj < pl->babies[0].size(); jj++) {
+        const int j = pl->babies[0][jj];
+        ab[0][j] = reinterpret_cast<uint64_t*>((uintptr_t)jj);   // slot index, not a pointer
+        if (j == 0) continue;
+        need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
+        const uint64_t g = galois_of_rot(c, j);
+        km.rot[km.n] = rot_of_galois(c, g);
+        km.key[km.n] = key_for(rk, g);
+        km.out[km.n] = nullptr;
+        km.max_rot = std::max(km.max_rot, km.rot[km.n]);
+        km.n++;
+      }
+      kmf = km;
+      continue;
+    }
     for (int j : pl->babies[ci]) {
       uint64_t* a = babies.p + bi++ * Qc * 2 * nlN;
       if (j == 0) {  // (P c0, P c1): Q limbs scaled by [P]_q, P limbs 0
@@ -1811,7 +1834,40 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   if (n_out == 0) return;
   const size_t zq = (size_t)Qc;   // pairs per z
   DBuf AB(c, (size_t)n_out * zq * 2 * nlN), Bp(c, (size_t)n_out * zq * nqN), D2(c, (size_t)n_out * zq * dn * nlN);
-  MacDev md(c, ml, pinned);
+  bool macs_done = false;
+  std::unique_ptr<MacDev> mdp;
+  if (fused) {
+    // the work list with baby slots instead of pointers
+    MacList fl = ml;
+    fl.term_size = sizeof(FusedTerm);
+    fl.terms.assign(ml.n_terms * sizeof(FusedTerm), 0);
+    for (size_t t = 0; t < ml.n_terms; t++) {
+      const MacTerm* mt = reinterpret_cast<const MacTerm*>(&ml.terms[t * ml.term_size]);
+      FusedTerm ft{};
+      ft.slot = (int)(uintptr_t)mt->x0;
+      for (int g = 0; g < kGiantPack; g++) ft.u[g] = mt->u[g];
+      std::memcpy(&fl.terms[t * sizeof(FusedTerm)], &ft, sizeof(FusedTerm));
+    }
+    mdp.reset(new MacDev(c, fl, pinned));
+    const bool has0 = !pl->babies[0].empty() && pl->babies[0][0] == 0;
+    BabyMacArgs bm{};
+    bm.terms = (const FusedTerm*)mdp->terms.p;
+    bm.groups = (const int4*)mdp->groups.p;
+    bm.n_groups = (int)ml.groups.size();
+    bm.n_slots = (int)pl->babies[0].size();
+    bm.slot0 = has0 ? 1 : 0;
+    bm.j0 = has0 ? 0 : -1;
+    bm.c1 = X + nqN;
+    bm.out = AB.p;
+    bm.out_stride = 2 * nlN;
+    bm.half = nlN;
+    bm.bytes = 8.0 * N * nl * (dn + 2.0 + kmf.n * 2.0 * dn + ml.n_u + 2.0 * n_out);
+    macs_done = launch_baby_mac(c->dc(), kmf, bm, mqp);
+    need(macs_done, HELRM_ERR_CONFIG, "fused baby/MAC kernel does not apply");   // guarded by `fused`
+  }
+  std::unique_ptr<MacDev> mdu;
+  if (!fused) mdu.reset(new MacDev(c, ml, pinned));
+  const MacDev& md = fused ? *mdp : *mdu;
   // (serialised while the per-kernel profiler is on, so each kernel's events time it alone)
   static const bool pipe_env = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
   const bool pipe = pipe_env && !c->prof.on;
@@ -1907,7 +1963,8 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   for (size_t gp = 0; !periodic && gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
     const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
-    if (!periodic) run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
+    if (!periodic && !macs_done)
+      run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
     if (pipe) c->join(sn, sm);
     std::vector<int> rot;   // rotating pairs of the chunk (zero giants need no key switch)
     for (int z = z0; z < z1; z++)

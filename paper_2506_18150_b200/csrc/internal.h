@@ -296,6 +296,29 @@ struct KipMulti {
 };
 void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map);
 
+// Fused D20 L2 + L3 for one ciphertext (k_baby_mac): a CTA computes every baby
+// pair of its 128-position tile of one limb into shared memory (babies
+// a.key[i] -> slot i + slot0, slot j0 = the rotation-0 pair (P c0, P c1) when
+// present) and then runs the inner sums of every giant pack against the
+// streamed plaintexts -- the baby pairs never go to HBM.
+struct FusedTerm {
+  int slot;                              // baby pair slot in shared memory
+  int pad;
+  const uint64_t* u[4];                  // plaintext per giant of the pack (D-form) or null
+};
+struct BabyMacArgs {
+  const FusedTerm* terms;
+  const int4* groups;                    // as launch_diag_mac
+  int n_groups;
+  int n_slots, slot0, j0;                // baby slots; first key slot; slot of rotation 0 (-1: none)
+  const uint64_t* c1;                    // [level+1][N] for the rotation-0 pair
+  uint64_t* out;                         // pair z at out + z out_stride (A), + half (B)
+  size_t out_stride, half;
+  double bytes;                          // algorithmic HBM bytes of the launch (profiler)
+};
+constexpr int kBabyMacTile = 128;
+bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map);
+
 // D20 L3 work list.  Giants are packed kGiantPack at a time: a term is one
 // baby pair x = (x0, x1) with the plaintext u of each giant of the pack that
 // uses it (null if none), so every baby value is loaded once per pack.  The

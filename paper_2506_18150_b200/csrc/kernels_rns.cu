@@ -451,6 +451,157 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   }
 }
 
+// D20 L2 + L3 fused for one ciphertext (see BabyMacArgs).  Phase 1 is
+// k_kip_multi on a 128-position tile (digits + c0 staged with a halo, keys
+// streamed, one baby per round) writing the pairs to shared memory; phase 2
+// is k_diag_mac<true, 1> reading the pairs from shared memory (4 terms per
+// round: 16 plaintext loads in flight per thread).
+template <int DNUM>
+__global__ void __launch_bounds__(kBabyMacTile) k_baby_mac(const __grid_constant__ KipMulti a,
+                                                          const __grid_constant__ BabyMacArgs m,
+                                                          const PrimeDev* __restrict__ primes,
+                                                          const __grid_constant__ LimbMap map, uint32_t N) {
+  constexpr int T = kBabyMacTile, G = kGiantPack;
+  extern __shared__ double shd[];
+  const int l = blockIdx.y, tid = threadIdx.x;
+  const uint32_t n = N / 2, p0 = blockIdx.x * T, half = p0 >= n ? n : 0;
+  const uint32_t span = T + a.max_rot;
+  double* sb = shd + (DNUM + 1) * span;             // baby pairs [slot][2][T]
+  const uint32_t chain = map.pr[l];
+  const PrimeDev& P = primes[chain];
+  const double q = P.qd, qi = P.qinv;
+  const bool has_c0 = l <= (int)a.level;
+  const int kown = (a.own && has_c0) ? l / a.alpha : -1;
+  for (uint32_t e = tid; e < span; e += T) {
+    uint32_t j = p0 - half + e;
+    j = j >= n ? j - n : j;
+    const size_t src = (size_t)l * N + half + j;
+#pragma unroll
+    for (int k = 0; k < DNUM; k++)
+      shd[k * span + e] = fm::u2d(k == kown ? a.own[src] : a.digits[(size_t)k * a.digit_stride + src]);
+    shd[DNUM * span + e] = has_c0 ? fm::u2d(a.c0[src]) : 0.0;
+  }
+  const uint32_t p = p0 + tid;
+  const double pm = has_c0 ? fm::u2c(a.p_mod[l], q) : 0.0;
+  // rotation-0 pair (P c0, P c1) over Q_l, 0 over P (D20 L2, j = 0)
+  if (m.j0 >= 0) {
+    double v0 = 0.0, v1 = 0.0;
+    if (has_c0) {
+      fm::FAcc x0, x1;
+      fm::fmac(x0, fm::u2d(a.c0[(size_t)l * N + p]), pm);
+      fm::fmac(x1, fm::u2d(m.c1[(size_t)l * N + p]), pm);
+      v0 = fm::fred(x0, q, qi);
+      v1 = fm::fred(x1, q, qi);
+    }
+    sb[(m.j0 * 2) * T + tid] = v0;
+    sb[(m.j0 * 2 + 1) * T + tid] = v1;
+  }
+  __syncthreads();
+  for (int j = 0; j < a.n; j++) {
+    const uint64_t* kb = a.key[j] + (size_t)chain * N + p;
+    uint64_t kv0[DNUM], kv1[DNUM];
+#pragma unroll
+    for (int k = 0; k < DNUM; k++) {
+      kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
+      kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
+    }
+    const uint32_t e = tid + a.rot[j];
+    fm::FAcc acc0, acc1;
+#pragma unroll
+    for (int k = 0; k < DNUM; k++) {
+      const double dv = shd[k * span + e];
+      fm::fmac(acc0, dv, fm::bits2d(kv0[k]));
+      fm::fmac(acc1, dv, fm::bits2d(kv1[k]));
+    }
+    if (has_c0) fm::fmac(acc0, shd[DNUM * span + e], pm);
+    const int sl = m.slot0 + j;
+    sb[(sl * 2) * T + tid] = fm::fred(acc0, q, qi);
+    sb[(sl * 2 + 1) * T + tid] = fm::fred(acc1, q, qi);
+  }
+  __syncthreads();
+  // phase 2: inner sums of every giant pack (the pack's term list staged in shared memory,
+  // so the plaintext loads do not wait on a pointer load)
+  __shared__ FusedTerm stm[64];
+  const size_t o = (size_t)l * N + p;
+  for (int gi = 0; gi < m.n_groups; gi++) {
+    const int4 gr = m.groups[gi];
+    fm::FAcc acc0[G], acc1[G];
+    int cnt = 0;
+    for (int t = 0; t < gr.y; t += 4) {
+      if (t % 64 == 0) {
+        __syncthreads();
+        for (int k = tid; k < min(64, gr.y - t); k += T) stm[k] = m.terms[gr.x + t + k];
+        __syncthreads();
+      }
+      const int nr = min(4, gr.y - t);
+      uint64_t u[4][G];
+      int sl[4];
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        if (r < nr) {
+          const FusedTerm& ft = stm[(t + r) % 64];
+          sl[r] = ft.slot;
+#pragma unroll
+          for (int g = 0; g < G; g++) u[r][g] = ft.u[g] ? __ldcs(ft.u[g] + o) : 0;
+        } else {
+          sl[r] = 0;
+#pragma unroll
+          for (int g = 0; g < G; g++) u[r][g] = 0;
+        }
+      }
+      if (cnt + 4 > fm::kFAccTerms) {
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+          fm::fold(acc0[g], q, qi);
+          fm::fold(acc1[g], q, qi);
+        }
+        cnt = 0;
+      }
+      cnt += 4;
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const double xa = sb[(sl[r] * 2) * T + tid], xb = sb[(sl[r] * 2 + 1) * T + tid];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+          const double ud = fm::bits2d(u[r][g]);
+          fm::fmac(acc0[g], ud, xa);
+          fm::fmac(acc1[g], ud, xb);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+      if (g < gr.w) {
+        uint64_t* dst = m.out + (size_t)(gr.z + g) * m.out_stride;
+        dst[o] = fm::c2u(fm::fred(acc0[g], q, qi), P.rc.q);
+        dst[m.half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
+      }
+    }
+  }
+}
+
+bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map) {
+  const size_t smem = ((size_t)(a.dnum + 1) * (kBabyMacTile + a.max_rot) + (size_t)m.n_slots * 2 * kBabyMacTile) * 8;
+  if (smem > 200 * 1024 || c.N % kBabyMacTile) return false;
+  decltype(&k_baby_mac<1>) kern = nullptr;
+  switch (a.dnum) {
+    case 1: kern = k_baby_mac<1>; break;
+    case 2: kern = k_baby_mac<2>; break;
+    case 3: kern = k_baby_mac<3>; break;
+    case 4: kern = k_baby_mac<4>; break;
+    case 5: kern = k_baby_mac<5>; break;
+    case 6: kern = k_baby_mac<6>; break;
+    case 7: kern = k_baby_mac<7>; break;
+    default: return false;
+  }
+  ProfScope ps_(c, "baby_mac", m.bytes);
+  HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<dim3(c.N / kBabyMacTile, map.n), kBabyMacTile, smem, c.stream>>>(a, m, c.primes, map, c.N);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+  return true;
+}
+
 // D20 L5: after ncclAllReduce(uint64, sum) of partial Q_l P accumulators
 // (each < q, at most 2^13 ranks -> no wrap), reduce every word mod its prime
 __global__ void k_modred(uint64_t* __restrict__ x, const PrimeDev* __restrict__ primes,
