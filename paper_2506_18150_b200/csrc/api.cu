@@ -1978,6 +1978,47 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
       modup_batch(c, Bp.p + za * zq * nqN, nqN, (int)G, l, D2.p + za * zq * dn * nlN, sn, false);
       if (pipe) c->join(sk, sn);
       const int zend = r1 < rot.size() ? rot[r1] : z1;
+      static const bool kgrun = getenv("HELRM_KIP_RUN") ? atoi(getenv("HELRM_KIP_RUN")) != 0 : true;
+      if (Qc == 1 && kgrun) {   // one accumulating key-switch pass per run of giants of an output block
+        KipGiants kg{};
+        auto flush = [&](int64_t o) {
+          if (kg.n == 0) return;
+          kg.digit_stride = nlN;
+          kg.dnum = (int)dn;
+          kg.add_rows = (int)nl;
+          kg.alpha = (int)P.alpha;
+          kg.level = (int)l;
+          kg.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+          kg.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+          kg.out0 = Oall + (size_t)o * 2 * nlN;
+          kg.out1 = kg.out0 + nlN;
+          launch_kip_giants(c->dc(sk), kg, mqp);
+          kg.n = 0;
+        };
+        int64_t cur_o = -1;
+        for (int z = zdone; z < zend; z++) {
+          const int64_t o = ml.oi[z].first, gi = pl->giants[o][ml.oi[z].second];
+          if (gi % (int64_t)P.n == 0) {
+            zero_giant(z);
+            continue;
+          }
+          if (o != cur_o || kg.n == kMaxGiantRun) {
+            flush(cur_o);
+            cur_o = o;
+          }
+          const uint64_t g = galois_of_rot(c, gi);
+          kg.digits[kg.n] = D2.p + (size_t)z * dn * nlN;
+          kg.own[kg.n] = Bp.p + (size_t)z * nqN;
+          kg.key[kg.n] = key_for(rk, g);
+          kg.add0[kg.n] = AB.p + (size_t)z * 2 * nlN;
+          kg.rot[kg.n] = rot_of_galois(c, g);
+          kg.n++;
+        }
+        flush(cur_o);
+        zdone = zend;
+        r0 = r1;
+        continue;
+      }
       for (int z = zdone; z < zend; z++) {
         const int64_t gi = pl->giants[ml.oi[z].first][ml.oi[z].second];
         if (gi % (int64_t)P.n == 0) {

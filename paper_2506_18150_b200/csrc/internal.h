@@ -270,6 +270,25 @@ struct KipArgs {
 };
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map);
 
+// Several giant steps of one output block in one pass (D20 L4):
+//   out0 += sum_g [ phi_g(A_g) + sum_k phi_g(D_{g,k}) b_{g,k} ],  out1 += sum_g sum_k phi_g(D_{g,k}) a_{g,k}
+// so the accumulators are read and written once for the run instead of once
+// per giant.  Common fields as KipArgs (add_mul = 1, accumulate = 1, nq = 1).
+constexpr int kMaxGiantRun = 16;
+struct KipGiants {
+  size_t digit_stride;
+  int dnum, add_rows, alpha, level, n;
+  size_t key_digit_stride, key_half_stride;
+  uint64_t* out0;
+  uint64_t* out1;
+  const uint64_t* digits[kMaxGiantRun];
+  const uint64_t* own[kMaxGiantRun];
+  const uint64_t* key[kMaxGiantRun];
+  const uint64_t* add0[kMaxGiantRun];
+  uint32_t rot[kMaxGiantRun];
+};
+void launch_kip_giants(const DevCtx& c, const KipGiants& a, const LimbMap& map);
+
 // all babies of one ciphertext (k_kip_multi)
 constexpr int kMaxBabies = 128;
 struct KipMulti {
