@@ -1886,7 +1886,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
                     Oq(z) + (size_t)q * 2 * nlN, m2);
   };
   static const int mac_ch = getenv("HELRM_MACCH") ? atoi(getenv("HELRM_MACCH")) : 4;   // MAC groups per launch
-  static const int ntt_ch = getenv("HELRM_NTTCH") ? atoi(getenv("HELRM_NTTCH")) : 8;   // giants per ModDown/ModUp batch
+  static const int ntt_ch = getenv("HELRM_NTTCH") ? atoi(getenv("HELRM_NTTCH")) : 16;   // giants per ModDown/ModUp batch
   // Output blocks that repeat block 0's work list with the baby pairs of their own input ct
   // (LLM layout L2: the 4 blocks share all 1279 plaintexts) run as one MAC launch in which
   // the blocks take the query role, so each plaintext value is loaded once per 2 blocks.

@@ -186,7 +186,9 @@ bool ntt_fwd_cluster(const DevCtx& c, const uint64_t* src, uint64_t* dst, size_t
   // measured 46% slower than the two-pass kernels (1 CTA of 1024 threads per SM cannot hide the
   // phase latencies; profiles/r01_ab_cluster.txt): off unless HELRM_NTT_CLUSTER=1
   static const int enabled = getenv("HELRM_NTT_CLUSTER") ? atoi(getenv("HELRM_NTT_CLUSTER")) : 0;
-  if (!enabled) return false;
+  // small launches (latency-bound chains such as RotSum's ModDown) may still prefer one kernel
+  static const size_t small_max = getenv("HELRM_NTT_CLUSTER_MAX") ? (size_t)atoi(getenv("HELRM_NTT_CLUSTER_MAX")) : 0;
+  if (!enabled && n_total > small_max) return false;
   auto k = din ? k_ntt_fwd_cl<true> : k_ntt_fwd_cl<false>;
   static bool attr_done[2] = {false, false};
   if (!attr_done[din]) {
