@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const int tp = (tw4[k >> 2] >> (8 * (k & 3))) & 0xff;
-      smu[tp * 16 + (sub ^ (tp & 15))] = d2u(r[k], q, qi, P.rc.q);
+      smu[tp * 16 + (sub ^ (tp & 15))] = fm::c2u(r[k], P.rc.q);   // centred by the last stage's reduction
     }
     __syncthreads();
     // block of rank g = 16 cta + i lives at slot positions (g / stride) n +
@@ -214,25 +214,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
     const int i = tid % 16, g = blockIdx.x * 16 + i;   // idx % 16 == tid % 16
     const size_t pbase = (size_t)(g >> lgs) * n + (g & (stride - 1));
+    // thread tid handles tp = tid / 16 + 16 it: tp & 15 is constant per thread, so the shared
+    // index advances by 256 and the global one by 16 << lgs per iteration
+    const int tp0 = tid / 16;
+    const uint64_t* sp0 = smu + tp0 * 16 + (i ^ (tp0 & 15));
+    const size_t gstep = (size_t)16 << lgs;
     if (epi.out == nullptr) {
-      uint64_t* dg = d + pbase;
-#pragma unroll 4
-      for (int idx = tid; idx < kTileElems; idx += kThreads) {
-        const int tp = idx / 16;
-        dg[(size_t)tp << lgs] = smu[tp * 16 + (i ^ (tp & 15))];
-      }
+      uint64_t* dg = d + pbase + ((size_t)tp0 << lgs);
+#pragma unroll
+      for (int it = 0; it < 16; it++) dg[it * gstep] = sp0[256 * it];
     } else {   // fused ModDown / rescale finish: out (+)= (y - t) s mod q
       const size_t pg = gl / map.n, lg = gl % map.n;
       const uint64_t qq = P.rc.q, sv = epi.s[lg], svp = epi.sp[lg];
-      const uint64_t* yg = epi.y + pg * epi.ys + lg * (size_t)N + pbase;
-      uint64_t* og = epi.out + pg * epi.os + lg * (size_t)N + pbase;
+      const uint64_t* yg = epi.y + pg * epi.ys + lg * (size_t)N + pbase + ((size_t)tp0 << lgs);
+      uint64_t* og = epi.out + pg * epi.os + lg * (size_t)N + pbase + ((size_t)tp0 << lgs);
 #pragma unroll 4
-      for (int idx = tid; idx < kTileElems; idx += kThreads) {
-        const int tp = idx / 16;
-        const size_t at = (size_t)tp << lgs;
-        uint64_t v = shoup(sub_mod(yg[at], smu[tp * 16 + (i ^ (tp & 15))], qq), sv, svp, qq);
-        if (epi.accumulate) v = add_mod(v, og[at], qq);
-        og[at] = v;
+      for (int it = 0; it < 16; it++) {
+        uint64_t v = shoup(sub_mod(yg[it * gstep], sp0[256 * it], qq), sv, svp, qq);
+        if (epi.accumulate) v = add_mod(v, og[it * gstep], qq);
+        og[it * gstep] = v;
       }
     }
   }
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
     const double2 nm = post ? post[gl % map.n] : P.ninvd;
     for (int k = 0; k < kEPT; k++) {
       const double v = mmul(r[k], nm.x, nm.y, q);
-      d[(size_t)(t + TS * k) * 256 + gsub] = d2u(v, q, qi, P.rc.q);
+      d[(size_t)(t + TS * k) * 256 + gsub] = fm::c2u(v, P.rc.q);   // |v| <= 0.75 q after mmul
     }
   }
 }
