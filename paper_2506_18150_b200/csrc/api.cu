@@ -1869,7 +1869,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   if (!fused) mdu.reset(new MacDev(c, ml, pinned));
   const MacDev& md = fused ? *mdp : *mdu;
   // (serialised while the per-kernel profiler is on, so each kernel's events time it alone)
-  static const bool pipe_env = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : true;
+  static const bool pipe_env = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) != 0 : false;
   const bool pipe = pipe_env && !c->prof.on;
   cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream, sm = pipe ? c->s_mac : c->stream;
   const int pers = pipe ? c->persist : 0;
