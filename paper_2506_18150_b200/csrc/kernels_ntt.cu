@@ -335,9 +335,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
 #pragma unroll
     for (int k = 0; k < kEPT; k++) d[(size_t)gsub * 256 + t + TS * k] = (uint64_t)__double_as_longlong(r[k]);
   } else {
-#pragma unroll
     // N^-1, or N^-1 times a per-limb factor (the y-form of a base conversion)
     const double2 nm = post ? post[gl % map.n] : P.ninvd;
+#pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const double v = mmul(r[k], nm.x, nm.y, q);
       d[(size_t)(t + TS * k) * 256 + gsub] = fm::c2u(v, P.rc.q);   // |v| <= 0.75 q after mmul

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhelrm.so")
+LIB_PATH = os.environ.get("HELRM_LIB") or os.path.join(_HERE, "lib", "libhelrm.so")   # override: A/B experiments
 
 HELRM_OK = 0
 ERRORS = {2: "CONFIG", 3: "LEVEL", 4: "CAPACITY", 5: "RANGE", 6: "LAYOUT", 7: "CUDA", 8: "NCCL", 9: "ALLOC", 10: "ARG"}
