@@ -437,3 +437,115 @@ def test_lookup_host_matches_lookup(name, torch_mod):
         want = h.lookup(E.ctx, plan, rk, cts[q * info.n_in_cts:(q + 1) * info.n_in_cts])
         for o in range(info.n_out_cts):
             assert np.array_equal(outs[q * info.n_out_cts + o], h.ct_export(E.ctx, want[o]).reshape(-1)), (q, o)
+
+
+@gpu
+def test_microbench_ntt_full_size_sampled(torch_mod):
+    """configs[4] at full size in the launch configuration bench.py times:
+    1024 ciphertexts x 2 x 24 limbs at N = 2^16 (49,152 limb transforms, 24
+    GiB) through helrm_ntt_fwd / helrm_ntt_inv; sampled limbs against the
+    oracle's NTT (first, middle, last chunk), and the inverse restores them."""
+    torch = torch_mod
+    E = env("criteo", torch)
+    PO = E.PO
+    L1 = PO.L + 1
+    n_polys = 2 * 1024
+    g = torch.Generator(device="cuda").manual_seed(99)
+    # residues below the smallest prime of the chain (uniform enough for a transform check)
+    qmin = min(PO.q)
+    buf = torch.randint(0, qmin, (n_polys * L1 * PO.N,), dtype=torch.int64, device="cuda", generator=g)
+    picks = [0, 7, n_polys * L1 // 2 + 3, n_polys * L1 - 1]          # global limb indices
+    before = {i: buf[i * PO.N:(i + 1) * PO.N].cpu().numpy().astype(np.uint64) for i in picks}
+    ptr = buf.data_ptr()
+    E.h.ntt_fwd(E.ctx, ptr, 0, L1, n_polys)
+    E.ctx.sync()
+    perm = _slot_to_natural(PO.N)
+    for i in picks:
+        q = PO.q[i % L1]
+        got = buf[i * PO.N:(i + 1) * PO.N].cpu().numpy().astype(np.uint64)[perm]
+        want = core.ntt(before[i][None, :], [q], PO)[0]
+        assert np.array_equal(got, want), i
+    E.h.ntt_inv(E.ctx, ptr, 0, L1, n_polys)
+    E.ctx.sync()
+    for i in picks:
+        assert np.array_equal(buf[i * PO.N:(i + 1) * PO.N].cpu().numpy().astype(np.uint64), before[i]), i
+    del buf
+    torch.cuda.empty_cache()
+
+
+@gpu
+def test_criteo_hoisted_rotations_sampled(torch_mod):
+    """configs[4] hoisted rotations at Criteo size: one ModUp, amounts 1..64
+    written to a ring (the bench's helrm_rotate_hoisted call), sampled
+    amounts bit-exact against the oracle's Rotate with the same keys."""
+    E = env("criteo", torch_mod)
+    h, PO, cfg = E.h, E.PO, E.cfg
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    osk = core.sk_gen(PO, cfg.seed)
+    amounts = list(range(1, 65))
+    check = [1, 37, 64]
+    rk = h.rotkeys_gen(E.ctx, sk, sorted({core.galois_elt(a, PO) for a in amounts}), cfg.seed)
+    ork = core.rotkeys_gen(PO, osk, [core.galois_elt(a, PO) for a in check], cfg.seed)
+    level = PO.L
+    coeff = _rand_ct(PO, level, 21)
+    Q = PO.q[: level + 1]
+    ct = h.ct_import(E.ctx, coeff, level, 1.0)
+    ring = [h.ct_alloc(E.ctx, level) for _ in amounts]
+    h.rotate_hoisted(E.ctx, rk, ct, amounts, ring)
+    oct_ = core.Ciphertext(core.ntt(coeff[0], Q, PO), core.ntt(coeff[1], Q, PO), level, 1)
+    for a in check:
+        want = core.ct_to_coeff(PO, core.rotate(PO, oct_, a, ork))
+        assert np.array_equal(h.ct_export(E.ctx, ring[a - 1]), want), a
+
+
+@gpu
+def test_criteo_batch64_sampled(torch_mod):
+    """configs[2] batch 64 in the bench's configuration (one helrm_lookup
+    call, default query chunking): sampled queries equal the batch-1 lookups
+    of the same ciphertexts (which tests/golden pins against the oracle)."""
+    E = env("criteo", torch_mod)
+    w = synth.make_workload("criteo", batch=4)
+    h, cfg = E.h, w.config
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    plan = h.plan_create(E.ctx, T, cfg.level)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N), cfg.seed)
+    cts = _encrypt_batch(E, w, T, pk, plan.info())
+    batch = [cts[i % 4] for i in range(64)]
+    outs = h.lookup(E.ctx, plan, rk, batch, 64)
+    for q in (0, 17, 42, 63):
+        single = h.lookup(E.ctx, plan, rk, [cts[q % 4]])[0]
+        assert np.array_equal(h.ct_export(E.ctx, outs[q]), h.ct_export(E.ctx, single)), q
+
+
+@gpu
+def test_lookup_error_and_degenerate_cases(torch_mod):
+    """Empty batch (no work, no outputs), an input at the wrong level (LEVEL),
+    a key set missing a rotation (LAYOUT), the serving call on a
+    single-hoisted plan (ARG)."""
+    E = env("tiny_b", torch_mod)
+    w = synth.make_workload("tiny_b")
+    h, cfg = E.h, w.config
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    plan = h.plan_create(E.ctx, T, cfg.level)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N), cfg.seed)
+    assert h.lookup(E.ctx, plan, rk, [], 0) == []
+    x = h.encode_query(T, w.indices[0], w.dense[0], cfg.n_slots)
+    low = h.encrypt(E.ctx, pk, x, cfg.level - 1, 5)
+    with pytest.raises(h.HelrmError) as e:
+        h.lookup(E.ctx, plan, rk, [low])
+    assert e.value.code == 3
+    ct = h.encrypt(E.ctx, pk, x, cfg.level, 5)
+    partial = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N)[:1], cfg.seed)
+    with pytest.raises(h.HelrmError) as e:
+        h.lookup(E.ctx, plan, partial, [ct])
+    assert e.value.code == 6
+    splan = h.plan_create(E.ctx, T, cfg.level, 0, 1)
+    coeff = np.ascontiguousarray(h.ct_export(E.ctx, ct).reshape(-1))
+    out = np.zeros(2 * (cfg.level) * cfg.N, dtype=np.uint64)
+    with pytest.raises(h.HelrmError) as e:
+        h.lookup_host(E.ctx, splan, rk, [coeff], 1.0, 1, [out])
+    assert e.value.code == 10
