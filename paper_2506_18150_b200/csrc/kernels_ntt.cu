@@ -133,9 +133,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
     }
   }
   // phase A: stages 0..3 on layout e = t + TS k (twiddles independent of t)
+  // Lazy reduction: a butterfly's product term is reduced by mmul (|r| <= 0.75 q for any
+  // |y| < 2^51), so only the additive inputs grow, by 0.75 q per stage.  Reducing the
+  // additive inputs (half the elements) before every even stage keeps every value below
+  // 2 q < 2^51 (q < 2^50): half the reductions of reducing everything every other stage.
 #pragma unroll
   for (int st = 0; st < 4; st++) {
     const int half = 8 >> st;
+    if ((st & 1) == 0) {
+#pragma unroll
+      for (int k = 0; k < kEPT; k++)
+        if ((k & half) == 0) r[k] = cred(r[k], q, qi);
+    }
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       if ((k & half) == 0) {
@@ -143,10 +152,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
         const double2 w = P1 ? twA[(1 << st) + (k >> (4 - st))] : twA[(1 << st) - 1 + (k >> (4 - st))];
         ct_bfly(r[k], r[k + half], w, q);
       }
-    }
-    if (st & 1) {
-#pragma unroll
-      for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
     }
   }
   if (SLOG > 4) {
@@ -166,6 +171,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
 #pragma unroll
     for (int st = 4; st < SLOG; st++) {
       const int half = S >> (st + 1);
+      if ((st & 1) == 0) {
+#pragma unroll
+        for (int k = 0; k < kEPT; k++)
+          if ((k & half) == 0) r[k] = cred(r[k], q, qi);
+      }
 #pragma unroll
       for (int k = 0; k < kEPT; k++) {
         if ((k & half) == 0) {
@@ -176,12 +186,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
           ct_bfly(r[k], r[k + half], w, q);
         }
       }
-      if ((st & 1) || st == SLOG - 1) {
-#pragma unroll
-        for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
-      }
     }
-  } else {
+  }
+  // pass 1 hands values below 2 q to pass 2 (whose first stage reduces its additive inputs);
+  // pass 2 reduces everything once before canonicalising
+  if (!P1) {
 #pragma unroll
     for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
   }
