@@ -29,16 +29,17 @@ def main(path):
         a["bytes"] += b
         a["grid"] += g
     res = {"source": path, "kernels": agg}
-    p1 = [v for k, v in agg.items() if k.startswith("k_ntt_fwd<8, 0>") or k.startswith("k_ntt_fwd<8, 2>")]
-    p2 = [v for k, v in agg.items() if k.startswith("k_ntt_fwd<8, 1>")]
+    p1 = [v for k, v in agg.items() if k.startswith("k_ntt_fwd<8, 0") or k.startswith("k_ntt_fwd<8, 2")]
+    p2 = [v for k, v in agg.items() if k.startswith("k_ntt_fwd<8, 1")]
     if p1 and p2:
         limbs = sum(v["grid"] for v in p1) / 16
         res["ntt_fwd_bytes_per_limb"] = round((sum(v["bytes"] for v in p1) + sum(v["bytes"] for v in p2)) / limbs)
         res["ntt_fwd_limbs"] = limbs
-    for k, key in (("k_diag_mac<1>", "diag_mac"), ("k_kip_multi<6>", "kip_multi")):
-        if k in agg:
-            res[key + "_bytes_per_launch"] = round(agg[k]["bytes"] / agg[k]["launches"])
-    kips = [v for k, v in agg.items() if k.startswith("k_kip<")]
+    for prefix, key in (("k_diag_mac", "diag_mac"), ("k_kip_multi", "kip_multi")):
+        ks = [v for k, v in agg.items() if k.startswith(prefix)]
+        if ks:
+            res[key + "_bytes_per_launch"] = round(sum(v["bytes"] for v in ks) / sum(v["launches"] for v in ks))
+    kips = [v for k, v in agg.items() if k.startswith("k_kip<") or k.startswith("k_kip_giants")]
     if kips:
         res["kip_bytes_per_launch"] = round(sum(v["bytes"] for v in kips) / sum(v["launches"] for v in kips))
     print(json.dumps(res, indent=1))
