@@ -101,6 +101,7 @@ struct helrm_ctx {
     uint64_t* X = nullptr;        // staged inputs [Qc][C][2][l+1][N]
     uint64_t* S = nullptr;        // outputs [O][Qc][2][l][N]
     void* pinned = nullptr;       // host copy of the MAC work list the graph re-uploads
+    uint64_t* scratch = nullptr;  // own NTT scratch (second serving slot)
     size_t uses = 0;
     uint64_t launches = 0;        // kernel launches inside the graph (added to the counter per replay)
     bool failed = false;
@@ -114,6 +115,7 @@ struct helrm_ctx {
         if (it->second.pinned) cudaFreeHost(it->second.pinned);
         dfree(it->second.X);
         dfree(it->second.S);
+        dfree(it->second.scratch);
         it = graphs.erase(it);
       } else {
         ++it;
@@ -907,6 +909,7 @@ void helrm_ctx_destroy(helrm_ctx* c) {
     if (kv.second.pinned) cudaFreeHost(kv.second.pinned);
     c->dfree(kv.second.X);
     c->dfree(kv.second.S);
+    c->dfree(kv.second.scratch);
   }
   c->graphs.clear();
   if (c->comm) nccl().commDestroy(c->comm);
@@ -2158,8 +2161,9 @@ static int64_t count_pairs(const helrm_plan* pl) {
 
 // graph cache entry of (plan, key set, chunk size): persistent staged inputs
 // X [Qc][C][2][l+1][N] and outputs S [O][Qc][2][l][N]
-static helrm_ctx::LookupGraph& graph_entry(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, int Qc) {
-  helrm_ctx::LookupGraph& G = c->graphs[std::make_tuple(pl->id, rk->id, Qc)];
+static helrm_ctx::LookupGraph& graph_entry(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, int Qc,
+                                           int slot = 0) {
+  helrm_ctx::LookupGraph& G = c->graphs[std::make_tuple(pl->id, rk->id, Qc + 1000 * slot)];
   if (!G.X) {
     const size_t nqN = (size_t)(pl->level + 1) * c->P.N, oN = 2 * (size_t)pl->level * c->P.N;
     G.X = (uint64_t*)c->dalloc((size_t)Qc * pl->C * 2 * nqN * 8);
@@ -2319,8 +2323,16 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
     const Params& P = c->P;
     const uint32_t l = p->level;
     const size_t nqN = (size_t)(l + 1) * P.N, oN = 2 * (size_t)l * P.N, C = p->C, O = p->O;
-    helrm_ctx::LookupGraph& G = graph_entry(c, p, rk, 1);
     (void)scale;   // the lookup's arithmetic does not depend on the input scale (D20: output scale Delta)
+    // Two serving slots: query q runs on slot q & 1 (its own graph, buffers, NTT scratch and
+    // stream), so one query's latency-bound tail (final ModDown, rescale, RotSum chain) overlaps
+    // the next query's HBM-bound baby steps and inner sums.
+    helrm_ctx::LookupGraph* Gs[2] = {&graph_entry(c, p, rk, 1, 0), &graph_entry(c, p, rk, 1, 1)};
+    if (!Gs[1]->scratch) Gs[1]->scratch = (uint64_t*)c->dalloc(ntt_scratch_words(P.log_n) * 8);
+    cudaStream_t user = c->stream;
+    uint64_t* base_scratch = c->scratch;
+    cudaStream_t ss[2] = {user, c->s_mac};
+    uint64_t* scr[2] = {base_scratch, Gs[1]->scratch};
     // double-buffered device staging: H[s] inputs (coefficient form), D[s] outputs
     DBuf H0(c, C * 2 * nqN), H1(c, C * 2 * nqN), D0(c, O * oN), D1(c, O * oN);
     uint64_t* H[2] = {H0.p, H1.p};
@@ -2331,13 +2343,26 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
     cudaEvent_t* used = c->hev + 2;
     cudaEvent_t* exp_ = c->hev + 4;
     cudaEvent_t* d2h = c->hev + 6;
-    c->join(c->s_h2d, c->stream);   // staging buffers allocated on the context stream
+    c->join(c->s_h2d, user);   // staging buffers allocated on the context stream
+    c->join(c->s_mac, user);
+    struct Restore {
+      helrm_ctx* c;
+      cudaStream_t st;
+      uint64_t* sc;
+      ~Restore() {
+        c->stream = st;
+        c->scratch = sc;
+      }
+    } restore{c, user, base_scratch};
     for (size_t q = 0; q < batch; q++) {
       const int b = (int)(q & 1);
+      helrm_ctx::LookupGraph& G = *Gs[b];
       if (q >= 2) HCUDA(cudaStreamWaitEvent(c->s_h2d, used[b], 0));
       for (size_t ci = 0; ci < C; ci++)
         HCUDA(cudaMemcpyAsync(H[b] + ci * 2 * nqN, in[q * C + ci], 2 * nqN * 8, cudaMemcpyHostToDevice, c->s_h2d));
       HCUDA(cudaEventRecord(h2d[b], c->s_h2d));
+      c->stream = ss[b];
+      c->scratch = scr[b];
       HCUDA(cudaStreamWaitEvent(c->stream, h2d[b], 0));
       ntt_fwd(c, H[b], G.X, 2 * C * (l + 1), P.map_q(l));   // coefficient -> NTT form, into the graph's inputs
       HCUDA(cudaEventRecord(used[b], c->stream));
@@ -2349,7 +2374,10 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
       for (size_t o = 0; o < O; o++)
         HCUDA(cudaMemcpyAsync(out[q * O + o], D[b] + o * oN, oN * 8, cudaMemcpyDeviceToHost, c->s_d2h));
       HCUDA(cudaEventRecord(d2h[b], c->s_d2h));
+      c->stream = user;
+      c->scratch = base_scratch;
     }
+    c->join(user, c->s_mac);
     c->join(c->stream, c->s_d2h);
     c->join(c->stream, c->s_h2d);
     HCUDA(cudaStreamSynchronize(c->stream));
