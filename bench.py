@@ -360,7 +360,7 @@ def run_gpu(args, world, rank, local):
     ins = [pin_in[i % len(pin_in)].numpy() for i in range(args.steps)]
     outs = [o.numpy() for o in pin_out]
     for i in range(max(2, args.warmup // 2)):   # each serving slot: eager run, then graph capture
-        helrm.lookup_host(ctx, plan, rk, ins[:2], 2.0 ** cfg.log_scale, 2, outs[:2])
+        helrm.lookup_host(ctx, plan, rk, ins[:3], 2.0 ** cfg.log_scale, 3, outs[:3])
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -137,7 +137,7 @@ struct helrm_ctx {
   cudaStream_t s_ntt = nullptr, s_kip = nullptr, s_mac = nullptr;
   cudaStream_t s_cap = nullptr;   // private stream the lookup graphs are captured on
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;   // copy streams of helrm_lookup_host
-  cudaEvent_t hev[8] = {};                          // its events (outside the pool the lookup recycles)
+  cudaEvent_t hev[12] = {};                         // its events (outside the pool the lookup recycles)
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
   cudaEvent_t ev() {
@@ -2327,24 +2327,34 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
     // Two serving slots: query q runs on slot q & 1 (its own graph, buffers, NTT scratch and
     // stream), so one query's latency-bound tail (final ModDown, rescale, RotSum chain) overlaps
     // the next query's HBM-bound baby steps and inner sums.
-    helrm_ctx::LookupGraph* Gs[2] = {&graph_entry(c, p, rk, 1, 0), &graph_entry(c, p, rk, 1, 1)};
-    if (!Gs[1]->scratch) Gs[1]->scratch = (uint64_t*)c->dalloc(ntt_scratch_words(P.log_n) * 8);
+    static const int nslot = std::max(1, std::min(3, getenv("HELRM_SLOTS") ? atoi(getenv("HELRM_SLOTS")) : 2));
+    helrm_ctx::LookupGraph* Gs[3] = {};
+    for (int k = 0; k < nslot; k++) {
+      Gs[k] = &graph_entry(c, p, rk, 1, k);
+      if (k > 0 && !Gs[k]->scratch) Gs[k]->scratch = (uint64_t*)c->dalloc(ntt_scratch_words(P.log_n) * 8);
+    }
     cudaStream_t user = c->stream;
     uint64_t* base_scratch = c->scratch;
-    cudaStream_t ss[2] = {user, c->s_mac};
-    uint64_t* scr[2] = {base_scratch, Gs[1]->scratch};
-    // double-buffered device staging: H[s] inputs (coefficient form), D[s] outputs
-    DBuf H0(c, C * 2 * nqN), H1(c, C * 2 * nqN), D0(c, O * oN), D1(c, O * oN);
-    uint64_t* H[2] = {H0.p, H1.p};
-    uint64_t* D[2] = {D0.p, D1.p};
+    cudaStream_t ss[3] = {user, c->s_mac, c->s_kip};
+    uint64_t* scr[3] = {base_scratch, Gs[1] ? Gs[1]->scratch : nullptr, Gs[2] ? Gs[2]->scratch : nullptr};
+    // per-slot device staging: H[s] inputs (coefficient form), D[s] outputs
+    std::vector<std::unique_ptr<DBuf>> HB, DB;
+    uint64_t* H[3] = {};
+    uint64_t* D[3] = {};
+    for (int k = 0; k < nslot; k++) {
+      HB.emplace_back(new DBuf(c, C * 2 * nqN));
+      DB.emplace_back(new DBuf(c, O * oN));
+      H[k] = HB.back()->p;
+      D[k] = DB.back()->p;
+    }
     if (!c->hev[0])
       for (auto& e : c->hev) HCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    cudaEvent_t* h2d = c->hev;
-    cudaEvent_t* used = c->hev + 2;
-    cudaEvent_t* exp_ = c->hev + 4;
-    cudaEvent_t* d2h = c->hev + 6;
+    cudaEvent_t* h2d = c->hev;       // 3 each
+    cudaEvent_t* used = c->hev + 3;
+    cudaEvent_t* exp_ = c->hev + 6;
+    cudaEvent_t* d2h = c->hev + 9;
     c->join(c->s_h2d, user);   // staging buffers allocated on the context stream
-    c->join(c->s_mac, user);
+    for (int k = 1; k < nslot; k++) c->join(ss[k], user);
     struct Restore {
       helrm_ctx* c;
       cudaStream_t st;
@@ -2355,9 +2365,9 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
       }
     } restore{c, user, base_scratch};
     for (size_t q = 0; q < batch; q++) {
-      const int b = (int)(q & 1);
+      const int b = (int)(q % nslot);
       helrm_ctx::LookupGraph& G = *Gs[b];
-      if (q >= 2) HCUDA(cudaStreamWaitEvent(c->s_h2d, used[b], 0));
+      if (q >= (size_t)nslot) HCUDA(cudaStreamWaitEvent(c->s_h2d, used[b], 0));
       for (size_t ci = 0; ci < C; ci++)
         HCUDA(cudaMemcpyAsync(H[b] + ci * 2 * nqN, in[q * C + ci], 2 * nqN * 8, cudaMemcpyHostToDevice, c->s_h2d));
       HCUDA(cudaEventRecord(h2d[b], c->s_h2d));
@@ -2367,7 +2377,7 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
       ntt_fwd(c, H[b], G.X, 2 * C * (l + 1), P.map_q(l));   // coefficient -> NTT form, into the graph's inputs
       HCUDA(cudaEventRecord(used[b], c->stream));
       run_graph_chunk(c, p, rk, G, 1);
-      if (q >= 2) HCUDA(cudaStreamWaitEvent(c->stream, d2h[b], 0));
+      if (q >= (size_t)nslot) HCUDA(cudaStreamWaitEvent(c->stream, d2h[b], 0));
       ntt_inv(c, G.S, D[b], 2 * O * l, P.map_q(l - 1));    // outputs back to coefficient form
       HCUDA(cudaEventRecord(exp_[b], c->stream));
       HCUDA(cudaStreamWaitEvent(c->s_d2h, exp_[b], 0));
@@ -2377,7 +2387,7 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
       c->stream = user;
       c->scratch = base_scratch;
     }
-    c->join(user, c->s_mac);
+    for (int k = 1; k < nslot; k++) c->join(user, ss[k]);
     c->join(c->stream, c->s_d2h);
     c->join(c->stream, c->s_h2d);
     HCUDA(cudaStreamSynchronize(c->stream));
