@@ -1643,22 +1643,27 @@ extern "C" {
 // caller, at least mac_list_bytes() -- a copy from pinned memory can be
 // captured into a CUDA graph)
 struct MacDev {
-  DBuf terms, groups;
-  MacDev(helrm_ctx* c, const MacList& ml, void** pinned = nullptr)
-      : terms(c, (ml.terms.size() + 7) / 8 + 1), groups(c, 2 * ml.groups.size() + 1) {
-    const size_t tb = ml.terms.size(), gb = ml.groups.size() * sizeof(int4);
+  DBuf terms, groups, extra;
+  MacDev(helrm_ctx* c, const MacList& ml, void** pinned = nullptr, const std::vector<char>& xtra = {})
+      : terms(c, (ml.terms.size() + 7) / 8 + 1), groups(c, 2 * ml.groups.size() + 1),
+        extra(c, (xtra.size() + 7) / 8 + 1) {
+    const size_t tb = ml.terms.size(), gb = ml.groups.size() * sizeof(int4), xb = xtra.size();
     const void* ht = ml.terms.data();
     const void* hg = ml.groups.data();
+    const void* hx = xtra.data();
     if (pinned) {   // allocated by the caller before the capture (mac_list_bytes)
       need(*pinned != nullptr, HELRM_ERR_ARG, "pinned MAC staging buffer missing");
       std::memcpy(*pinned, ht, tb);
       std::memcpy((char*)*pinned + tb, hg, gb);
+      if (xb) std::memcpy((char*)*pinned + tb + gb, hx, xb);
       ht = *pinned;
       hg = (const char*)*pinned + tb;
+      hx = (const char*)*pinned + tb + gb;
     }
     HostTimer ht_("MacDev upload");
     HCUDA(cudaMemcpyAsync(terms.p, ht, tb, cudaMemcpyHostToDevice, c->stream));
     HCUDA(cudaMemcpyAsync(groups.p, hg, gb, cudaMemcpyHostToDevice, c->stream));
+    if (xb) HCUDA(cudaMemcpyAsync(extra.p, hx, xb, cudaMemcpyHostToDevice, c->stream));
   }
 };
 
@@ -1868,8 +1873,33 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     macs_done = launch_baby_mac(c->dc(), kmf, bm, mqp);
     need(macs_done, HELRM_ERR_CONFIG, "fused baby/MAC kernel does not apply");   // guarded by `fused`
   }
+  // output blocks sharing every plaintext (LLM layout L2): dense (giant, baby slot) table of
+  // block 0's plaintexts for k_block_mac
+  std::vector<char> utab;
+  int blk_zb = 0;
+  if (same_babies && pl->O == (int64_t)C && pl->O == 4 && ml.groups.size() % pl->O == 0) {
+    const size_t gb0 = ml.groups.size() / pl->O, nbb = pl->babies[0].size();
+    blk_zb = ml.groups[gb0].z;
+    std::vector<const uint64_t*> U((size_t)blk_zb * nbb, nullptr);
+    bool ok = blk_zb > 0;
+    for (size_t g = 0; ok && g < gb0; g++) {
+      const int4 gr = ml.groups[g];
+      for (int t = 0; ok && t < gr.y; t++) {
+        const MacTerm* mt = reinterpret_cast<const MacTerm*>(&ml.terms[(size_t)(gr.x + t) * ml.term_size]);
+        const size_t off = (size_t)(mt->x0 - babies.p);
+        ok = off % (2 * nlN) == 0 && off / (2 * nlN) < nbb;
+        for (int gi = 0; ok && gi < gr.w; gi++) U[(size_t)(gr.z + gi) * nbb + off / (2 * nlN)] = mt->u[gi];
+      }
+    }
+    if (ok) {
+      const char* b = reinterpret_cast<const char*>(U.data());
+      utab.assign(b, b + U.size() * sizeof(const uint64_t*));
+    } else {
+      blk_zb = 0;
+    }
+  }
   std::unique_ptr<MacDev> mdu;
-  if (!fused) mdu.reset(new MacDev(c, ml, pinned));
+  if (!fused) mdu.reset(new MacDev(c, ml, pinned, utab));
   const MacDev& md = fused ? *mdp : *mdu;
   // (serialised while the per-kernel profiler is on, so each kernel's events time it alone)
   // default: on for batched chunks (measured 158 vs 148 lookups/s at batch 64), off for batch 1
@@ -1916,8 +1946,26 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     for (int z = 0; periodic && z < zb; z++)
       for (int64_t o = 1; periodic && o < pl->O; o++)
         periodic = pl->giants[o][ml.oi[z + o * zb].second] == pl->giants[0][ml.oi[z].second];
-    if (periodic) run_macs(c, ml, md, 0, g_blk, AB.p, zq * 2 * nlN, mqp, true, (int)pl->O, nbb * 2 * nlN,
-                           (size_t)zb * 2 * nlN, sm, pers);
+    static const bool blk_env = getenv("HELRM_BLOCK_MAC") ? atoi(getenv("HELRM_BLOCK_MAC")) != 0 : false;
+    bool done = false;
+    if (periodic && blk_env && blk_zb == zb && !utab.empty()) {
+      BlockMacArgs ba{};
+      ba.U = reinterpret_cast<const uint64_t* const*>(md.extra.p);
+      ba.X = babies.p;
+      ba.xq = nbb * 2 * nlN;
+      ba.out = AB.p;
+      ba.zb = zb;
+      ba.nb = (int)nbb;
+      ba.nblk = (int)pl->O;
+      ba.nlN = nlN;
+      double nu = 0;
+      for (size_t g = 0; g < g_blk; g++) nu += ml.gu[g];
+      ba.bytes = 8.0 * N * nl * (nu + pl->O * (2.0 * nbb + 2.0 * zb));
+      done = launch_block_mac(c->dc(sm), ba, mqp);
+    }
+    if (periodic && !done)
+      run_macs(c, ml, md, 0, g_blk, AB.p, zq * 2 * nlN, mqp, true, (int)pl->O, nbb * 2 * nlN, (size_t)zb * 2 * nlN,
+               sm, pers);
   }
   if (periodic) {
     // giant steps of every block, then one key switch per giant with the blocks as queries
@@ -2169,7 +2217,10 @@ static helrm_ctx::LookupGraph& graph_entry(helrm_ctx* c, const helrm_plan* pl, c
     G.X = (uint64_t*)c->dalloc((size_t)Qc * pl->C * 2 * nqN * 8);
     G.S = (uint64_t*)c->dalloc((size_t)pl->O * Qc * oN * 8);
     // MAC work list bound: every term carries >= 1 plaintext, every group >= 1 pair
-    HCUDA(cudaMallocHost(&G.pinned, (size_t)pl->n_diag * sizeof(MacTermW) + count_pairs(pl) * sizeof(int4) + 64));
+    size_t nbb = 0;
+    for (auto& b : pl->babies) nbb = std::max(nbb, b.size());
+    HCUDA(cudaMallocHost(&G.pinned, (size_t)pl->n_diag * sizeof(MacTermW) + count_pairs(pl) * sizeof(int4) +
+                                        (size_t)count_pairs(pl) * nbb * 8 + 64));
   }
   return G;
 }

@@ -336,6 +336,22 @@ struct BabyMacArgs {
   double bytes;                          // algorithmic HBM bytes of the launch (profiler)
 };
 constexpr int kBabyMacTile = 128;
+
+// D20 L3 for output blocks that share every plaintext (LLM layout L2): a CTA
+// stages the baby pairs of all blocks for 16 positions of one limb in shared
+// memory; 8 workers per position each own up to 3 giants and run their exact
+// FP64 MACs for all blocks, so every plaintext value is loaded from HBM once
+// and every baby value once.
+struct BlockMacArgs {
+  const uint64_t* const* U;              // [zb][nb] plaintext per (giant, baby slot) or null (device table)
+  const uint64_t* X;                     // baby slot jj of block o at X + o xq + jj 2 nlN (A), + nlN (B)
+  size_t xq;
+  uint64_t* out;                         // pair (o, z) at out + (o zb + z) 2 nlN (A), + nlN (B)
+  int zb, nb, nblk;
+  size_t nlN;
+  double bytes;
+};
+bool launch_block_mac(const DevCtx& c, const BlockMacArgs& a, const LimbMap& map);
 bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map);
 
 // D20 L3 work list.  Giants are packed kGiantPack at a time: a term is one

@@ -6,6 +6,8 @@
 //
 // Layout: polynomials are [limb][N] uint64, NTT form in slot order; one
 // thread per coefficient, blockIdx.y = limb, coalesced 8-byte accesses.
+#include <cuda_pipeline.h>
+
 #include "internal.h"
 #include "fmath.cuh"
 
@@ -736,6 +738,107 @@ bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, c
   ProfScope ps_(c, "baby_mac", m.bytes);
   HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<dim3(c.N / kBabyMacTile, map.n), kBabyMacTile, smem, c.stream>>>(a, m, c.primes, map, c.N);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+  return true;
+}
+
+// The plaintext values stream through a cp.async ring of kBmStages terms in
+// shared memory (no registers held by loads in flight: ~40 KB in flight per
+// SM at 2 CTAs/SM, what the HBM latency needs).
+constexpr int kBmStages = 8;
+template <int NBLK, int GT>
+__global__ void __launch_bounds__(128) k_block_mac(const __grid_constant__ BlockMacArgs a,
+                                                  const PrimeDev* __restrict__ primes,
+                                                  const __grid_constant__ LimbMap map, uint32_t N) {
+  constexpr int T = 16, W = 8;
+  extern __shared__ double sx[];                 // [nb][NBLK][2][T] babies, then the ring [S][zb][T]
+  double* ring = sx + (size_t)a.nb * NBLK * 2 * T;
+  const int tid = threadIdx.x, pl = tid % T, w = tid / T;
+  const int l = blockIdx.y;
+  const uint32_t p0 = blockIdx.x * T, p = p0 + pl;
+  const PrimeDev& P = primes[map.pr[l]];
+  const double q = P.qd, qi = P.qinv;
+  const size_t lo = (size_t)l * N;
+  const int zb = a.zb, nb = a.nb;
+  // ring fill for term jj into stage jj % S: value (z, pl') copied by thread (z * T + pl') % 128
+  auto issue = [&](int jj) {
+    double* st = ring + (size_t)(jj % kBmStages) * zb * T;
+    for (int e = tid; e < zb * T; e += 128) {
+      const int z = e / T, pp = e % T;
+      const uint64_t* u = a.U[(size_t)z * nb + jj];
+      if (u) __pipeline_memcpy_async(st + e, u + lo + p0 + pp, 8);
+      else st[e] = 0.0;
+    }
+  };
+  for (int jj = 0; jj < kBmStages - 1; jj++) {
+    if (jj < nb) issue(jj);
+    __pipeline_commit();
+  }
+  // stage the baby pairs (coalesced rows of T positions)
+  for (int row = w; row < nb * NBLK * 2; row += W) {
+    const int jj = row / (NBLK * 2), o = (row / 2) % NBLK, cp = row % 2;
+    const uint64_t* x = a.X + (size_t)o * a.xq + (size_t)jj * 2 * a.nlN + (size_t)cp * a.nlN;
+    sx[row * T + pl] = fm::bits2d(x[lo + p]);
+  }
+  fm::FAcc acc[GT][NBLK][2];
+  int cnt = 0;
+  for (int jj = 0; jj < nb; jj++) {
+    if (jj + kBmStages - 1 < nb) issue(jj + kBmStages - 1);
+    __pipeline_commit();
+    __pipeline_wait_prior(kBmStages - 1);   // term jj landed
+    __syncthreads();
+    const double* st = ring + (size_t)(jj % kBmStages) * zb * T;
+    double uv[GT];
+#pragma unroll
+    for (int g = 0; g < GT; g++) {
+      const int z = w + W * g;
+      uv[g] = z < zb ? st[z * T + pl] : 0.0;
+    }
+    if (cnt + 1 > fm::kFAccTerms) {
+#pragma unroll
+      for (int g = 0; g < GT; g++)
+#pragma unroll
+        for (int o = 0; o < NBLK; o++) {
+          fm::fold(acc[g][o][0], q, qi);
+          fm::fold(acc[g][o][1], q, qi);
+        }
+      cnt = 0;
+    }
+    cnt++;
+    const double* xr = sx + (size_t)jj * NBLK * 2 * T + pl;
+#pragma unroll
+    for (int o = 0; o < NBLK; o++) {
+      const double xa = xr[(o * 2) * T], xb = xr[(o * 2 + 1) * T];
+#pragma unroll
+      for (int g = 0; g < GT; g++) {
+        fm::fmac(acc[g][o][0], uv[g], xa);
+        fm::fmac(acc[g][o][1], uv[g], xb);
+      }
+    }
+    __syncthreads();   // stage jj % S is refilled by the next iteration's issue
+  }
+#pragma unroll
+  for (int g = 0; g < GT; g++) {
+    const int z = w + W * g;
+    if (z >= zb) continue;
+#pragma unroll
+    for (int o = 0; o < NBLK; o++) {
+      uint64_t* dst = a.out + (size_t)(o * zb + z) * 2 * a.nlN + lo + p;
+      dst[0] = fm::c2u(fm::fred(acc[g][o][0], q, qi), P.rc.q);
+      dst[a.nlN] = fm::c2u(fm::fred(acc[g][o][1], q, qi), P.rc.q);
+    }
+  }
+}
+
+bool launch_block_mac(const DevCtx& c, const BlockMacArgs& a, const LimbMap& map) {
+  if (a.nblk != 4 || a.zb > 24 || c.N % 16) return false;
+  const size_t smem = ((size_t)a.nb * a.nblk * 2 * 16 + (size_t)kBmStages * a.zb * 16) * 8;
+  if (smem > 200 * 1024) return false;
+  auto kern = a.zb <= 8 ? k_block_mac<4, 1> : a.zb <= 16 ? k_block_mac<4, 2> : k_block_mac<4, 3>;
+  HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfScope ps_(c, "diag_mac", a.bytes);
+  kern<<<dim3(c.N / 16, map.n), 128, smem, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
   return true;
