@@ -508,8 +508,10 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   __shared__ MacTerm tm[kChunk];
   const uint32_t tiles = N / blockDim.x, total = tiles * (uint32_t)n_groups * (uint32_t)map.n;
   for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
-    const int4 gr = groups[(w / tiles) % n_groups];
-    const uint32_t p = (w % tiles) * blockDim.x + threadIdx.x;
+    // pack fastest: the packs of one (limb, tile) run back to back, so their shared baby
+    // pairs come from L2 after the first (per limb they can exceed L2: 256 MB for the LLM)
+    const int4 gr = groups[w % n_groups];
+    const uint32_t p = ((w / n_groups) % tiles) * blockDim.x + threadIdx.x;
     const int l = (int)(w / (tiles * n_groups));
     const PrimeDev& P = primes[map.pr[l]];
     const double q = P.qd, qi = P.qinv;
