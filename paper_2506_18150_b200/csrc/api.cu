@@ -93,6 +93,7 @@ struct helrm_ctx {
   uint64_t* scratch = nullptr;
   std::map<int, LevelConst> lconst;
   std::map<std::pair<int, int>, uint32_t*> modup_lidx;   // (level, G) -> NTT limb table of modup_batch
+  std::map<std::pair<int, int>, uint32_t*> pm_lidx;      // (G, n) -> prime-major limb table
   // CUDA-graph replay of the double-hoisted lookup (one graph per plan, key
   // set and query-chunk size): the ~400 launches, allocations and copies of a
   // lookup are enqueued once at capture; a replay costs one graph launch.
@@ -460,13 +461,17 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
 static const uint32_t* modup_lidx(helrm_ctx* c, uint32_t l, int G, size_t* count) {
   const Params& P = c->P;
   const uint32_t nl = l + 1 + P.K, dn = P.dnum(l);
+  // prime-major: a launch's CTAs run in table order, so the limbs of one prime
+  // follow each other and its 1 MiB pass-2 twiddle table stays in L2
+  static const bool pm = getenv("HELRM_NTT_PM") ? atoi(getenv("HELRM_NTT_PM")) != 0 : true;
   std::vector<uint32_t> v;
-  for (int g = 0; g < G; g++)
-    for (uint32_t k = 0; k < dn; k++) {
-      const uint32_t lo = k * P.alpha, hi = std::min((k + 1) * P.alpha, l + 1);
-      for (uint32_t r = 0; r < nl; r++)
+  for (uint32_t r = 0; r < nl; r++)
+    for (int g = 0; g < G; g++)
+      for (uint32_t k = 0; k < dn; k++) {
+        const uint32_t lo = k * P.alpha, hi = std::min((k + 1) * P.alpha, l + 1);
         if (r < lo || r >= hi) v.push_back(((uint32_t)g * dn + k) * nl + r);
-    }
+      }
+  if (!pm) std::sort(v.begin(), v.end());
   *count = v.size();
   auto key = std::make_pair((int)l, G);
   auto it = c->modup_lidx.find(key);
@@ -476,6 +481,26 @@ static const uint32_t* modup_lidx(helrm_ctx* c, uint32_t l, int G, size_t* count
   HCUDA(cudaStreamSynchronize(c->stream));
   c->owned.push_back(d);
   c->modup_lidx.emplace(key, d);
+  return d;
+}
+
+// Prime-major limb table for a launch over G polynomials of n limbs each
+// (launch limb -> layout limb g n + r, r outer): consecutive CTAs share a
+// prime and its pass-2 twiddles.  nullptr (identity) when G == 1.
+static const uint32_t* pm_lidx(helrm_ctx* c, int G, uint32_t n) {
+  static const bool pm = getenv("HELRM_NTT_PM") ? atoi(getenv("HELRM_NTT_PM")) != 0 : true;
+  if (!pm || G <= 1) return nullptr;
+  auto key = std::make_pair(G, (int)n);
+  auto it = c->pm_lidx.find(key);
+  if (it != c->pm_lidx.end()) return it->second;
+  std::vector<uint32_t> v;
+  for (uint32_t r = 0; r < n; r++)
+    for (int g = 0; g < G; g++) v.push_back((uint32_t)g * n + r);
+  uint32_t* d = (uint32_t*)c->dalloc(v.size() * 4);
+  HCUDA(cudaMemcpyAsync(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  HCUDA(cudaStreamSynchronize(c->stream));
+  c->owned.push_back(d);
+  c->pm_lidx.emplace(key, d);
   return d;
 }
 
@@ -495,7 +520,8 @@ static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int 
   // step 2: one conversion launch over (g, digit) writing the rows outside
   // the digit; step 3: one NTT over exactly those limbs.  The digit's own
   // limbs are copied unchanged (NTT form).
-  launch_ntt_inv(c->dc(st), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post);
+  launch_ntt_inv(c->dc(st), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post,
+                 pm_lidx(c, G, (uint32_t)nq));
   static const bool fuse = getenv("HELRM_FUSECONV") ? atoi(getenv("HELRM_FUSECONV")) != 0 : false;
   if (fuse) {   // conversion computed inside the NTT's pass 1 (no conversion kernel, no round trip)
     NttConvIn cv;
@@ -529,7 +555,7 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   if (!st) st = c->stream;
   DBuf yp(c, G * P.K * N, st), t(c, G * nq * N, st);
   launch_ntt_inv(c->dc(st), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
-                 lc.moddown_post);
+                 lc.moddown_post, pm_lidx(c, G, P.K));
   static const bool fuse = getenv("HELRM_FUSECONV") ? atoi(getenv("HELRM_FUSECONV")) != 0 : false;
   NttConvIn cv;
   if (fuse) {
@@ -550,7 +576,7 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   epi.s = lc.pinv;
   epi.sp = lc.pinvs;
   epi.accumulate = accumulate ? 1 : 0;
-  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, !fuse, nullptr, &epi,
+  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, !fuse, pm_lidx(c, G, (uint32_t)nq), &epi,
                  fuse ? &cv : nullptr);
 }
 
@@ -583,7 +609,7 @@ static void rescale_ct(helrm_ctx* c, const uint64_t* x, uint32_t l, uint64_t* ou
   epi.os = l * N;
   epi.s = lc.qlinv;
   epi.sp = lc.qlinvs;
-  launch_ntt_fwd(c->dc(), r.p, r.p, c->scratch, 2 * G * l, P.map_q(l - 1), 0, 0, false, nullptr, &epi);
+  launch_ntt_fwd(c->dc(), r.p, r.p, c->scratch, 2 * G * l, P.map_q(l - 1), 0, 0, false, pm_lidx(c, 2 * G, l), &epi);
 }
 
 static uint32_t rot_of_galois(helrm_ctx* c, uint64_t g) {
