@@ -87,7 +87,7 @@ struct helrm_ctx {
   uint64_t* dtw = nullptr;
   uint32_t* dslotpos = nullptr;
   uint32_t* dgrp = nullptr;
-  uint8_t* deinv = nullptr;
+  const double* dtwb = nullptr;
   uint8_t* dtpos = nullptr;
   uint64_t* dcdt = nullptr;
   uint64_t* scratch = nullptr;
@@ -159,7 +159,7 @@ struct helrm_ctx {
 
   int persist = 0;                // persistent CTAs per SM for the HBM-bound kernels (0 = full grids)
   DevCtx dc(cudaStream_t s = nullptr, int pers = 0) {
-    return DevCtx{dprimes, dslotpos, dgrp, deinv, dtpos, P.log_n, P.N, s ? s : stream, pers, &launches, &prof};
+    return DevCtx{dprimes, dslotpos, dgrp, dtwb, dtpos, P.log_n, P.N, s ? s : stream, pers, &launches, &prof};
   }
 
   void* dalloc(size_t bytes, cudaStream_t s = nullptr) {
@@ -837,6 +837,7 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       std::vector<uint64_t> bits(tw.size());
       std::memcpy(bits.data(), tw.data(), tw.size() * 8);
       c->dtw = c->upload_u64(bits);
+      c->dtwb = reinterpret_cast<const double*>(c->dtw);
     }
     c->hprimes.resize(np);
     for (size_t i = 0; i < np; i++) {
@@ -889,9 +890,7 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       c->dgrp = (uint32_t*)c->dalloc(nb * 4);
       c->owned.push_back(c->dgrp);
       HCUDA(cudaMemcpyAsync(c->dgrp, grp.data(), nb * 4, cudaMemcpyHostToDevice, c->stream));
-      c->deinv = (uint8_t*)c->dalloc(N);
-      c->owned.push_back(c->deinv);
-      HCUDA(cudaMemcpyAsync(c->deinv, einv.data(), N, cudaMemcpyHostToDevice, c->stream));
+      ntt_set_grp(P.log_n, grp.data(), nb);
       // rank of each element's slot position within its block (inverse of einv); the
       // pass-2 / pass-A swizzle needs tp(16 t + k) mod 16 distinct over t for every k
       std::vector<uint8_t> tpos(N);

@@ -143,7 +143,7 @@ struct DevCtx {
   const PrimeDev* primes;     // device array, chain-indexed
   const uint32_t* slotpos;    // [N] slot position of bitrev index r
   const uint32_t* ntt_grp;    // [N/256] 256-blocks ordered by (half, slot residue): 16 per pass-2 CTA
-  const uint8_t* ntt_einv;    // [N] per block: element index of its tp-th smallest slot position
+  const double* ntt_twb;      // NTT twiddle tables of every prime, 4 N + 1024 doubles per prime
   const uint8_t* ntt_tpos;    // [N] per block: rank of element e's slot position within the block
   uint32_t log_n, N;
   cudaStream_t stream;
@@ -207,6 +207,8 @@ void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
                     const NttConvIn* conv = nullptr);
 // single-kernel forward NTT on 4-CTA clusters (kernels_ntt_cl.cu), N = 2^16;
 // false if it does not apply (the caller then runs the two-pass kernels)
+// pass-2 / pass-A block grouping into constant memory (a function of log N only)
+void ntt_set_grp(uint32_t log_n, const uint32_t* grp, size_t n);
 bool ntt_fwd_cluster(const DevCtx& c, const uint64_t* src, uint64_t* dst, size_t n_total, const LimbMap& map,
                      size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi& epi);
 // post (optional, per limb of map): final factor (w, w/q) replacing N^-1

@@ -42,6 +42,15 @@
 
 namespace helrm {
 
+// pass-2 / pass-A block grouping per log N (12..16): read through the constant
+// cache at CTA start instead of a dependent global load
+__constant__ uint32_t c_ntt_grp[5][256];
+
+void ntt_set_grp(uint32_t log_n, const uint32_t* grp, size_t n) {
+  if (log_n < 12 || log_n > 16 || n > 256) throw Error(HELRM_ERR_CONFIG, "NTT supports 12 <= log N <= 16");
+  HCUDA(cudaMemcpyToSymbol(c_ntt_grp, grp, n * 4, (size_t)(log_n - 12) * 256 * 4));
+}
+
 namespace {
 constexpr int kEPT = 16;                     // elements per thread
 constexpr int kTileElems = 4096;             // elements per CTA
@@ -78,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
-                                                      const uint8_t* __restrict__ einv,
+                                                      const double* __restrict__ twb,
                                                       const uint8_t* __restrict__ tpos,
                                                       const uint32_t* __restrict__ lidx,
                                                       const __grid_constant__ NttEpi epi,
@@ -89,16 +98,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
   const size_t gl = lidx ? lidx[limb0 + limb] : limb0 + limb;
-  const PrimeDev& P = primes[map.pr[gl % map.n]];
+  const int pr = map.pr[gl % map.n];
+  const PrimeDev& P = primes[pr];
   const double q = P.qd, qi = P.qinv;
+  const double* tb = twb + (size_t)pr * (4 * (size_t)N + 1024);   // [tw1 256][tw2 N][itw1 256][itw2 N] (w, w/q)
   const size_t goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
   const uint64_t* s = src + (P1 ? goff : limb * N);  // pass 1 reads the caller's limb
   uint64_t* d = dst + (P1 ? limb * N : goff);        // pass 2 writes the caller's limb
   const int tid = threadIdx.x;
   const int sub = P1 ? tid % SUBS : tid / TS;
   const int t = P1 ? tid / SUBS : tid % TS;
-  const int gsub = P1 ? blockIdx.x * SUBS + sub : (int)grp[blockIdx.x * SUBS + sub];
-  const double2* __restrict__ twA = P1 ? P.tw1 : P.tw2 + (size_t)gsub * 256;
+  const int gsub = P1 ? blockIdx.x * SUBS + sub : (int)c_ntt_grp[log_n - 12][blockIdx.x * SUBS + sub];
+  const double2* __restrict__ tw1 = reinterpret_cast<const double2*>(tb);
+  const double2* __restrict__ twA = P1 ? tw1 : reinterpret_cast<const double2*>(tb + 512) + (size_t)gsub * 256;
   double r[kEPT];
   if (MODE == 3) {
     // D14 on the fly: out_r = sum_b y[row0 + b] cf[b] mod q_r (centred), the y-form sources
@@ -167,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
       const int e = kEPT * t + k;
       r[k] = P1 ? sm[e * SUBS + sub] : sm[sub * kBlkPad + pidx(e)];
     }
-    const double2* __restrict__ twB = P1 ? P.tw1 : twA + 15 + t;  // phase-B twiddle j of thread t at 15 + 16 j + t
+    const double2* __restrict__ twB = P1 ? tw1 : twA + 15 + t;  // phase-B twiddle j of thread t at 15 + 16 j + t
 #pragma unroll
     for (int st = 4; st < SLOG; st++) {
       const int half = S >> (st + 1);
@@ -255,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
                                                       const uint32_t* __restrict__ grp,
-                                                      const uint8_t* __restrict__ einv,
+                                                      const double* __restrict__ twb,
                                                       const uint8_t* __restrict__ tpos,
                                                       const double2* __restrict__ post,
                                                       const uint32_t* __restrict__ lidx) {
@@ -264,16 +276,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
   const int N = 1 << log_n;
   const size_t limb = blockIdx.y;
   const size_t gl = lidx ? lidx[limb0 + limb] : limb0 + limb;
-  const PrimeDev& P = primes[map.pr[gl % map.n]];
+  const int pr = map.pr[gl % map.n];
+  const PrimeDev& P = primes[pr];
   const double q = P.qd, qi = P.qinv;
+  const double* tb = twb + (size_t)pr * (4 * (size_t)N + 1024) + 2 * (size_t)N + 512;   // itw1, itw2
   const size_t goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
   const uint64_t* s = src + (MODE == 1 ? goff : limb * N);  // pass A gathers the caller's limb
   uint64_t* d = dst + (MODE == 1 ? limb * N : goff);        // pass B writes the caller's limb
   const int tid = threadIdx.x;
   const int sub = MODE == 0 ? tid % SUBS : tid / TS;
   const int t = MODE == 0 ? tid / SUBS : tid % TS;
-  const int gsub = MODE == 0 ? blockIdx.x * SUBS + sub : (int)grp[blockIdx.x * SUBS + sub];
-  const double2* __restrict__ twA = MODE == 0 ? P.itw1 : P.itw2 + (size_t)gsub * 256;
+  const int gsub = MODE == 0 ? blockIdx.x * SUBS + sub : (int)c_ntt_grp[log_n - 12][blockIdx.x * SUBS + sub];
+  const double2* __restrict__ itw1 = reinterpret_cast<const double2*>(tb);
+  const double2* __restrict__ twA = MODE == 0 ? itw1 : reinterpret_cast<const double2*>(tb + 512) + (size_t)gsub * 256;
   double r[kEPT];
   if (MODE == 1) {
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
@@ -300,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
     }
   }
   if (SLOG > 4) {
-    const double2* __restrict__ twB = MODE == 0 ? P.itw1 : twA + 15 + t;  // phase-B twiddle j of thread t at 15 + 16 j + t
+    const double2* __restrict__ twB = MODE == 0 ? itw1 : twA + 15 + t;  // phase-B twiddle j of thread t at 15 + 16 j + t
 #pragma unroll
     for (int st = SLOG - 1; st >= 4; st--) {
       const int half = S >> (st + 1);
@@ -390,13 +405,13 @@ static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
            : cv.nb_max <= 4 ? k_ntt_fwd<SLOG, 3, 4> : k_ntt_fwd<SLOG, 3, 8>;
     allow_xsmem(k1);
     k1<<<dim3(g1, cnt), kThreads, ntt_xsmem(), c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
-                                                 c.ntt_einv, c.ntt_tpos, lidx, epi, cv);
+                                                 c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
     allow_xsmem(k_ntt_fwd<8, 1>);
     k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, ntt_xsmem(), c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, lidx, epi, cv);
+                                                               c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
   }
   *c.launches += 2;
 }
@@ -411,13 +426,13 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
     allow_xsmem(k_ntt_inv<8, 1>);
     k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, ntt_xsmem(), c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
-                                                               c.ntt_grp, c.ntt_einv, c.ntt_tpos, nullptr, lidx);
+                                                               c.ntt_grp, c.ntt_twb, c.ntt_tpos, nullptr, lidx);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
     allow_xsmem(k_ntt_inv<SLOG, 0>);
     k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, ntt_xsmem(), c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                                  c.ntt_grp, c.ntt_einv, c.ntt_tpos, post, lidx);
+                                                                  c.ntt_grp, c.ntt_twb, c.ntt_tpos, post, lidx);
   }
   *c.launches += 2;
 }

@@ -136,7 +136,7 @@ __global__ void k_automorph(const uint64_t* __restrict__ a, uint64_t* __restrict
 // its conversion's table in shared memory, each thread loads its nb sources
 // once and produces all rows.  grid (N/256, G ncv).
 
-template <int NB>
+template <int NB, int PT = 1>
 __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict__ tab, int ncv, int rows,
                                                    const uint64_t* __restrict__ y, size_t y_stride,
                                                    uint64_t* __restrict__ out, size_t osg, size_t osk, uint32_t N) {
@@ -145,22 +145,32 @@ __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict_
   const ConvRowDev* tk = tab + (size_t)k * rows;
   for (int r = threadIdx.x; r < rows; r += blockDim.x) st[r] = tk[r];
   __syncthreads();
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  // PT positions per thread, 256 apart (each table row read from shared memory once per PT outputs)
+  const uint32_t i = blockIdx.x * blockDim.x * PT + threadIdx.x;
   if (i >= N) return;
   const int nb = st[0].nb;
   const uint64_t* src = y + (size_t)g * y_stride + (size_t)st[0].src_row0 * N + i;
-  double v[NB];
+  double v[PT][NB];
 #pragma unroll
-  for (int b = 0; b < NB; b++) v[b] = b < nb ? fm::u2d(src[(size_t)b * N]) : 0.0;  // missing sources = 0
+  for (int u = 0; u < PT; u++)
+#pragma unroll
+    for (int b = 0; b < NB; b++) v[u][b] = b < nb ? fm::u2d(src[(size_t)b * N + 256 * u]) : 0.0;  // missing sources = 0
   uint64_t* o = out + (size_t)g * osg + (size_t)k * osk + i;
 #pragma unroll 2
   for (int r = 0; r < rows; r++) {
-    if (st[r].out_row < 0) continue;
+    const int orow = st[r].out_row;
+    if (orow < 0) continue;
     const double q = st[r].q, qi = st[r].qinv;
-    double acc = 0.0;
+    double2 cf[NB];
 #pragma unroll
-    for (int b = 0; b < NB; b++) acc += fm::mmul(v[b], st[r].cf[b].x, st[r].cf[b].y, q);  // each in [-q/2, q/2]
-    o[(size_t)st[r].out_row * N] = (uint64_t)__double_as_longlong(fm::cred(acc, q, qi));
+    for (int b = 0; b < NB; b++) cf[b] = st[r].cf[b];
+#pragma unroll
+    for (int u = 0; u < PT; u++) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < NB; b++) acc += fm::mmul(v[u][b], cf[b].x, cf[b].y, q);  // each in [-q/2, q/2]
+      o[(size_t)orow * N + 256 * u] = (uint64_t)__double_as_longlong(fm::cred(acc, q, qi));
+    }
   }
 }
 
@@ -920,11 +930,15 @@ void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows,
                       size_t y_stride, uint64_t* out, size_t out_stride_g, size_t out_stride_k, int G,
                       const LimbMap& out_map) {
   ProfScope ps_(c, "conv", 8.0 * c.N * (double)G * ncv * (rows + 4));
+  static const int pt = getenv("HELRM_CONV_PT") ? atoi(getenv("HELRM_CONV_PT")) : 2;
   auto kern = nb_max <= 1 ? k_conv_rows<1> : nb_max <= 2 ? k_conv_rows<2> : nb_max <= 4 ? k_conv_rows<4>
                                                                                      : k_conv_rows<8>;
+  if (pt == 2)
+    kern = nb_max <= 1 ? k_conv_rows<1, 2> : nb_max <= 2 ? k_conv_rows<2, 2> : nb_max <= 4 ? k_conv_rows<4, 2>
+                                                                                         : k_conv_rows<8, 2>;
   (void)out_map;
-  kern<<<dim3(c.N / 256, G * ncv), 256, 0, c.stream>>>(tab, ncv, rows, y, y_stride, out, out_stride_g, out_stride_k,
-                                                       c.N);
+  kern<<<dim3(c.N / (256 * pt), G * ncv), 256, 0, c.stream>>>(tab, ncv, rows, y, y_stride, out, out_stride_g,
+                                                              out_stride_k, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
