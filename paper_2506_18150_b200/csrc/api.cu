@@ -1930,7 +1930,8 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   // default: on for batched chunks (measured 158 vs 148 lookups/s at batch 64), off for batch 1
   // (7.16 vs 7.22 ms); HELRM_PIPE overrides
   static const int pipe_env = getenv("HELRM_PIPE") ? atoi(getenv("HELRM_PIPE")) : -1;
-  const bool pipe = (pipe_env < 0 ? Qc > 1 : pipe_env != 0) && !c->prof.on;
+  static const bool trace_pipe = getenv("HELRM_TRACE_PIPE") && atoi(getenv("HELRM_TRACE_PIPE")) != 0;
+  const bool pipe = (pipe_env < 0 ? Qc > 1 : pipe_env != 0) && (!c->prof.on || trace_pipe);
   cudaStream_t sn = pipe ? c->s_ntt : c->stream, sk = pipe ? c->s_kip : c->stream, sm = pipe ? c->s_mac : c->stream;
   const int pers = pipe ? c->persist : 0;
   if (pipe) {

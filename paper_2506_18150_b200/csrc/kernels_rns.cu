@@ -1018,6 +1018,10 @@ void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int
   // algorithmic bytes: every plaintext once, every distinct baby pair and output once per query
   ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + nq * (2.0 * n_x_distinct + 2.0 * n_out)));
   (void)wide;
+  static const int bulk = getenv("HELRM_MAC_BULK") ? atoi(getenv("HELRM_MAC_BULK")) : 0;
+  if (bulk && nq == 1 && x_dform && !wide &&
+      launch_diag_mac_bulk(c, (const MacTerm*)terms, groups, n_groups, out, out_stride, (size_t)map.n * c.N, map))
+    return;
   if (nq == 1 && c.persist == 0) {
     auto k1 = x_dform ? k_diag_mac1<true> : k_diag_mac1<false>;
     k1<<<dim3(c.N / kT, n_groups, map.n), kT, 0, c.stream>>>((const MacTerm*)terms, groups, out, out_stride,
