@@ -378,7 +378,8 @@ using MacTermW = MacTermT<kWidePack>;
 // wide: terms are MacTermW (batched kernel, nq >= 1), else MacTerm.
 // batch-1 inner sums fed by bulk async copies (kernels_mac_bulk.cu); false if it does not apply
 bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
-                          size_t out_stride, size_t half, const LimbMap& map);
+                          size_t out_stride, size_t half, const LimbMap& map, int nq = 1, size_t xq = 0,
+                          size_t oq = 0);
 void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int n_groups, double n_u_total,
                      double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
                      bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0, bool wide = false);

@@ -26,11 +26,15 @@
 namespace helrm {
 
 namespace {
-constexpr int kBulkSlots = 2 + kGiantPack;             // x0, x1, u[0..3]
-constexpr int kTile = 256;                               // positions per work item (consumer threads)
-constexpr uint32_t kSlotBytes = kTile * 8;               // 2 KiB
-constexpr uint32_t kStageBytes = kBulkSlots * kSlotBytes;   // 12 KiB
-constexpr int kProducers = 4;                           // producer warps
+constexpr int kTile = 256;                 // positions per work item (consumer threads)
+constexpr uint32_t kSlotBytes = kTile * 8;   // 2 KiB
+// producer warps: 4 (2 at QN = 4: its consumers hold 128 accumulator registers; measured
+// 5520 against 5420 token lookups/s with 3)
+template <int QN>
+__host__ __device__ constexpr int bulk_producers() { return QN >= 4 ? 2 : 4; }
+// stage: x0 of QN queries, x1 of QN queries, the kGiantPack plaintexts
+template <int QN>
+__host__ __device__ constexpr int bulk_slots() { return 2 * QN + kGiantPack; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -62,63 +66,73 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 }  // namespace
 
-// grid: persistent CTAs; block: 256 consumers + 1 producer warp; dynamic smem:
-// stages x 12 KiB ring + 2 stages mbarriers + stage masks.
-__global__ void __launch_bounds__(kTile + 32 * kProducers, 2)
+// grid: persistent CTAs; block: 256 consumers + kProducers producer warps;
+// dynamic smem: stages x (2 QN + 4) 2 KiB slots + per stage two mbarriers
+// and a plaintext mask.  nq queries (a multiple of QN): query k reads its
+// baby pairs at x + k xq and writes out + k oq (the plaintexts are shared);
+// QN of them per pass over the terms.
+template <int QN, int kProducers = bulk_producers<QN>()>
+__global__ void __launch_bounds__(kTile + 32 * kProducers, 1)
     k_diag_mac_bulk(const MacTerm* __restrict__ terms, const int4* __restrict__ groups, int n_groups,
                     uint64_t* __restrict__ out, size_t out_stride, size_t half, const PrimeDev* __restrict__ primes,
-                    const __grid_constant__ LimbMap map, uint32_t N, int stages) {
-  constexpr int G = kGiantPack;
+                    const __grid_constant__ LimbMap map, uint32_t N, int stages, int nq, size_t xq, size_t oq) {
+  constexpr int G = kGiantPack, NS = bulk_slots<QN>();
+  constexpr uint32_t SB = NS * kSlotBytes;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * SB);
   uint64_t* empty = full + stages;
   int* smask = reinterpret_cast<int*>(empty + stages);
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], 1);        // the producer's arrive (plus the copies' bytes)
+      mbar_init(&full[s], 1);             // the producer's arrive (plus the copies' bytes)
       mbar_init(&empty[s], kTile / 32);   // every consumer warp releases the stage
     }
   }
   __syncthreads();
   const uint32_t tiles = N / kTile, total = tiles * (uint32_t)n_groups * (uint32_t)map.n;
+  const int nqc = nq / QN;   // query chunks per work item
   if (tid >= kTile) {
     // ---------------- producer warps ----------------
-    // kProducers warps, lane 0 each: term j of the CTA's sequence goes to warp j % kProducers
-    // (stages % kProducers == 0, so every stage has one owner and its waits stay in phase
-    // order).  An issued bulk copy occupies its warp for a while, so several warps issue in
-    // parallel.  Per term: wait for the stage, arm its barrier with the byte count, issue the
-    // (up to) six 2 KiB copies.  The next term's pointers are loaded before the wait.
+    // Lane 0 of kProducers warps: item j of the CTA's sequence of (query chunk, term) items
+    // goes to warp j % kProducers (stages % kProducers == 0, so every stage has one owner
+    // and its waits stay in phase order).  An issued bulk copy occupies its warp for a
+    // while, so several warps issue in parallel.  Per item: wait for the stage, arm its
+    // barrier with the byte count, issue the 2 KiB copies.
     const int pw = (tid - kTile) >> 5;
     if ((tid & 31) != 0) return;
     uint32_t j = 0;
     for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
       const int4 gr = groups[w % n_groups];   // pack fastest (as k_diag_mac): packs of a tile share baby pairs in L2
       const size_t o0 = (size_t)(w / (tiles * n_groups)) * N + ((w / n_groups) % tiles) * kTile;
-      int t = (int)((kProducers + pw - j % kProducers) % kProducers);   // first term of this warp
-      j += t;
-      MacTerm m{};
-      if (t < gr.y) m = terms[gr.x + t];
-      for (; t < gr.y; t += kProducers, j += kProducers) {
-        const MacTerm cur = m;
-        if (t + kProducers < gr.y) m = terms[gr.x + t + kProducers];
+      const int items = nqc * gr.y;
+      int it = (int)((kProducers + pw - j % kProducers) % kProducers);   // this warp's first item
+      j += it;
+      for (; it < items; it += kProducers, j += kProducers) {
+        const int qc = it / gr.y, t = it % gr.y;
+        const MacTerm m = terms[gr.x + t];
         const int stage = (int)(j % (uint32_t)stages);
         const uint32_t phase = (j / (uint32_t)stages) & 1u;
-        const uint64_t* src[kBulkSlots] = {cur.x0, cur.x1, cur.u[0], cur.u[1], cur.u[2], cur.u[3]};
         int mask = 0;
 #pragma unroll
-        for (int k = 0; k < kBulkSlots; k++)
-          if (src[k]) mask |= 1 << k;
+        for (int g = 0; g < G; g++)
+          if (m.u[g]) mask |= 1 << g;
         mbar_wait(&empty[stage], phase ^ 1);
         smask[stage] = mask;
-        mbar_arrive_expect_tx(&full[stage], (uint32_t)__popc(mask) * kSlotBytes);
-        unsigned char* st = ring + (size_t)stage * kStageBytes;
+        mbar_arrive_expect_tx(&full[stage], (uint32_t)(2 * QN + __popc(mask)) * kSlotBytes);
+        unsigned char* st = ring + (size_t)stage * SB;
 #pragma unroll
-        for (int k = 0; k < kBulkSlots; k++)
-          if (src[k]) bulk_g2s(st + k * kSlotBytes, src[k] + o0, kSlotBytes, &full[stage]);
+        for (int k = 0; k < QN; k++) {
+          const size_t xo = o0 + (size_t)(qc * QN + k) * xq;
+          bulk_g2s(st + k * kSlotBytes, m.x0 + xo, kSlotBytes, &full[stage]);
+          bulk_g2s(st + (QN + k) * kSlotBytes, m.x1 + xo, kSlotBytes, &full[stage]);
+        }
+#pragma unroll
+        for (int g = 0; g < G; g++)
+          if (m.u[g]) bulk_g2s(st + (2 * QN + g) * kSlotBytes, m.u[g] + o0, kSlotBytes, &full[stage]);
       }
-      j -= (uint32_t)(t - gr.y);   // j = count of terms so far (t overshot gr.y)
+      j -= (uint32_t)(it - items);   // j = items so far (it overshot by it - items)
     }
     return;
   }
@@ -131,66 +145,90 @@ __global__ void __launch_bounds__(kTile + 32 * kProducers, 2)
     const size_t o = (size_t)l * N + ((w / n_groups) % tiles) * kTile + tid;
     const PrimeDev& P = primes[map.pr[l]];
     const double q = P.qd, qi = P.qinv;
-    fm::FAcc acc0[G], acc1[G];
-    int cnt = 0;
-    for (int t = 0; t < gr.y; t++) {
-      mbar_wait(&full[stage], phase);
-      const int mask = smask[stage];
-      const double* st = reinterpret_cast<const double*>(ring + (size_t)stage * kStageBytes);
-      const double xa = st[tid], xb = st[kTile + tid];
-      double u[G];
+    for (int qc = 0; qc < nqc; qc++) {
+      fm::FAcc acc0[QN][G], acc1[QN][G];
+      int cnt = 0;
+      for (int t = 0; t < gr.y; t++) {
+        mbar_wait(&full[stage], phase);
+        const int mask = smask[stage];
+        const double* st = reinterpret_cast<const double*>(ring + (size_t)stage * SB);
+        double xa[QN], xb[QN], u[G];
 #pragma unroll
-      for (int g = 0; g < G; g++) u[g] = (mask >> (2 + g)) & 1 ? st[(2 + g) * kTile + tid] : 0.0;
-      __syncwarp();   // the warp's operands are in registers: the stage may be refilled
-      if ((tid & 31) == 0) mbar_arrive(&empty[stage]);
-      if (++stage == stages) {
-        stage = 0;
-        phase ^= 1;
+        for (int k = 0; k < QN; k++) {
+          xa[k] = st[k * kTile + tid];
+          xb[k] = st[(QN + k) * kTile + tid];
+        }
+#pragma unroll
+        for (int g = 0; g < G; g++) u[g] = (mask >> g) & 1 ? st[(2 * QN + g) * kTile + tid] : 0.0;
+        __syncwarp();   // the warp's operands are in registers: the stage may be refilled
+        if ((tid & 31) == 0) mbar_arrive(&empty[stage]);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (cnt == fm::kFAccTerms) {
+#pragma unroll
+          for (int k = 0; k < QN; k++)
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+              fm::fold(acc0[k][g], q, qi);
+              fm::fold(acc1[k][g], q, qi);
+            }
+          cnt = 0;
+        }
+        cnt++;
+#pragma unroll
+        for (int k = 0; k < QN; k++)
+#pragma unroll
+          for (int g = 0; g < G; g++) {
+            fm::fmac(acc0[k][g], u[g], xa[k]);
+            fm::fmac(acc1[k][g], u[g], xb[k]);
+          }
       }
-      if (cnt == fm::kFAccTerms) {
+#pragma unroll
+      for (int k = 0; k < QN; k++)
 #pragma unroll
         for (int g = 0; g < G; g++) {
-          fm::fold(acc0[g], q, qi);
-          fm::fold(acc1[g], q, qi);
+          if (g < gr.w) {
+            uint64_t* dst = out + (size_t)(gr.z + g) * out_stride + (size_t)(qc * QN + k) * oq;
+            dst[o] = fm::c2u(fm::fred(acc0[k][g], q, qi), P.rc.q);
+            dst[half + o] = fm::c2u(fm::fred(acc1[k][g], q, qi), P.rc.q);
+          }
         }
-        cnt = 0;
-      }
-      cnt++;
-#pragma unroll
-      for (int g = 0; g < G; g++) {
-        fm::fmac(acc0[g], u[g], xa);
-        fm::fmac(acc1[g], u[g], xb);
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-      if (g < gr.w) {
-        uint64_t* dst = out + (size_t)(gr.z + g) * out_stride;
-        dst[o] = fm::c2u(fm::fred(acc0[g], q, qi), P.rc.q);
-        dst[half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
-      }
     }
   }
 }
 
-bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
-                          size_t out_stride, size_t half, const LimbMap& map) {
-  if (c.N % kTile) return false;
-  static const int stages_env = getenv("HELRM_MACB_STAGES") ? atoi(getenv("HELRM_MACB_STAGES")) : 8;
-  const int stages = std::max(kProducers, stages_env / kProducers * kProducers);   // a multiple of kProducers
+template <int QN>
+static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
+                        size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq) {
+  static const int stages_env = getenv("HELRM_MACB_STAGES") ? atoi(getenv("HELRM_MACB_STAGES")) : 0;
+  constexpr size_t SB = (size_t)bulk_slots<QN>() * kSlotBytes;
+  // default: as many stages as fit in ~200 KiB (16 at 12 KiB, 8 at 24 KiB), a multiple of kProducers
+  constexpr int kProducers = bulk_producers<QN>();
+  const int want = stages_env > 0 ? stages_env : (int)(200 * 1024 / SB);
+  const int stages = std::max(kProducers, want / kProducers * kProducers);
   static const int per_sm = getenv("HELRM_MACB_CTAS") ? atoi(getenv("HELRM_MACB_CTAS")) : 1;
-  const size_t smem = (size_t)stages * (kStageBytes + 8 + 8 + 4);
-  static bool attr = false;
-  if (!attr) {
-    HCUDA(cudaFuncSetAttribute(k_diag_mac_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  const size_t smem = (size_t)stages * (SB + 8 + 8 + 4);
+  static size_t attr = 0;
+  if (attr != smem) {
+    HCUDA(cudaFuncSetAttribute(k_diag_mac_bulk<QN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
   }
   const unsigned total = (c.N / kTile) * (unsigned)n_groups * map.n;
   const unsigned grid = std::min<unsigned>(total, 148u * (unsigned)per_sm);
-  k_diag_mac_bulk<<<grid, kTile + 32 * kProducers, smem, c.stream>>>(terms, groups, n_groups, out, out_stride, half, c.primes, map,
-                                                        c.N, stages);
+  k_diag_mac_bulk<QN><<<grid, kTile + 32 * kProducers, smem, c.stream>>>(terms, groups, n_groups, out, out_stride,
+                                                                         half, c.primes, map, c.N, stages, nq, xq, oq);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
+}
+
+bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
+                          size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq) {
+  if (c.N % kTile || nq < 1) return false;
+  if (nq % 4 == 0) bulk_launch<4>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
+  else if (nq % 2 == 0) bulk_launch<2>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
+  else bulk_launch<1>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
   return true;
 }
 

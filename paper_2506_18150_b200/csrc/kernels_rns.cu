@@ -1018,9 +1018,11 @@ void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int
   // algorithmic bytes: every plaintext once, every distinct baby pair and output once per query
   ProfScope ps_(c, "diag_mac", 8.0 * c.N * map.n * (n_u_total + nq * (2.0 * n_x_distinct + 2.0 * n_out)));
   (void)wide;
-  static const int bulk = getenv("HELRM_MAC_BULK") ? atoi(getenv("HELRM_MAC_BULK")) : 0;
-  if (bulk && nq == 1 && x_dform && !wide &&
-      launch_diag_mac_bulk(c, (const MacTerm*)terms, groups, n_groups, out, out_stride, (size_t)map.n * c.N, map))
+  static const int bulk = getenv("HELRM_MAC_BULK") ? atoi(getenv("HELRM_MAC_BULK")) : 2;
+  // bulk-copy kernel: HELRM_MAC_BULK=1 for batch 1 only, 2 for every batch
+  if (bulk && (nq == 1 || bulk == 2) && x_dform && !wide && c.persist == 0 &&
+      launch_diag_mac_bulk(c, (const MacTerm*)terms, groups, n_groups, out, out_stride, (size_t)map.n * c.N, map, nq,
+                           xq, oq))
     return;
   if (nq == 1 && c.persist == 0) {
     auto k1 = x_dform ? k_diag_mac1<true> : k_diag_mac1<false>;

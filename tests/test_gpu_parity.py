@@ -552,21 +552,25 @@ def test_lookup_error_and_degenerate_cases(torch_mod):
 
 
 @gpu
-@pytest.mark.parametrize("knobs", [
-    {"HELRM_MAC_BULK": "1"},                                                   # bulk-copy (TMA) MAC
-    {"HELRM_MAC_BULK": "1", "HELRM_PIPE": "1", "HELRM_MACCH": "1", "HELRM_NTTCH": "4"},   # pipelined giants
+@pytest.mark.parametrize("knobs,test", [
+    ({"HELRM_MAC_BULK": "0"}, "test_criteo_full_size_matches_oracle_golden"),      # register-fed MAC
+    ({"HELRM_MAC_BULK": "0"}, "test_batched_lookup_bit_exact_vs_oracle"),
+    ({"HELRM_MAC_BULK": "0"}, "test_llm_full_size_plan_and_decryption"),
+    ({"HELRM_PIPE": "1", "HELRM_MACCH": "1", "HELRM_NTTCH": "4"},                  # pipelined giant steps
+     "test_criteo_full_size_matches_oracle_golden"),
 ])
-def test_criteo_golden_under_engine_knobs(knobs):
-    """The full-size Criteo golden check in a fresh process with alternative
-    engine paths switched on (the knobs are read once per process): the
-    bulk-copy MAC kernel (kernels_mac_bulk.cu) and the stream-pipelined giant
-    steps must give the same bit-exact output ciphertext."""
+def test_parity_under_engine_knobs(knobs, test):
+    """Parity tests in a fresh process with alternative engine paths switched
+    on (the knobs are read once per process): the register-fed MAC kernels
+    (k_diag_mac1 / k_diag_mac; the default is the bulk-copy kernel,
+    kernels_mac_bulk.cu) and the stream-pipelined giant steps must give the
+    same bit-exact outputs."""
     import os
     import subprocess
     import sys
     env = dict(os.environ, **knobs)
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_parity.py") + "::test_criteo_full_size_matches_oracle_golden"],
+                        os.path.join(here, "test_gpu_parity.py") + "::" + test],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
