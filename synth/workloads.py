@@ -44,7 +44,8 @@ CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431,
                 495595, 10, 822, 1375]
 CRITEO_VOCAB_SEED = 230
 
-CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "llm", "llm_small", "microbench")
+CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "criteo_c2", "criteo_c2_small", "llm",
+                "llm_small", "microbench")
 
 
 def subtable_rows(k: int, p: int) -> int:
@@ -108,6 +109,14 @@ _CONFIGS = {
     "uci": Config("uci", 14, [(40, 8)], [(40, 2)], 36, 7, 1),
     "criteo": Config("criteo", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
     "criteo_b64": Config("criteo_b64", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=64),
+    # a less compressed Criteo model (PAPER.md:459-463, Table 2 threshold 5e4; :470): tables
+    # with vocab <= 5e4 stay one-hot, the rest are digit-decomposed in base 1024 ->
+    # 47,798 input slots = 2 input cts and 1024 diagonals (the paper: 47,759 slots,
+    # "1024 non-zero diagonals ... two ciphertexts")
+    "criteo_c2": Config("criteo_c2", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
+    # the same shape scaled to the Tiny ring so the oracle runs it live: vocab sqrt(k),
+    # one-hot below 1000 rows, base 32 above -> 2,944 slots = 2 input cts of 2048
+    "criteo_c2_small": Config("criteo_c2_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
     "llm": Config("llm", 16, [(50, 20)], [(50, 4)], 40, 19, 1),
     # LLM-L2 layout scaled to the Tiny ring so the oracle runs it live: 64 tokens
     # of a 1000 x 48 table (base 32, 2 digits), stride 128 -> 4 in / 4 out cts
@@ -151,6 +160,17 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
     if name in ("criteo", "criteo_b64"):
         tables = [Table(k, 16, 64, rng.normal(0.0, 0.05, size=(subtable_rows(k, 64), 16))) for k in CRITEO_VOCAB]
         idx = np.array([[_zipf_index(rng, k) for k in CRITEO_VOCAB] for _ in range(B)], dtype=np.int64)
+        return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))
+    if name in ("criteo_c2", "criteo_c2_small"):
+        small = name == "criteo_c2_small"
+        vocab = [max(2, int(round(k ** 0.5))) for k in CRITEO_VOCAB] if small else CRITEO_VOCAB
+        thr, base = (1000, 32) if small else (50000, 1024)
+        tables = []
+        for k in vocab:
+            p = 0 if k <= thr else base
+            rows = k if p == 0 else subtable_rows(k, p)
+            tables.append(Table(k, 16, p, rng.normal(0.0, 0.05, size=(rows, 16))))
+        idx = np.array([[_zipf_index(rng, k) for k in vocab] for _ in range(B)], dtype=np.int64)
         return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))
     if name in ("llm", "llm_small"):
         V, d, p, m, stride = (50257, 768, 256, 128, 1024) if name == "llm" else (1000, 48, 32, 64, 128)

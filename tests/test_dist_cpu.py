@@ -61,7 +61,7 @@ def _worker(rank, world, name, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,port", [("uci", 29531), ("llm_small", 29533)])
+@pytest.mark.parametrize("name,port", [("uci", 29531), ("llm_small", 29533), ("criteo_c2_small", 29535)])
 def test_giant_partition_allreduce_is_bit_exact(name, port):
     world = 2
     ctx = mp.get_context("spawn")

@@ -244,7 +244,7 @@ def _gpu_lookup(E, w, mode=0, n1=0):
 
 @gpu
 @pytest.mark.parametrize("name,mode", [("tiny_a", 0), ("tiny_b", 0), ("uci", 0), ("uci", 1), ("tiny_b", 1),
-                                       ("llm_small", 0), ("llm_small", 1)])
+                                       ("llm_small", 0), ("llm_small", 1), ("criteo_c2_small", 0)])
 def test_lookup_bit_exact_vs_oracle(name, mode, torch_mod):
     E = env(name, torch_mod)
     w = synth.make_workload(name)
@@ -323,7 +323,25 @@ def test_llm_full_size_plan_and_decryption(torch_mod):
 
 
 @gpu
-@pytest.mark.parametrize("name", ["uci", "llm_small"])
+def test_criteo_c2_full_size_plan_and_decryption(torch_mod):
+    """The 2-input-ct Criteo shape at full size (Table 2 threshold
+    5e4: 47,798 one-hot slots, 1024 diagonals, giants shared by both cts):
+    plan counts and the decrypted output against the float64 gather (the
+    bit-exact check of a 2-ct lookup is criteo_c2_small)."""
+    E = env("criteo_c2", torch_mod)
+    w = synth.make_workload("criteo_c2")
+    plan, sk, outs = _gpu_lookup(E, w)
+    info = plan.info()
+    assert (info.n_in_cts, info.n_out_cts, info.n_diag, info.n1, info.n2_max, info.n_rotations) == (2, 1, 1024, 32,
+                                                                                                    16, 52)
+    lay = lk.layout(w)
+    y = lk.gather(lay, w.indices[0])
+    z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
+    assert np.abs(z[: lay.M] - y).max() < 1e-3
+
+
+@gpu
+@pytest.mark.parametrize("name", ["uci", "llm_small", "criteo_c2_small"])
 def test_lookup_dist_single_rank_matches_lookup(name, torch_mod):
     """helrm_lookup_dist on a 1-rank NCCL communicator (the only GPU a gpurun
     box has) runs the partitioned code path (broadcast, partial accumulators,
@@ -357,7 +375,7 @@ def _encrypt_batch(E, w, T, pk, info):
 
 
 @gpu
-@pytest.mark.parametrize("name,batch", [("tiny_b", 3), ("uci", 3), ("llm_small", 2)])
+@pytest.mark.parametrize("name,batch", [("tiny_b", 3), ("uci", 3), ("llm_small", 2), ("criteo_c2_small", 2)])
 def test_batched_lookup_bit_exact_vs_oracle(name, batch, torch_mod):
     """One helrm_lookup call over `batch` queries (the query-batched engine:
     shared key and plaintext reads, query loops inside the key-switch and MAC

@@ -247,3 +247,29 @@ def test_llm_small_lookup_decrypts_to_gather():
     assert (run.plan.C, run.plan.O, len(run.plan.u_slots), run.plan.n1) == (4, 4, 111, 16)
     z = np.concatenate([core.decrypt_decode(run.P, run.sk, o) for o in run.outs[0]])
     assert np.abs(z[: run.lay.M] - lk.gather(run.lay, w.indices[0])).max() < 1e-3
+
+
+def test_criteo_c2_small_lookup_decrypts_to_gather():
+    """Two input ciphertexts (the less compressed Criteo model of PAPER.md
+    Table 2, scaled to the Tiny ring): 2,944 one-hot slots over 2 cts, 1024
+    diagonals (512 per ct), the 15 giant rotations shared by both cts; the
+    output decrypts to the float64 gather."""
+    w = synth.make_workload("criteo_c2_small")
+    run = lk.run_config(w)
+    assert (run.plan.C, run.plan.O, len(run.plan.u_slots), run.plan.n1, run.plan.n_diag) == (2, 1, 1024, 32, 1024)
+    z = core.decrypt_decode(run.P, run.sk, run.outs[0][0])
+    assert np.abs(z[: run.lay.M] - lk.gather(run.lay, w.indices[0])).max() < 1e-3
+
+
+def test_criteo_c2_full_size_plan_counts():
+    """The full-size 2-ct Criteo shape (the 10^3x model "has 1024
+    non-zero diagonals and requires two ciphertexts"): 47,798 input slots, C = 2,
+    1024 diagonals, n1 = 32, n2 = 16, 52 rotation keys (31 babies + 15 giants +
+    RotSum 6 -- the same key set as the 1-ct model)."""
+    w = synth.make_workload("criteo_c2")
+    lay = lk.layout(w)
+    assert sum(len(t.weights) for t in w.tables) == 47798
+    n = 1 << 15
+    plan = lk.make_plan(lay, n, 23)
+    assert (plan.C, plan.O, len(plan.u_slots), plan.n1, plan.n2, plan.n_diag) == (2, 1, 1024, 32, [16], 1024)
+    assert len(plan.rotation_amounts(types.SimpleNamespace(n=n))) == 52

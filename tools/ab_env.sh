@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B timing of env-switched variants: ./tools/ab_env.sh "ENV1=.. ENV2=.." "..."
 for v in "$@"; do
-  env $v python bench.py --steps 10 --warmup 3 --skip-cpu-baseline --skip-micro --skip-batch --skip-llm > gpurun_out/ab_tmp.json 2>/dev/null
+  env $v python bench.py --steps 10 --warmup 3 --skip-cpu-baseline --skip-micro --skip-batch --skip-llm --skip-c2 > gpurun_out/ab_tmp.json 2>/dev/null
   python - "$v" <<'PY'
 import json, sys
 d = json.load(open("gpurun_out/ab_tmp.json"))

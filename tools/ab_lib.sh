@@ -1,6 +1,6 @@
 #!/bin/bash
 for v in "$@"; do
-  env $v python bench.py --steps 5 --warmup 3 --skip-cpu-baseline --skip-batch --skip-llm --rot-cts 2 > gpurun_out/ab_tmp.json 2>/dev/null
+  env $v python bench.py --steps 5 --warmup 3 --skip-cpu-baseline --skip-batch --skip-llm --skip-c2 --rot-cts 2 > gpurun_out/ab_tmp.json 2>/dev/null
   python - "$v" <<'PY'
 import json, sys
 d = json.load(open("gpurun_out/ab_tmp.json"))
