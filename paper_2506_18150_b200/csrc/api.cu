@@ -2010,10 +2010,44 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     }
     if (pipe) c->join(sk, sn);
     if (pipe) c->join(sk, sm);
+    // runs of giants accumulated in registers, the blocks sharing every key value (KipGiants
+    // with nq = O): the output blocks are read and written once per run instead of per giant
+    static const bool kgrun_p = getenv("HELRM_KIP_RUN") ? atoi(getenv("HELRM_KIP_RUN")) != 0 : true;
+    const bool runs = kgrun_p && (pl->O == 1 || pl->O == 2 || pl->O == 4);
+    KipGiants kg{};
+    auto flush = [&]() {
+      if (kg.n == 0) return;
+      kg.digit_stride = nlN;
+      kg.dnum = (int)dn;
+      kg.add_rows = (int)nl;
+      kg.alpha = (int)P.alpha;
+      kg.level = (int)l;
+      kg.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+      kg.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+      kg.out0 = Oall;
+      kg.out1 = Oall + nlN;
+      kg.nq = (int)pl->O;
+      kg.dq = (size_t)zb * dn * nlN;
+      kg.ownq = (size_t)zb * nqN;
+      kg.aq = (size_t)zb * 2 * nlN;
+      kg.oq = 2 * nlN;
+      launch_kip_giants(c->dc(sk), kg, mqp);
+      kg.n = 0;
+    };
     for (int z = 0; z < zb; z++) {
       const int64_t gi = pl->giants[0][ml.oi[z].second];
       if (gi % (int64_t)P.n == 0) {
         for (int64_t o = 0; o < pl->O; o++) zero_giant(z + (int)o * zb);
+        continue;
+      }
+      if (runs) {
+        const uint64_t g = galois_of_rot(c, gi);
+        kg.digits[kg.n] = D2.p + (size_t)z * dn * nlN;
+        kg.own[kg.n] = Bp.p + (size_t)z * nqN;
+        kg.key[kg.n] = key_for(rk, g);
+        kg.add0[kg.n] = AB.p + (size_t)z * 2 * nlN;
+        kg.rot[kg.n] = rot_of_galois(c, g);
+        if (++kg.n == kMaxGiantRun) flush();
         continue;
       }
       KipArgs a{};
@@ -2039,6 +2073,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
       a.level = (int)l;
       launch_kip(c->dc(sk, pers), a, mqp);
     }
+    flush();
   }
   for (size_t gp = 0; !periodic && gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);

@@ -283,6 +283,10 @@ struct KipGiants {
   size_t key_digit_stride, key_half_stride;
   uint64_t* out0;
   uint64_t* out1;
+  // nq queries (output blocks) share every key value: query r reads digits[g] + r dq,
+  // own[g] + r ownq, add0[g] + r aq and accumulates into out + r oq (nq = 1: strides unused)
+  int nq = 1;
+  size_t dq = 0, ownq = 0, aq = 0, oq = 0;
   const uint64_t* digits[kMaxGiantRun];
   const uint64_t* own[kMaxGiantRun];
   const uint64_t* key[kMaxGiantRun];

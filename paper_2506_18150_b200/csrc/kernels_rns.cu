@@ -291,62 +291,93 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
 
 // A run of giant steps into one output block (KipGiants): every giant adds
 // dnum + 1 exact FP64 MACs per output to the same accumulators (folded every
-// 2 giants), the output block is read once and written once.
-template <int DNUM>
-__global__ void __launch_bounds__(256, 3) k_kip_giants(const __grid_constant__ KipGiants a,
-                                                      const PrimeDev* __restrict__ primes,
-                                                      const __grid_constant__ LimbMap map, uint32_t N) {
+// 2 giants while 2 (dnum + 1) <= kFAccTerms, else every giant), the output
+// block is read once and written once.  NQ queries (the LLM's output blocks)
+// share each key value: the key is loaded once per giant for all of them.
+template <int DNUM, int NQ>
+__global__ void __launch_bounds__(256, NQ > 1 ? 2 : 3) k_kip_giants(const __grid_constant__ KipGiants a,
+                                                                   const PrimeDev* __restrict__ primes,
+                                                                   const __grid_constant__ LimbMap map, uint32_t N) {
+  constexpr int kFoldEvery = 2 * (DNUM + 1) <= fm::kFAccTerms ? 2 : 1;
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   const uint32_t chain = map.pr[l];
   const PrimeDev& P = primes[chain];
   const double q = P.qd, qi = P.qinv;
   const size_t o = (size_t)l * N + p;
-  const uint64_t pv0 = a.out0[o], pv1 = a.out1[o];
+  uint64_t pv0[NQ], pv1[NQ];
+#pragma unroll
+  for (int r = 0; r < NQ; r++) {
+    pv0[r] = a.out0[(size_t)r * a.oq + o];
+    pv1[r] = a.out1[(size_t)r * a.oq + o];
+  }
   const int kown = l <= a.level ? l / a.alpha : -1;
   const bool add = l < a.add_rows;
-  fm::FAcc acc0, acc1;
+  fm::FAcc acc0[NQ], acc1[NQ];
   for (int g = 0; g < a.n; g++) {
-    if (g > 0 && (g & 1) == 0) {   // (dnum + 1) terms per giant: fold every second giant
-      fm::fold(acc0, q, qi);
-      fm::fold(acc1, q, qi);
+    if (g > 0 && g % kFoldEvery == 0) {
+#pragma unroll
+      for (int r = 0; r < NQ; r++) {
+        fm::fold(acc0[r], q, qi);
+        fm::fold(acc1[r], q, qi);
+      }
     }
     const uint32_t sp = rot_src(p, a.rot[g], N / 2);
     const uint64_t* kb = a.key[g] + (size_t)chain * N + p;
     const uint64_t* dg = a.digits[g] + (size_t)l * N + sp;
-    uint64_t dv[DNUM], kv0[DNUM], kv1[DNUM];
+    const uint64_t* og = a.own[g] + (size_t)l * N + sp;
+    const uint64_t* ag = a.add0[g] + (size_t)l * N + sp;
+    uint64_t kv0[DNUM], kv1[DNUM], dv[NQ][DNUM], av[NQ];
 #pragma unroll
     for (int k = 0; k < DNUM; k++) {
-      dv[k] = k == kown ? a.own[g][(size_t)l * N + sp] : dg[(size_t)k * a.digit_stride];
       kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
       kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
     }
-    const uint64_t av = add ? a.add0[g][(size_t)l * N + sp] : 0;
 #pragma unroll
-    for (int k = 0; k < DNUM; k++) {
-      const double d = fm::u2d(dv[k]);
-      fm::fmac(acc0, d, fm::bits2d(kv0[k]));
-      fm::fmac(acc1, d, fm::bits2d(kv1[k]));
+    for (int r = 0; r < NQ; r++) {
+#pragma unroll
+      for (int k = 0; k < DNUM; k++)
+        dv[r][k] = k == kown ? og[(size_t)r * a.ownq] : dg[(size_t)r * a.dq + (size_t)k * a.digit_stride];
+      av[r] = add ? ag[(size_t)r * a.aq] : 0;
     }
-    if (add) fm::fmac(acc0, fm::u2d(av), 1.0);
+#pragma unroll
+    for (int r = 0; r < NQ; r++) {
+#pragma unroll
+      for (int k = 0; k < DNUM; k++) {
+        const double d = fm::u2d(dv[r][k]);
+        fm::fmac(acc0[r], d, fm::bits2d(kv0[k]));
+        fm::fmac(acc1[r], d, fm::bits2d(kv1[k]));
+      }
+      if (add) fm::fmac(acc0[r], fm::u2d(av[r]), 1.0);
+    }
   }
-  a.out0[o] = add_mod(fm::c2u(fm::fred(acc0, q, qi), P.rc.q), pv0, P.rc.q);
-  a.out1[o] = add_mod(fm::c2u(fm::fred(acc1, q, qi), P.rc.q), pv1, P.rc.q);
+#pragma unroll
+  for (int r = 0; r < NQ; r++) {
+    a.out0[(size_t)r * a.oq + o] = add_mod(fm::c2u(fm::fred(acc0[r], q, qi), P.rc.q), pv0[r], P.rc.q);
+    a.out1[(size_t)r * a.oq + o] = add_mod(fm::c2u(fm::fred(acc1[r], q, qi), P.rc.q), pv1[r], P.rc.q);
+  }
 }
 
 void launch_kip_giants(const DevCtx& c, const KipGiants& a, const LimbMap& map) {
-  ProfScope ps_(c, "kip", 8.0 * c.N * (a.n * (3.0 * a.dnum * map.n + a.add_rows) + 4.0 * map.n));
-  decltype(&k_kip_giants<1>) kern = nullptr;
+  ProfScope ps_(c, "kip",
+                8.0 * c.N * (a.n * (2.0 * a.dnum * map.n + a.nq * (a.dnum * map.n + a.add_rows)) + 4.0 * a.nq * map.n));
+  decltype(&k_kip_giants<1, 1>) kern = nullptr;
+#define HELRM_KG_CASE(D)                                                                        \
+  case D:                                                                                       \
+    kern = a.nq == 4 ? k_kip_giants<D, 4> : a.nq == 2 ? k_kip_giants<D, 2> : k_kip_giants<D, 1>; \
+    break;
+  if (a.nq != 1 && a.nq != 2 && a.nq != 4) throw Error(HELRM_ERR_CONFIG, "giant runs support 1, 2 or 4 queries");
   switch (a.dnum) {
-    case 1: kern = k_kip_giants<1>; break;
-    case 2: kern = k_kip_giants<2>; break;
-    case 3: kern = k_kip_giants<3>; break;
-    case 4: kern = k_kip_giants<4>; break;
-    case 5: kern = k_kip_giants<5>; break;
-    case 6: kern = k_kip_giants<6>; break;
-    case 7: kern = k_kip_giants<7>; break;
+    HELRM_KG_CASE(1)
+    HELRM_KG_CASE(2)
+    HELRM_KG_CASE(3)
+    HELRM_KG_CASE(4)
+    HELRM_KG_CASE(5)
+    HELRM_KG_CASE(6)
+    HELRM_KG_CASE(7)
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
+#undef HELRM_KG_CASE
   kern<<<dim3(c.N / kT, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
