@@ -71,8 +71,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // and a plaintext mask.  nq queries (a multiple of QN): query k reads its
 // baby pairs at x + k xq and writes out + k oq (the plaintexts are shared);
 // QN of them per pass over the terms.
-template <int QN, int kProducers = bulk_producers<QN>()>
-__global__ void __launch_bounds__(kTile + 32 * kProducers, 1)
+// QS consumer threads per position, each taking QN / QS queries (QS = 2 at
+// QN = 4 gives 16 consumer warps instead of 8 but measured 5730 against 5850
+// token lookups/s: the 576-thread CTA spills; kept at 1)
+template <int QN>
+__host__ __device__ constexpr int bulk_qsplit() { return 1; }
+template <int QN, int kProducers = bulk_producers<QN>(), int QS = bulk_qsplit<QN>()>
+__global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
     k_diag_mac_bulk(const MacTerm* __restrict__ terms, const int4* __restrict__ groups, int n_groups,
                     uint64_t* __restrict__ out, size_t out_stride, size_t half, const PrimeDev* __restrict__ primes,
                     const __grid_constant__ LimbMap map, uint32_t N, int stages, int nq, size_t xq, size_t oq) {
@@ -87,20 +92,21 @@ __global__ void __launch_bounds__(kTile + 32 * kProducers, 1)
   if (tid == 0) {
     for (int s = 0; s < stages; s++) {
       mbar_init(&full[s], 1);             // the producer's arrive (plus the copies' bytes)
-      mbar_init(&empty[s], kTile / 32);   // every consumer warp releases the stage
+      mbar_init(&empty[s], kTile * QS / 32);   // every consumer warp releases the stage
     }
   }
   __syncthreads();
   const uint32_t tiles = N / kTile, total = tiles * (uint32_t)n_groups * (uint32_t)map.n;
   const int nqc = nq / QN;   // query chunks per work item
-  if (tid >= kTile) {
+  constexpr int kCons = kTile * QS, QT = QN / QS;   // consumer threads, queries per consumer thread
+  if (tid >= kCons) {
     // ---------------- producer warps ----------------
     // Lane 0 of kProducers warps: item j of the CTA's sequence of (query chunk, term) items
     // goes to warp j % kProducers (stages % kProducers == 0, so every stage has one owner
     // and its waits stay in phase order).  An issued bulk copy occupies its warp for a
     // while, so several warps issue in parallel.  Per item: wait for the stage, arm its
     // barrier with the byte count, issue the 2 KiB copies.
-    const int pw = (tid - kTile) >> 5;
+    const int pw = (tid - kCons) >> 5;
     if ((tid & 31) != 0) return;
     uint32_t j = 0;
     for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
@@ -136,30 +142,31 @@ __global__ void __launch_bounds__(kTile + 32 * kProducers, 1)
     }
     return;
   }
-  // ---------------- consumers: one position each ----------------
+  // ---------------- consumers: one position and QT queries each ----------------
+  const int pos = tid % kTile, qh = tid / kTile;   // queries qh QT .. qh QT + QT - 1 of a chunk
   int stage = 0;
   uint32_t phase = 0;
   for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
     const int4 gr = groups[w % n_groups];
     const int l = (int)(w / (tiles * n_groups));
-    const size_t o = (size_t)l * N + ((w / n_groups) % tiles) * kTile + tid;
+    const size_t o = (size_t)l * N + ((w / n_groups) % tiles) * kTile + pos;
     const PrimeDev& P = primes[map.pr[l]];
     const double q = P.qd, qi = P.qinv;
     for (int qc = 0; qc < nqc; qc++) {
-      fm::FAcc acc0[QN][G], acc1[QN][G];
+      fm::FAcc acc0[QT][G], acc1[QT][G];
       int cnt = 0;
       for (int t = 0; t < gr.y; t++) {
         mbar_wait(&full[stage], phase);
         const int mask = smask[stage];
         const double* st = reinterpret_cast<const double*>(ring + (size_t)stage * SB);
-        double xa[QN], xb[QN], u[G];
+        double xa[QT], xb[QT], u[G];
 #pragma unroll
-        for (int k = 0; k < QN; k++) {
-          xa[k] = st[k * kTile + tid];
-          xb[k] = st[(QN + k) * kTile + tid];
+        for (int k = 0; k < QT; k++) {
+          xa[k] = st[(qh * QT + k) * kTile + pos];
+          xb[k] = st[(QN + qh * QT + k) * kTile + pos];
         }
 #pragma unroll
-        for (int g = 0; g < G; g++) u[g] = (mask >> g) & 1 ? st[(2 * QN + g) * kTile + tid] : 0.0;
+        for (int g = 0; g < G; g++) u[g] = (mask >> g) & 1 ? st[(2 * QN + g) * kTile + pos] : 0.0;
         __syncwarp();   // the warp's operands are in registers: the stage may be refilled
         if ((tid & 31) == 0) mbar_arrive(&empty[stage]);
         if (++stage == stages) {
@@ -168,7 +175,7 @@ __global__ void __launch_bounds__(kTile + 32 * kProducers, 1)
         }
         if (cnt == fm::kFAccTerms) {
 #pragma unroll
-          for (int k = 0; k < QN; k++)
+          for (int k = 0; k < QT; k++)
 #pragma unroll
             for (int g = 0; g < G; g++) {
               fm::fold(acc0[k][g], q, qi);
@@ -178,7 +185,7 @@ __global__ void __launch_bounds__(kTile + 32 * kProducers, 1)
         }
         cnt++;
 #pragma unroll
-        for (int k = 0; k < QN; k++)
+        for (int k = 0; k < QT; k++)
 #pragma unroll
           for (int g = 0; g < G; g++) {
             fm::fmac(acc0[k][g], u[g], xa[k]);
@@ -186,11 +193,11 @@ __global__ void __launch_bounds__(kTile + 32 * kProducers, 1)
           }
       }
 #pragma unroll
-      for (int k = 0; k < QN; k++)
+      for (int k = 0; k < QT; k++)
 #pragma unroll
         for (int g = 0; g < G; g++) {
           if (g < gr.w) {
-            uint64_t* dst = out + (size_t)(gr.z + g) * out_stride + (size_t)(qc * QN + k) * oq;
+            uint64_t* dst = out + (size_t)(gr.z + g) * out_stride + (size_t)(qc * QN + qh * QT + k) * oq;
             dst[o] = fm::c2u(fm::fred(acc0[k][g], q, qi), P.rc.q);
             dst[half + o] = fm::c2u(fm::fred(acc1[k][g], q, qi), P.rc.q);
           }
@@ -217,7 +224,7 @@ static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* group
   }
   const unsigned total = (c.N / kTile) * (unsigned)n_groups * map.n;
   const unsigned grid = std::min<unsigned>(total, 148u * (unsigned)per_sm);
-  k_diag_mac_bulk<QN><<<grid, kTile + 32 * kProducers, smem, c.stream>>>(terms, groups, n_groups, out, out_stride,
+  k_diag_mac_bulk<QN><<<grid, kTile * bulk_qsplit<QN>() + 32 * kProducers, smem, c.stream>>>(terms, groups, n_groups, out, out_stride,
                                                                          half, c.primes, map, c.N, stages, nq, xq, oq);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
@@ -226,8 +233,9 @@ static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* group
 bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
                           size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq) {
   if (c.N % kTile || nq < 1) return false;
-  if (nq % 4 == 0) bulk_launch<4>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
-  else if (nq % 2 == 0) bulk_launch<2>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
+  static const int qmax = getenv("HELRM_MACB_QMAX") ? atoi(getenv("HELRM_MACB_QMAX")) : 4;
+  if (nq % 4 == 0 && qmax >= 4) bulk_launch<4>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
+  else if (nq % 2 == 0 && qmax >= 2) bulk_launch<2>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
   else bulk_launch<1>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
   return true;
 }
