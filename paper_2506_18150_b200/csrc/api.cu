@@ -268,6 +268,11 @@ cudaEvent_t Profiler::get() {
 static const bool g_hostprof = getenv("HELRM_HOSTPROF") && atoi(getenv("HELRM_HOSTPROF")) != 0;
 static std::map<std::string, std::pair<uint64_t, double>> g_hostt;
 bool hostprof_on() { return g_hostprof; }
+bool pdl_on() {
+  // measured neutral inside the lookup graphs (6.82-6.85 ms either way): off unless HELRM_PDL=1
+  static const bool on = getenv("HELRM_PDL") ? atoi(getenv("HELRM_PDL")) != 0 : false;
+  return on;
+}
 void hostprof_add(const char* name, double us) {
   auto& e = g_hostt[name];
   e.first++;

@@ -152,6 +152,35 @@ struct DevCtx {
   Profiler* prof;
 };
 
+// Programmatic dependent launch (HELRM_PDL=1; off by default: measured neutral).  A kernel launched
+// with launch_pdl may be scheduled while its stream predecessor is finishing:
+// its CTAs become resident and wait in pdl_wait_trigger() (griddepcontrol.wait)
+// until the predecessor has completed and its writes are visible, so a chain
+// of small dependent kernels (RotSum, ModUp/ModDown) does not pay a launch
+// gap per boundary.  Every kernel launched this way calls pdl_wait_trigger()
+// before touching memory; the trigger lets its own successor be scheduled
+// once all of its CTAs are running.
+bool pdl_on();
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait_trigger() {
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = pdl_on() ? at : nullptr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  HCUDA(cudaLaunchKernelEx(&cfg, k, args...));
+}
+#endif
+
 // host-side time per call site (HELRM_HOSTPROF=1; diagnostics of launch overhead)
 bool hostprof_on();
 void hostprof_add(const char* name, double us);

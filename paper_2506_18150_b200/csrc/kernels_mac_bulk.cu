@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
     k_diag_mac_bulk(const MacTerm* __restrict__ terms, const int4* __restrict__ groups, int n_groups,
                     uint64_t* __restrict__ out, size_t out_stride, size_t half, const PrimeDev* __restrict__ primes,
                     const __grid_constant__ LimbMap map, uint32_t N, int stages, int nq, size_t xq, size_t oq) {
+  pdl_wait_trigger();
   constexpr int G = kGiantPack, NS = bulk_slots<QN>();
   constexpr uint32_t SB = NS * kSlotBytes;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -224,8 +225,7 @@ static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* group
   }
   const unsigned total = (c.N / kTile) * (unsigned)n_groups * map.n;
   const unsigned grid = std::min<unsigned>(total, 148u * (unsigned)per_sm);
-  k_diag_mac_bulk<QN><<<grid, kTile * bulk_qsplit<QN>() + 32 * kProducers, smem, c.stream>>>(terms, groups, n_groups, out, out_stride,
-                                                                         half, c.primes, map, c.N, stages, nq, xq, oq);
+  launch_pdl(k_diag_mac_bulk<QN>, dim3(grid), dim3(kTile * bulk_qsplit<QN>() + 32 * kProducers), smem, c.stream, terms, groups, n_groups, out, out_stride, half, c.primes, map, c.N, stages, nq, xq, oq);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }

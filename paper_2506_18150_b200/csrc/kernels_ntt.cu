@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
                                                       const uint32_t* __restrict__ lidx,
                                                       const __grid_constant__ NttEpi epi,
                                                       const __grid_constant__ NttConvIn cv) {
+  pdl_wait_trigger();
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   constexpr bool P1 = MODE != 1;  // MODE 2: pass 1 on centred doubles (conversion output); MODE 3: conversion fused
   __shared__ double sm[P1 ? kTileElems : 16 * kBlkPad];
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
                                                       const uint8_t* __restrict__ tpos,
                                                       const double2* __restrict__ post,
                                                       const uint32_t* __restrict__ lidx) {
+  pdl_wait_trigger();
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   __shared__ double sm[MODE == 0 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
@@ -404,14 +406,13 @@ static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
       k1 = cv.nb_max <= 1 ? k_ntt_fwd<SLOG, 3, 1> : cv.nb_max <= 2 ? k_ntt_fwd<SLOG, 3, 2>
            : cv.nb_max <= 4 ? k_ntt_fwd<SLOG, 3, 4> : k_ntt_fwd<SLOG, 3, 8>;
     allow_xsmem(k1);
-    k1<<<dim3(g1, cnt), kThreads, ntt_xsmem(), c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp,
-                                                 c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
+    launch_pdl(k1, dim3(g1, cnt), dim3(kThreads), ntt_xsmem(), c.stream, src, scratch, c.primes, map, off, ss, c.log_n,
+               c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
     allow_xsmem(k_ntt_fwd<8, 1>);
-    k_ntt_fwd<8, 1><<<dim3(g2, cnt), kThreads, ntt_xsmem(), c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                               c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
+    launch_pdl(k_ntt_fwd<8, 1>, dim3(dim3(g2, cnt)), dim3(kThreads), ntt_xsmem(), c.stream, scratch, dst, c.primes, map, off, ds, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
   }
   *c.launches += 2;
 }
@@ -425,14 +426,12 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
   {
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
     allow_xsmem(k_ntt_inv<8, 1>);
-    k_ntt_inv<8, 1><<<dim3(g2, cnt), kThreads, ntt_xsmem(), c.stream>>>(src, scratch, c.primes, map, off, ss, c.log_n,
-                                                               c.ntt_grp, c.ntt_twb, c.ntt_tpos, nullptr, lidx);
+    launch_pdl(k_ntt_inv<8, 1>, dim3(dim3(g2, cnt)), dim3(kThreads), ntt_xsmem(), c.stream, src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, nullptr, lidx);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
     allow_xsmem(k_ntt_inv<SLOG, 0>);
-    k_ntt_inv<SLOG, 0><<<dim3(g1, cnt), kThreads, ntt_xsmem(), c.stream>>>(scratch, dst, c.primes, map, off, ds, c.log_n,
-                                                                  c.ntt_grp, c.ntt_twb, c.ntt_tpos, post, lidx);
+    launch_pdl(k_ntt_inv<SLOG, 0>, dim3(dim3(g1, cnt)), dim3(kThreads), ntt_xsmem(), c.stream, scratch, dst, c.primes, map, off, ds, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, post, lidx);
   }
   *c.launches += 2;
 }

@@ -79,6 +79,7 @@ __global__ void k_sample_small(int64_t* __restrict__ out, uint32_t N, uint64_t b
 // op 0: a + b, 1: a - b, 2: a * b, 3: -a
 __global__ void k_binary(int op, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                          uint64_t* __restrict__ out, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
@@ -100,6 +101,7 @@ __global__ void k_scalar_mul(const uint64_t* __restrict__ a, uint64_t* __restric
                              const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N,
                              const uint64_t* __restrict__ s, const uint64_t* __restrict__ sp, int dform_out,
                              size_t as, size_t os) {
+  pdl_wait_trigger();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
@@ -123,6 +125,7 @@ __global__ void k_dform(uint64_t* __restrict__ x, size_t n, uint32_t log_n, cons
 __global__ void k_automorph(const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
                             const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map, uint32_t N, uint32_t rot,
                             int accumulate) {
+  pdl_wait_trigger();
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (p >= N) return;
@@ -140,6 +143,7 @@ template <int NB, int PT = 1>
 __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict__ tab, int ncv, int rows,
                                                    const uint64_t* __restrict__ y, size_t y_stride,
                                                    uint64_t* __restrict__ out, size_t osg, size_t osk, uint32_t N) {
+  pdl_wait_trigger();
   __shared__ ConvRowDev st[kMaxLimbs];
   const int g = blockIdx.y / ncv, k = blockIdx.y % ncv;
   const ConvRowDev* tk = tab + (size_t)k * rows;
@@ -179,6 +183,7 @@ __global__ void k_sub_scale(const uint64_t* __restrict__ y, size_t ys, const uin
                             uint64_t* __restrict__ out, size_t os, const PrimeDev* __restrict__ primes,
                             const __grid_constant__ LimbMap map, uint32_t N, const uint64_t* __restrict__ s,
                             const uint64_t* __restrict__ sp) {
+  pdl_wait_trigger();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y, g = blockIdx.z;
   if (i >= N) return;
@@ -191,6 +196,7 @@ __global__ void k_sub_scale(const uint64_t* __restrict__ y, size_t ys, const uin
 __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint64_t ql, uint64_t* __restrict__ out,
                                size_t os, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map,
                                uint32_t N) {
+  pdl_wait_trigger();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
@@ -219,6 +225,7 @@ __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint6
 template <int DNUM, int QR>
 __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
                                              const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   // work item w = (tile, limb); a grid smaller than the work loops (persistent CTAs)
   const uint32_t tiles = N / blockDim.x, total = tiles * (uint32_t)map.n;
   for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
@@ -298,6 +305,7 @@ template <int DNUM, int NQ>
 __global__ void __launch_bounds__(256, NQ > 1 ? 2 : 3) k_kip_giants(const __grid_constant__ KipGiants a,
                                                                    const PrimeDev* __restrict__ primes,
                                                                    const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   constexpr int kFoldEvery = 2 * (DNUM + 1) <= fm::kFAccTerms ? 2 : 1;
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
@@ -378,7 +386,7 @@ void launch_kip_giants(const DevCtx& c, const KipGiants& a, const LimbMap& map) 
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
 #undef HELRM_KG_CASE
-  kern<<<dim3(c.N / kT, map.n), kT, 0, c.stream>>>(a, c.primes, map, c.N);
+  launch_pdl(kern, dim3(dim3(c.N / kT, map.n)), dim3(kT), 0, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -395,6 +403,7 @@ template <int DNUM>
 __global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ KipMulti a,
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   extern __shared__ double shd[];
   const int l = blockIdx.y;
   const uint32_t n = N / 2, tile = blockDim.x;
@@ -460,6 +469,7 @@ __global__ void __launch_bounds__(256) k_diag_mac1(const MacTerm* __restrict__ t
                                                   uint64_t* __restrict__ out, size_t out_stride, size_t half,
                                                   const PrimeDev* __restrict__ primes,
                                                   const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   constexpr int G = kGiantPack;
   constexpr int kChunk = 64;
   __shared__ MacTerm tm[kChunk];
@@ -544,6 +554,7 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
                                                   const PrimeDev* __restrict__ primes,
                                                   const __grid_constant__ LimbMap map, uint32_t N, int nq, size_t xq,
                                                   size_t oq, int n_groups) {
+  pdl_wait_trigger();
   constexpr int G = kGiantPack;
   constexpr int kChunk = 64;
   __shared__ MacTerm tm[kChunk];
@@ -645,6 +656,7 @@ __global__ void __launch_bounds__(kBabyMacTile) k_baby_mac(const __grid_constant
                                                           const __grid_constant__ BabyMacArgs m,
                                                           const PrimeDev* __restrict__ primes,
                                                           const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   constexpr int T = kBabyMacTile, G = kGiantPack;
   extern __shared__ double shd[];
   const int l = blockIdx.y, tid = threadIdx.x;
@@ -780,7 +792,7 @@ bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, c
   }
   ProfScope ps_(c, "baby_mac", m.bytes);
   HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<dim3(c.N / kBabyMacTile, map.n), kBabyMacTile, smem, c.stream>>>(a, m, c.primes, map, c.N);
+  launch_pdl(kern, dim3(dim3(c.N / kBabyMacTile, map.n)), dim3(kBabyMacTile), smem, c.stream, a, m, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
   return true;
@@ -794,6 +806,7 @@ template <int NBLK, int GT>
 __global__ void __launch_bounds__(128) k_block_mac(const __grid_constant__ BlockMacArgs a,
                                                   const PrimeDev* __restrict__ primes,
                                                   const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   constexpr int T = 16, W = 8;
   extern __shared__ double sx[];                 // [nb][NBLK][2][T] babies, then the ring [S][zb][T]
   double* ring = sx + (size_t)a.nb * NBLK * 2 * T;
@@ -881,7 +894,7 @@ bool launch_block_mac(const DevCtx& c, const BlockMacArgs& a, const LimbMap& map
   auto kern = a.zb <= 8 ? k_block_mac<4, 1> : a.zb <= 16 ? k_block_mac<4, 2> : k_block_mac<4, 3>;
   HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfScope ps_(c, "diag_mac", a.bytes);
-  kern<<<dim3(c.N / 16, map.n), 128, smem, c.stream>>>(a, c.primes, map, c.N);
+  launch_pdl(kern, dim3(dim3(c.N / 16, map.n)), dim3(128), smem, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
   return true;
@@ -891,6 +904,7 @@ bool launch_block_mac(const DevCtx& c, const BlockMacArgs& a, const LimbMap& map
 // (each < q, at most 2^13 ranks -> no wrap), reduce every word mod its prime
 __global__ void k_modred(uint64_t* __restrict__ x, const PrimeDev* __restrict__ primes,
                          const __grid_constant__ LimbMap map, uint32_t N) {
+  pdl_wait_trigger();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int l = blockIdx.y;
   if (i >= N) return;
@@ -928,7 +942,7 @@ void launch_sample_small(const DevCtx& c, int64_t* out, uint64_t base, int kind,
 
 void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, const LimbMap& map) {
   ProfScope ps_(c, "binary", 8.0 * c.N * map.n * (op == 3 ? 2 : 3));
-  k_binary<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(op, a, b, out, c.primes, map, c.N);
+  launch_pdl(k_binary, dim3(grid_for(c.N, map.n)), dim3(kT), 0, c.stream, op, a, b, out, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -936,8 +950,7 @@ void launch_binary(const DevCtx& c, int op, const uint64_t* a, const uint64_t* b
 void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, const uint64_t* s,
                        const uint64_t* sp, int dform_out, int G, size_t as, size_t os) {
   ProfScope ps_(c, "scalar_mul", 16.0 * c.N * map.n * G);
-  k_scalar_mul<<<dim3((c.N + kT - 1) / kT, map.n, G), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, s, sp,
-                                                                          dform_out, as, os);
+  launch_pdl(k_scalar_mul, dim3(dim3((c.N + kT - 1) / kT, map.n, G)), dim3(kT), 0, c.stream, a, out, c.primes, map, c.N, s, sp, dform_out, as, os);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -952,7 +965,7 @@ void launch_dform(const DevCtx& c, uint64_t* x, size_t n, const LimbMap& map, in
 void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
                       int accumulate) {
   ProfScope ps_(c, "automorph", 8.0 * c.N * map.n * (accumulate ? 3 : 2));
-  k_automorph<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(a, out, c.primes, map, c.N, rot, accumulate);
+  launch_pdl(k_automorph, dim3(grid_for(c.N, map.n)), dim3(kT), 0, c.stream, a, out, c.primes, map, c.N, rot, accumulate);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -968,8 +981,7 @@ void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows,
     kern = nb_max <= 1 ? k_conv_rows<1, 2> : nb_max <= 2 ? k_conv_rows<2, 2> : nb_max <= 4 ? k_conv_rows<4, 2>
                                                                                          : k_conv_rows<8, 2>;
   (void)out_map;
-  kern<<<dim3(c.N / (256 * pt), G * ncv), 256, 0, c.stream>>>(tab, ncv, rows, y, y_stride, out, out_stride_g,
-                                                              out_stride_k, c.N);
+  launch_pdl(kern, dim3(dim3(c.N / (256 * pt), G * ncv)), dim3(256), 0, c.stream, tab, ncv, rows, y, y_stride, out, out_stride_g, out_stride_k, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -977,15 +989,14 @@ void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows,
 void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
                       size_t os, int G, const LimbMap& map, const uint64_t* s, const uint64_t* sp) {
   ProfScope ps_(c, "sub_scale", 24.0 * c.N * map.n * G);
-  k_sub_scale<<<dim3((c.N + kT - 1) / kT, map.n, G), kT, 0, c.stream>>>(y, ys, t, ts, out, os, c.primes, map, c.N, s,
-                                                                        sp);
+  launch_pdl(k_sub_scale, dim3(dim3((c.N + kT - 1) / kT, map.n, G)), dim3(kT), 0, c.stream, y, ys, t, ts, out, os, c.primes, map, c.N, s, sp);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map) {
   ProfScope ps_(c, "modred", 16.0 * c.N * map.n);
-  k_modred<<<grid_for(c.N, map.n), kT, 0, c.stream>>>(x, c.primes, map, c.N);
+  launch_pdl(k_modred, dim3(grid_for(c.N, map.n)), dim3(kT), 0, c.stream, x, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -993,7 +1004,7 @@ void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map) {
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,
                          const LimbMap& map) {
   ProfScope ps_(c, "rescale_prep", 8.0 * c.N * (1 + map.n) * G);
-  k_rescale_prep<<<dim3((c.N + kT - 1) / kT, map.n, G), kT, 0, c.stream>>>(xl, xs, ql, out, os, c.primes, map, c.N);
+  launch_pdl(k_rescale_prep, dim3(dim3((c.N + kT - 1) / kT, map.n, G)), dim3(kT), 0, c.stream, xl, xs, ql, out, os, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -1015,7 +1026,7 @@ void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
   }
   const unsigned total = (c.N / kT) * map.n;
   const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
-  kern<<<grid, kT, 0, c.stream>>>(a, c.primes, map, c.N);
+  launch_pdl(kern, dim3(grid), dim3(kT), 0, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -1038,7 +1049,7 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
   if (smem > 48 * 1024) HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<dim3(c.N / tile, map.n, (unsigned)zq), tile, smem, c.stream>>>(a, c.primes, map, c.N);
+  launch_pdl(kern, dim3(dim3(c.N / tile, map.n, (unsigned)zq)), dim3(tile), smem, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -1057,8 +1068,7 @@ void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int
     return;
   if (nq == 1 && c.persist == 0) {
     auto k1 = x_dform ? k_diag_mac1<true> : k_diag_mac1<false>;
-    k1<<<dim3(c.N / kT, n_groups, map.n), kT, 0, c.stream>>>((const MacTerm*)terms, groups, out, out_stride,
-                                                             (size_t)map.n * c.N, c.primes, map, c.N);
+    launch_pdl(k1, dim3(dim3(c.N / kT, n_groups, map.n)), dim3(kT), 0, c.stream, (const MacTerm*)terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map, c.N);
     (*c.launches)++;
     HCUDA(cudaGetLastError());
     return;
@@ -1070,8 +1080,7 @@ void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int
                                            : nq > 1 ? k_diag_mac<false, 2> : k_diag_mac<false, 1>);
   const unsigned total = (c.N / kT) * n_groups * map.n;
   const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
-  kern<<<grid, kT, 0, c.stream>>>((const MacTerm*)terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map,
-                                  c.N, nq, xq, oq, n_groups);
+  launch_pdl(kern, dim3(grid), dim3(kT), 0, c.stream, (const MacTerm*)terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map, c.N, nq, xq, oq, n_groups);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
