@@ -385,6 +385,8 @@ def run_gpu(args, world, rank, local):
         secondary["llm_128_tokens"] = llm_lookup(args, helrm, torch, stream, world, dev)
     if not args.skip_c2:
         secondary["criteo_c2_b1"] = c2_lookup(args, helrm, torch, stream, world, dev)
+        # LLM generation step: one sampled token's embedding, 768 dims
+        secondary["llm_gen_token"] = shape_lookup(helrm, torch, stream, world, dev, "llm_gen")
 
     return {
         "value": value, "ms": ms / args.steps, "launches": launches, "clocks": clk.summary(),
@@ -451,6 +453,48 @@ def batch_lookup(args, ctx, helrm, torch, stream, plan, rk, cts, world, B=64):
     ms = max_over_ranks(e0.elapsed_time(e1), world) / reps
     return {"batch": B, "ms_per_batch": round(ms, 3), "lookups_per_s": round(world * B * 1e3 / ms, 2),
             "inputs": f"{len(cts)} encrypted queries cycled"}
+
+
+def shape_lookup(helrm, torch, stream, world, dev, name, reps=5):
+    """Batch-1 lookup of a secondary workload shape on its own context: device
+    time per lookup (max over ranks) and the plan's counts."""
+    import synth
+    w = synth.make_workload(name)
+    cfg = w.config
+    P = helrm.params_from_config(cfg)
+    ctx = helrm.Context(P, dev, stream.cuda_stream)
+    t0 = time.time()
+    T = helrm.tables_create(P, w.tables, w.n_dense)
+    plan = helrm.plan_create(ctx, T, cfg.level)
+    info = plan.info()
+    sk = helrm.sk_gen(ctx, cfg.seed)
+    pk = helrm.pk_gen(ctx, sk, cfg.seed)
+    rk = helrm.rotkeys_gen(ctx, sk, plan.galois(cfg.N), cfg.seed)
+    x = helrm.encode_query(T, w.indices[0], w.dense[0], info.n_in_cts * cfg.n_slots)
+    cts = [helrm.encrypt(ctx, pk, x[c * cfg.n_slots:(c + 1) * cfg.n_slots], cfg.level, (cfg.seed << 20) | c)
+           for c in range(info.n_in_cts)]
+    ctx.sync()
+    setup = time.time() - t0
+    for _ in range(3):
+        for o in helrm.lookup(ctx, plan, rk, cts):
+            o.close()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        for o in helrm.lookup(ctx, plan, rk, cts):
+            o.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / reps
+    res = {"ms_per_lookup": round(ms, 3), "lookups_per_s": round(world * 1e3 / ms, 2), "in_cts": info.n_in_cts,
+           "n_diag": info.n_diag, "n1": info.n1, "rotation_keys": info.n_rotations, "setup_s": round(setup, 1),
+           "diag_GiB": round(info.diag_bytes / 2**30, 2), "keys_GiB": round(rk.nbytes() / 2**30, 2)}
+    for h in (rk, pk, sk, plan, T):
+        h.close()
+    ctx.close()
+    return res
 
 
 def c2_lookup(args, helrm, torch, stream, world, dev):

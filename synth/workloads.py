@@ -45,7 +45,7 @@ CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431,
 CRITEO_VOCAB_SEED = 230
 
 CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "criteo_c2", "criteo_c2_small", "llm",
-                "llm_small", "microbench")
+                "llm_small", "llm_gen", "llm_gen_small", "microbench")
 
 
 def subtable_rows(k: int, p: int) -> int:
@@ -121,6 +121,11 @@ _CONFIGS = {
     # LLM-L2 layout scaled to the Tiny ring so the oracle runs it live: 64 tokens
     # of a 1000 x 48 table (base 32, 2 digits), stride 128 -> 4 in / 4 out cts
     "llm_small": Config("llm_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    # LLM generation step: the one sampled token of the 50257 x 768
+    # table (base 256, 2 digits) -> a sparse matrix-vector product, 512 one-hot slots in,
+    # 768 out; and the same on the Tiny ring (1000 x 48, base 32) for the live oracle
+    "llm_gen": Config("llm_gen", 16, [(50, 20)], [(50, 4)], 40, 19, 1),
+    "llm_gen_small": Config("llm_gen_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
     "microbench": Config("microbench", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=1024),
 }
 
@@ -172,6 +177,11 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
             tables.append(Table(k, 16, p, rng.normal(0.0, 0.05, size=(rows, 16))))
         idx = np.array([[_zipf_index(rng, k) for k in vocab] for _ in range(B)], dtype=np.int64)
         return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))
+    if name in ("llm_gen", "llm_gen_small"):
+        V, d, p = (50257, 768, 256) if name == "llm_gen" else (1000, 48, 32)
+        w = rng.normal(0.0, 0.02, size=(subtable_rows(V, p), d))
+        idx = rng.integers(0, V, size=(B, 1)).astype(np.int64)
+        return Workload(cfg, [Table(V, d, p, w)], 0, idx, np.zeros((B, 0)))
     if name in ("llm", "llm_small"):
         V, d, p, m, stride = (50257, 768, 256, 128, 1024) if name == "llm" else (1000, 48, 32, 64, 128)
         w = rng.normal(0.0, 0.02, size=(subtable_rows(V, p), d))

@@ -244,7 +244,8 @@ def _gpu_lookup(E, w, mode=0, n1=0):
 
 @gpu
 @pytest.mark.parametrize("name,mode", [("tiny_a", 0), ("tiny_b", 0), ("uci", 0), ("uci", 1), ("tiny_b", 1),
-                                       ("llm_small", 0), ("llm_small", 1), ("criteo_c2_small", 0)])
+                                       ("llm_small", 0), ("llm_small", 1), ("criteo_c2_small", 0),
+                                       ("llm_gen_small", 0)])
 def test_lookup_bit_exact_vs_oracle(name, mode, torch_mod):
     E = env(name, torch_mod)
     w = synth.make_workload(name)
@@ -338,6 +339,22 @@ def test_criteo_c2_full_size_plan_and_decryption(torch_mod):
     y = lk.gather(lay, w.indices[0])
     z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
     assert np.abs(z[: lay.M] - y).max() < 1e-3
+
+
+@gpu
+def test_llm_gen_full_size_decryption(torch_mod):
+    """LLM generation step at full size (one token of the 50257 x 768 GPT-2
+    table): plan counts and the decrypted 768-dim embedding
+    against the float64 gather (bit-exact check: llm_gen_small)."""
+    E = env("llm", torch_mod)
+    w = synth.make_workload("llm_gen")
+    plan, sk, outs = _gpu_lookup(E, w)
+    info = plan.info()
+    assert (info.n_in_cts, info.n_out_cts, info.n_diag, info.n1, info.n2_max, info.n_rotations, info.mbar) == (
+        1, 1, 1024, 32, 32, 67, 1024)
+    lay = lk.layout(w)
+    z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
+    assert np.abs(z[: lay.M] - lk.gather(lay, w.indices[0])).max() < 1e-3
 
 
 @gpu

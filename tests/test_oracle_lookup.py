@@ -273,3 +273,26 @@ def test_criteo_c2_full_size_plan_counts():
     plan = lk.make_plan(lay, n, 23)
     assert (plan.C, plan.O, len(plan.u_slots), plan.n1, plan.n2, plan.n_diag) == (2, 1, 1024, 32, [16], 1024)
     assert len(plan.rotation_amounts(types.SimpleNamespace(n=n))) == 52
+
+
+def test_llm_gen_small_lookup_decrypts_to_gather():
+    """LLM generation step (one sampled token looked up per
+    step, a sparse matrix-vector product) on the Tiny ring: 1000 x 48 table,
+    base 32 -> 64 one-hot slots, 64 diagonals; decrypts to the gather."""
+    w = synth.make_workload("llm_gen_small")
+    run = lk.run_config(w)
+    assert (run.plan.C, run.plan.O, run.plan.n_diag, run.plan.n1, run.plan.mbar) == (1, 1, 64, 8, 64)
+    z = core.decrypt_decode(run.P, run.sk, run.outs[0][0])
+    assert np.abs(z[: run.lay.M] - lk.gather(run.lay, w.indices[0])).max() < 1e-3
+
+
+def test_llm_gen_full_size_plan_counts():
+    """Generation step at full size (GPT-2 table, base 256: 512 slots in, 768
+    out): mbar = 1024, 1024 diagonals, n1 = 32, n2 = 32, 67 rotation keys
+    (31 babies + 31 giants + RotSum log2(n / 1024) = 5)."""
+    w = synth.make_workload("llm_gen")
+    lay = lk.layout(w)
+    n = 1 << 15
+    plan = lk.make_plan(lay, n, 19)
+    assert (plan.C, plan.O, plan.n_diag, plan.n1, plan.n2, plan.mbar) == (1, 1, 1024, 32, [32], 1024)
+    assert len(plan.rotation_amounts(types.SimpleNamespace(n=n))) == 67
