@@ -45,7 +45,7 @@ CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431,
 CRITEO_VOCAB_SEED = 230
 
 CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "criteo_c2", "criteo_c2_small", "llm",
-                "llm_small", "llm_gen", "llm_gen_small", "microbench")
+                "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "microbench")
 
 
 def subtable_rows(k: int, p: int) -> int:
@@ -106,6 +106,9 @@ class Workload:
 _CONFIGS = {
     "tiny_a": Config("tiny_a", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
     "tiny_b": Config("tiny_b", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    # edge case of the key switch: one special prime (alpha = 1) under 7 ciphertext primes,
+    # so dnum = 7 at the lookup level (the largest the library accepts), Tiny-B's table
+    "tiny_dnum7": Config("tiny_dnum7", 12, [(40, 1), (30, 6)], [(40, 1)], 30, 6, 1),
     "uci": Config("uci", 14, [(40, 8)], [(40, 2)], 36, 7, 1),
     "criteo": Config("criteo", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
     "criteo_b64": Config("criteo_b64", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=64),
@@ -147,7 +150,7 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
         cfg.batch = batch
     rng = np.random.default_rng(cfg.seed)
     B = cfg.batch
-    if name in ("tiny_a", "tiny_b"):
+    if name in ("tiny_a", "tiny_b", "tiny_dnum7"):
         if name == "tiny_a":
             w = rng.uniform(-1.0, 1.0, size=(256, 16))
             tables = [Table(256, 16, 0, w)]

@@ -245,7 +245,7 @@ def _gpu_lookup(E, w, mode=0, n1=0):
 @gpu
 @pytest.mark.parametrize("name,mode", [("tiny_a", 0), ("tiny_b", 0), ("uci", 0), ("uci", 1), ("tiny_b", 1),
                                        ("llm_small", 0), ("llm_small", 1), ("criteo_c2_small", 0),
-                                       ("llm_gen_small", 0)])
+                                       ("llm_gen_small", 0), ("tiny_dnum7", 0), ("tiny_dnum7", 1)])
 def test_lookup_bit_exact_vs_oracle(name, mode, torch_mod):
     E = env(name, torch_mod)
     w = synth.make_workload(name)
@@ -392,7 +392,8 @@ def _encrypt_batch(E, w, T, pk, info):
 
 
 @gpu
-@pytest.mark.parametrize("name,batch", [("tiny_b", 3), ("uci", 3), ("llm_small", 2), ("criteo_c2_small", 2)])
+@pytest.mark.parametrize("name,batch", [("tiny_b", 3), ("uci", 3), ("llm_small", 2), ("criteo_c2_small", 2),
+                                        ("tiny_dnum7", 3)])
 def test_batched_lookup_bit_exact_vs_oracle(name, batch, torch_mod):
     """One helrm_lookup call over `batch` queries (the query-batched engine:
     shared key and plaintext reads, query loops inside the key-switch and MAC

@@ -296,3 +296,14 @@ def test_llm_gen_full_size_plan_counts():
     plan = lk.make_plan(lay, n, 19)
     assert (plan.C, plan.O, plan.n_diag, plan.n1, plan.n2, plan.mbar) == (1, 1, 1024, 32, [32], 1024)
     assert len(plan.rotation_amounts(types.SimpleNamespace(n=n))) == 67
+
+
+def test_tiny_dnum7_lookup_decrypts_to_gather():
+    """Key-switch edge case: alpha = K = 1 under 7 ciphertext primes gives
+    dnum = 7 digits at the lookup level (the library's maximum); the lookup
+    still decrypts to the gather."""
+    w = synth.make_workload("tiny_dnum7")
+    run = lk.run_config(w)
+    assert run.P.dnum(w.config.level) == 7
+    z = core.decrypt_decode(run.P, run.sk, run.outs[0][0])
+    assert np.abs(z[: run.lay.M] - lk.gather(run.lay, w.indices[0])).max() < 1e-3
