@@ -1900,7 +1900,8 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     bm.out_stride = 2 * nlN;
     bm.half = nlN;
     bm.bytes = 8.0 * N * nl * (dn + 2.0 + kmf.n * 2.0 * dn + ml.n_u + 2.0 * n_out);
-    macs_done = launch_baby_mac(c->dc(), kmf, bm, mqp);
+    static const int fused_mode = getenv("HELRM_FUSED_BM") ? atoi(getenv("HELRM_FUSED_BM")) : 0;
+    macs_done = fused_mode == 2 ? launch_baby_mac_bulk(c->dc(), kmf, bm, mqp) : launch_baby_mac(c->dc(), kmf, bm, mqp);
     need(macs_done, HELRM_ERR_CONFIG, "fused baby/MAC kernel does not apply");   // guarded by `fused`
   }
   // output blocks sharing every plaintext (LLM layout L2): dense (giant, baby slot) table of

@@ -388,6 +388,8 @@ struct BlockMacArgs {
 };
 bool launch_block_mac(const DevCtx& c, const BlockMacArgs& a, const LimbMap& map);
 bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map);
+// the same fused step fed by bulk async copies (kernels_mac_bulk.cu; HELRM_FUSED_BM=2)
+bool launch_baby_mac_bulk(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map);
 
 // D20 L3 work list.  Giants are packed kGiantPack at a time: a term is one
 // baby pair x = (x0, x1) with the plaintext u of each giant of the pack that

@@ -594,6 +594,8 @@ def test_lookup_error_and_degenerate_cases(torch_mod):
     ({"HELRM_MAC_BULK": "0"}, "test_llm_full_size_plan_and_decryption"),
     ({"HELRM_PIPE": "1", "HELRM_MACCH": "1", "HELRM_NTTCH": "4"},                  # pipelined giant steps
      "test_criteo_full_size_matches_oracle_golden"),
+    ({"HELRM_FUSED_BM": "2"}, "test_criteo_full_size_matches_oracle_golden"),     # fused baby + MAC (bulk)
+    ({"HELRM_FUSED_BM": "2"}, "test_lookup_bit_exact_vs_oracle"),
     ({"HELRM_PDL": "1"}, "test_criteo_full_size_matches_oracle_golden"),          # programmatic dependent launch
     ({"HELRM_PDL": "1"}, "test_lookup_bit_exact_vs_oracle"),
 ])
