@@ -387,6 +387,8 @@ def run_gpu(args, world, rank, local):
         secondary["criteo_c2_b1"] = c2_lookup(args, helrm, torch, stream, world, dev)
         # LLM generation step: one sampled token's embedding, 768 dims
         secondary["llm_gen_token"] = shape_lookup(helrm, torch, stream, world, dev, "llm_gen")
+        # a dense 512 -> 256 linear layer on the same engine, Criteo parameters
+        secondary["mlp_512x256"] = shape_lookup(helrm, torch, stream, world, dev, "mlp_512x256")
 
     return {
         "value": value, "ms": ms / args.steps, "launches": launches, "clocks": clk.summary(),

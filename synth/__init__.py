@@ -16,6 +16,7 @@ from .workloads import (  # noqa: F401
     Table,
     Workload,
     config_by_name,
+    dense_inputs,
     make_workload,
     microbench_seed,
     subtable_rows,

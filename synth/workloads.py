@@ -45,7 +45,8 @@ CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431,
 CRITEO_VOCAB_SEED = 230
 
 CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "criteo_c2", "criteo_c2_small", "llm",
-                "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "criteo_c17", "microbench")
+                "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "criteo_c17", "mlp_small", "mlp_512x256",
+                "microbench")
 
 
 def subtable_rows(k: int, p: int) -> int:
@@ -132,6 +133,12 @@ _CONFIGS = {
     # 768 out; and the same on the Tiny ring (1000 x 48, base 32) for the live oracle
     "llm_gen": Config("llm_gen", 16, [(50, 20)], [(50, 4)], 40, 19, 1),
     "llm_gen_small": Config("llm_gen_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    # a dense linear layer on the same BSGS engine (fully connected layers by
+    # pre-rotated diagonals and baby/giant steps; the DLRM's bottom/top MLPs, :654): the
+    # "table" is the weight matrix W (in x out, one row per input slot), the input a dense
+    # encrypted vector x, the output W^T x
+    "mlp_small": Config("mlp_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    "mlp_512x256": Config("mlp_512x256", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
     "microbench": Config("microbench", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=1024),
 }
 
@@ -188,6 +195,10 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
         w = rng.normal(0.0, 0.02, size=(subtable_rows(V, p), d))
         idx = rng.integers(0, V, size=(B, 1)).astype(np.int64)
         return Workload(cfg, [Table(V, d, p, w)], 0, idx, np.zeros((B, 0)))
+    if name in ("mlp_small", "mlp_512x256"):
+        fan_in, fan_out = (64, 32) if name == "mlp_small" else (512, 256)
+        w = rng.normal(0.0, 1.0 / np.sqrt(fan_in), size=(fan_in, fan_out))
+        return Workload(cfg, [Table(fan_in, fan_out, 0, w)], 0, np.zeros((B, 1), dtype=np.int64), np.zeros((B, 0)))
     if name in ("llm", "llm_small"):
         V, d, p, m, stride = (50257, 768, 256, 128, 1024) if name == "llm" else (1000, 48, 32, 64, 128)
         w = rng.normal(0.0, 0.02, size=(subtable_rows(V, p), d))
@@ -200,3 +211,13 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
 def microbench_seed() -> int:
     """Seed of the microbench's uniform limbs (D9 purpose 9 streams)."""
     return _CONFIGS["microbench"].seed
+
+
+def dense_inputs(name: str, batch: int = 1) -> np.ndarray:
+    """Encrypted input vectors of the dense linear-layer configs (mlp_*):
+    U[-1, 1], one row per query, from the config seed's second stream (the
+    weights use the first)."""
+    cfg = config_by_name(name)
+    fan_in = 64 if name == "mlp_small" else 512
+    rng = np.random.default_rng([cfg.seed, 2])
+    return rng.uniform(-1.0, 1.0, size=(batch, fan_in))

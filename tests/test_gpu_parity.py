@@ -358,6 +358,34 @@ def test_llm_gen_full_size_decryption(torch_mod):
 
 
 @gpu
+@pytest.mark.parametrize("name", ["mlp_small", "mlp_512x256"])
+def test_dense_linear_layer(name, torch_mod):
+    """A dense linear layer on the lookup engine: the weight
+    matrix as the table, a dense encrypted input.  mlp_small: the output
+    ciphertext equals the oracle's bit for bit; both: decrypts to x W."""
+    E = env(name, torch_mod)
+    w = synth.make_workload(name)
+    x = synth.dense_inputs(name)[0]
+    cfg, h = w.config, E.h
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    plan = h.plan_create(E.ctx, T, cfg.level)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N), cfg.seed)
+    z = np.zeros(cfg.n_slots)
+    z[: len(x)] = x
+    ct = h.encrypt(E.ctx, pk, z, cfg.level, cfg.seed << 20)
+    out = h.lookup(E.ctx, plan, rk, [ct])
+    want = x @ w.tables[0].weights
+    y = h.decrypt_decode(E.ctx, sk, out[0])
+    assert np.abs(y[: len(want)] - want).max() < 1e-3
+    if name == "mlp_small":
+        import test_oracle_lookup as tol
+        _, _, P, _, _, _, ref = tol._dense_layer_run(name)
+        assert np.array_equal(h.ct_export(E.ctx, out[0]), core.ct_to_coeff(P, ref[0]))
+
+
+@gpu
 @pytest.mark.parametrize("name", ["uci", "llm_small", "criteo_c2_small"])
 def test_lookup_dist_single_rank_matches_lookup(name, torch_mod):
     """helrm_lookup_dist on a 1-rank NCCL communicator (the only GPU a gpurun

@@ -307,3 +307,30 @@ def test_tiny_dnum7_lookup_decrypts_to_gather():
     assert run.P.dnum(w.config.level) == 7
     z = core.decrypt_decode(run.P, run.sk, run.outs[0][0])
     assert np.abs(z[: run.lay.M] - lk.gather(run.lay, w.indices[0])).max() < 1e-3
+
+
+def _dense_layer_run(name):
+    w = synth.make_workload(name)
+    x = synth.dense_inputs(name)[0]
+    cfg = w.config
+    P = core.params_from_config(cfg)
+    lay = lk.layout(w)
+    plan = lk.make_plan(lay, P.n, cfg.level)
+    sk = core.sk_gen(P, cfg.seed)
+    pk = core.pk_gen(P, sk, cfg.seed)
+    rk = core.rotkeys_gen(P, sk, plan.galois(P), cfg.seed)
+    z = np.zeros(P.n)
+    z[: len(x)] = x
+    ct = core.encrypt(P, pk, z, cfg.level, cfg.seed << 20)
+    out = lk.lookup(P, plan, lk.encode_plan(P, plan), rk, [ct])
+    return w, x, P, plan, sk, ct, out
+
+
+def test_dense_linear_layer_on_the_lookup_engine():
+    """fully connected layers run on the same diagonal/BSGS
+    machinery.  With the weight matrix W (64 x 32) as the "table" and a dense
+    encrypted x, the lookup decrypts to the matrix-vector product x W."""
+    w, x, P, plan, sk, ct, out = _dense_layer_run("mlp_small")
+    assert (plan.n_diag, plan.n1, plan.mbar) == (32, 8, 32)
+    y = core.decrypt_decode(P, sk, out[0])
+    assert np.abs(y[:32] - x @ w.tables[0].weights).max() < 1e-3
