@@ -387,6 +387,8 @@ def run_gpu(args, world, rank, local):
         secondary["criteo_c2_b1"] = c2_lookup(args, helrm, torch, stream, world, dev)
         # LLM generation step: one sampled token's embedding, 768 dims
         secondary["llm_gen_token"] = shape_lookup(helrm, torch, stream, world, dev, "llm_gen")
+        # the Criteo lookup at input level 4, where Orion places it
+        secondary["criteo_l4_b1"] = shape_lookup(helrm, torch, stream, world, dev, "criteo_l4", reps=10)
         # a dense 512 -> 256 linear layer on the same engine, Criteo parameters
         secondary["mlp_512x256"] = shape_lookup(helrm, torch, stream, world, dev, "mlp_512x256")
 

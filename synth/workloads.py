@@ -45,8 +45,8 @@ CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431,
 CRITEO_VOCAB_SEED = 230
 
 CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "criteo_c2", "criteo_c2_small", "llm",
-                "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "criteo_c17", "mlp_small", "mlp_512x256",
-                "microbench")
+                "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "criteo_c17", "criteo_l4", "mlp_small",
+                "mlp_512x256", "microbench")
 
 
 def subtable_rows(k: int, p: int) -> int:
@@ -113,6 +113,8 @@ _CONFIGS = {
     "uci": Config("uci", 14, [(40, 8)], [(40, 2)], 36, 7, 1),
     "criteo": Config("criteo", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
     "criteo_b64": Config("criteo_b64", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=64),
+    # the lookup where Orion places it in the ReLU DLRM: input level 4, same tables
+    "criteo_l4": Config("criteo_l4", 16, [(50, 24)], [(50, 4)], 40, 4, 1),
     # a less compressed Criteo model (PAPER.md:459-463, Table 2 threshold 5e4; :470): tables
     # with vocab <= 5e4 stay one-hot, the rest are digit-decomposed in base 1024 ->
     # 47,798 input slots = 2 input cts and 1024 diagonals (the paper: 47,759 slots,
@@ -175,7 +177,7 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
         idx = np.array([[rng.integers(0, k) for k in vocab] for _ in range(B)], dtype=np.int64)
         dense = rng.uniform(0.0, 1.0, size=(B, 13))
         return Workload(cfg, tables, 13, idx, dense)
-    if name in ("criteo", "criteo_b64"):
+    if name in ("criteo", "criteo_b64", "criteo_l4"):
         tables = [Table(k, 16, 64, rng.normal(0.0, 0.05, size=(subtable_rows(k, 64), 16))) for k in CRITEO_VOCAB]
         idx = np.array([[_zipf_index(rng, k) for k in CRITEO_VOCAB] for _ in range(B)], dtype=np.int64)
         return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))

@@ -358,6 +358,21 @@ def test_llm_gen_full_size_decryption(torch_mod):
 
 
 @gpu
+def test_criteo_level4_decryption(torch_mod):
+    """The Criteo lookup at input level 4, where Orion places the embedding in
+    the ReLU DLRM: 5 + 4 limbs, dnum 2; the plan counts match
+    the level-23 plan and the output decrypts to the float64 gather."""
+    E = env("criteo", torch_mod)
+    w = synth.make_workload("criteo_l4")
+    plan, sk, outs = _gpu_lookup(E, w)
+    info = plan.info()
+    assert (info.n_diag, info.n1, info.n2_max, info.n_rotations) == (512, 32, 16, 52)
+    lay = lk.layout(w)
+    z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
+    assert np.abs(z[: lay.M] - lk.gather(lay, w.indices[0])).max() < 1e-3
+
+
+@gpu
 @pytest.mark.parametrize("name", ["mlp_small", "mlp_512x256"])
 def test_dense_linear_layer(name, torch_mod):
     """A dense linear layer on the lookup engine: the weight
