@@ -373,6 +373,40 @@ def test_criteo_level4_decryption(torch_mod):
 
 
 @gpu
+def test_dense_sparse_extraction_matches_oracle(torch_mod):
+    """PAPER.md:654 dense/sparse extraction as single-diagonal plans on the
+    engine (tests/test_oracle_lookup.py builds them): the GPU outputs equal the
+    oracle's bit for bit and decrypt to the two parts of the query vector."""
+    import test_oracle_lookup as tol
+    E = env("uci", torch_mod)
+    w = synth.make_workload("uci")
+    lay, dense, sparse = tol._extraction_workloads(w)
+    h, cfg = E.h, w.config
+    x = lk.encode_query(lay, w.indices[0], w.dense[0])
+    P = core.params_from_config(cfg)
+    sk_ref = core.sk_gen(P, cfg.seed)
+    pk_ref = core.pk_gen(P, sk_ref, cfg.seed)
+    z = np.zeros(P.n)
+    z[: len(x)] = x
+    ct_ref = core.encrypt(P, pk_ref, z, cfg.level, cfg.seed << 20)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    ct = h.encrypt(E.ctx, pk, z, cfg.level, cfg.seed << 20)
+    for wl, want in ((dense, x[: w.n_dense]), (sparse, x[w.n_dense:])):
+        T = h.tables_create(E.P, wl.tables, wl.n_dense)
+        plan = h.plan_create(E.ctx, T, cfg.level)
+        assert plan.info().n_diag == 1
+        rk = h.rotkeys_gen(E.ctx, sk, plan.galois(cfg.N), cfg.seed)
+        out = h.lookup(E.ctx, plan, rk, [ct])
+        ref_plan = lk.make_plan(lk.layout(wl), P.n, cfg.level)
+        rk_ref = core.rotkeys_gen(P, sk_ref, ref_plan.galois(P), cfg.seed)
+        ref = lk.lookup(P, ref_plan, lk.encode_plan(P, ref_plan), rk_ref, [ct_ref])
+        assert np.array_equal(h.ct_export(E.ctx, out[0]), core.ct_to_coeff(P, ref[0]))
+        got = h.decrypt_decode(E.ctx, sk, out[0])
+        assert np.abs(got[: len(want)] - want).max() < 1e-3
+
+
+@gpu
 @pytest.mark.parametrize("name", ["mlp_small", "mlp_512x256"])
 def test_dense_linear_layer(name, torch_mod):
     """A dense linear layer on the lookup engine: the weight

@@ -334,3 +334,38 @@ def test_dense_linear_layer_on_the_lookup_engine():
     assert (plan.n_diag, plan.n1, plan.mbar) == (32, 8, 32)
     y = core.decrypt_decode(P, sk, out[0])
     assert np.abs(y[:32] - x @ w.tables[0].weights).max() < 1e-3
+
+
+def _extraction_workloads(w):
+    """the server splits the client's [dense || one-hot] vector
+    into a dense and a sparse ciphertext.  Mask + rotate is a linear map with a
+    single non-zero diagonal, so it runs on the same engine: identity "tables"
+    reading slots [0, n_dense) and [n_dense, K) and writing from slot 0."""
+    import dataclasses
+    lay = lk.layout(w)
+    nd, ns = w.n_dense, lay.K - w.n_dense
+    dense = dataclasses.replace(w, tables=[synth.Table(nd, nd, 0, np.eye(nd), in_off=0, out_off=0)], n_dense=0)
+    sparse = dataclasses.replace(w, tables=[synth.Table(ns, ns, 0, np.eye(ns), in_off=nd, out_off=0)], n_dense=0)
+    return lay, dense, sparse
+
+
+def test_dense_sparse_extraction_on_the_lookup_engine():
+    """UCI query: the dense extraction returns the 13 dense features, the
+    sparse extraction the one-hot segments moved to slot 0 (each a plan with
+    one non-zero diagonal)."""
+    w = synth.make_workload("uci")
+    lay, dense, sparse = _extraction_workloads(w)
+    x = lk.encode_query(lay, w.indices[0], w.dense[0])
+    P = core.params_from_config(w.config)
+    sk = core.sk_gen(P, w.config.seed)
+    pk = core.pk_gen(P, sk, w.config.seed)
+    z = np.zeros(P.n)
+    z[: len(x)] = x
+    ct = core.encrypt(P, pk, z, w.config.level, w.config.seed << 20)
+    for wl, want in ((dense, x[: w.n_dense]), (sparse, x[w.n_dense:])):
+        plan = lk.make_plan(lk.layout(wl), P.n, w.config.level)
+        assert plan.n_diag == 1
+        rk = core.rotkeys_gen(P, sk, plan.galois(P), w.config.seed)
+        out = lk.lookup(P, plan, lk.encode_plan(P, plan), rk, [ct])
+        got = core.decrypt_decode(P, sk, out[0])
+        assert np.abs(got[: len(want)] - want).max() < 1e-3
