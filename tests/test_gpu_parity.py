@@ -435,7 +435,7 @@ def test_dense_linear_layer(name, torch_mod):
 
 
 @gpu
-@pytest.mark.parametrize("name", ["uci", "llm_small", "criteo_c2_small"])
+@pytest.mark.parametrize("name", ["uci", "llm_small", "criteo_c2_small", "llm_gen_small", "tiny_dnum7"])
 def test_lookup_dist_single_rank_matches_lookup(name, torch_mod):
     """helrm_lookup_dist on a 1-rank NCCL communicator (the only GPU a gpurun
     box has) runs the partitioned code path (broadcast, partial accumulators,
@@ -470,7 +470,7 @@ def _encrypt_batch(E, w, T, pk, info):
 
 @gpu
 @pytest.mark.parametrize("name,batch", [("tiny_b", 3), ("uci", 3), ("llm_small", 2), ("criteo_c2_small", 2),
-                                        ("tiny_dnum7", 3)])
+                                        ("tiny_dnum7", 3), ("llm_gen_small", 3)])
 def test_batched_lookup_bit_exact_vs_oracle(name, batch, torch_mod):
     """One helrm_lookup call over `batch` queries (the query-batched engine:
     shared key and plaintext reads, query loops inside the key-switch and MAC
@@ -528,7 +528,7 @@ def test_criteo_batched_equals_single(torch_mod):
 
 
 @gpu
-@pytest.mark.parametrize("name", ["uci", "llm_small"])
+@pytest.mark.parametrize("name", ["uci", "llm_small", "criteo_c2_small", "llm_gen_small"])
 def test_lookup_host_matches_lookup(name, torch_mod):
     """helrm_lookup_host (host coefficient-form buffers, copies pipelined
     against the lookups, CUDA-graph replay from the second query) equals
