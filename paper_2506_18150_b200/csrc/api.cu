@@ -1772,6 +1772,9 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     km.out_half = nlN;
     km.nq = (int)C;
     km.qk = std::min((int)C, 4);
+    // many input cts: their CTAs of one (tile, limb) run side by side and share the key tiles in L2
+    static const int zf = getenv("HELRM_KM_ZFAST") ? atoi(getenv("HELRM_KM_ZFAST")) : 1;
+    km.zfast = zf && C > 4 ? 1 : 0;
     km.dq = dn * nlN;
     km.cq = 2 * nqN;
     km.oq = nb * 2 * nlN;

@@ -344,6 +344,7 @@ struct KipMulti {
   // out[j] + q oq; a CTA stages qk queries' tiles and applies each key value to all
   int nq = 1, qk = 1;
   size_t dq = 0, cq = 0, oq = 0;
+  int zfast = 0;                   // query groups fastest in the grid (their key reads meet in L2)
   const uint64_t* own = nullptr;   // as KipArgs::own (the c1 of each query)
   size_t ownq = 0;
   int alpha = 1;

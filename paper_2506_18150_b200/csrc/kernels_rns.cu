@@ -407,13 +407,15 @@ __global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ Ki
   extern __shared__ double shd[];
   const int l = blockIdx.y;
   const uint32_t n = N / 2, tile = blockDim.x;
-  const uint32_t p0 = blockIdx.x * tile, half = p0 >= n ? n : 0;
+  const uint32_t zq = (uint32_t)((a.nq + a.qk - 1) / a.qk);
+  const uint32_t tix = a.zfast ? blockIdx.x / zq : blockIdx.x, zix = a.zfast ? blockIdx.x % zq : blockIdx.z;
+  const uint32_t p0 = tix * tile, half = p0 >= n ? n : 0;
   const uint32_t span = tile + a.max_rot;
   const uint32_t chain = map.pr[l];
   const PrimeDev& P = primes[chain];
   const double q = P.qd, qi = P.qinv;
   const bool has_c0 = l <= (int)a.level;
-  const int q0 = blockIdx.z * a.qk, nqc = min(a.qk, a.nq - q0);   // this CTA's queries
+  const int q0 = (int)zix * a.qk, nqc = min(a.qk, a.nq - q0);   // this CTA's queries
   const int slab = (DNUM + 1) * span;                              // doubles per staged query
   // stage D_k (and c0) tiles + halo of every query of the CTA
   const int kown = (a.own && has_c0) ? l / a.alpha : -1;   // digit whose own limb this row is
@@ -1049,7 +1051,8 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
   if (smem > 48 * 1024) HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  launch_pdl(kern, dim3(dim3(c.N / tile, map.n, (unsigned)zq)), dim3(tile), smem, c.stream, a, c.primes, map, c.N);
+  const dim3 grid = a.zfast ? dim3(c.N / tile * (unsigned)zq, map.n, 1) : dim3(c.N / tile, map.n, (unsigned)zq);
+  launch_pdl(kern, grid, dim3(tile), smem, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }

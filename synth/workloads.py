@@ -45,7 +45,7 @@ CRITEO_VOCAB = [3, 6970, 2744503, 9007069, 1240, 3227764, 8408764, 2256022, 431,
 CRITEO_VOCAB_SEED = 230
 
 CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "criteo_c2", "criteo_c2_small", "llm",
-                "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "criteo_c17", "criteo_l4", "mlp_small",
+                "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "criteo_c17", "criteo_c9_small", "criteo_l4", "mlp_small",
                 "mlp_512x256", "microbench")
 
 
@@ -123,6 +123,9 @@ _CONFIGS = {
     # the same shape scaled to the Tiny ring so the oracle runs it live: vocab sqrt(k),
     # one-hot below 1000 rows, base 32 above -> 2,944 slots = 2 input cts of 2048
     "criteo_c2_small": Config("criteo_c2_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    # many input cts on the Tiny ring (every sqrt-vocab table one-hot: 16,529 slots = 9 cts of
+    # 2048) so the oracle checks the many-ct paths live
+    "criteo_c9_small": Config("criteo_c9_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
     # the 10^2x model (569,545 slots, 18 input cts): one-hot up to 2.2e5
     # rows, base 1024 above -> 535,963 slots = 17 input cts, 8704 diagonals (119 GiB)
     "criteo_c17": Config("criteo_c17", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
@@ -181,10 +184,11 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
         tables = [Table(k, 16, 64, rng.normal(0.0, 0.05, size=(subtable_rows(k, 64), 16))) for k in CRITEO_VOCAB]
         idx = np.array([[_zipf_index(rng, k) for k in CRITEO_VOCAB] for _ in range(B)], dtype=np.int64)
         return Workload(cfg, tables, 0, idx, np.zeros((B, 0)))
-    if name in ("criteo_c2", "criteo_c2_small", "criteo_c17"):
-        small = name == "criteo_c2_small"
+    if name in ("criteo_c2", "criteo_c2_small", "criteo_c17", "criteo_c9_small"):
+        small = name in ("criteo_c2_small", "criteo_c9_small")
         vocab = [max(2, int(round(k ** 0.5))) for k in CRITEO_VOCAB] if small else CRITEO_VOCAB
-        thr, base = (1000, 32) if small else (220000, 1024) if name == "criteo_c17" else (50000, 1024)
+        thr, base = {"criteo_c2_small": (1000, 32), "criteo_c9_small": (3001, 32), "criteo_c17": (220000, 1024),
+                     "criteo_c2": (50000, 1024)}[name]
         tables = []
         for k in vocab:
             p = 0 if k <= thr else base

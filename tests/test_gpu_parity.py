@@ -245,7 +245,8 @@ def _gpu_lookup(E, w, mode=0, n1=0):
 @gpu
 @pytest.mark.parametrize("name,mode", [("tiny_a", 0), ("tiny_b", 0), ("uci", 0), ("uci", 1), ("tiny_b", 1),
                                        ("llm_small", 0), ("llm_small", 1), ("criteo_c2_small", 0),
-                                       ("llm_gen_small", 0), ("tiny_dnum7", 0), ("tiny_dnum7", 1)])
+                                       ("llm_gen_small", 0), ("tiny_dnum7", 0), ("tiny_dnum7", 1),
+                                       ("criteo_c9_small", 0)])
 def test_lookup_bit_exact_vs_oracle(name, mode, torch_mod):
     E = env(name, torch_mod)
     w = synth.make_workload(name)
