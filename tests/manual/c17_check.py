@@ -2,12 +2,12 @@
 535,963 one-hot slots, 8704 diagonals, ~119 GiB of QP-NTT plaintexts in HBM)
 on one B200: plan counts, decryption against the float64 gather and the
 batch-1 lookup time.  Too large for the test suite's shared process; run
-alone:  python tools/c17_check.py > profiles/<round>_c17.txt"""
+alone:  python tests/manual/c17_check.py > profiles/<round>_c17.txt"""
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 

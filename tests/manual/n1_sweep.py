@@ -1,5 +1,8 @@
+"""BSGS split sweep (n1 = 32 / 64 / 16) of the Criteo batch-1 lookup on one B200: time and the
+decrypted output against the float64 gather (test infrastructure: the gather is the oracle's).
+Run alone:  python tests/manual/n1_sweep.py"""
 import os, sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, numpy as np
 import synth
 from paper_2506_18150_b200 import helrm
