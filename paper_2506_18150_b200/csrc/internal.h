@@ -268,8 +268,6 @@ void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const 
 void launch_dform(const DevCtx& c, uint64_t* x, size_t n, const LimbMap& map, int dir);
 void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const LimbMap& map, uint32_t rot,
                       int accumulate);
-void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
-                      size_t os, int G, const LimbMap& map, const uint64_t* s, const uint64_t* sp);
 // out[l] = in[l] mod q_l for in < 2^64 (after a uint64 sum all-reduce)
 void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map);
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,

@@ -178,20 +178,6 @@ __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict_
   }
 }
 
-// out[g][l] = (y[g][l] - t[g][l]) * s[l] mod q_l  (ModDown / rescale finish), z = g
-__global__ void k_sub_scale(const uint64_t* __restrict__ y, size_t ys, const uint64_t* __restrict__ t, size_t ts,
-                            uint64_t* __restrict__ out, size_t os, const PrimeDev* __restrict__ primes,
-                            const __grid_constant__ LimbMap map, uint32_t N, const uint64_t* __restrict__ s,
-                            const uint64_t* __restrict__ sp) {
-  pdl_wait_trigger();
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int l = blockIdx.y, g = blockIdx.z;
-  if (i >= N) return;
-  const uint64_t q = primes[map.pr[l]].rc.q;
-  const size_t o = (size_t)l * N + i;
-  out[g * os + o] = shoup(sub_mod(y[g * ys + o], t[g * ts + o], q), s[l], sp[l], q);
-}
-
 // D17: r = ((x + h) mod q_l) - h, then r mod q_i for the remaining limbs; z = polynomial
 __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint64_t ql, uint64_t* __restrict__ out,
                                size_t os, const PrimeDev* __restrict__ primes, const __grid_constant__ LimbMap map,
@@ -984,14 +970,6 @@ void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows,
                                                                                          : k_conv_rows<8, 2>;
   (void)out_map;
   launch_pdl(kern, dim3(dim3(c.N / (256 * pt), G * ncv)), dim3(256), 0, c.stream, tab, ncv, rows, y, y_stride, out, out_stride_g, out_stride_k, c.N);
-  (*c.launches)++;
-  HCUDA(cudaGetLastError());
-}
-
-void launch_sub_scale(const DevCtx& c, const uint64_t* y, size_t ys, const uint64_t* t, size_t ts, uint64_t* out,
-                      size_t os, int G, const LimbMap& map, const uint64_t* s, const uint64_t* sp) {
-  ProfScope ps_(c, "sub_scale", 24.0 * c.N * map.n * G);
-  launch_pdl(k_sub_scale, dim3(dim3((c.N + kT - 1) / kT, map.n, G)), dim3(kT), 0, c.stream, y, ys, t, ts, out, os, c.primes, map, c.N, s, sp);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
