@@ -699,13 +699,24 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
-    world, rank, local = dist_setup(args.gpus)
-    r = run_gpu(args, world, rank, local)
-    cpu = None
-    if rank == 0 and world == 1 and not args.skip_cpu_baseline:
-        s, sample, cores, parts = oracle_lookup_seconds()
-        cpu = {"value": round(1.0 / s, 6), "unit": "lookups/s", "cores": cores, "kind": "oracle", "sample": sample,
-               "parts_s": parts}
+    # stdout carries exactly the one JSON line: everything else written to fd 1 while the run
+    # goes on (NCCL's "NCCL version ..." banner at communicator init, library prints) is sent
+    # to stderr at the file-descriptor level
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        world, rank, local = dist_setup(args.gpus)
+        r = run_gpu(args, world, rank, local)
+        cpu = None
+        if rank == 0 and world == 1 and not args.skip_cpu_baseline:
+            s, sample, cores, parts = oracle_lookup_seconds()
+            cpu = {"value": round(1.0 / s, 6), "unit": "lookups/s", "cores": cores, "kind": "oracle",
+                   "sample": sample, "parts_s": parts}
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved_stdout, 1)
+        os.close(saved_stdout)
     if rank == 0:
         info = r["info"]
         line = {"metric": metric, "value": round(r["value"], 3), "unit": "lookups/s", "n_gpus": world,
