@@ -254,7 +254,11 @@ def roofline_from_stats(stats, steps, cfg):
                     "share_of_step": round(ms / tot, 3),
                     "algorithmic_bytes_per_limb": 16 * N,
                     "traffic": tr.get("ntt_fwd_bytes_per_limb"),
-                    "traffic_unit": "dram bytes per limb transform (ncu, profiles/ncu_traffic.json)"})
+                    "traffic_unit": "dram bytes per limb transform (ncu, profiles/ncu_traffic.json)",
+                    # ncu sm__pipe_fp64_cycles_active (time-weighted): the pipe is busier than frac
+                    # because reductions and conversions add ~2.75 FP64 ops per 8-op butterfly
+                    "fp64_pipe_frac": tr.get("ntt_fwd_fp64_pipe_frac"),
+                    "fp64_pipe_frac_p1_p2": [tr.get("ntt_fwd_p1_fp64_pipe_frac"), tr.get("ntt_fwd_p2_fp64_pipe_frac")]})
     hk = {}
     for k in ("diag_mac", "kip_multi", "kip"):
         v = stats.get(k)
