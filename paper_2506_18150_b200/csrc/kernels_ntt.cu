@@ -82,34 +82,31 @@ __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double 
 //   MODE 0 (pass 1): sub-transform = column (stride 256); twiddles tw1[2^st + i].
 //   MODE 1 (pass 2): sub-transform = 256-block B; twiddles tw2[B][...]:
 //     [0, 15): phase A, 2^st - 1 + i_loc;  15 + 16 j + t: thread t's phase-B twiddle j.
-template <int SLOG, int MODE, int NB = 1>
-__global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
-                                                      const PrimeDev* __restrict__ primes,
-                                                      const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
-                                                      const uint32_t* __restrict__ grp,
-                                                      const double* __restrict__ twb,
-                                                      const uint8_t* __restrict__ tpos,
-                                                      const uint32_t* __restrict__ lidx,
-                                                      const __grid_constant__ NttEpi epi,
-                                                      const __grid_constant__ NttConvIn cv) {
-  pdl_wait_trigger();
+// The body of one CTA: tile bx of launch limb `limb`; the pass-1 -> pass-2
+// intermediate of that limb lives at scratch + slot N.  CG: scratch reads
+// bypass L1 (the fused kernel reuses scratch slots inside one launch).
+template <int SLOG, int MODE, int NB = 1, bool CG = false>
+__device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t limb, size_t slot,
+                                             const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                             const PrimeDev* __restrict__ primes, const LimbMap& map, size_t limb0,
+                                             size_t gstride, int log_n, const double* __restrict__ twb,
+                                             const uint8_t* __restrict__ tpos, const uint32_t* __restrict__ lidx,
+                                             const NttEpi& epi, const NttConvIn& cv) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
   constexpr bool P1 = MODE != 1;  // MODE 2: pass 1 on centred doubles (conversion output); MODE 3: conversion fused
-  __shared__ double sm[P1 ? kTileElems : 16 * kBlkPad];
   const int N = 1 << log_n;
-  const size_t limb = blockIdx.y;
   const size_t gl = lidx ? lidx[limb0 + limb] : limb0 + limb;
   const int pr = map.pr[gl % map.n];
   const PrimeDev& P = primes[pr];
   const double q = P.qd, qi = P.qinv;
   const double* tb = twb + (size_t)pr * (4 * (size_t)N + 1024);   // [tw1 256][tw2 N][itw1 256][itw2 N] (w, w/q)
   const size_t goff = (gl / map.n) * gstride + (gl % map.n) * (size_t)N;
-  const uint64_t* s = src + (P1 ? goff : limb * N);  // pass 1 reads the caller's limb
-  uint64_t* d = dst + (P1 ? limb * N : goff);        // pass 2 writes the caller's limb
+  const uint64_t* s = src + (P1 ? goff : slot * N);  // pass 1 reads the caller's limb
+  uint64_t* d = dst + (P1 ? slot * N : goff);        // pass 2 writes the caller's limb
   const int tid = threadIdx.x;
   const int sub = P1 ? tid % SUBS : tid / TS;
   const int t = P1 ? tid / SUBS : tid % TS;
-  const int gsub = P1 ? blockIdx.x * SUBS + sub : (int)c_ntt_grp[log_n - 12][blockIdx.x * SUBS + sub];
+  const int gsub = P1 ? bx * SUBS + sub : (int)c_ntt_grp[log_n - 12][bx * SUBS + sub];
   const double2* __restrict__ tw1 = reinterpret_cast<const double2*>(tb);
   const double2* __restrict__ twA = P1 ? tw1 : reinterpret_cast<const double2*>(tb + 512) + (size_t)gsub * 256;
   double r[kEPT];
@@ -141,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
       } else if (MODE == 0) {
         r[k] = u2d(s[(size_t)e * 256 + gsub]);
       } else {
-        r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
+        r[k] = __longlong_as_double((long long)(CG ? __ldcg(s + (size_t)gsub * 256 + e) : s[(size_t)gsub * 256 + e]));
       }
     }
   }
@@ -234,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
     // block of rank g = 16 cta + i lives at slot positions (g / stride) n +
     // (g % stride) + stride tp; for a given tp the 16 blocks are adjacent
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
-    const int i = tid % 16, g = blockIdx.x * 16 + i;   // idx % 16 == tid % 16
+    const int i = tid % 16, g = (int)bx * 16 + i;   // idx % 16 == tid % 16
     const size_t pbase = (size_t)(g >> lgs) * n + (g & (stride - 1));
     // thread tid handles tp = tid / 16 + 16 it: tp & 15 is constant per thread, so the shared
     // index advances by 256 and the global one by 16 << lgs per iteration
@@ -256,6 +253,102 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
         if (epi.accumulate) v = add_mod(v, og[it * gstep], qq);
         og[it * gstep] = v;
       }
+    }
+  }
+}
+
+template <int SLOG, int MODE, int NB = 1>
+__global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                                      const PrimeDev* __restrict__ primes,
+                                                      const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
+                                                      const uint32_t* __restrict__ grp,
+                                                      const double* __restrict__ twb,
+                                                      const uint8_t* __restrict__ tpos,
+                                                      const uint32_t* __restrict__ lidx,
+                                                      const __grid_constant__ NttEpi epi,
+                                                      const __grid_constant__ NttConvIn cv) {
+  pdl_wait_trigger();
+  __shared__ double sm[MODE != 1 ? kTileElems : 16 * kBlkPad];
+  (void)grp;
+  ntt_fwd_body<SLOG, MODE, NB>(sm, blockIdx.x, blockIdx.y, blockIdx.y, src, dst, primes, map, limb0, gstride, log_n, twb,
+                               tpos, lidx, epi, cv);
+}
+
+// Both forward passes in one persistent launch (HELRM_NTT_FUSED): CTAs claim
+// work items in a fixed order from a global counter.  Step u holds the g1
+// pass-1 tiles of limb u and the g2 pass-2 tiles of limb u - kFusedLag, so a
+// limb's pass 2 runs ~kFusedLag limbs after its pass 1, while its intermediate
+// (a ring of kFusedSlots limb slots in the scratch, 32 MiB at N = 2^16) is
+// still in L2: pass 2 reads it from L2 instead of HBM, and HBM sees one read
+// and one write per coefficient.  A pass-2 tile waits until the limb's g1
+// pass-1 tiles have signalled; a pass-1 tile reusing a slot waits until the
+// previous occupant's g2 pass-2 tiles have read it.  Every wait is on items
+// with smaller indices, all claimed by running CTAs, so the launch always
+// makes progress.  sync: [0] the work counter, [1 + L] pass-1 tiles done of
+// limb L, [1 + n + L] pass-2 tiles done (zeroed before the launch).
+// Measured slower than the two launches (Criteo b1 7.10 vs 6.86 ms, microbenchmark 1677 vs
+// 1882 GB/s; larger or smaller lags, and a static round-robin deal instead of the claim
+// counter, are slower still): the per-item claim and the waits cost more than the L2-resident
+// intermediate saves.  Off unless HELRM_NTT_FUSED=1.
+constexpr int kFusedLag = 24, kFusedSlots = 64;   // defaults (HELRM_NTT_LAG / HELRM_NTT_SLOTS)
+
+__device__ __forceinline__ void spin_until(const int* flag, int target) {
+  while (atomicAdd(const_cast<int*>(flag), 0) < target) __nanosleep(64);
+}
+
+template <int SLOG, int MODE0>
+__global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd_fused(const uint64_t* __restrict__ src,
+                                                               uint64_t* __restrict__ dst, uint64_t* __restrict__ scratch,
+                                                               const PrimeDev* __restrict__ primes,
+                                                               const __grid_constant__ LimbMap map, size_t n,
+                                                               size_t gstride, size_t dstride, int log_n,
+                                                               const double* __restrict__ twb,
+                                                               const uint8_t* __restrict__ tpos,
+                                                               const uint32_t* __restrict__ lidx,
+                                                               const __grid_constant__ NttEpi epi, int* __restrict__ sync,
+                                                               int lag, int slots) {
+  __shared__ double sm[16 * kBlkPad > kTileElems ? 16 * kBlkPad : kTileElems];
+  __shared__ int item_s;
+  const int N = 1 << log_n;
+  const int g1 = (1 << SLOG) / kEPT, g2 = (N / 256) / 16, per = g1 + g2;
+  const size_t total = (n + lag) * (size_t)per;
+  int* done1 = sync + 1;
+  int* done2 = sync + 1 + n;
+  const NttConvIn cv{};
+  for (;;) {
+    if (threadIdx.x == 0) item_s = atomicAdd(sync, 1);
+    __syncthreads();
+    const size_t item = (size_t)item_s;
+    __syncthreads();   // item_s is rewritten by the next claim
+    if (item >= total) return;
+    const size_t step = item / per;
+    const int r = (int)(item % per);
+    if (r < g1) {   // pass 1 of limb `step`
+      if (step >= n) continue;
+      const size_t L = step, slot = L % slots;
+      if (L >= (size_t)slots) {   // the slot's previous limb must have been read by its pass 2
+        if (threadIdx.x == 0) spin_until(done2 + (L - slots), g2);
+        __syncthreads();
+      }
+      ntt_fwd_body<SLOG, MODE0, 1, true>(sm, (unsigned)r, L, slot, src, scratch, primes, map, 0, gstride, log_n, twb,
+                                         tpos, lidx, epi, cv);
+      __syncthreads();   // every thread's scratch writes are issued
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(done1 + L, 1);
+      }
+    } else {        // pass 2 of limb `step - kFusedLag`
+      if (step < (size_t)lag) continue;
+      const size_t L = step - lag, slot = L % slots;
+      if (threadIdx.x == 0) {
+        spin_until(done1 + L, g1);
+        __threadfence();
+      }
+      __syncthreads();
+      ntt_fwd_body<8, 1, 1, true>(sm, (unsigned)(r - g1), L, slot, scratch, dst, primes, map, 0, dstride, log_n, twb,
+                                  tpos, lidx, epi, cv);
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(done2 + L, 1);
     }
   }
 }
@@ -442,6 +535,32 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
   *c.launches += 2;
 }
 
+static bool ntt_fwd_fused(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
+                          const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi& epi) {
+  static const int env = getenv("HELRM_NTT_FUSED") ? atoi(getenv("HELRM_NTT_FUSED")) : 0;
+  static const size_t min_limbs = getenv("HELRM_NTT_FUSED_MIN") ? (size_t)atoi(getenv("HELRM_NTT_FUSED_MIN")) : 128;
+  if (!env || c.log_n != 16 || n_total < min_limbs) return false;
+  static const int lag = getenv("HELRM_NTT_LAG") ? atoi(getenv("HELRM_NTT_LAG")) : kFusedLag;
+  static const int slots = getenv("HELRM_NTT_SLOTS") ? atoi(getenv("HELRM_NTT_SLOTS")) : kFusedSlots;
+  if (slots <= lag) return false;   // a slot must outlive its limb's lag
+  // the scratch holds the slot ring, then the work counter and per-limb flags (each stream that
+  // runs NTTs concurrently has its own scratch, so the flags are private to the launch)
+  const size_t sync_words = ((2 * n_total + 1) * sizeof(int) + 7) / 8;
+  if ((size_t)slots * c.N + sync_words > chunk_limbs(c.N) * c.N) return false;
+  int* sync = reinterpret_cast<int*>(scratch + (size_t)slots * c.N);
+  HCUDA(cudaMemsetAsync(sync, 0, (2 * n_total + 1) * sizeof(int), c.stream));
+  ProfScope ps_(c, "ntt_fwd_fused", 16.0 * c.N * n_total);
+  auto k = din ? k_ntt_fwd_fused<8, 2> : k_ntt_fwd_fused<8, 0>;
+  static int occ = 0;
+  if (!occ) HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0));
+  const unsigned grid = 148u * (unsigned)std::max(1, occ);
+  k<<<grid, kThreads, 0, c.stream>>>(src, dst, scratch, c.primes, map, n_total, ss, ds, c.log_n, c.ntt_twb, c.ntt_tpos,
+                                     lidx, epi, sync, lag, slots);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+  return true;
+}
+
 template <bool FWD>
 static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t ss, size_t ds, const double2* post, bool din, const uint32_t* lidx,
@@ -449,6 +568,7 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
   if (ss == 0) ss = (size_t)map.n * c.N;
   if (ds == 0) ds = (size_t)map.n * c.N;
   if (FWD && !cv.tab && ntt_fwd_cluster(c, src, dst, n_total, map, ss, ds, din, lidx, epi)) return;
+  if (FWD && !cv.tab && ntt_fwd_fused(c, src, dst, scratch, n_total, map, ss, ds, din, lidx, epi)) return;
   const size_t ch = chunk_limbs(c.N);
   for (size_t off = 0; off < n_total; off += ch) {
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);

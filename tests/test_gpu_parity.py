@@ -674,6 +674,8 @@ def test_lookup_error_and_degenerate_cases(torch_mod):
      "test_criteo_full_size_matches_oracle_golden"),
     ({"HELRM_FUSED_BM": "2"}, "test_criteo_full_size_matches_oracle_golden"),     # fused baby + MAC (bulk)
     ({"HELRM_FUSED_BM": "2"}, "test_lookup_bit_exact_vs_oracle"),
+    ({"HELRM_NTT_FUSED": "1"}, "test_criteo_full_size_matches_oracle_golden"),    # one-launch forward NTT
+    ({"HELRM_NTT_FUSED": "1"}, "test_microbench_ntt_full_size_sampled"),
     ({"HELRM_PDL": "1"}, "test_criteo_full_size_matches_oracle_golden"),          # programmatic dependent launch
     ({"HELRM_PDL": "1"}, "test_lookup_bit_exact_vs_oracle"),
 ])
