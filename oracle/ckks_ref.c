@@ -165,8 +165,12 @@ void or_sample_gauss(uint64_t seed, uint64_t stream, size_t N, const uint64_t* t
  * z: n = N/2 real slots (double); only non-zero slots enter the sum (adding
  * an exact zero term changes nothing).  delta: the scale (an integer <= 2^53
  * or a power of two, exactly representable).  out: int64 coefficients.
+ * tie[i] := 1 when the binary128 value of coefficient i lies within 2^-40 of
+ * a half-integer: D6 then requires an exact recomputation (the caller does it
+ * with 200-bit mpmath, oracle/textbook.py), since the rounding direction is
+ * not decided by a ~113-bit sum there.
  * Returns 0, or 2 (HELRM_ERR_CONFIG) if some |m_i| >= 2^62. */
-int or_encode(const double* z, size_t N, double delta, int64_t* out) {
+int or_encode(const double* z, size_t N, double delta, int64_t* out, uint8_t* tie) {
   size_t n = N / 2, twoN = 2 * N;
   __float128* ctab = (__float128*)malloc(sizeof(__float128) * twoN);
   size_t* e = (size_t*)malloc(sizeof(size_t) * n);
@@ -178,6 +182,7 @@ int or_encode(const double* z, size_t N, double delta, int64_t* out) {
   for (size_t j = 0; j < n; j++) if (z[j] != 0.0) nz[nnz++] = j;
   __float128 coef = 2 * (__float128)delta / (__float128)N;
   const __float128 lim = 4611686018427387904.0Q; /* 2^62 */
+  const __float128 eps = 9.094947017729282379150390625e-13Q; /* 2^-40 */
   int status = 0;
   for (size_t i = 0; i < N; i++) {
     __float128 acc = 0;
@@ -185,24 +190,12 @@ int or_encode(const double* z, size_t N, double delta, int64_t* out) {
       size_t j = nz[t];
       acc += (__float128)z[j] * ctab[(uint64_t)((unsigned long long)e[j] * i % twoN)];
     }
-    __float128 v = roundq(coef * acc); /* round half away from zero */
+    __float128 x = coef * acc;
+    tie[i] = fabsq(x - floorq(x) - 0.5Q) < eps;
+    __float128 v = roundq(x); /* round half away from zero */
     if (fabsq(v) >= lim) { status = 2; v = 0; }
     out[i] = (int64_t)v;
   }
   free(ctab); free(e); free(nz);
   return status;
-}
-
-/* Fraction distance check used by the D6 pin tests: returns the binary128
- * value of (2 Delta/N) * sum_j z_j cos(pi e_j i/N) for one coefficient i. */
-double or_encode_coeff_frac(const double* z, size_t N, double delta, size_t i) {
-  size_t n = N / 2, twoN = 2 * N;
-  __float128 acc = 0;
-  size_t ej = 1;
-  for (size_t j = 0; j < n; j++) {
-    if (z[j] != 0.0) acc += (__float128)z[j] * cosq(M_PIq * (__float128)((unsigned long long)ej * i % twoN) / (__float128)N);
-    ej = (ej * 5) % twoN;
-  }
-  __float128 v = 2 * (__float128)delta / (__float128)N * acc;
-  return (double)(v - floorq(v));
 }

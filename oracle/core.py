@@ -70,10 +70,8 @@ def lib():
             L.or_sample_uniform.argtypes = [u64, u64, u64, sz, u64p]
             L.or_sample_ternary.argtypes = [u64, u64, sz, i64p]
             L.or_sample_gauss.argtypes = [u64, u64, sz, u64p, i64p]
-            L.or_encode.argtypes = [dp, sz, ctypes.c_double, i64p]
+            L.or_encode.argtypes = [dp, sz, ctypes.c_double, i64p, ctypes.POINTER(ctypes.c_uint8)]
             L.or_encode.restype = ctypes.c_int
-            L.or_encode_coeff_frac.argtypes = [dp, sz, ctypes.c_double, sz]
-            L.or_encode_coeff_frac.restype = ctypes.c_double
             _LIB = L
     return _LIB
 
@@ -387,14 +385,25 @@ def sample_gauss(seed: int, strm: int, N: int) -> np.ndarray:
 # "Encoding": inverse FFT, scale by Delta, round to nearest integer)
 # --------------------------------------------------------------------------
 def encode(z: np.ndarray, delta: int, N: int) -> np.ndarray:
-    """D6: m_i = RHA((2 Delta/N) sum_j z_j cos(pi e_j i/N)), binary128 sums."""
+    """D6: m_i = RHA((2 Delta/N) sum_j z_j cos(pi e_j i/N)), binary128 sums;
+    a coefficient whose binary128 value lies within 2^-40 of a half-integer
+    is recomputed exactly (200-bit mpmath, textbook.encode_mp_coeff), as D6
+    requires."""
+    from . import textbook
     z = np.ascontiguousarray(z, dtype=np.float64)
     assert z.shape == (N // 2,)
     assert float(delta) == delta, "Delta must be exactly representable"
     out = np.empty(N, dtype=np.int64)
-    st = lib().or_encode(z.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), N, float(delta), _pi64(out))
+    tie = np.zeros(N, dtype=np.uint8)
+    st = lib().or_encode(z.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), N, float(delta), _pi64(out),
+                         tie.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
     if st != 0:
         raise ValueError("HELRM_ERR_CONFIG: |encoded coefficient| >= 2^62")
+    for i in np.flatnonzero(tie):
+        v = textbook.encode_mp_coeff(z, int(delta), N, int(i))
+        if abs(v) >= 1 << 62:
+            raise ValueError("HELRM_ERR_CONFIG: |encoded coefficient| >= 2^62")
+        out[i] = v
     return out
 
 

@@ -147,45 +147,83 @@ def next_pow2(x: int) -> int:
     return p
 
 
+def _box_offsets(b: Block, o: int, c: int, n: int) -> List[int]:
+    """Offsets t (mod n) whose diagonal line s -> (o n + s, c n + (s + t) mod n)
+    (mbar = n) can cross block b's box of W: rows [R_b, R_b + d_b) x columns
+    [I_b, I_b + w_b), both clipped to output ct o / input ct c.  For s in the
+    box's row range [s0, s1) and column position v in [v0, v1), t = v - s."""
+    s0, s1 = max(b.R, o * n) - o * n, min(b.R + b.d, (o + 1) * n) - o * n
+    v0, v1 = max(b.I, c * n) - c * n, min(b.I + b.w, (c + 1) * n) - c * n
+    if s0 >= s1 or v0 >= v1:
+        return []
+    lo, hi = v0 - (s1 - 1), (v1 - 1) - s0
+    if hi - lo + 1 >= n:
+        return list(range(n))
+    return [t % n for t in range(lo, hi + 1)]
+
+
 def hybrid_diagonals(lay: Layout, n: int):
-    """diag_{o,c,t}[s] = W[o n + (s mod mbar)][c n + ((s + t) mod n)] (0 out of
-    range), t in [0, mbar); returns mbar, O, C and {(o, c, t): vector} for the
-    diagonals that are not identically zero.  Built entry by entry: each
-    non-zero W[r][u] lands in exactly one (o, c, t, s)."""
+    """D19 hybrid diagonals, evaluated from their definition:
+
+        diag_{o,c,t}[s] = W[o n + (s mod mbar)][c n + ((s + t) mod n)]
+
+    for t in [0, mbar), s in [0, n), 0 where the index falls outside W, with
+    W[R_b + col][I_b + row] = S_b[row][col] and 0 elsewhere.  Returns mbar, O,
+    C and {(o, c, t): vector} for the diagonals that are not identically zero.
+
+    W is zero outside the block boxes, so for each t only the positions s
+    whose row o n + (s mod mbar) lies in some block can be non-zero: those s
+    are enumerated per block (every s with s mod mbar = r - o n), and W is read
+    at (row(s), col(s, t)) there.  When mbar < n every t in [0, mbar) is
+    evaluated; when mbar = n (O, C may exceed 1) only the offsets whose line
+    crosses a block's box (_box_offsets) -- every other t reads W only outside
+    the boxes."""
     mbar = min(next_pow2(lay.M), n)
     O = -(-lay.M // n)
     C = -(-lay.K // n)
-    diags: Dict[Tuple[int, int, int], np.ndarray] = {}
+    # the stacked block entries: S_b[row][col] at flat[off_b + row d_b + col]
+    offs, acc = [], 0
     for b in lay.blocks:
-        rows = np.arange(b.w)
-        cols = np.arange(b.d)
-        rr, cc = np.meshgrid(rows, cols, indexing="ij")
-        vals = b.S[rr, cc].ravel()
-        r_out = (b.R + cc).ravel()          # W row
-        u_in = (b.I + rr).ravel()           # W column
-        o = r_out // n
-        c = u_in // n
-        if mbar < n:
-            s_mod = r_out % mbar            # s = s_mod + a mbar, t = (u - s) mod n in [0, mbar)
-            t = (u_in % n - s_mod) % mbar
-            s = ((u_in % n - t) % n)
-        else:
-            s = r_out % n
-            t = (u_in % n - s) % n
-        keys = np.stack([o, c, t], axis=1)
-        order = np.lexsort((t, c, o))
-        keys, s_sorted, v_sorted = keys[order], s[order], vals[order]
-        uniq, start = np.unique(keys, axis=0, return_index=True)
-        bounds = list(start) + [len(keys)]
-        for q_, (kk, a0) in enumerate(zip(uniq, start)):
-            a1 = bounds[q_ + 1]
-            key = (int(kk[0]), int(kk[1]), int(kk[2]))
-            vec = diags.get(key)
-            if vec is None:
+        offs.append(acc)
+        acc += b.w * b.d
+    flat = np.concatenate([b.S.ravel() for b in lay.blocks]) if lay.blocks else np.zeros(0)
+    diags: Dict[Tuple[int, int, int], np.ndarray] = {}
+    for o in range(O):
+        # every (s, W row, block) with row(s) = o n + (s mod mbar) inside a block's rows
+        S_, R_, B_ = [], [], []
+        for bi, b in enumerate(lay.blocks):
+            r = np.arange(max(b.R, o * n), min(b.R + b.d, (o + 1) * n))
+            r = r[(r - o * n) < mbar]                   # row(s) never exceeds o n + mbar - 1
+            if len(r) == 0:
+                continue
+            a = np.arange(n // mbar)
+            s = ((r - o * n)[:, None] + mbar * a[None, :]).ravel()
+            S_.append(s)
+            R_.append(np.repeat(r, len(a)))
+            B_.append(np.full(len(s), bi))
+        if not S_:
+            continue
+        s_all, r_all, b_all = np.concatenate(S_), np.concatenate(R_), np.concatenate(B_)
+        I_b = np.array([b.I for b in lay.blocks])[b_all]
+        w_b = np.array([b.w for b in lay.blocks])[b_all]
+        d_b = np.array([b.d for b in lay.blocks])[b_all]
+        R_b = np.array([b.R for b in lay.blocks])[b_all]
+        off_b = np.array(offs)[b_all]
+        for c in range(C):
+            if mbar < n:
+                cand = range(mbar)
+            else:
+                cand = sorted({t for b in lay.blocks for t in _box_offsets(b, o, c, n)})
+            for t in cand:
+                u = c * n + (s_all + t) % n             # W column of position s
+                inside = (u >= I_b) & (u < I_b + w_b)
+                if not inside.any():
+                    continue
+                vals = flat[off_b[inside] + (u[inside] - I_b[inside]) * d_b[inside] + (r_all[inside] - R_b[inside])]
                 vec = np.zeros(n)
-                diags[key] = vec
-            np.add.at(vec, s_sorted[a0:a1], v_sorted[a0:a1])
-    diags = {k: v for k, v in diags.items() if np.any(v != 0)}
+                np.add.at(vec, s_all[inside], vals)
+                if np.any(vec != 0):
+                    diags[(o, c, t)] = vec
     return mbar, O, C, diags
 
 

@@ -5,6 +5,7 @@ the C oracle (tests/test_oracle_pins.py).  Nothing here is fast or clever.
   negacyclic_mul  schoolbook product in Z_q[X]/(X^N + 1)
   ntt_eval        a(psi^{2i+1}) by Horner                   (D4)
   encode_mp       m_i = RHA((2 Delta/N) sum_j z_j cos(pi e_j i/N)) at 200 bits (D6)
+  encode_mp_coeff one coefficient of encode_mp (the oracle's exact D6 recomputation)
   decode_mp       z_j = Re(sum_i m_i zeta^{e_j i}) / Delta   (D7)
 """
 from __future__ import annotations
@@ -60,6 +61,20 @@ def encode_mp(z: Sequence[float], delta: int, N: int, prec: int = 200) -> List[i
                     acc += mpmath.mpf(z[j]) * cos_tab[(e[j] * i) % (2 * N)]
             out.append(rha(c * acc))
     return out
+
+
+def encode_mp_coeff(z: Sequence[float], delta: int, N: int, i: int, prec: int = 200) -> int:
+    """Coefficient i of encode_mp alone (the D6 exact recomputation)."""
+    import mpmath
+    n = N // 2
+    with mpmath.workprec(prec):
+        acc = mpmath.mpf(0)
+        ej = 1
+        for j in range(n):
+            if z[j] != 0:
+                acc += mpmath.mpf(float(z[j])) * mpmath.cos(mpmath.pi * ((ej * i) % (2 * N)) / N)
+            ej = ej * 5 % (2 * N)
+        return rha(mpmath.mpf(2) * delta / N * acc)
 
 
 def encode_mp_frac(z: Sequence[float], delta: int, N: int, prec: int = 200) -> List[float]:

@@ -217,3 +217,55 @@ def test_decode_inverts_encode():
     N2 = 32
     m2 = [int(v) for v in np.random.default_rng(4).integers(-10**9, 10**9, N2)]
     assert np.allclose(core.decode(m2, 1 << 20, N2), textbook.decode_mp(m2, 1 << 20, N2), rtol=0, atol=1e-9)
+
+
+def _sm_py(z):
+    M = 2**64 - 1
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def _word_py(seed, strm, k):
+    """D9 in pure Python: SM((seed ^ SM(stream)) + (k + 1) gamma mod 2^64)."""
+    return _sm_py(((seed ^ _sm_py(strm)) + (k + 1) * 0x9E3779B97F4A7C15) & (2**64 - 1))
+
+
+def test_samplers_known_answers_from_d10_statement():
+    """D10 restated in pure Python, coefficient by coefficient, checked
+    against the oracle's samplers on the first 64 coefficients and a few far
+    ones: coefficient i uses words 2i (value / magnitude) and 2i + 1 (low
+    half of UniformMod, sign of the Gaussian).  Swapping the two words, the
+    128-bit word order, or the sign bit's source fails this test."""
+    seed, N = 0xC0FFEE, 1 << 12
+    idx = list(range(64)) + [1000, 2047, 4095]
+    q = CRITEO_Q[3]
+    su = core.sample_uniform(seed, core.stream(2, c=3), q, N)
+    st = core.sample_ternary(seed, core.stream(1), N)
+    sg = core.sample_gauss(seed, core.stream(5, 7, 2), N)
+    T = core.gauss_cdt()
+    for i in idx:
+        w0 = _word_py(seed, core.stream(2, c=3), 2 * i)
+        w1 = _word_py(seed, core.stream(2, c=3), 2 * i + 1)
+        assert int(su[i]) == ((w0 << 64) | w1) % q                        # UniformMod(q)
+        r = _word_py(seed, core.stream(1), 2 * i) % 3
+        assert int(st[i]) == {0: 0, 1: 1, 2: -1}[r]                       # Ternary
+        g0 = _word_py(seed, core.stream(5, 7, 2), 2 * i)
+        g1 = _word_py(seed, core.stream(5, 7, 2), 2 * i + 1)
+        mag = min(k for k in range(20) if g0 < T[k])                     # min{k : w_2i < T[k]}
+        assert int(sg[i]) == (-mag if (g1 & 1) and mag > 0 else mag)      # sign from w_{2i+1} & 1
+    # the negative branch and magnitudes > 1 both occur in the checked range
+    assert (sg[:64] < 0).any() and (np.abs(sg[:64]) > 1).any()
+
+
+def test_encode_exact_ties_round_half_away():
+    """D6: RHA on exact ties.  z = c 1 gives m_0 = Delta c exactly; with
+    Delta c = k + 1/2 the coefficient is a tie (fraction exactly 1/2), which the
+    binary128 sum cannot decide alone: the oracle flags it (within 2^-40 of
+    1/2) and recomputes it exactly, rounding away from zero."""
+    N, delta = 64, 1 << 30
+    for k in (5, -6, 123456):
+        c = (k + 0.5) / delta
+        m = core.encode(np.full(N // 2, c), delta, N)
+        want = k + 1 if k >= 0 else k       # RHA: 5.5 -> 6, -5.5 -> -6
+        assert int(m[0]) == want and not m[1:].any()

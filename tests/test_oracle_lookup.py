@@ -369,3 +369,64 @@ def test_dense_sparse_extraction_on_the_lookup_engine():
         out = lk.lookup(P, plan, lk.encode_plan(P, plan), rk, [ct])
         got = core.decrypt_decode(P, sk, out[0])
         assert np.abs(got[: len(want)] - want).max() < 1e-3
+
+
+def _diagonals_brute_force(W: np.ndarray, n: int):
+    """D19 written out with no shortcut: every t in [0, mbar), every s in
+    [0, n), W read at (o n + (s mod mbar), c n + ((s + t) mod n)), 0 outside W."""
+    M, K = W.shape
+    mbar = min(lk.next_pow2(M), n)
+    O, C = -(-M // n), -(-K // n)
+    out = {}
+    s = np.arange(n)
+    for o in range(O):
+        for c in range(C):
+            for t in range(mbar):
+                rows = o * n + s % mbar
+                cols = c * n + (s + t) % n
+                ok = (rows < M) & (cols < K)
+                v = np.zeros(n)
+                v[ok] = W[rows[ok], cols[ok]]
+                if np.any(v != 0):
+                    out[(o, c, t)] = v
+    return mbar, O, C, out
+
+
+def _random_block_layout(rng, n_dense, n_blocks, n, gap=True):
+    tables, I, R = [], n_dense, 0
+    for _ in range(n_blocks):
+        k, d = int(rng.integers(1, 40)), int(rng.integers(1, 24))
+        if gap:
+            I += int(rng.integers(0, 3 * n // 4))
+            R += int(rng.integers(0, n // 2))
+        tables.append(synth.Table(k, d, 0, rng.normal(size=(k, d)), in_off=I, out_off=R))
+        I, R = I + k, R + d
+    return types.SimpleNamespace(n_dense=n_dense, tables=tables)
+
+
+@pytest.mark.parametrize("name", ["tiny_a", "tiny_b", "uci", "llm_gen_small", "mlp_small"])
+def test_hybrid_diagonals_equal_brute_force_configs(name):
+    """The planner's D19 extraction equals D19 evaluated at every (o, c, t, s)."""
+    w = synth.make_workload(name)
+    lay = lk.layout(w)
+    n = w.config.n_slots
+    got = lk.hybrid_diagonals(lay, n)
+    want = _diagonals_brute_force(lk.dense_matrix(lay), n)
+    assert got[:3] == want[:3] and got[3].keys() == want[3].keys()
+    for k, v in want[3].items():
+        assert np.array_equal(got[3][k], v)
+
+
+def test_hybrid_diagonals_equal_brute_force_random_multi_ct():
+    """Random block layouts with gaps: mbar < n and mbar = n with O, C > 1
+    (several output and input ciphertexts, blocks straddling ct borders)."""
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        n = int(rng.choice([16, 32, 64]))
+        w = _random_block_layout(rng, int(rng.integers(0, 5)), int(rng.integers(1, 6)), n, gap=trial % 2 == 0)
+        lay = lk.layout(w)
+        got = lk.hybrid_diagonals(lay, n)
+        want = _diagonals_brute_force(lk.dense_matrix(lay), n)
+        assert got[:3] == want[:3] and got[3].keys() == want[3].keys(), trial
+        for k, v in want[3].items():
+            assert np.array_equal(got[3][k], v)
