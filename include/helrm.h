@@ -122,6 +122,31 @@ helrm_status helrm_sk_export(helrm_ctx* c, const helrm_sk* s, int64_t* coeff, si
 helrm_status helrm_pk_export(helrm_ctx* c, const helrm_pk* p, uint64_t* coeff, size_t n_words);
 helrm_status helrm_rotkeys_export(helrm_ctx* c, const helrm_rotkeys* r, uint64_t g, uint64_t* coeff, size_t n_words);
 size_t helrm_rotkeys_bytes(const helrm_rotkeys* r);
+/* Galois elements held by a key set, ascending (n = count; up to cap written) */
+helrm_status helrm_rotkeys_galois(const helrm_rotkeys* r, uint64_t* g, size_t cap, size_t* n);
+
+/* Key import: client keys generated elsewhere (keys are client material,
+ * PAPER.md:142 "with a given public key", :163 "a unique key is needed for
+ * each rotation offset"), in the canonical coefficient form of the exports
+ * above.  The words are copied to the context's device and converted to the
+ * library's internal form (NTT slot order; rotation keys in D-form).
+ * Ownership: the caller keeps its buffers; the handles are the library's.
+ * Errors: ARG on a NULL pointer or a short buffer; RANGE if a word is not a
+ * residue in [0, q) of its limb (sk: |coefficient| > 2^40); CONFIG if g is
+ * not a power of 5 mod 2N (D8).
+ *   sk:   int64[N] secret coefficients (D11: ternary)
+ *   pk:   uint64 [2][L+1][N] (b, a)
+ *   rotation keys: key i for Galois element galois[i] at coeff[i],
+ *         uint64 [dnum(L)][2][L+1+K][N] (b_k, a_k) per digit k (D11);
+ *         words_per_key >= dnum(L) 2 (L+1+K) N.  A repeated g keeps the last. */
+helrm_status helrm_sk_import(helrm_ctx* c, const int64_t* coeff, size_t n_words, helrm_sk** out);
+helrm_status helrm_pk_import(helrm_ctx* c, const uint64_t* coeff, size_t n_words, helrm_pk** out);
+helrm_status helrm_rotkeys_import(helrm_ctx* c, const uint64_t* galois, size_t n, const uint64_t* const* coeff,
+                                  size_t words_per_key, helrm_rotkeys** out);
+/* Upload one more key (same form as one key of helrm_rotkeys_import) into
+ * an existing key set, e.g. streamed from the client one rotation at a time;
+ * replaces a key already held for g. */
+helrm_status helrm_rotkeys_upload(helrm_ctx* c, helrm_rotkeys* rk, uint64_t g, const uint64_t* coeff, size_t n_words);
 
 /* ---- tables and client query (S0) --------- */
 typedef struct {
@@ -180,6 +205,9 @@ helrm_status helrm_plan_info(const helrm_plan* p, helrm_plan_info_t* out);
 /* rotation amounts needing a key (babies, giants, RotSum), ascending;
  * the Galois element of amount a is 5^a mod 2N */
 helrm_status helrm_plan_rotations(const helrm_plan* p, int64_t* amounts, size_t cap, size_t* n);
+/* the plan's D19 Galois list {5^a mod 2N : a in helrm_plan_rotations},
+ * ascending: the keys the client must generate (n = count, <= cap written) */
+helrm_status helrm_plan_galois(const helrm_plan* p, uint64_t* g, size_t cap, size_t* n);
 
 /* ---- the hot path (D20-D22) --------------------------------------------- */
 /* in: batch x C ciphertexts (query-major), all at the plan's level; out:
@@ -234,13 +262,25 @@ helrm_status helrm_comm_unique_id(uint8_t* id);
 /* Create the context's communicator (NCCL is loaded at run time). */
 helrm_status helrm_comm_init(helrm_ctx* c, const uint8_t* id, int rank, int world);
 /* helrm_lookup with the giant steps split over the ranks: rank 0's inputs are
- * broadcast (every rank passes buffers at the plan's level, e.g. from
- * helrm_ct_alloc), each rank computes the partial Q_l P accumulators of its
- * giant range, ncclAllReduce(uint64, sum) + a mod-q kernel combine them, and
- * every rank finishes (ModDown, rescale, RotSum).  Bit-identical to
- * helrm_lookup for every world size (only exact modular sums are split). */
+ * broadcast into each rank's staging buffer (every rank passes cts at the
+ * plan's level, e.g. from helrm_ct_alloc; none is modified), each rank
+ * computes the partial Q_l P accumulators of its giant range,
+ * ncclAllReduce(uint64, sum) + a mod-q kernel combine them, and every rank
+ * finishes (ModDown, rescale, RotSum).  Bit-identical to helrm_lookup for
+ * every world size (only exact modular sums are split, D23). */
 helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
                                size_t batch, helrm_ct** out);
+/* The same partition emulated in one process (parity harness of the
+ * multi-GPU combine on one GPU): the `parts` giant ranges run one after
+ * another, their partial accumulators are summed as plain uint64 words (the
+ * all-reduce's arithmetic) and reduced by the same mod-q kernel, then L6-L8.
+ * 1 <= parts < 8192 (ARG otherwise).  Bit-identical to helrm_lookup. */
+helrm_status helrm_lookup_dist_virtual(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                       const helrm_ct* const* in, size_t batch, int parts, helrm_ct** out);
+/* The combine's reduction alone (D23 L5), in place: n_polys R_{Q_level P}
+ * polynomials [n_polys][level+1+K][N] at `dev` whose words are sums of
+ * residues (< 2^64) become residues mod their limb's prime. */
+helrm_status helrm_modred(helrm_ctx* c, uint64_t* dev, uint32_t level, size_t n_polys);
 
 const char* helrm_last_error(void);
 const char* helrm_version(void);

@@ -54,6 +54,15 @@ void need(bool ok, helrm_status code, const char* msg) {
 }
 }  // namespace
 
+// Every entry point that enqueues work for a context first makes the
+// context's device current (a process may hold contexts on several devices).
+struct DevGuard {
+  explicit DevGuard(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) HCUDA(cudaSetDevice(dev));
+  }
+};
+
 // ============================================================================
 // handles
 // ============================================================================
@@ -73,7 +82,6 @@ struct LevelConst {
   double2* modup_post = nullptr;   // [l+1]
   ConvRowDev* modup_tab = nullptr; // [dnum(l)][modup_rows]: the rows outside digit k
   int modup_rows = 0;
-  ConvRowDev* modup_dtab = nullptr; // [dnum(l)][l+1+K]: row r of digit k (own rows unused), for the fused NTT
   double2* moddown_post = nullptr; // [K]
   ConvRowDev* moddown_tab = nullptr; // [l+1]
 };
@@ -158,21 +166,28 @@ struct helrm_ctx {
   }
 
   int persist = 0;                // persistent CTAs per SM for the HBM-bound kernels (0 = full grids)
+  int n_sm = 148;                 // multiprocessor count of `device`
+  cudaMemPool_t pool = nullptr;   // private stream-ordered pool (the device's default pool is left alone)
   DevCtx dc(cudaStream_t s = nullptr, int pers = 0) {
-    return DevCtx{dprimes, dslotpos, dgrp, dtwb, dtpos, P.log_n, P.N, s ? s : stream, pers, &launches, &prof};
+    return DevCtx{dprimes, dslotpos, dgrp, dtwb, dtpos, P.log_n, P.N, s ? s : stream, pers, n_sm, &launches, &prof};
   }
 
   void* dalloc(size_t bytes, cudaStream_t s = nullptr) {
     HostTimer ht_("cudaMallocAsync");
     void* p = nullptr;
     if (bytes == 0) bytes = 8;
-    cudaError_t e = cudaMallocAsync(&p, bytes, s ? s : stream);
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, s ? s : stream);
     if (e != cudaSuccess) throw Error(HELRM_ERR_ALLOC, std::string("device allocation failed: ") + cudaGetErrorString(e));
     return p;
   }
   void dfree(void* p, cudaStream_t s = nullptr) {
     HostTimer ht_("cudaFreeAsync");
     if (p) cudaFreeAsync(p, s ? s : stream);
+  }
+  // give memory freed by destroyed plans / key sets back to the device
+  void trim() {
+    cudaStreamSynchronize(stream);
+    cudaMemPoolTrimTo(pool, 0);
   }
   uint64_t* upload_u64(const std::vector<uint64_t>& v) {
     uint64_t* d = (uint64_t*)dalloc(v.size() * 8);
@@ -430,20 +445,6 @@ static const LevelConst& level_const(helrm_ctx* c, uint32_t l) {
     };
     lc.modup_post = (double2*)up(upost.data(), upost.size() * sizeof(double2));
     lc.modup_tab = (ConvRowDev*)up(utab.data(), utab.size() * sizeof(ConvRowDev));
-    {
-      std::vector<ConvRowDev> dt((size_t)dn * nl);
-      for (uint32_t k = 0; k < dn; k++) {
-        for (uint32_t r = 0; r < nl; r++) {   // same sources as the compacted table, keyed by row
-          dt[(size_t)k * nl + r] = utab[(size_t)k * urows];
-          dt[(size_t)k * nl + r].out_row = -1;
-        }
-        for (uint32_t j = 0; j < urows; j++) {
-          const ConvRowDev& e = utab[(size_t)k * urows + j];
-          if (e.out_row >= 0) dt[(size_t)k * nl + e.out_row] = e;
-        }
-      }
-      lc.modup_dtab = (ConvRowDev*)up(dt.data(), dt.size() * sizeof(ConvRowDev));
-    }
     lc.moddown_post = (double2*)up(dpost.data(), dpost.size() * sizeof(double2));
     lc.moddown_tab = (ConvRowDev*)up(dtab.data(), dtab.size() * sizeof(ConvRowDev));
     HCUDA(cudaStreamSynchronize(c->stream));
@@ -527,21 +528,9 @@ static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int 
   // limbs are copied unchanged (NTT form).
   launch_ntt_inv(c->dc(st), in, y.p, c->scratch, G * nq, P.map_q(l), in_stride, nq * N, lc.modup_post,
                  pm_lidx(c, G, (uint32_t)nq));
-  static const bool fuse = getenv("HELRM_FUSECONV") ? atoi(getenv("HELRM_FUSECONV")) != 0 : false;
-  if (fuse) {   // conversion computed inside the NTT's pass 1 (no conversion kernel, no round trip)
-    NttConvIn cv;
-    cv.tab = lc.modup_dtab;
-    cv.tab_rows = (int)nl;
-    cv.ncv = (int)dn;
-    cv.nb_max = (int)P.alpha;
-    cv.y = y.p;
-    cv.ys = nq * N;
-    launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, false, lidx, nullptr, &cv);
-  } else {
-    launch_conv_rows(c->dc(st), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
-                     nl * N, G, P.map_qp(l));
-    launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
-  }
+  launch_conv_rows(c->dc(st), lc.modup_tab, (int)dn, lc.modup_rows, (int)P.alpha, y.p, nq * N, out, dn * nl * N,
+                   nl * N, G, P.map_qp(l));
+  launch_ntt_fwd(c->dc(st), out, out, c->scratch, n_conv, P.map_qp(l), 0, 0, true, lidx);
   HostTimer ht_("modup own-limb copies");
   for (size_t k = 0; copy_own && k < dn; k++) {
     const size_t lo = k * P.alpha, hi = std::min<size_t>((k + 1) * P.alpha, l + 1);
@@ -561,18 +550,7 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   DBuf yp(c, G * P.K * N, st), t(c, G * nq * N, st);
   launch_ntt_inv(c->dc(st), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
                  lc.moddown_post, pm_lidx(c, G, P.K));
-  static const bool fuse = getenv("HELRM_FUSECONV") ? atoi(getenv("HELRM_FUSECONV")) != 0 : false;
-  NttConvIn cv;
-  if (fuse) {
-    cv.tab = lc.moddown_tab;
-    cv.tab_rows = (int)nq;
-    cv.ncv = 1;
-    cv.nb_max = (int)P.K;
-    cv.y = yp.p;
-    cv.ys = P.K * N;
-  } else {
-    launch_conv_rows(c->dc(st), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
-  }
+  launch_conv_rows(c->dc(st), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
   NttEpi epi;
   epi.y = y;
   epi.ys = ys;
@@ -581,8 +559,7 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   epi.s = lc.pinv;
   epi.sp = lc.pinvs;
   epi.accumulate = accumulate ? 1 : 0;
-  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, !fuse, pm_lidx(c, G, (uint32_t)nq), &epi,
-                 fuse ? &cv : nullptr);
+  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true, pm_lidx(c, G, (uint32_t)nq), &epi);
 }
 
 static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t* out) {
@@ -770,6 +747,7 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
     c->P = p->P;
     c->device = device;
     c->stream = (cudaStream_t)stream;
+    HCUDA(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device));
     {
       int lo_prio = 0, hi_prio = 0;
       HCUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
@@ -780,22 +758,27 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
       HCUDA(cudaStreamCreateWithPriority(&c->s_ntt, cudaStreamNonBlocking, mode == 1 ? hi_prio : lo_prio));
       HCUDA(cudaStreamCreateWithPriority(&c->s_kip, cudaStreamNonBlocking, mode == 3 ? hi_prio : lo_prio));
       HCUDA(cudaStreamCreateWithPriority(&c->s_mac, cudaStreamNonBlocking, mode == 3 ? hi_prio : lo_prio));
-      const char* pe = getenv("HELRM_PERSIST");
-      c->persist = pe ? atoi(pe) : 0;
       HCUDA(cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking));
       HCUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
       HCUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
     }
-    cudaMemPool_t pool;
-    HCUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    HCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     {
+      // a private pool: memory freed by the lookup's temporaries is kept for the next
+      // lookup (release threshold: unlimited) without changing the device's default
+      // pool that other allocators of the process (PyTorch) use; trimmed when plans,
+      // key sets or the context are destroyed
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      HCUDA(cudaMemPoolCreate(&c->pool, &props));
+      uint64_t thr = UINT64_MAX;
+      HCUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
       // stream-ordered reuse across the side streams must not add hidden
       // dependencies (they would serialise the pipelined giant steps)
-      const char* e = getenv("HELRM_POOLDEP");
-      int dep = e ? atoi(e) : 0;
-      HCUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &dep));
+      int dep = 0;
+      HCUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &dep));
     }
     const Params& P = c->P;
     const size_t N = P.N, np = P.primes.size();
@@ -924,12 +907,17 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
     HCUDA(cudaStreamSynchronize(c->stream));
     *out = c;
   });
-  if (st != HELRM_OK) delete c;
+  if (st != HELRM_OK && c) {
+    if (c->pool) cudaMemPoolDestroy(c->pool);
+    delete c;
+  }
   return st;
 }
 
 void helrm_ctx_destroy(helrm_ctx* c) {
   if (!c) return;
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != c->device) cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   if (c->s_ntt) cudaStreamSynchronize(c->s_ntt);
   if (c->s_kip) cudaStreamSynchronize(c->s_kip);
@@ -954,12 +942,14 @@ void helrm_ctx_destroy(helrm_ctx* c) {
   if (c->s_mac) cudaStreamDestroy(c->s_mac);
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   delete c;
 }
 
 helrm_status helrm_ctx_sync(helrm_ctx* c) {
   return guard([&] {
     need(c, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     HCUDA(cudaStreamSynchronize(c->stream));
   });
 }
@@ -969,6 +959,7 @@ uint64_t helrm_ctx_launches(const helrm_ctx* c) { return c ? c->launches : 0; }
 helrm_status helrm_ctx_profile(helrm_ctx* c, int enable) {
   return guard([&] {
     need(c, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     HCUDA(cudaStreamSynchronize(c->stream));
     for (auto& r : c->prof.recs) {
       c->prof.pool.push_back(r.a);
@@ -1035,6 +1026,7 @@ helrm_status helrm_sk_gen(helrm_ctx* c, uint64_t seed, helrm_sk** out) {
   if (out) *out = nullptr;
   return guard([&] {
     need(c && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     const Params& P = c->P;
     helrm_sk* sk = new helrm_sk{c, nullptr, std::vector<int64_t>(P.N)};
     const uint32_t nall = P.L + 1 + P.K;
@@ -1046,6 +1038,7 @@ helrm_status helrm_sk_gen(helrm_ctx* c, uint64_t seed, helrm_sk** out) {
 
 void helrm_sk_destroy(helrm_sk* s) {
   if (!s) return;
+  DevGuard dg_(s->c->device);
   s->c->dfree(s->sntt);
   delete s;
 }
@@ -1054,6 +1047,7 @@ helrm_status helrm_pk_gen(helrm_ctx* c, const helrm_sk* sk, uint64_t seed, helrm
   if (out) *out = nullptr;
   return guard([&] {
     need(c && sk && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     const Params& P = c->P;
     const size_t N = P.N, nq = P.L + 1;
     helrm_pk* pk = new helrm_pk{c, (uint64_t*)c->dalloc(2 * nq * N * 8)};
@@ -1072,6 +1066,7 @@ helrm_status helrm_pk_gen(helrm_ctx* c, const helrm_sk* sk, uint64_t seed, helrm
 
 void helrm_pk_destroy(helrm_pk* p) {
   if (!p) return;
+  DevGuard dg_(p->c->device);
   p->c->dfree(p->d);
   delete p;
 }
@@ -1082,6 +1077,7 @@ helrm_status helrm_rotkeys_gen(helrm_ctx* c, const helrm_sk* sk, const uint64_t*
   helrm_rotkeys* rk = nullptr;
   helrm_status st = guard([&] {
     need(c && sk && out && (galois || n == 0), HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     const Params& P = c->P;
     const size_t N = P.N, nall = P.L + 1 + P.K, dn = P.dnum(P.L);
     rk = new helrm_rotkeys{c, {}, dn * 2 * nall * N};
@@ -1119,8 +1115,10 @@ helrm_status helrm_rotkeys_gen(helrm_ctx* c, const helrm_sk* sk, const uint64_t*
 
 void helrm_rotkeys_destroy(helrm_rotkeys* r) {
   if (!r) return;
+  DevGuard dg_(r->c->device);
   r->c->drop_graphs(r->id);
   for (auto& kv : r->keys) r->c->dfree(kv.second);
+  r->c->trim();
   delete r;
 }
 
@@ -1129,6 +1127,7 @@ size_t helrm_rotkeys_bytes(const helrm_rotkeys* r) { return r ? r->keys.size() *
 helrm_status helrm_sk_export(helrm_ctx* c, const helrm_sk* s, int64_t* coeff, size_t n_words) {
   return guard([&] {
     need(c && s && coeff && n_words >= c->P.N, HELRM_ERR_ARG, "bad argument");
+    DevGuard dg_(c->device);
     std::copy(s->s.begin(), s->s.end(), coeff);
   });
 }
@@ -1144,6 +1143,7 @@ static void export_ntt(helrm_ctx* c, const uint64_t* d, size_t npolys, const Lim
 helrm_status helrm_pk_export(helrm_ctx* c, const helrm_pk* p, uint64_t* coeff, size_t n_words) {
   return guard([&] {
     need(c && p && coeff && n_words >= (size_t)2 * (c->P.L + 1) * c->P.N, HELRM_ERR_ARG, "bad argument");
+    DevGuard dg_(c->device);
     export_ntt(c, p->d, 2, c->P.map_q(c->P.L), coeff);
   });
 }
@@ -1151,11 +1151,142 @@ helrm_status helrm_pk_export(helrm_ctx* c, const helrm_pk* p, uint64_t* coeff, s
 helrm_status helrm_rotkeys_export(helrm_ctx* c, const helrm_rotkeys* r, uint64_t g, uint64_t* coeff, size_t n_words) {
   return guard([&] {
     need(c && r && coeff && n_words >= r->words_per_key, HELRM_ERR_ARG, "bad argument");
+    DevGuard dg_(c->device);
     const Params& P = c->P;
     DBuf tmp(c, r->words_per_key);
     HCUDA(cudaMemcpyAsync(tmp.p, key_for(r, g), r->words_per_key * 8, cudaMemcpyDeviceToDevice, c->stream));
     launch_dform(c->dc(), tmp.p, r->words_per_key, P.map_range(0, P.L + 1 + P.K), 0);
     export_ntt(c, tmp.p, 2 * P.dnum(P.L), P.map_range(0, P.L + 1 + P.K), coeff);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// key import (client keys generated elsewhere, e.g. by the CPU oracle): the
+// canonical coefficient form of the *_export calls
+// ---------------------------------------------------------------------------
+// every word of npolys polynomials of map's limbs is a residue in [0, q)
+static void check_canonical(helrm_ctx* c, const uint64_t* h, size_t npolys, const LimbMap& m) {
+  const size_t N = c->P.N;
+  for (size_t p = 0; p < npolys; p++)
+    for (int l = 0; l < m.n; l++) {
+      const uint64_t q = c->P.primes[m.pr[l]];
+      const uint64_t* row = h + (p * m.n + l) * N;
+      for (size_t i = 0; i < N; i++)
+        if (row[i] >= q) throw Error(HELRM_ERR_RANGE, "imported word is not a residue in [0, q)");
+    }
+}
+
+static void upload_ntt(helrm_ctx* c, const uint64_t* host, size_t npolys, const LimbMap& m, uint64_t* d) {
+  check_canonical(c, host, npolys, m);
+  HCUDA(cudaMemcpyAsync(d, host, npolys * m.n * c->P.N * 8, cudaMemcpyHostToDevice, c->stream));
+  ntt_fwd(c, d, d, npolys * m.n, m);
+}
+
+helrm_status helrm_sk_import(helrm_ctx* c, const int64_t* coeff, size_t n_words, helrm_sk** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && coeff && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
+    const Params& P = c->P;
+    need(n_words >= P.N, HELRM_ERR_ARG, "buffer too small");
+    for (size_t i = 0; i < P.N; i++)
+      need(coeff[i] >= -((int64_t)1 << 40) && coeff[i] <= ((int64_t)1 << 40), HELRM_ERR_RANGE,
+           "secret coefficient outside [-2^40, 2^40]");
+    helrm_sk* sk = new helrm_sk{c, nullptr, std::vector<int64_t>(coeff, coeff + P.N)};
+    const uint32_t nall = P.L + 1 + P.K;
+    sk->sntt = (uint64_t*)c->dalloc((size_t)nall * P.N * 8);
+    DBuf s(c, P.N);
+    HCUDA(cudaMemcpyAsync(s.p, coeff, P.N * 8, cudaMemcpyHostToDevice, c->stream));
+    const LimbMap m = P.map_range(0, nall);
+    launch_reduce_signed(c->dc(), (const int64_t*)s.p, sk->sntt, m);
+    ntt_fwd(c, sk->sntt, sk->sntt, m.n, m);
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = sk;
+  });
+}
+
+helrm_status helrm_pk_import(helrm_ctx* c, const uint64_t* coeff, size_t n_words, helrm_pk** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    need(c && coeff && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
+    const Params& P = c->P;
+    const size_t words = (size_t)2 * (P.L + 1) * P.N;
+    need(n_words >= words, HELRM_ERR_ARG, "buffer too small");
+    helrm_pk* pk = new helrm_pk{c, (uint64_t*)c->dalloc(words * 8)};
+    try {
+      upload_ntt(c, coeff, 2, P.map_q(P.L), pk->d);
+      HCUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+      helrm_pk_destroy(pk);
+      throw;
+    }
+    *out = pk;
+  });
+}
+
+// one key [dnum(L)][2][L+1+K][N] (coefficient form) into rk under Galois element g
+static void rotkey_upload(helrm_ctx* c, helrm_rotkeys* rk, uint64_t g, const uint64_t* coeff) {
+  const Params& P = c->P;
+  need(g % 2 == 1 && g < 2 * (uint64_t)P.N, HELRM_ERR_ARG, "Galois element must be odd and < 2N");
+  (void)rot_of_galois(c, g);   // a power of 5 (the rotations of D8)
+  const LimbMap m = P.map_range(0, P.L + 1 + P.K);
+  uint64_t* key = (uint64_t*)c->dalloc(rk->words_per_key * 8);
+  try {
+    upload_ntt(c, coeff, 2 * P.dnum(P.L), m, key);
+  } catch (...) {
+    c->dfree(key);
+    throw;
+  }
+  launch_dform(c->dc(), key, rk->words_per_key, m, 1);   // keys live in D-form (FP64 MACs)
+  auto it = rk->keys.find(g);
+  if (it != rk->keys.end()) c->dfree(it->second);
+  rk->keys[g] = key;
+  c->drop_graphs(rk->id);   // captured lookups point at the replaced key
+}
+
+helrm_status helrm_rotkeys_import(helrm_ctx* c, const uint64_t* galois, size_t n, const uint64_t* const* coeff,
+                                  size_t words_per_key, helrm_rotkeys** out) {
+  if (out) *out = nullptr;
+  helrm_rotkeys* rk = nullptr;
+  helrm_status st = guard([&] {
+    need(c && out && ((galois && coeff) || n == 0), HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
+    const Params& P = c->P;
+    rk = new helrm_rotkeys{c, {}, (size_t)P.dnum(P.L) * 2 * (P.L + 1 + P.K) * P.N};
+    need(words_per_key >= rk->words_per_key, HELRM_ERR_ARG, "buffer too small");
+    for (size_t i = 0; i < n; i++) {
+      need(coeff[i] != nullptr, HELRM_ERR_ARG, "null key buffer");
+      rotkey_upload(c, rk, galois[i], coeff[i]);
+    }
+    HCUDA(cudaStreamSynchronize(c->stream));
+    *out = rk;
+  });
+  if (st != HELRM_OK && rk) helrm_rotkeys_destroy(rk);
+  return st;
+}
+
+helrm_status helrm_rotkeys_upload(helrm_ctx* c, helrm_rotkeys* rk, uint64_t g, const uint64_t* coeff,
+                                  size_t n_words) {
+  return guard([&] {
+    need(c && rk && coeff && rk->c == c, HELRM_ERR_ARG, "bad argument");
+    DevGuard dg_(c->device);
+    need(n_words >= rk->words_per_key, HELRM_ERR_ARG, "buffer too small");
+    rotkey_upload(c, rk, g, coeff);
+    HCUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+helrm_status helrm_rotkeys_galois(const helrm_rotkeys* r, uint64_t* g, size_t cap, size_t* n) {
+  return guard([&] {
+    need(r && n, HELRM_ERR_ARG, "null argument");
+    *n = r->keys.size();
+    need(g || cap == 0, HELRM_ERR_ARG, "null argument");
+    size_t i = 0;
+    for (auto& kv : r->keys) {
+      if (i >= cap) break;
+      g[i++] = kv.first;
+    }
   });
 }
 
@@ -1280,6 +1411,7 @@ helrm_status helrm_encrypt(helrm_ctx* c, const helrm_pk* pk, const double* slots
   if (out) *out = nullptr;
   return guard([&] {
     need(c && pk && slots && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     const Params& P = c->P;
     need(n_slots <= P.n, HELRM_ERR_CAPACITY, "more slots than N/2");
     need(level <= P.L, HELRM_ERR_LEVEL, "level above L");
@@ -1307,6 +1439,7 @@ helrm_status helrm_ct_alloc(helrm_ctx* c, uint32_t level, double scale, helrm_ct
   if (out) *out = nullptr;
   return guard([&] {
     need(c && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(level <= c->P.L, HELRM_ERR_LEVEL, "level above L");
     *out = new_ct(c, level, scale);
   });
@@ -1316,6 +1449,7 @@ helrm_status helrm_ct_import(helrm_ctx* c, const uint64_t* coeff, uint32_t level
   if (out) *out = nullptr;
   return guard([&] {
     need(c && coeff && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(level <= c->P.L, HELRM_ERR_LEVEL, "level above L");
     helrm_ct* ct = new_ct(c, level, scale);
     const size_t words = (size_t)2 * (level + 1) * c->P.N;
@@ -1329,6 +1463,7 @@ helrm_status helrm_ct_import(helrm_ctx* c, const uint64_t* coeff, uint32_t level
 helrm_status helrm_ct_export(helrm_ctx* c, const helrm_ct* ct, uint64_t* coeff, size_t n_words) {
   return guard([&] {
     need(c && ct && coeff, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(n_words >= (size_t)2 * (ct->level + 1) * c->P.N, HELRM_ERR_ARG, "buffer too small");
     export_ntt(c, ct->d, 2, c->P.map_q(ct->level), coeff);
   });
@@ -1351,6 +1486,7 @@ helrm_status helrm_ct_device_ptr(const helrm_ct* ct, uint64_t** dev) {
 
 void helrm_ct_destroy(helrm_ct* ct) {
   if (!ct) return;
+  DevGuard dg_(ct->c->device);
   ct->c->dfree(ct->d);
   delete ct;
 }
@@ -1359,6 +1495,7 @@ helrm_status helrm_decrypt_decode(helrm_ctx* c, const helrm_sk* sk, const helrm_
                                   size_t n_slots) {
   return guard([&] {
     need(c && sk && ct && slots, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     const Params& P = c->P;
     const size_t N = P.N, nq = ct->level + 1;
     LimbMap m = P.map_q(ct->level);
@@ -1390,6 +1527,7 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
   helrm_plan* pl = nullptr;
   helrm_status st = guard([&] {
     need(c && T && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     const Params& P = c->P;
     need(level >= 1 && level <= P.L, HELRM_ERR_LEVEL, "lookup needs 1 <= level <= L");
     need(mode == HELRM_MODE_DOUBLE || mode == HELRM_MODE_SINGLE, HELRM_ERR_ARG, "bad mode");
@@ -1536,9 +1674,11 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
 }
 
 void helrm_plan_destroy(helrm_plan* p) {
-  if (p && p->c) p->c->drop_graphs(p->id);
   if (!p) return;
+  DevGuard dg_(p->c->device);
+  p->c->drop_graphs(p->id);
   p->c->dfree(p->diag);
+  p->c->trim();
   delete p;
 }
 
@@ -1571,6 +1711,19 @@ helrm_status helrm_plan_rotations(const helrm_plan* p, int64_t* amounts, size_t 
       need(cap >= p->rotations.size(), HELRM_ERR_ARG, "buffer too small");
       std::copy(p->rotations.begin(), p->rotations.end(), amounts);
     }
+  });
+}
+
+helrm_status helrm_plan_galois(const helrm_plan* p, uint64_t* g, size_t cap, size_t* n) {
+  return guard([&] {
+    need(p && n, HELRM_ERR_ARG, "null argument");
+    // D19 Galois list {5^a mod 2N : a in the rotation amounts}, ascending
+    std::vector<uint64_t> v;
+    for (int64_t a : p->rotations) v.push_back(galois_of_rot(p->c, a));
+    std::sort(v.begin(), v.end());
+    *n = v.size();
+    need(g || cap == 0, HELRM_ERR_ARG, "null argument");
+    for (size_t i = 0; i < v.size() && i < cap; i++) g[i] = v[i];
   });
 }
 
@@ -1746,9 +1899,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   size_t n_baby = 0;
   for (auto& bl : pl->babies) n_baby += bl.size();
   DBuf D(c, C * Qc * dn * nlN);
-  const bool fused_pre = (getenv("HELRM_FUSED_BM") ? atoi(getenv("HELRM_FUSED_BM")) != 0 : false) && Qc == 1 &&
-                         C == 1 && pl->babies[0].size() <= 48;
-  DBuf babies(c, fused_pre ? 1 : std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
+  DBuf babies(c, std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
   size_t bi = 0;
   bool same_babies = Qc == 1 && C > 1;
   for (size_t ci = 1; same_babies && ci < C; ci++) same_babies = pl->babies[ci] == pl->babies[0];
@@ -1799,10 +1950,6 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     }
     if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
-  // batch 1, one input ct: baby steps and inner sums fused in one kernel (no baby pairs in HBM)
-  static const bool fuse_env = getenv("HELRM_FUSED_BM") ? atoi(getenv("HELRM_FUSED_BM")) != 0 : false;
-  const bool fused = fuse_env && Qc == 1 && C == 1 && pl->babies[0].size() <= 48;
-  KipMulti kmf{};
   for (size_t ci = 0; !same_babies && ci < C; ci++) {
     const uint64_t* c0 = X + ci * 2 * nqN;
     uint64_t* Dc = D.p + ci * Qc * dn * nlN;
@@ -1825,22 +1972,6 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     km.dq = dn * nlN;
     km.cq = xs;
     km.oq = 2 * nlN;
-    if (fused) {   // keys only: k_baby_mac computes the pairs into shared memory
-      for (size_t jj = 0; jj < pl->babies[0].size(); jj++) {
-        const int j = pl->babies[0][jj];
-        ab[0][j] = reinterpret_cast<uint64_t*>((uintptr_t)jj);   // slot index, not a pointer
-        if (j == 0) continue;
-        need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
-        const uint64_t g = galois_of_rot(c, j);
-        km.rot[km.n] = rot_of_galois(c, g);
-        km.key[km.n] = key_for(rk, g);
-        km.out[km.n] = nullptr;
-        km.max_rot = std::max(km.max_rot, km.rot[km.n]);
-        km.n++;
-      }
-      kmf = km;
-      continue;
-    }
     for (int j : pl->babies[ci]) {
       uint64_t* a = babies.p + bi++ * Qc * 2 * nlN;
       if (j == 0) {  // (P c0, P c1): Q limbs scaled by [P]_q, P limbs 0
@@ -1875,66 +2006,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   if (n_out == 0) return;
   const size_t zq = (size_t)Qc;   // pairs per z
   DBuf AB(c, (size_t)n_out * zq * 2 * nlN), Bp(c, (size_t)n_out * zq * nqN), D2(c, (size_t)n_out * zq * dn * nlN);
-  bool macs_done = false;
-  std::unique_ptr<MacDev> mdp;
-  if (fused) {
-    // the work list with baby slots instead of pointers
-    MacList fl = ml;
-    fl.term_size = sizeof(FusedTerm);
-    fl.terms.assign(ml.n_terms * sizeof(FusedTerm), 0);
-    for (size_t t = 0; t < ml.n_terms; t++) {
-      const MacTerm* mt = reinterpret_cast<const MacTerm*>(&ml.terms[t * ml.term_size]);
-      FusedTerm ft{};
-      ft.slot = (int)(uintptr_t)mt->x0;
-      for (int g = 0; g < kGiantPack; g++) ft.u[g] = mt->u[g];
-      std::memcpy(&fl.terms[t * sizeof(FusedTerm)], &ft, sizeof(FusedTerm));
-    }
-    mdp.reset(new MacDev(c, fl, pinned));
-    const bool has0 = !pl->babies[0].empty() && pl->babies[0][0] == 0;
-    BabyMacArgs bm{};
-    bm.terms = (const FusedTerm*)mdp->terms.p;
-    bm.groups = (const int4*)mdp->groups.p;
-    bm.n_groups = (int)ml.groups.size();
-    bm.n_slots = (int)pl->babies[0].size();
-    bm.slot0 = has0 ? 1 : 0;
-    bm.j0 = has0 ? 0 : -1;
-    bm.c1 = X + nqN;
-    bm.out = AB.p;
-    bm.out_stride = 2 * nlN;
-    bm.half = nlN;
-    bm.bytes = 8.0 * N * nl * (dn + 2.0 + kmf.n * 2.0 * dn + ml.n_u + 2.0 * n_out);
-    static const int fused_mode = getenv("HELRM_FUSED_BM") ? atoi(getenv("HELRM_FUSED_BM")) : 0;
-    macs_done = fused_mode == 2 ? launch_baby_mac_bulk(c->dc(), kmf, bm, mqp) : launch_baby_mac(c->dc(), kmf, bm, mqp);
-    need(macs_done, HELRM_ERR_CONFIG, "fused baby/MAC kernel does not apply");   // guarded by `fused`
-  }
-  // output blocks sharing every plaintext (LLM layout L2): dense (giant, baby slot) table of
-  // block 0's plaintexts for k_block_mac
-  std::vector<char> utab;
-  int blk_zb = 0;
-  if (same_babies && pl->O == (int64_t)C && pl->O == 4 && ml.groups.size() % pl->O == 0) {
-    const size_t gb0 = ml.groups.size() / pl->O, nbb = pl->babies[0].size();
-    blk_zb = ml.groups[gb0].z;
-    std::vector<const uint64_t*> U((size_t)blk_zb * nbb, nullptr);
-    bool ok = blk_zb > 0;
-    for (size_t g = 0; ok && g < gb0; g++) {
-      const int4 gr = ml.groups[g];
-      for (int t = 0; ok && t < gr.y; t++) {
-        const MacTerm* mt = reinterpret_cast<const MacTerm*>(&ml.terms[(size_t)(gr.x + t) * ml.term_size]);
-        const size_t off = (size_t)(mt->x0 - babies.p);
-        ok = off % (2 * nlN) == 0 && off / (2 * nlN) < nbb;
-        for (int gi = 0; ok && gi < gr.w; gi++) U[(size_t)(gr.z + gi) * nbb + off / (2 * nlN)] = mt->u[gi];
-      }
-    }
-    if (ok) {
-      const char* b = reinterpret_cast<const char*>(U.data());
-      utab.assign(b, b + U.size() * sizeof(const uint64_t*));
-    } else {
-      blk_zb = 0;
-    }
-  }
-  std::unique_ptr<MacDev> mdu;
-  if (!fused) mdu.reset(new MacDev(c, ml, pinned, utab));
-  const MacDev& md = fused ? *mdp : *mdu;
+  const MacDev md(c, ml, pinned);
   // (serialised while the per-kernel profiler is on, so each kernel's events time it alone)
   // default: on for batched chunks (measured 158 vs 148 lookups/s at batch 64), off for batch 1
   // (7.16 vs 7.22 ms); HELRM_PIPE overrides
@@ -1981,24 +2053,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     for (int z = 0; periodic && z < zb; z++)
       for (int64_t o = 1; periodic && o < pl->O; o++)
         periodic = pl->giants[o][ml.oi[z + o * zb].second] == pl->giants[0][ml.oi[z].second];
-    static const bool blk_env = getenv("HELRM_BLOCK_MAC") ? atoi(getenv("HELRM_BLOCK_MAC")) != 0 : false;
-    bool done = false;
-    if (periodic && blk_env && blk_zb == zb && !utab.empty()) {
-      BlockMacArgs ba{};
-      ba.U = reinterpret_cast<const uint64_t* const*>(md.extra.p);
-      ba.X = babies.p;
-      ba.xq = nbb * 2 * nlN;
-      ba.out = AB.p;
-      ba.zb = zb;
-      ba.nb = (int)nbb;
-      ba.nblk = (int)pl->O;
-      ba.nlN = nlN;
-      double nu = 0;
-      for (size_t g = 0; g < g_blk; g++) nu += ml.gu[g];
-      ba.bytes = 8.0 * N * nl * (nu + pl->O * (2.0 * nbb + 2.0 * zb));
-      done = launch_block_mac(c->dc(sm), ba, mqp);
-    }
-    if (periodic && !done)
+    if (periodic)
       run_macs(c, ml, md, 0, g_blk, AB.p, zq * 2 * nlN, mqp, true, (int)pl->O, nbb * 2 * nlN, (size_t)zb * 2 * nlN,
                sm, pers);
   }
@@ -2087,7 +2142,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   for (size_t gp = 0; !periodic && gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
     const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
-    if (!periodic && !macs_done)
+    if (!periodic)
       run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
     if (pipe) c->join(sn, sm);
     std::vector<int> rot;   // rotating pairs of the chunk (zero giants need no key switch)
@@ -2439,6 +2494,7 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
                                const uint64_t* const* in, double scale, size_t batch, uint64_t* const* out) {
   return guard([&] {
     need(c && p && rk && (in || batch == 0) && (out || batch == 0), HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(p->mode == HELRM_MODE_DOUBLE, HELRM_ERR_ARG, "helrm_lookup_host runs the double-hoisted mode");
     for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
     const Params& P = c->P;
@@ -2521,6 +2577,7 @@ helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys
     for (size_t i = 0; i < batch * (p ? p->O : 0); i++) out[i] = nullptr;
   return guard([&] {
     need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
     for (size_t q = 0; q < batch; q++) {
       c->evnext = 0;
@@ -2544,6 +2601,7 @@ helrm_status helrm_lookup(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys
 helrm_status helrm_ntt_fwd(helrm_ctx* c, uint64_t* dev, uint32_t first, uint32_t n_limbs, size_t n_polys) {
   return guard([&] {
     need(c && dev, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(first + n_limbs <= c->P.primes.size() && n_limbs >= 1, HELRM_ERR_ARG, "prime range outside the chain");
     ntt_fwd(c, dev, dev, (size_t)n_limbs * n_polys, c->P.map_range(first, n_limbs));
   });
@@ -2552,6 +2610,7 @@ helrm_status helrm_ntt_fwd(helrm_ctx* c, uint64_t* dev, uint32_t first, uint32_t
 helrm_status helrm_ntt_inv(helrm_ctx* c, uint64_t* dev, uint32_t first, uint32_t n_limbs, size_t n_polys) {
   return guard([&] {
     need(c && dev, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(first + n_limbs <= c->P.primes.size() && n_limbs >= 1, HELRM_ERR_ARG, "prime range outside the chain");
     ntt_inv(c, dev, dev, (size_t)n_limbs * n_polys, c->P.map_range(first, n_limbs));
   });
@@ -2560,6 +2619,7 @@ helrm_status helrm_ntt_inv(helrm_ctx* c, uint64_t* dev, uint32_t first, uint32_t
 helrm_status helrm_modup(helrm_ctx* c, const uint64_t* in, uint32_t level, uint32_t digit, uint64_t* out) {
   return guard([&] {
     need(c && in && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(level <= c->P.L && digit < c->P.dnum(level), HELRM_ERR_LEVEL, "bad level/digit");
     modup(c, in, level, (int)digit, out);
   });
@@ -2568,6 +2628,7 @@ helrm_status helrm_modup(helrm_ctx* c, const uint64_t* in, uint32_t level, uint3
 helrm_status helrm_moddown(helrm_ctx* c, const uint64_t* in, uint32_t level, uint64_t* out) {
   return guard([&] {
     need(c && in && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(level <= c->P.L, HELRM_ERR_LEVEL, "bad level");
     moddown(c, in, level, out);
   });
@@ -2577,6 +2638,7 @@ helrm_status helrm_rescale(helrm_ctx* c, const helrm_ct* in, helrm_ct** out) {
   if (out) *out = nullptr;
   return guard([&] {
     need(c && in && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(in->level >= 1, HELRM_ERR_LEVEL, "rescale at level 0");
     helrm_ct* r = new_ct(c, in->level - 1, in->scale / (double)c->P.primes[in->level]);
     rescale_ct(c, in->d, in->level, r->d);
@@ -2588,6 +2650,7 @@ helrm_status helrm_rotate(helrm_ctx* c, const helrm_rotkeys* rk, const helrm_ct*
   if (out) *out = nullptr;
   return guard([&] {
     need(c && rk && in && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     helrm_ct* r = new_ct(c, in->level, in->scale);
     rotate(c, in, rk, k, r);
     *out = r;
@@ -2598,6 +2661,7 @@ helrm_status helrm_rotate_hoisted(helrm_ctx* c, const helrm_rotkeys* rk, const h
                                   size_t n_amounts, helrm_ct* const* ring, size_t n_ring) {
   return guard([&] {
     need(c && rk && in && amounts && ring && n_ring > 0, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     const uint32_t l = in->level;
     for (size_t i = 0; i < n_ring; i++) need(ring[i] && ring[i]->level == l, HELRM_ERR_LEVEL, "ring ct level");
     DBuf D(c, (size_t)c->P.dnum(l) * (l + 1 + c->P.K) * c->P.N);
@@ -2610,6 +2674,7 @@ helrm_status helrm_ct_random(helrm_ctx* c, uint64_t seed, uint32_t ct_index, uin
   if (out) *out = nullptr;
   return guard([&] {
     need(c && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
     need(level <= c->P.L, HELRM_ERR_LEVEL, "level above L");
     helrm_ct* ct = new_ct(c, level, std::ldexp(1.0, c->P.log_scale));
     LimbMap m = c->P.map_q(level);
@@ -2645,6 +2710,7 @@ helrm_status helrm_comm_unique_id(uint8_t* id) {
 helrm_status helrm_comm_init(helrm_ctx* c, const uint8_t* id, int rank, int world) {
   return guard([&] {
     need(c && id && world >= 1 && rank >= 0 && rank < world, HELRM_ERR_ARG, "bad argument");
+    DevGuard dg_(c->device);
     HCUDA(cudaSetDevice(c->device));
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
@@ -2656,39 +2722,87 @@ helrm_status helrm_comm_init(helrm_ctx* c, const uint8_t* id, int rank, int worl
   });
 }
 
+// D20 with the giant pairs split over `parts` partitions: partition r
+// computes the partial Q_l P accumulators of its giant range
+// (helrm_dist_range), the partials are summed as uint64 words without
+// reduction (what ncclAllReduce(ncclUint64, ncclSum) does), k_modred reduces
+// them, and L6-L8 finish.  world > 1: this rank's partition, NCCL combine;
+// virt > 0: all `virt` partitions in this process, one after another on the
+// context stream, summed by a device kernel (the emulation of the collective
+// on one GPU: nothing waits on another rank).
+static void lookup_split(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                         size_t batch, helrm_ct** out, int virt) {
+  need(p->mode == HELRM_MODE_DOUBLE, HELRM_ERR_ARG, "the distributed lookup runs the double-hoisted mode");
+  for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
+  const Params& P = c->P;
+  const size_t nlN = (size_t)(p->level + 1 + P.K) * P.N, nqN = (size_t)(p->level + 1) * P.N;
+  const size_t owords = (size_t)p->O * 2 * nlN;
+  const int parts = virt > 0 ? virt : c->world;
+  for (size_t q = 0; q < batch; q++) {
+    const helrm_ct* const* cin = in + q * p->C;
+    DBuf O(c, owords), X(c, (size_t)p->C * 2 * nqN), S(c, (size_t)p->O * 2 * p->level * P.N);
+    for (int64_t ci = 0; ci < p->C; ci++) {
+      need(cin[ci] != nullptr && cin[ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's");
+      if (virt == 0 && c->world > 1)   // the query lives on rank 0: broadcast it into every rank's staging buffer
+        HNCCL(nccl().broadcast(cin[ci]->d, X.p + ci * 2 * nqN, 2 * nqN, ncclUint64, 0, c->comm, c->stream));
+      else
+        HCUDA(cudaMemcpyAsync(X.p + ci * 2 * nqN, cin[ci]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    HCUDA(cudaMemsetAsync(O.p, 0, owords * 8, c->stream));
+    if (virt > 0) {
+      DBuf part(c, owords);
+      for (int r = 0; r < virt; r++) {
+        int64_t lo = 0, hi = 0;
+        (void)helrm_dist_range(count_pairs(p), virt, r, &lo, &hi);
+        HCUDA(cudaMemsetAsync(part.p, 0, owords * 8, c->stream));
+        lookup_double_part(c, p, rk, X.p, 1, lo, hi, part.p);
+        launch_add_u64(c->dc(), O.p, part.p, owords);   // the all-reduce's exact uint64 sum
+      }
+    } else {
+      int64_t lo = 0, hi = INT64_MAX;
+      (void)helrm_dist_range(count_pairs(p), c->world, c->rank, &lo, &hi);
+      lookup_double_part(c, p, rk, X.p, 1, lo, hi, O.p);
+      if (c->world > 1)
+        HNCCL(nccl().allReduce(O.p, O.p, owords, ncclUint64, ncclSum, c->comm, c->stream));
+    }
+    // L5: each partial word is < q, so the sum is < parts q < 2^64 (parts < 2^13); reduce mod q
+    if (parts > 1)
+      for (int64_t h = 0; h < 2 * p->O; h++) launch_modred(c->dc(), O.p + (size_t)h * nlN, P.map_qp(p->level));
+    lookup_finish(c, p, rk, O.p, 1, S.p);
+    emit_outputs(c, p, S.p, 1, cin[0]->scale, out + q * p->O);
+  }
+}
+
 helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
                                size_t batch, helrm_ct** out) {
   if (out)
     for (size_t i = 0; i < batch * (p ? p->O : 0); i++) out[i] = nullptr;
   return guard([&] {
     need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
-    need(p->mode == HELRM_MODE_DOUBLE, HELRM_ERR_ARG, "the distributed lookup runs the double-hoisted mode");
-    for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
-    const Params& P = c->P;
-    const size_t nlN = (size_t)(p->level + 1 + P.K) * P.N;
-    int64_t lo = 0, hi = INT64_MAX;
-    (void)helrm_dist_range(count_pairs(p), c->world, c->rank, &lo, &hi);
-    for (size_t q = 0; q < batch; q++) {
-      const helrm_ct* const* cin = in + q * p->C;
-      for (int64_t ci = 0; ci < p->C; ci++) {
-        need(cin[ci] != nullptr && cin[ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's");
-        if (c->world > 1)   // the query lives on rank 0: broadcast it (in place on every rank's buffer)
-          HNCCL(nccl().broadcast(cin[ci]->d, cin[ci]->d, (size_t)2 * (p->level + 1) * P.N, ncclUint64, 0, c->comm,
-                                 c->stream));
-      }
-      DBuf O(c, (size_t)p->O * 2 * nlN), X(c, (size_t)p->C * 2 * (p->level + 1) * P.N),
-          S(c, (size_t)p->O * 2 * p->level * P.N);
-      HCUDA(cudaMemsetAsync(O.p, 0, (size_t)p->O * 2 * nlN * 8, c->stream));
-      stage_inputs(c, cin, p->C, 2 * (p->level + 1) * P.N, X.p);
-      lookup_double_part(c, p, rk, X.p, 1, lo, hi, O.p);
-      if (c->world > 1) {
-        // L5: exact sum of the partial accumulators (each < q, so < world q < 2^64), then mod q
-        HNCCL(nccl().allReduce(O.p, O.p, (size_t)p->O * 2 * nlN, ncclUint64, ncclSum, c->comm, c->stream));
-        for (int64_t h = 0; h < 2 * p->O; h++) launch_modred(c->dc(), O.p + (size_t)h * nlN, P.map_qp(p->level));
-      }
-      lookup_finish(c, p, rk, O.p, 1, S.p);
-      emit_outputs(c, p, S.p, 1, cin[0]->scale, out + q * p->O);
-    }
+    DevGuard dg_(c->device);
+    lookup_split(c, p, rk, in, batch, out, 0);
+  });
+}
+
+helrm_status helrm_lookup_dist_virtual(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                       const helrm_ct* const* in, size_t batch, int parts, helrm_ct** out) {
+  if (out)
+    for (size_t i = 0; i < batch * (p ? p->O : 0); i++) out[i] = nullptr;
+  return guard([&] {
+    need(c && p && rk && in && out && parts >= 1 && parts < 8192, HELRM_ERR_ARG, "bad argument");
+    DevGuard dg_(c->device);
+    lookup_split(c, p, rk, in, batch, out, parts);
+  });
+}
+
+helrm_status helrm_modred(helrm_ctx* c, uint64_t* dev, uint32_t level, size_t n_polys) {
+  return guard([&] {
+    need(c && (dev || n_polys == 0), HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
+    need(level <= c->P.L, HELRM_ERR_LEVEL, "level above L");
+    const LimbMap m = c->P.map_qp(level);
+    for (size_t i = 0; i < n_polys; i++) launch_modred(c->dc(), dev + i * m.n * c->P.N, m);
+    HCUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -148,6 +148,7 @@ struct DevCtx {
   uint32_t log_n, N;
   cudaStream_t stream;
   int persist;                // > 0: HBM-bound MAC / key-switch kernels run persistent, persist CTAs per SM
+  int n_sm;                   // multiprocessors of the context's device (148 on B200)
   uint64_t* launches;         // host counter
   Profiler* prof;
 };
@@ -215,16 +216,6 @@ struct NttEpi {
   const uint64_t* sp = nullptr;
   int accumulate = 0;            // out += instead of out =
 };
-// Optional base conversion fused into the forward NTT's pass 1 (D14 inside
-// ModUp / ModDown): limb gl = (poly, row r) with poly = g ncv + k is not read
-// from src but computed as sum_b y_g[row0 + b] cf_kr[b] mod q_r from the
-// y-form sources y + g ys (tab[k tab_rows + r] holds row0, nb, cf).
-struct NttConvIn {
-  const ConvRowDev* tab = nullptr;
-  int tab_rows = 0, ncv = 1, nb_max = 0;
-  const uint64_t* y = nullptr;
-  size_t ys = 0;
-};
 // NTT over n_total limbs: limb y = (poly y / map.n, limb y % map.n) lives at
 // src + (y / map.n) * src_stride + (y % map.n) * N (same for dst; stride 0 =
 // contiguous polys of map.n limbs).  src == dst allowed.
@@ -232,14 +223,9 @@ struct NttConvIn {
 // lidx (optional device table): launch limb v is layout limb lidx[v]
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0, bool din = false,
-                    const uint32_t* lidx = nullptr, const NttEpi* epi = nullptr,
-                    const NttConvIn* conv = nullptr);
-// single-kernel forward NTT on 4-CTA clusters (kernels_ntt_cl.cu), N = 2^16;
-// false if it does not apply (the caller then runs the two-pass kernels)
+                    const uint32_t* lidx = nullptr, const NttEpi* epi = nullptr);
 // pass-2 / pass-A block grouping into constant memory (a function of log N only)
 void ntt_set_grp(uint32_t log_n, const uint32_t* grp, size_t n);
-bool ntt_fwd_cluster(const DevCtx& c, const uint64_t* src, uint64_t* dst, size_t n_total, const LimbMap& map,
-                     size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi& epi);
 // post (optional, per limb of map): final factor (w, w/q) replacing N^-1
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t src_stride = 0, size_t dst_stride = 0,
@@ -270,6 +256,8 @@ void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const L
                       int accumulate);
 // out[l] = in[l] mod q_l for in < 2^64 (after a uint64 sum all-reduce)
 void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map);
+// x[i] += y[i] as uint64 words, i < n (the exact sum of the all-reduce)
+void launch_add_u64(const DevCtx& c, uint64_t* x, const uint64_t* y, size_t n);
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,
                          const LimbMap& map);
 
@@ -348,47 +336,6 @@ struct KipMulti {
   int alpha = 1;
 };
 void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map);
-
-// Fused D20 L2 + L3 for one ciphertext (k_baby_mac): a CTA computes every baby
-// pair of its 128-position tile of one limb into shared memory (babies
-// a.key[i] -> slot i + slot0, slot j0 = the rotation-0 pair (P c0, P c1) when
-// present) and then runs the inner sums of every giant pack against the
-// streamed plaintexts -- the baby pairs never go to HBM.
-struct FusedTerm {
-  int slot;                              // baby pair slot in shared memory
-  int pad;
-  const uint64_t* u[4];                  // plaintext per giant of the pack (D-form) or null
-};
-struct BabyMacArgs {
-  const FusedTerm* terms;
-  const int4* groups;                    // as launch_diag_mac
-  int n_groups;
-  int n_slots, slot0, j0;                // baby slots; first key slot; slot of rotation 0 (-1: none)
-  const uint64_t* c1;                    // [level+1][N] for the rotation-0 pair
-  uint64_t* out;                         // pair z at out + z out_stride (A), + half (B)
-  size_t out_stride, half;
-  double bytes;                          // algorithmic HBM bytes of the launch (profiler)
-};
-constexpr int kBabyMacTile = 128;
-
-// D20 L3 for output blocks that share every plaintext (LLM layout L2): a CTA
-// stages the baby pairs of all blocks for 16 positions of one limb in shared
-// memory; 8 workers per position each own up to 3 giants and run their exact
-// FP64 MACs for all blocks, so every plaintext value is loaded from HBM once
-// and every baby value once.
-struct BlockMacArgs {
-  const uint64_t* const* U;              // [zb][nb] plaintext per (giant, baby slot) or null (device table)
-  const uint64_t* X;                     // baby slot jj of block o at X + o xq + jj 2 nlN (A), + nlN (B)
-  size_t xq;
-  uint64_t* out;                         // pair (o, z) at out + (o zb + z) 2 nlN (A), + nlN (B)
-  int zb, nb, nblk;
-  size_t nlN;
-  double bytes;
-};
-bool launch_block_mac(const DevCtx& c, const BlockMacArgs& a, const LimbMap& map);
-bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map);
-// the same fused step fed by bulk async copies (kernels_mac_bulk.cu; HELRM_FUSED_BM=2)
-bool launch_baby_mac_bulk(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map);
 
 // D20 L3 work list.  Giants are packed kGiantPack at a time: a term is one
 // baby pair x = (x0, x1) with the plaintext u of each giant of the pack that

@@ -85,15 +85,15 @@ __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double 
 // The body of one CTA: tile bx of launch limb `limb`; the pass-1 -> pass-2
 // intermediate of that limb lives at scratch + slot N.  CG: scratch reads
 // bypass L1 (the fused kernel reuses scratch slots inside one launch).
-template <int SLOG, int MODE, int NB = 1, bool CG = false>
+template <int SLOG, int MODE, bool CG = false>
 __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t limb, size_t slot,
                                              const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                              const PrimeDev* __restrict__ primes, const LimbMap& map, size_t limb0,
                                              size_t gstride, int log_n, const double* __restrict__ twb,
                                              const uint8_t* __restrict__ tpos, const uint32_t* __restrict__ lidx,
-                                             const NttEpi& epi, const NttConvIn& cv) {
+                                             const NttEpi& epi) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
-  constexpr bool P1 = MODE != 1;  // MODE 2: pass 1 on centred doubles (conversion output); MODE 3: conversion fused
+  constexpr bool P1 = MODE != 1;  // MODE 2: pass 1 on centred doubles (conversion output)
   const int N = 1 << log_n;
   const size_t gl = lidx ? lidx[limb0 + limb] : limb0 + limb;
   const int pr = map.pr[gl % map.n];
@@ -110,26 +110,7 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
   const double2* __restrict__ tw1 = reinterpret_cast<const double2*>(tb);
   const double2* __restrict__ twA = P1 ? tw1 : reinterpret_cast<const double2*>(tb + 512) + (size_t)gsub * 256;
   double r[kEPT];
-  if (MODE == 3) {
-    // D14 on the fly: out_r = sum_b y[row0 + b] cf[b] mod q_r (centred), the y-form sources
-    // being shared by every converted row of the digit (L2-resident)
-    const size_t poly = gl / map.n;
-    const ConvRowDev& cr = cv.tab[(size_t)(poly % cv.ncv) * cv.tab_rows + gl % map.n];
-    const uint64_t* ysrc = cv.y + (poly / cv.ncv) * cv.ys + (size_t)cr.src_row0 * N;
-    const int nb = cr.nb;
-    double2 cf[NB];
-#pragma unroll
-    for (int b = 0; b < NB; b++) cf[b] = cr.cf[b];
-#pragma unroll
-    for (int k = 0; k < kEPT; k++) {
-      const size_t pos = (size_t)(t + TS * k) * 256 + gsub;
-      double acc = 0.0;
-#pragma unroll
-      for (int b = 0; b < NB; b++)
-        if (b < nb) acc += mmul(u2d(ysrc[(size_t)b * N + pos]), cf[b].x, cf[b].y, q);   // each in [-q/2, q/2]
-      r[k] = cred(acc, q, qi);
-    }
-  } else {
+  {
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const int e = t + TS * k;
@@ -257,7 +238,7 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
   }
 }
 
-template <int SLOG, int MODE, int NB = 1>
+template <int SLOG, int MODE>
 __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                                       const PrimeDev* __restrict__ primes,
                                                       const __grid_constant__ LimbMap map, size_t limb0, size_t gstride, int log_n,
@@ -265,92 +246,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd(const uint64_t* __restr
                                                       const double* __restrict__ twb,
                                                       const uint8_t* __restrict__ tpos,
                                                       const uint32_t* __restrict__ lidx,
-                                                      const __grid_constant__ NttEpi epi,
-                                                      const __grid_constant__ NttConvIn cv) {
+                                                      const __grid_constant__ NttEpi epi) {
   pdl_wait_trigger();
   __shared__ double sm[MODE != 1 ? kTileElems : 16 * kBlkPad];
   (void)grp;
-  ntt_fwd_body<SLOG, MODE, NB>(sm, blockIdx.x, blockIdx.y, blockIdx.y, src, dst, primes, map, limb0, gstride, log_n, twb,
-                               tpos, lidx, epi, cv);
-}
-
-// Both forward passes in one persistent launch (HELRM_NTT_FUSED): CTAs claim
-// work items in a fixed order from a global counter.  Step u holds the g1
-// pass-1 tiles of limb u and the g2 pass-2 tiles of limb u - kFusedLag, so a
-// limb's pass 2 runs ~kFusedLag limbs after its pass 1, while its intermediate
-// (a ring of kFusedSlots limb slots in the scratch, 32 MiB at N = 2^16) is
-// still in L2: pass 2 reads it from L2 instead of HBM, and HBM sees one read
-// and one write per coefficient.  A pass-2 tile waits until the limb's g1
-// pass-1 tiles have signalled; a pass-1 tile reusing a slot waits until the
-// previous occupant's g2 pass-2 tiles have read it.  Every wait is on items
-// with smaller indices, all claimed by running CTAs, so the launch always
-// makes progress.  sync: [0] the work counter, [1 + L] pass-1 tiles done of
-// limb L, [1 + n + L] pass-2 tiles done (zeroed before the launch).
-// Measured slower than the two launches (Criteo b1 7.10 vs 6.86 ms, microbenchmark 1677 vs
-// 1882 GB/s; larger or smaller lags, and a static round-robin deal instead of the claim
-// counter, are slower still): the per-item claim and the waits cost more than the L2-resident
-// intermediate saves.  Off unless HELRM_NTT_FUSED=1.
-constexpr int kFusedLag = 24, kFusedSlots = 64;   // defaults (HELRM_NTT_LAG / HELRM_NTT_SLOTS)
-
-__device__ __forceinline__ void spin_until(const int* flag, int target) {
-  while (atomicAdd(const_cast<int*>(flag), 0) < target) __nanosleep(64);
-}
-
-template <int SLOG, int MODE0>
-__global__ void __launch_bounds__(kThreads, 4) k_ntt_fwd_fused(const uint64_t* __restrict__ src,
-                                                               uint64_t* __restrict__ dst, uint64_t* __restrict__ scratch,
-                                                               const PrimeDev* __restrict__ primes,
-                                                               const __grid_constant__ LimbMap map, size_t n,
-                                                               size_t gstride, size_t dstride, int log_n,
-                                                               const double* __restrict__ twb,
-                                                               const uint8_t* __restrict__ tpos,
-                                                               const uint32_t* __restrict__ lidx,
-                                                               const __grid_constant__ NttEpi epi, int* __restrict__ sync,
-                                                               int lag, int slots) {
-  __shared__ double sm[16 * kBlkPad > kTileElems ? 16 * kBlkPad : kTileElems];
-  __shared__ int item_s;
-  const int N = 1 << log_n;
-  const int g1 = (1 << SLOG) / kEPT, g2 = (N / 256) / 16, per = g1 + g2;
-  const size_t total = (n + lag) * (size_t)per;
-  int* done1 = sync + 1;
-  int* done2 = sync + 1 + n;
-  const NttConvIn cv{};
-  for (;;) {
-    if (threadIdx.x == 0) item_s = atomicAdd(sync, 1);
-    __syncthreads();
-    const size_t item = (size_t)item_s;
-    __syncthreads();   // item_s is rewritten by the next claim
-    if (item >= total) return;
-    const size_t step = item / per;
-    const int r = (int)(item % per);
-    if (r < g1) {   // pass 1 of limb `step`
-      if (step >= n) continue;
-      const size_t L = step, slot = L % slots;
-      if (L >= (size_t)slots) {   // the slot's previous limb must have been read by its pass 2
-        if (threadIdx.x == 0) spin_until(done2 + (L - slots), g2);
-        __syncthreads();
-      }
-      ntt_fwd_body<SLOG, MODE0, 1, true>(sm, (unsigned)r, L, slot, src, scratch, primes, map, 0, gstride, log_n, twb,
-                                         tpos, lidx, epi, cv);
-      __syncthreads();   // every thread's scratch writes are issued
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(done1 + L, 1);
-      }
-    } else {        // pass 2 of limb `step - kFusedLag`
-      if (step < (size_t)lag) continue;
-      const size_t L = step - lag, slot = L % slots;
-      if (threadIdx.x == 0) {
-        spin_until(done1 + L, g1);
-        __threadfence();
-      }
-      __syncthreads();
-      ntt_fwd_body<8, 1, 1, true>(sm, (unsigned)(r - g1), L, slot, scratch, dst, primes, map, 0, dstride, log_n, twb,
-                                  tpos, lidx, epi, cv);
-      __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(done2 + L, 1);
-    }
-  }
+  ntt_fwd_body<SLOG, MODE>(sm, blockIdx.x, blockIdx.y, blockIdx.y, src, dst, primes, map, limb0, gstride, log_n, twb,
+                           tpos, lidx, epi);
 }
 
 // Inverse (Gentleman-Sande), mirror of k_ntt_fwd.
@@ -471,17 +372,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
 }
 
 // ---------------------------------------------------------------- launchers
-// extra dynamic shared memory per NTT CTA (HELRM_NTT_SMEM bytes): caps NTT CTAs per SM so
-// that concurrent HBM-bound kernels of the pipeline find room on every SM (experiment knob)
-static size_t ntt_xsmem() {
-  static const size_t v = getenv("HELRM_NTT_SMEM") ? (size_t)atoi(getenv("HELRM_NTT_SMEM")) : 0;
-  return v;
-}
-template <class K>
-static void allow_xsmem(K k) {
-  if (ntt_xsmem()) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ntt_xsmem());
-}
-
 static size_t chunk_limbs(int N) {
   static const size_t env = getenv("HELRM_NTT_CHUNK") ? (size_t)atoi(getenv("HELRM_NTT_CHUNK")) : 0;
   // 256 MiB of scratch per chunk (512 limbs at N = 2^16): larger launches lose less to partial
@@ -495,23 +385,19 @@ size_t ntt_scratch_words(int log_n) { return chunk_limbs(1 << log_n) * ((size_t)
 template <int SLOG>
 static void fwd_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, unsigned cnt,
                       const LimbMap& map, size_t off, size_t ss, size_t ds, bool din, const uint32_t* lidx,
-                      const NttEpi& epi, const NttConvIn& cv) {
+                      const NttEpi& epi) {
   constexpr int TS = (1 << SLOG) / kEPT;
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_fwd_p1", 8.0 * c.N * cnt);
-    decltype(&k_ntt_fwd<SLOG, 0>) k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
-    if (cv.tab)
-      k1 = cv.nb_max <= 1 ? k_ntt_fwd<SLOG, 3, 1> : cv.nb_max <= 2 ? k_ntt_fwd<SLOG, 3, 2>
-           : cv.nb_max <= 4 ? k_ntt_fwd<SLOG, 3, 4> : k_ntt_fwd<SLOG, 3, 8>;
-    allow_xsmem(k1);
-    launch_pdl(k1, dim3(g1, cnt), dim3(kThreads), ntt_xsmem(), c.stream, src, scratch, c.primes, map, off, ss, c.log_n,
-               c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
+    auto k1 = din ? k_ntt_fwd<SLOG, 2> : k_ntt_fwd<SLOG, 0>;
+    launch_pdl(k1, dim3(g1, cnt), dim3(kThreads), 0, c.stream, src, scratch, c.primes, map, off, ss, c.log_n,
+               c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi);
   }
   {
     ProfScope ps_(c, "ntt_fwd_p2", 8.0 * c.N * cnt);
-    allow_xsmem(k_ntt_fwd<8, 1>);
-    launch_pdl(k_ntt_fwd<8, 1>, dim3(dim3(g2, cnt)), dim3(kThreads), ntt_xsmem(), c.stream, scratch, dst, c.primes, map, off, ds, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi, cv);
+    launch_pdl(k_ntt_fwd<8, 1>, dim3(dim3(g2, cnt)), dim3(kThreads), 0, c.stream, scratch, dst, c.primes, map, off, ds,
+               c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, lidx, epi);
   }
   *c.launches += 2;
 }
@@ -524,57 +410,27 @@ static void inv_chunk(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint6
   const int g1 = TS, g2 = (c.N / 256) / 16;
   {
     ProfScope ps_(c, "ntt_inv_pa", 8.0 * c.N * cnt);
-    allow_xsmem(k_ntt_inv<8, 1>);
-    launch_pdl(k_ntt_inv<8, 1>, dim3(dim3(g2, cnt)), dim3(kThreads), ntt_xsmem(), c.stream, src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, nullptr, lidx);
+    launch_pdl(k_ntt_inv<8, 1>, dim3(dim3(g2, cnt)), dim3(kThreads), 0, c.stream, src, scratch, c.primes, map, off, ss, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, nullptr, lidx);
   }
   {
     ProfScope ps_(c, "ntt_inv_pb", 8.0 * c.N * cnt);
-    allow_xsmem(k_ntt_inv<SLOG, 0>);
-    launch_pdl(k_ntt_inv<SLOG, 0>, dim3(dim3(g1, cnt)), dim3(kThreads), ntt_xsmem(), c.stream, scratch, dst, c.primes, map, off, ds, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, post, lidx);
+    launch_pdl(k_ntt_inv<SLOG, 0>, dim3(dim3(g1, cnt)), dim3(kThreads), 0, c.stream, scratch, dst, c.primes, map, off, ds, c.log_n, c.ntt_grp, c.ntt_twb, c.ntt_tpos, post, lidx);
   }
   *c.launches += 2;
-}
-
-static bool ntt_fwd_fused(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                          const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi& epi) {
-  static const int env = getenv("HELRM_NTT_FUSED") ? atoi(getenv("HELRM_NTT_FUSED")) : 0;
-  static const size_t min_limbs = getenv("HELRM_NTT_FUSED_MIN") ? (size_t)atoi(getenv("HELRM_NTT_FUSED_MIN")) : 128;
-  if (!env || c.log_n != 16 || n_total < min_limbs) return false;
-  static const int lag = getenv("HELRM_NTT_LAG") ? atoi(getenv("HELRM_NTT_LAG")) : kFusedLag;
-  static const int slots = getenv("HELRM_NTT_SLOTS") ? atoi(getenv("HELRM_NTT_SLOTS")) : kFusedSlots;
-  if (slots <= lag) return false;   // a slot must outlive its limb's lag
-  // the scratch holds the slot ring, then the work counter and per-limb flags (each stream that
-  // runs NTTs concurrently has its own scratch, so the flags are private to the launch)
-  const size_t sync_words = ((2 * n_total + 1) * sizeof(int) + 7) / 8;
-  if ((size_t)slots * c.N + sync_words > chunk_limbs(c.N) * c.N) return false;
-  int* sync = reinterpret_cast<int*>(scratch + (size_t)slots * c.N);
-  HCUDA(cudaMemsetAsync(sync, 0, (2 * n_total + 1) * sizeof(int), c.stream));
-  ProfScope ps_(c, "ntt_fwd_fused", 16.0 * c.N * n_total);
-  auto k = din ? k_ntt_fwd_fused<8, 2> : k_ntt_fwd_fused<8, 0>;
-  static int occ = 0;
-  if (!occ) HCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0));
-  const unsigned grid = 148u * (unsigned)std::max(1, occ);
-  k<<<grid, kThreads, 0, c.stream>>>(src, dst, scratch, c.primes, map, n_total, ss, ds, c.log_n, c.ntt_twb, c.ntt_tpos,
-                                     lidx, epi, sync, lag, slots);
-  (*c.launches)++;
-  HCUDA(cudaGetLastError());
-  return true;
 }
 
 template <bool FWD>
 static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
                     const LimbMap& map, size_t ss, size_t ds, const double2* post, bool din, const uint32_t* lidx,
-                    const NttEpi& epi = NttEpi{}, const NttConvIn& cv = NttConvIn{}) {
+                    const NttEpi& epi = NttEpi{}) {
   if (ss == 0) ss = (size_t)map.n * c.N;
   if (ds == 0) ds = (size_t)map.n * c.N;
-  if (FWD && !cv.tab && ntt_fwd_cluster(c, src, dst, n_total, map, ss, ds, din, lidx, epi)) return;
-  if (FWD && !cv.tab && ntt_fwd_fused(c, src, dst, scratch, n_total, map, ss, ds, din, lidx, epi)) return;
   const size_t ch = chunk_limbs(c.N);
   for (size_t off = 0; off < n_total; off += ch) {
     const unsigned cnt = (unsigned)std::min(ch, n_total - off);
 #define HELRM_NTT_CASE(LG, SL)                                                  \
   case LG:                                                                      \
-    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din, lidx, epi, cv);    \
+    if (FWD) fwd_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, din, lidx, epi);        \
     else inv_chunk<SL>(c, src, dst, scratch, cnt, map, off, ss, ds, post, lidx);        \
     break;
     switch (c.log_n) {
@@ -591,10 +447,8 @@ static void ntt_any(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_
 }
 
 void launch_ntt_fwd(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,
-                    const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi* epi,
-                    const NttConvIn* conv) {
-  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din, lidx, epi ? *epi : NttEpi{},
-                conv ? *conv : NttConvIn{});
+                    const LimbMap& map, size_t ss, size_t ds, bool din, const uint32_t* lidx, const NttEpi* epi) {
+  ntt_any<true>(c, src, dst, scratch, n_total, map, ss, ds, nullptr, din, lidx, epi ? *epi : NttEpi{});
 }
 
 void launch_ntt_inv(const DevCtx& c, const uint64_t* src, uint64_t* dst, uint64_t* scratch, size_t n_total,

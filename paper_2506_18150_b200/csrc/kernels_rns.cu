@@ -634,260 +634,6 @@ __global__ void __launch_bounds__(256) k_diag_mac(const MacTerm* __restrict__ te
   }
 }
 
-// D20 L2 + L3 fused for one ciphertext (see BabyMacArgs).  Phase 1 is
-// k_kip_multi on a 128-position tile (digits + c0 staged with a halo, keys
-// streamed, one baby per round) writing the pairs to shared memory; phase 2
-// is k_diag_mac<true, 1> reading the pairs from shared memory (4 terms per
-// round: 16 plaintext loads in flight per thread).
-template <int DNUM>
-__global__ void __launch_bounds__(kBabyMacTile) k_baby_mac(const __grid_constant__ KipMulti a,
-                                                          const __grid_constant__ BabyMacArgs m,
-                                                          const PrimeDev* __restrict__ primes,
-                                                          const __grid_constant__ LimbMap map, uint32_t N) {
-  pdl_wait_trigger();
-  constexpr int T = kBabyMacTile, G = kGiantPack;
-  extern __shared__ double shd[];
-  const int l = blockIdx.y, tid = threadIdx.x;
-  const uint32_t n = N / 2, p0 = blockIdx.x * T, half = p0 >= n ? n : 0;
-  const uint32_t span = T + a.max_rot;
-  double* sb = shd + (DNUM + 1) * span;             // baby pairs [slot][2][T]
-  const uint32_t chain = map.pr[l];
-  const PrimeDev& P = primes[chain];
-  const double q = P.qd, qi = P.qinv;
-  const bool has_c0 = l <= (int)a.level;
-  const int kown = (a.own && has_c0) ? l / a.alpha : -1;
-  for (uint32_t e = tid; e < span; e += T) {
-    uint32_t j = p0 - half + e;
-    j = j >= n ? j - n : j;
-    const size_t src = (size_t)l * N + half + j;
-#pragma unroll
-    for (int k = 0; k < DNUM; k++)
-      shd[k * span + e] = fm::u2d(k == kown ? a.own[src] : a.digits[(size_t)k * a.digit_stride + src]);
-    shd[DNUM * span + e] = has_c0 ? fm::u2d(a.c0[src]) : 0.0;
-  }
-  const uint32_t p = p0 + tid;
-  const double pm = has_c0 ? fm::u2c(a.p_mod[l], q) : 0.0;
-  // rotation-0 pair (P c0, P c1) over Q_l, 0 over P (D20 L2, j = 0)
-  if (m.j0 >= 0) {
-    double v0 = 0.0, v1 = 0.0;
-    if (has_c0) {
-      fm::FAcc x0, x1;
-      fm::fmac(x0, fm::u2d(a.c0[(size_t)l * N + p]), pm);
-      fm::fmac(x1, fm::u2d(m.c1[(size_t)l * N + p]), pm);
-      v0 = fm::fred(x0, q, qi);
-      v1 = fm::fred(x1, q, qi);
-    }
-    sb[(m.j0 * 2) * T + tid] = v0;
-    sb[(m.j0 * 2 + 1) * T + tid] = v1;
-  }
-  __syncthreads();
-  for (int j = 0; j < a.n; j++) {
-    const uint64_t* kb = a.key[j] + (size_t)chain * N + p;
-    uint64_t kv0[DNUM], kv1[DNUM];
-#pragma unroll
-    for (int k = 0; k < DNUM; k++) {
-      kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
-      kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
-    }
-    const uint32_t e = tid + a.rot[j];
-    fm::FAcc acc0, acc1;
-#pragma unroll
-    for (int k = 0; k < DNUM; k++) {
-      const double dv = shd[k * span + e];
-      fm::fmac(acc0, dv, fm::bits2d(kv0[k]));
-      fm::fmac(acc1, dv, fm::bits2d(kv1[k]));
-    }
-    if (has_c0) fm::fmac(acc0, shd[DNUM * span + e], pm);
-    const int sl = m.slot0 + j;
-    sb[(sl * 2) * T + tid] = fm::fred(acc0, q, qi);
-    sb[(sl * 2 + 1) * T + tid] = fm::fred(acc1, q, qi);
-  }
-  __syncthreads();
-  // phase 2: inner sums of every giant pack (the pack's term list staged in shared memory,
-  // so the plaintext loads do not wait on a pointer load)
-  __shared__ FusedTerm stm[64];
-  const size_t o = (size_t)l * N + p;
-  for (int gi = 0; gi < m.n_groups; gi++) {
-    const int4 gr = m.groups[gi];
-    fm::FAcc acc0[G], acc1[G];
-    int cnt = 0;
-    for (int t = 0; t < gr.y; t += 4) {
-      if (t % 64 == 0) {
-        __syncthreads();
-        for (int k = tid; k < min(64, gr.y - t); k += T) stm[k] = m.terms[gr.x + t + k];
-        __syncthreads();
-      }
-      const int nr = min(4, gr.y - t);
-      uint64_t u[4][G];
-      int sl[4];
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        if (r < nr) {
-          const FusedTerm& ft = stm[(t + r) % 64];
-          sl[r] = ft.slot;
-#pragma unroll
-          for (int g = 0; g < G; g++) u[r][g] = ft.u[g] ? __ldcs(ft.u[g] + o) : 0;
-        } else {
-          sl[r] = 0;
-#pragma unroll
-          for (int g = 0; g < G; g++) u[r][g] = 0;
-        }
-      }
-      if (cnt + 4 > fm::kFAccTerms) {
-#pragma unroll
-        for (int g = 0; g < G; g++) {
-          fm::fold(acc0[g], q, qi);
-          fm::fold(acc1[g], q, qi);
-        }
-        cnt = 0;
-      }
-      cnt += 4;
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const double xa = sb[(sl[r] * 2) * T + tid], xb = sb[(sl[r] * 2 + 1) * T + tid];
-#pragma unroll
-        for (int g = 0; g < G; g++) {
-          const double ud = fm::bits2d(u[r][g]);
-          fm::fmac(acc0[g], ud, xa);
-          fm::fmac(acc1[g], ud, xb);
-        }
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-      if (g < gr.w) {
-        uint64_t* dst = m.out + (size_t)(gr.z + g) * m.out_stride;
-        dst[o] = fm::c2u(fm::fred(acc0[g], q, qi), P.rc.q);
-        dst[m.half + o] = fm::c2u(fm::fred(acc1[g], q, qi), P.rc.q);
-      }
-    }
-  }
-}
-
-bool launch_baby_mac(const DevCtx& c, const KipMulti& a, const BabyMacArgs& m, const LimbMap& map) {
-  const size_t smem = ((size_t)(a.dnum + 1) * (kBabyMacTile + a.max_rot) + (size_t)m.n_slots * 2 * kBabyMacTile) * 8;
-  if (smem > 200 * 1024 || c.N % kBabyMacTile) return false;
-  decltype(&k_baby_mac<1>) kern = nullptr;
-  switch (a.dnum) {
-    case 1: kern = k_baby_mac<1>; break;
-    case 2: kern = k_baby_mac<2>; break;
-    case 3: kern = k_baby_mac<3>; break;
-    case 4: kern = k_baby_mac<4>; break;
-    case 5: kern = k_baby_mac<5>; break;
-    case 6: kern = k_baby_mac<6>; break;
-    case 7: kern = k_baby_mac<7>; break;
-    default: return false;
-  }
-  ProfScope ps_(c, "baby_mac", m.bytes);
-  HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  launch_pdl(kern, dim3(dim3(c.N / kBabyMacTile, map.n)), dim3(kBabyMacTile), smem, c.stream, a, m, c.primes, map, c.N);
-  (*c.launches)++;
-  HCUDA(cudaGetLastError());
-  return true;
-}
-
-// The plaintext values stream through a cp.async ring of kBmStages terms in
-// shared memory (no registers held by loads in flight: ~40 KB in flight per
-// SM at 2 CTAs/SM, what the HBM latency needs).
-constexpr int kBmStages = 8;
-template <int NBLK, int GT>
-__global__ void __launch_bounds__(128) k_block_mac(const __grid_constant__ BlockMacArgs a,
-                                                  const PrimeDev* __restrict__ primes,
-                                                  const __grid_constant__ LimbMap map, uint32_t N) {
-  pdl_wait_trigger();
-  constexpr int T = 16, W = 8;
-  extern __shared__ double sx[];                 // [nb][NBLK][2][T] babies, then the ring [S][zb][T]
-  double* ring = sx + (size_t)a.nb * NBLK * 2 * T;
-  const int tid = threadIdx.x, pl = tid % T, w = tid / T;
-  const int l = blockIdx.y;
-  const uint32_t p0 = blockIdx.x * T, p = p0 + pl;
-  const PrimeDev& P = primes[map.pr[l]];
-  const double q = P.qd, qi = P.qinv;
-  const size_t lo = (size_t)l * N;
-  const int zb = a.zb, nb = a.nb;
-  // ring fill for term jj into stage jj % S: value (z, pl') copied by thread (z * T + pl') % 128
-  auto issue = [&](int jj) {
-    double* st = ring + (size_t)(jj % kBmStages) * zb * T;
-    for (int e = tid; e < zb * T; e += 128) {
-      const int z = e / T, pp = e % T;
-      const uint64_t* u = a.U[(size_t)z * nb + jj];
-      if (u) __pipeline_memcpy_async(st + e, u + lo + p0 + pp, 8);
-      else st[e] = 0.0;
-    }
-  };
-  for (int jj = 0; jj < kBmStages - 1; jj++) {
-    if (jj < nb) issue(jj);
-    __pipeline_commit();
-  }
-  // stage the baby pairs (coalesced rows of T positions)
-  for (int row = w; row < nb * NBLK * 2; row += W) {
-    const int jj = row / (NBLK * 2), o = (row / 2) % NBLK, cp = row % 2;
-    const uint64_t* x = a.X + (size_t)o * a.xq + (size_t)jj * 2 * a.nlN + (size_t)cp * a.nlN;
-    sx[row * T + pl] = fm::bits2d(x[lo + p]);
-  }
-  fm::FAcc acc[GT][NBLK][2];
-  int cnt = 0;
-  for (int jj = 0; jj < nb; jj++) {
-    if (jj + kBmStages - 1 < nb) issue(jj + kBmStages - 1);
-    __pipeline_commit();
-    __pipeline_wait_prior(kBmStages - 1);   // term jj landed
-    __syncthreads();
-    const double* st = ring + (size_t)(jj % kBmStages) * zb * T;
-    double uv[GT];
-#pragma unroll
-    for (int g = 0; g < GT; g++) {
-      const int z = w + W * g;
-      uv[g] = z < zb ? st[z * T + pl] : 0.0;
-    }
-    if (cnt + 1 > fm::kFAccTerms) {
-#pragma unroll
-      for (int g = 0; g < GT; g++)
-#pragma unroll
-        for (int o = 0; o < NBLK; o++) {
-          fm::fold(acc[g][o][0], q, qi);
-          fm::fold(acc[g][o][1], q, qi);
-        }
-      cnt = 0;
-    }
-    cnt++;
-    const double* xr = sx + (size_t)jj * NBLK * 2 * T + pl;
-#pragma unroll
-    for (int o = 0; o < NBLK; o++) {
-      const double xa = xr[(o * 2) * T], xb = xr[(o * 2 + 1) * T];
-#pragma unroll
-      for (int g = 0; g < GT; g++) {
-        fm::fmac(acc[g][o][0], uv[g], xa);
-        fm::fmac(acc[g][o][1], uv[g], xb);
-      }
-    }
-    __syncthreads();   // stage jj % S is refilled by the next iteration's issue
-  }
-#pragma unroll
-  for (int g = 0; g < GT; g++) {
-    const int z = w + W * g;
-    if (z >= zb) continue;
-#pragma unroll
-    for (int o = 0; o < NBLK; o++) {
-      uint64_t* dst = a.out + (size_t)(o * zb + z) * 2 * a.nlN + lo + p;
-      dst[0] = fm::c2u(fm::fred(acc[g][o][0], q, qi), P.rc.q);
-      dst[a.nlN] = fm::c2u(fm::fred(acc[g][o][1], q, qi), P.rc.q);
-    }
-  }
-}
-
-bool launch_block_mac(const DevCtx& c, const BlockMacArgs& a, const LimbMap& map) {
-  if (a.nblk != 4 || a.zb > 24 || c.N % 16) return false;
-  const size_t smem = ((size_t)a.nb * a.nblk * 2 * 16 + (size_t)kBmStages * a.zb * 16) * 8;
-  if (smem > 200 * 1024) return false;
-  auto kern = a.zb <= 8 ? k_block_mac<4, 1> : a.zb <= 16 ? k_block_mac<4, 2> : k_block_mac<4, 3>;
-  HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  ProfScope ps_(c, "diag_mac", a.bytes);
-  launch_pdl(kern, dim3(dim3(c.N / 16, map.n)), dim3(128), smem, c.stream, a, c.primes, map, c.N);
-  (*c.launches)++;
-  HCUDA(cudaGetLastError());
-  return true;
-}
-
 // D20 L5: after ncclAllReduce(uint64, sum) of partial Q_l P accumulators
 // (each < q, at most 2^13 ranks -> no wrap), reduce every word mod its prime
 __global__ void k_modred(uint64_t* __restrict__ x, const PrimeDev* __restrict__ primes,
@@ -900,6 +646,12 @@ __global__ void k_modred(uint64_t* __restrict__ x, const PrimeDev* __restrict__ 
   const size_t o = (size_t)l * N + i;
   const uint64_t v = x[o];
   x[o] = v - mulhi64(v, rc.mu) * rc.q >= rc.q ? v - mulhi64(v, rc.mu) * rc.q - rc.q : v - mulhi64(v, rc.mu) * rc.q;
+}
+
+// x += y as plain uint64 words (the sum ncclAllReduce(ncclUint64, ncclSum) computes)
+__global__ void k_add_u64(uint64_t* __restrict__ x, const uint64_t* __restrict__ y, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    x[i] += y[i];
 }
 
 // ---------------- launchers ----------------
@@ -945,7 +697,7 @@ void launch_scalar_mul(const DevCtx& c, const uint64_t* a, uint64_t* out, const 
 
 void launch_dform(const DevCtx& c, uint64_t* x, size_t n, const LimbMap& map, int dir) {
   ProfScope ps_(c, "dform", 16.0 * n);
-  k_dform<<<148 * 8, 256, 0, c.stream>>>(x, n, c.log_n, c.primes, map, dir);
+  k_dform<<<c.n_sm * 8, 256, 0, c.stream>>>(x, n, c.log_n, c.primes, map, dir);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -981,6 +733,13 @@ void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map) {
   HCUDA(cudaGetLastError());
 }
 
+void launch_add_u64(const DevCtx& c, uint64_t* x, const uint64_t* y, size_t n) {
+  ProfScope ps_(c, "add_u64", 24.0 * n);
+  k_add_u64<<<(unsigned)std::min<size_t>((n + kT - 1) / kT, (size_t)c.n_sm * 16), kT, 0, c.stream>>>(x, y, n);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+}
+
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,
                          const LimbMap& map) {
   ProfScope ps_(c, "rescale_prep", 8.0 * c.N * (1 + map.n) * G);
@@ -1005,7 +764,7 @@ void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
   const unsigned total = (c.N / kT) * map.n;
-  const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
+  const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, (unsigned)c.n_sm * c.persist) : total;
   launch_pdl(kern, dim3(grid), dim3(kT), 0, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
@@ -1060,7 +819,7 @@ void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int
                       : (nq % 4 == 0 && q4 ? k_diag_mac<false, 4>
                                            : nq > 1 ? k_diag_mac<false, 2> : k_diag_mac<false, 1>);
   const unsigned total = (c.N / kT) * n_groups * map.n;
-  const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, 148u * c.persist) : total;
+  const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, (unsigned)c.n_sm * c.persist) : total;
   launch_pdl(kern, dim3(grid), dim3(kT), 0, c.stream, (const MacTerm*)terms, groups, out, out_stride, (size_t)map.n * c.N, c.primes, map, c.N, nq, xq, oq, n_groups);
   (*c.launches)++;
   HCUDA(cudaGetLastError());

@@ -102,6 +102,14 @@ _SIGS = {
     "helrm_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
     "helrm_comm_init": [_vp, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int],
     "helrm_lookup_dist": [_vp, _vp, _vp, _pp, _sz, _pp],
+    "helrm_lookup_dist_virtual": [_vp, _vp, _vp, _pp, _sz, ctypes.c_int, _pp],
+    "helrm_modred": [_vp, _vp, _u32, _sz],
+    "helrm_plan_galois": [_vp, _u64p, _sz, ctypes.POINTER(_sz)],
+    "helrm_rotkeys_galois": [_vp, _u64p, _sz, ctypes.POINTER(_sz)],
+    "helrm_sk_import": [_vp, _i64p, _sz, _pp],
+    "helrm_pk_import": [_vp, _u64p, _sz, _pp],
+    "helrm_rotkeys_import": [_vp, _u64p, _sz, _pp, _sz, _pp],
+    "helrm_rotkeys_upload": [_vp, _vp, _u64, _u64p, _sz],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_L, _name)
@@ -126,7 +134,10 @@ EXPORTED = sorted(list(_SIGS) + ["helrm_params_destroy", "helrm_ctx_destroy", "h
                                  "helrm_rotkeys_destroy", "helrm_tables_destroy", "helrm_ct_destroy",
                                  "helrm_plan_destroy", "helrm_last_error", "helrm_version", "helrm_ctx_launches",
                                  "helrm_rotkeys_bytes", "helrm_ctx_profile", "helrm_ctx_profile_json", "helrm_dist_range",
-                                 "helrm_comm_unique_id", "helrm_comm_init", "helrm_lookup_dist"])
+                                 "helrm_comm_unique_id", "helrm_comm_init", "helrm_lookup_dist",
+                                 "helrm_lookup_dist_virtual", "helrm_modred", "helrm_plan_galois",
+                                 "helrm_rotkeys_galois", "helrm_sk_import", "helrm_pk_import",
+                                 "helrm_rotkeys_import", "helrm_rotkeys_upload"])
 
 
 def _check(code: int):
@@ -285,6 +296,13 @@ class RotKeys(_Handle):
     def nbytes(self) -> int:
         return int(_L.helrm_rotkeys_bytes(self.h))
 
+    def galois(self) -> List[int]:
+        n = ctypes.c_size_t()
+        _check(_L.helrm_rotkeys_galois(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, np.uint64)
+        _check(_L.helrm_rotkeys_galois(self.h, _u64ptr(out) if out.size else None, out.size, ctypes.byref(n)))
+        return [int(x) for x in out]
+
 
 def ctx_create(params: Params, device: int = 0, stream: int = 0) -> Context:
     return Context(params, device, stream)
@@ -307,6 +325,36 @@ def rotkeys_gen(ctx: Context, sk: SecretKey, galois: Sequence[int], seed: int) -
     h = ctypes.c_void_p()
     _check(_L.helrm_rotkeys_gen(ctx.h, sk.h, _u64ptr(g) if g.size else None, g.size, seed, ctypes.byref(h)))
     return RotKeys(h, ctx)
+
+
+def sk_import(ctx: Context, coeff: np.ndarray) -> SecretKey:
+    a = np.ascontiguousarray(coeff, dtype=np.int64)
+    h = ctypes.c_void_p()
+    _check(_L.helrm_sk_import(ctx.h, a.ctypes.data_as(_i64p), a.size, ctypes.byref(h)))
+    return SecretKey(h, ctx)
+
+
+def pk_import(ctx: Context, coeff: np.ndarray) -> PublicKey:
+    a = np.ascontiguousarray(coeff, dtype=np.uint64)
+    h = ctypes.c_void_p()
+    _check(_L.helrm_pk_import(ctx.h, _u64ptr(a), a.size, ctypes.byref(h)))
+    return PublicKey(h, ctx)
+
+
+def rotkeys_import(ctx: Context, keys: dict) -> RotKeys:
+    """keys: {galois element: uint64 [dnum][2][L+1+K][N] coefficient form}."""
+    gs = np.array(list(keys), dtype=np.uint64)
+    arrs = [np.ascontiguousarray(keys[int(g)], dtype=np.uint64) for g in gs]
+    wpk = min((a.size for a in arrs), default=0)
+    ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    h = ctypes.c_void_p()
+    _check(_L.helrm_rotkeys_import(ctx.h, _u64ptr(gs) if gs.size else None, gs.size, ptrs, wpk, ctypes.byref(h)))
+    return RotKeys(h, ctx)
+
+
+def rotkeys_upload(ctx: Context, rk: RotKeys, g: int, coeff: np.ndarray) -> None:
+    a = np.ascontiguousarray(coeff, dtype=np.uint64)
+    _check(_L.helrm_rotkeys_upload(ctx.h, rk.h, g, _u64ptr(a), a.size))
 
 
 def sk_export(ctx: Context, sk: SecretKey) -> np.ndarray:
@@ -405,8 +453,14 @@ class Plan(_Handle):
         _check(_L.helrm_plan_rotations(self.h, out.ctypes.data_as(_i64p), out.size, ctypes.byref(n)))
         return [int(x) for x in out]
 
-    def galois(self, N: int) -> List[int]:
-        return sorted({pow(5, a, 2 * N) for a in self.rotations()})
+    def galois(self, N: Optional[int] = None) -> List[int]:
+        """helrm_plan_galois: the D19 Galois list, computed by the library
+        (N is accepted for backwards compatibility and ignored)."""
+        n = ctypes.c_size_t()
+        _check(_L.helrm_plan_galois(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, np.uint64)
+        _check(_L.helrm_plan_galois(self.h, _u64ptr(out) if out.size else None, out.size, ctypes.byref(n)))
+        return [int(x) for x in out]
 
 
 def plan_create(ctx: Context, tables: Tables, level: int, n1: int = 0, mode: int = MODE_DOUBLE) -> Plan:
@@ -489,6 +543,20 @@ def comm_unique_id() -> bytes:
 def comm_init(ctx: Context, uid: bytes, rank: int, world: int):
     buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
     _check(_L.helrm_comm_init(ctx.h, buf, rank, world))
+
+
+def lookup_dist_virtual(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Ciphertext], parts: int,
+                        batch: int = 1) -> List[Ciphertext]:
+    info = plan.info()
+    assert len(cts) == batch * info.n_in_cts
+    ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
+    outs = (ctypes.c_void_p * (batch * info.n_out_cts))()
+    _check(_L.helrm_lookup_dist_virtual(ctx.h, plan.h, rk.h, ins, batch, parts, outs))
+    return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]
+
+
+def modred(ctx: Context, dev, level: int, n_polys: int = 1):
+    _check(_L.helrm_modred(ctx.h, _devptr(dev), level, n_polys))
 
 
 def lookup_dist(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Ciphertext], batch: int = 1) -> List[Ciphertext]:

@@ -49,17 +49,26 @@ def main(name: str, queries=None):
     out["diag0_sha"] = sha(core.intt(u[0], P.qp(cfg.level), P))
     t_look = 0.0
     for q in qs:
-        cts = lk.query_cts(P, pk, lay, plan, w.indices[q], w.dense[q], cfg.level, cfg.seed, q)
+        if name.startswith("mlp"):
+            # dense linear layer: the encrypted input is synth.dense_inputs' row q at seed << 20 | q
+            z = np.zeros(P.n)
+            x = synth.dense_inputs(name, q + 1)[q]
+            z[: len(x)] = x
+            cts = [core.encrypt(P, pk, z, cfg.level, (cfg.seed << 20) | q)]
+        else:
+            cts = lk.query_cts(P, pk, lay, plan, w.indices[q], w.dense[q], cfg.level, cfg.seed, q)
         t0 = time.time()
         res = lk.lookup(P, plan, u, rk, cts)
         t_look += time.time() - t0
-        z = core.decrypt_decode(P, sk, res[0])
-        y = lk.gather(lay, w.indices[q])
+        z = np.concatenate([core.decrypt_decode(P, sk, r) for r in res])
+        y = x @ w.tables[0].weights if name.startswith("mlp") else lk.gather(lay, w.indices[q])
         err = float(np.abs(z[: lay.M] - y).max())
         out["queries"].append({"q": q, "in_sha": [sha(core.ct_to_coeff(P, c)) for c in cts],
                                "out_sha": [sha(core.ct_to_coeff(P, r)) for r in res],
                                "dec_err": err})
         print(name, q, "err", err, flush=True)
+    out["plan"] = {"n_diag": plan.n_diag, "n_unique": len(plan.u_slots), "n1": plan.n1, "C": plan.C, "O": plan.O,
+                   "mbar": plan.mbar, "n_rotations": len(plan.rotation_amounts(P))}
     out["seconds"] = {"keys": t_keys, "encode_diagonals": t_enc, "lookup_per_query": t_look / len(qs),
                       "total": time.time() - t}
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"{name}.json")

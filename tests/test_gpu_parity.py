@@ -301,6 +301,22 @@ def test_criteo_full_size_matches_oracle_golden(torch_mod):
     assert np.abs(zz[:, : lay.M] - y).max() < 1e-3
 
 
+def _golden_outputs(E, name, outs):
+    """The output ciphertexts of query 0 against the SHA-256 digests the CPU
+    oracle wrote for this config (tests/golden/<name>.json, written by
+    tests/golden/make_golden.py from oracle/ only)."""
+    import hashlib
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", name + ".json")))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype="<u8").tobytes()).hexdigest()
+    want = gold["queries"][0]["out_sha"]
+    assert len(outs) == len(want)
+    for o, h in zip(outs, want):
+        assert sha(E.h.ct_export(E.ctx, o)) == h
+    return gold
+
+
 @gpu
 def test_llm_full_size_plan_and_decryption(torch_mod):
     """LLM-style config at full size (N = 2^16, 20 + 4 primes, 128 tokens of
@@ -309,8 +325,9 @@ def test_llm_full_size_plan_and_decryption(torch_mod):
     63 babies + 20 giants, giant 12 being amount 1 = baby 1 (SURVEY.md 8.0
     counts 83 by not merging it; tests/test_oracle_lookup.py re-derives 82 on
     the oracle's plan) -- 4 in / 4 out cts) and every decrypted output block against
-    the float64 gather.  (The oracle cannot encode 1279 dense diagonals at
-    this size in test time; the bit-exact check of this layout is llm_small.)"""
+    the float64 gather, and all four output ciphertexts against the oracle's
+    digests (tests/golden/llm.json: the oracle run at full size, 20 + 4
+    primes, dnum 5, offline)."""
     E = env("llm", torch_mod)
     w = synth.make_workload("llm")
     plan, sk, outs = _gpu_lookup(E, w)
@@ -318,6 +335,7 @@ def test_llm_full_size_plan_and_decryption(torch_mod):
     assert (info.n_in_cts, info.n_out_cts, info.n_unique, info.n1, info.n2_max, info.n_rotations) == (4, 4, 1279, 64,
                                                                                                       20, 82)
     assert info.mbar == w.config.n_slots and info.n_diag == 4 * 1279
+    _golden_outputs(E, "llm", outs[0])
     lay = lk.layout(w)
     y = lk.gather(lay, w.indices[0])
     z = np.concatenate([E.h.decrypt_decode(E.ctx, sk, o) for o in outs[0]])
@@ -328,14 +346,15 @@ def test_llm_full_size_plan_and_decryption(torch_mod):
 def test_criteo_c2_full_size_plan_and_decryption(torch_mod):
     """The 2-input-ct Criteo shape at full size (Table 2 threshold
     5e4: 47,798 one-hot slots, 1024 diagonals, giants shared by both cts):
-    plan counts and the decrypted output against the float64 gather (the
-    bit-exact check of a 2-ct lookup is criteo_c2_small)."""
+    plan counts, the output against the oracle's digest (tests/golden/
+    criteo_c2.json) and the decrypted output against the float64 gather."""
     E = env("criteo_c2", torch_mod)
     w = synth.make_workload("criteo_c2")
     plan, sk, outs = _gpu_lookup(E, w)
     info = plan.info()
     assert (info.n_in_cts, info.n_out_cts, info.n_diag, info.n1, info.n2_max, info.n_rotations) == (2, 1, 1024, 32,
                                                                                                     16, 52)
+    _golden_outputs(E, "criteo_c2", outs[0])
     lay = lk.layout(w)
     y = lk.gather(lay, w.indices[0])
     z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
@@ -345,14 +364,16 @@ def test_criteo_c2_full_size_plan_and_decryption(torch_mod):
 @gpu
 def test_llm_gen_full_size_decryption(torch_mod):
     """LLM generation step at full size (one token of the 50257 x 768 GPT-2
-    table): plan counts and the decrypted 768-dim embedding
-    against the float64 gather (bit-exact check: llm_gen_small)."""
+    table): plan counts, the output against the oracle's digest
+    (tests/golden/llm_gen.json) and the decrypted 768-dim embedding against
+    the float64 gather."""
     E = env("llm", torch_mod)
     w = synth.make_workload("llm_gen")
     plan, sk, outs = _gpu_lookup(E, w)
     info = plan.info()
     assert (info.n_in_cts, info.n_out_cts, info.n_diag, info.n1, info.n2_max, info.n_rotations, info.mbar) == (
         1, 1, 1024, 32, 32, 67, 1024)
+    _golden_outputs(E, "llm_gen", outs[0])
     lay = lk.layout(w)
     z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
     assert np.abs(z[: lay.M] - lk.gather(lay, w.indices[0])).max() < 1e-3
@@ -362,12 +383,14 @@ def test_llm_gen_full_size_decryption(torch_mod):
 def test_criteo_level4_decryption(torch_mod):
     """The Criteo lookup at input level 4, where Orion places the embedding in
     the ReLU DLRM: 5 + 4 limbs, dnum 2; the plan counts match
-    the level-23 plan and the output decrypts to the float64 gather."""
+    the level-23 plan, the output equals the oracle's digest
+    (tests/golden/criteo_l4.json) and decrypts to the float64 gather."""
     E = env("criteo", torch_mod)
     w = synth.make_workload("criteo_l4")
     plan, sk, outs = _gpu_lookup(E, w)
     info = plan.info()
     assert (info.n_diag, info.n1, info.n2_max, info.n_rotations) == (512, 32, 16, 52)
+    _golden_outputs(E, "criteo_l4", outs[0])
     lay = lk.layout(w)
     z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
     assert np.abs(z[: lay.M] - lk.gather(lay, w.indices[0])).max() < 1e-3
@@ -412,7 +435,8 @@ def test_dense_sparse_extraction_matches_oracle(torch_mod):
 def test_dense_linear_layer(name, torch_mod):
     """A dense linear layer on the lookup engine: the weight
     matrix as the table, a dense encrypted input.  mlp_small: the output
-    ciphertext equals the oracle's bit for bit; both: decrypts to x W."""
+    ciphertext equals the oracle's bit for bit; mlp_512x256: equals the
+    oracle's digest (tests/golden/mlp_512x256.json); both: decrypts to x W."""
     E = env(name, torch_mod)
     w = synth.make_workload(name)
     x = synth.dense_inputs(name)[0]
@@ -429,6 +453,8 @@ def test_dense_linear_layer(name, torch_mod):
     want = x @ w.tables[0].weights
     y = h.decrypt_decode(E.ctx, sk, out[0])
     assert np.abs(y[: len(want)] - want).max() < 1e-3
+    if name == "mlp_512x256":
+        _golden_outputs(E, name, out)
     if name == "mlp_small":
         import test_oracle_lookup as tol
         _, _, P, _, _, _, ref = tol._dense_layer_run(name)
@@ -672,10 +698,6 @@ def test_lookup_error_and_degenerate_cases(torch_mod):
     ({"HELRM_MAC_BULK": "0"}, "test_llm_full_size_plan_and_decryption"),
     ({"HELRM_PIPE": "1", "HELRM_MACCH": "1", "HELRM_NTTCH": "4"},                  # pipelined giant steps
      "test_criteo_full_size_matches_oracle_golden"),
-    ({"HELRM_FUSED_BM": "2"}, "test_criteo_full_size_matches_oracle_golden"),     # fused baby + MAC (bulk)
-    ({"HELRM_FUSED_BM": "2"}, "test_lookup_bit_exact_vs_oracle"),
-    ({"HELRM_NTT_FUSED": "1"}, "test_criteo_full_size_matches_oracle_golden"),    # one-launch forward NTT
-    ({"HELRM_NTT_FUSED": "1"}, "test_microbench_ntt_full_size_sampled"),
     ({"HELRM_PDL": "1"}, "test_criteo_full_size_matches_oracle_golden"),          # programmatic dependent launch
     ({"HELRM_PDL": "1"}, "test_lookup_bit_exact_vs_oracle"),
 ])
