@@ -132,72 +132,118 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # ------------------------------------------------------------------ oracle timing
-def oracle_lookup_seconds(threads: int = 0):
-    """CPU oracle (oracle/, as it stands) on a bounded sample of the Criteo
-    lookup: each primitive the double-hoisted lookup is made of is timed once
-    on Criteo parameters (random residues and random key material -- validity
-    is irrelevant to the arithmetic), then composed with the exact operation
-    counts of the Criteo plan.  Returns (seconds per lookup, sample text, cores)."""
-    import synth
+class OracleSample:
+    """The CPU oracle (oracle/, as it stands: scalar __int128 C per limb,
+    limbs farmed out to a thread pool) running a bounded slice of the real
+    Criteo batch-1 lookup on the real encrypted query, phase by phase in D20's
+    order, each phase through the oracle's own functions:
+
+      L1  ModUp of c1, all dnum digits                       (whole)
+      L2  `nb` of the plan's 31 lazy baby key switches         (sample)
+      L3  the inner-sum terms (u (.) a, u (.) b) of giant 1 that use
+          the sampled babies and baby 0                        (sample)
+      L4  giant 1's step: ModDown(B), key switch, + phi(A)     (sample)
+      L6/L7 ModDown of both halves and rescale                  (whole)
+      L8  1 of the 6 RotSum rotations                          (sample)
+
+    Each phase is timed; the lookup time is the sum of the phase times, the
+    sampled ones scaled by the plan's counts (31 babies, 512 inner-sum terms,
+    15 rotating giants, 6 RotSum rotations).  Setup (params, plan, keys for
+    the sampled rotations, the sampled diagonals encoded, the query
+    encrypted) is not timed."""
+
+    def __init__(self, n_baby=2):
+        import synth
+        from oracle import core
+        from oracle import lookup as lk
+        self.core, self.lk = core, lk
+        w = synth.make_workload("criteo")
+        cfg = w.config
+        P = core.params_from_config(cfg)
+        lay = lk.layout(w)
+        plan = lk.make_plan(lay, P.n, cfg.level)
+        self.P, self.plan, self.l = P, plan, cfg.level
+        sk = core.sk_gen(P, cfg.seed)
+        pk = core.pk_gen(P, sk, cfg.seed)
+        self.cts = lk.query_cts(P, pk, lay, plan, w.indices[0], w.dense[0], cfg.level, cfg.seed, 0)
+        self.babies = [j for j in plan.babies[0] if j][:n_baby]
+        self.gi = next(i for i, e in enumerate(plan.entries[0]) if e and plan.giants[0][i])
+        self.terms = [(c, j, uid) for (c, j, uid) in plan.entries[0][self.gi] if j in [0] + self.babies]
+        amts = self.babies + [plan.giants[0][self.gi], plan.mbar]
+        self.rk = core.rotkeys_gen(P, sk, sorted({core.galois_elt(a, P) for a in amts}), cfg.seed)
+        qp = P.qp(self.l)
+        ms = core.encode_many([plan.u_slots[uid] for (_, _, uid) in self.terms], P.q[self.l], P.N)
+        self.u = {uid: core.ntt(core.reduce_signed(m, qp), qp, P) for (_, _, uid), m in zip(self.terms, ms)}
+        self.counts = {"babies": sum(1 for j in plan.babies[0] if j), "terms": sum(len(e) for e in plan.entries[0]),
+                       "giants": sum(1 for i, e in enumerate(plan.entries[0]) if e and plan.giants[0][i]),
+                       "rotsum": int(round(math.log2(P.n // plan.mbar)))}
+        self.desc = (f"one real slice of the Criteo b1 lookup on the encrypted query (oracle functions, D20 order): "
+                     f"L1 ModUp (all {P.dnum(self.l)} digits), {len(self.babies)} of {self.counts['babies']} baby "
+                     f"key switches, {len(self.terms)} of {self.counts['terms']} inner-sum terms, 1 of "
+                     f"{self.counts['giants']} giant steps, final ModDown + rescale, 1 of {self.counts['rotsum']} "
+                     f"RotSum rotations; sampled phases scaled by the plan's counts")
+
+    def step(self):
+        """Run the slice once: (estimated seconds per lookup, seconds spent, phase times)."""
+        core, P, l, plan = self.core, self.P, self.l, self.plan
+        ct = self.cts[0]
+        qp = P.qp(l)
+        T = {}
+        clk = time.perf_counter
+        t0 = clk()
+        D = [core.modup(P, ct.c1, l, k) for k in range(P.dnum(l))]                      # L1
+        T["L1_modup"] = clk() - t0
+        t0 = clk()
+        ab = {0: (core.lift_P(P, ct.c0, l), core.lift_P(P, ct.c1, l))}
+        for j in self.babies:                                                            # L2
+            ab[j] = core.rotate_lazy(P, ct, j, self.rk, D=D)
+        T["L2_babies"] = clk() - t0
+        t0 = clk()
+        A = np.zeros((len(qp), P.N), dtype=np.uint64)
+        B = np.zeros_like(A)
+        for (c, j, uid) in self.terms:                                                   # L3
+            a, b = ab[j]
+            A = core.vadd(A, core.vmul(self.u[uid], a, qp), qp)
+            B = core.vadd(B, core.vmul(self.u[uid], b, qp), qp)
+        T["L3_terms"] = clk() - t0
+        t0 = clk()
+        g = core.galois_elt(plan.giants[0][self.gi], P)                                  # L4
+        G0, G1 = core.keyswitch(P, core.moddown(P, B, l), g, self.rk, l)
+        O0 = core.vadd(core.automorph_ntt(A, g, P.N), G0, qp)
+        O1 = G1
+        T["L4_giant"] = clk() - t0
+        t0 = clk()
+        out = core.Ciphertext(core.moddown(P, O0, l), core.moddown(P, O1, l), l, ct.scale * P.q[l])   # L6
+        out = core.rescale(P, out)                                                       # L7
+        T["L6_L7_finish"] = clk() - t0
+        t0 = clk()
+        core.ct_add(P, out, core.rotate(P, out, plan.mbar, self.rk))                    # L8 (one of the fold)
+        T["L8_rotsum"] = clk() - t0
+        k = self.counts
+        est = (T["L1_modup"] + T["L2_babies"] * k["babies"] / len(self.babies)
+               + T["L3_terms"] * k["terms"] / len(self.terms) + T["L4_giant"] * k["giants"]
+               + T["L6_L7_finish"] + T["L8_rotsum"] * k["rotsum"])
+        return est, sum(T.values()), {kk: round(v, 4) for kk, v in T.items()}
+
+
+def oracle_baseline(single_thread=True):
+    """cpu_baseline leg: the oracle slice on all host cores (2nd of 2 runs) and,
+    separately, on one thread; lookups/s from the scaled phase times."""
     from oracle import core
-    from oracle import lookup as lk
-    if threads:
-        core.set_threads(threads)
-    cfg = synth.config_by_name("criteo")
-    w = synth.make_workload("criteo")
-    P = core.params_from_config(cfg)
-    plan = lk.make_plan(lk.layout(w), P.n, cfg.level)
-    l = cfg.level
-    qp = P.qp(l)
-    rng = np.random.default_rng(0)
-    rand = lambda primes: np.stack([rng.integers(0, q, size=P.N, dtype=np.uint64) for q in primes])
-    c0, c1 = rand(P.q[: l + 1]), rand(P.q[: l + 1])
-    g = core.galois_elt(1, P)
-    rk = core.RotKeys(P)
-    allp = P.q + P.p
-    key = [(rand(allp), rand(allp)) for _ in range(P.dnum(l))]
-    rk.keys[g] = key
-    t = {}
-    for _ in range(2):                     # second pass is the timed one (first warms allocations)
-        t.update(_oracle_parts(P, core, l, qp, c0, c1, g, rk))
-    n_baby = sum(1 for j in plan.babies[0] if j)
-    n_mac = sum(len(e) for e in plan.entries[0])
-    n_giant = sum(1 for i, e in enumerate(plan.entries[0]) if e and plan.giants[0][i])
-    n_rotsum = int(round(math.log2(P.n // plan.mbar)))
-    rot_full = t["modup_all"] + t["baby_kip"] + 2 * t["moddown"]
-    total = (t["modup_all"] + n_baby * t["baby_kip"] + n_mac * t["mac"]
-             + n_giant * (t["moddown"] + t["modup_all"] + t["giant_kip"])
-             + 2 * t["moddown"] + t["rescale"] + n_rotsum * rot_full)
-    sample = (f"oracle primitives timed on Criteo parameters (ModUp x{P.dnum(l)} digits, 1 baby key switch, "
-              f"1 diagonal MAC, ModDown, 1 giant key switch, rescale; 2nd of 2 passes), composed by the plan's "
-              f"counts: {n_baby} baby KS + {n_mac} MACs + {n_giant} giants + {n_rotsum} RotSum rotations")
-    return total, sample, core.threads(), {k: round(v, 4) for k, v in t.items()}
-
-
-def _oracle_parts(P, core, l, qp, c0, c1, g, rk):
-    t = {}
-    t0 = time.perf_counter()
-    D = [core.modup(P, c1, l, k) for k in range(P.dnum(l))]
-    t["modup_all"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    a, b = core.rotate_lazy(P, core.Ciphertext(c0, c1, l, 1), 1, rk, D=D)
-    t["baby_kip"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    A = core.vadd(a, core.vmul(a, b, qp), qp)
-    B = core.vadd(b, core.vmul(b, a, qp), qp)
-    t["mac"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    Bp = core.moddown(P, B, l)
-    t["moddown"] = time.perf_counter() - t0
-    D2 = [core.modup(P, Bp, l, k) for k in range(P.dnum(l))]
-    t0 = time.perf_counter()
-    G0, G1 = core.keyswitch_digits(P, D2, g, rk, l)
-    core.vadd(core.automorph_ntt(A, g, P.N), G0, qp)
-    t["giant_kip"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    core.rescale(P, core.Ciphertext(Bp, Bp, l, 1))
-    t["rescale"] = time.perf_counter() - t0
-    return t
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    core.set_threads(cores)
+    s = OracleSample()
+    s.step()
+    est, spent, parts = s.step()
+    out = {"value": round(1.0 / est, 6), "unit": "lookups/s", "cores": core.threads(), "kind": "oracle",
+           "sample": s.desc, "est_s_per_lookup": round(est, 2), "sample_s": round(spent, 2), "parts_s": parts}
+    if single_thread:
+        core.set_threads(1)
+        est1, spent1, parts1 = s.step()
+        out["single_thread"] = {"value": round(1.0 / est1, 6), "cores": 1, "est_s_per_lookup": round(est1, 2),
+                                "sample_s": round(spent1, 2), "parts_s": parts1}
+        core.set_threads(cores)
+    return out
 
 
 # ------------------------------------------------------------------ roofline
@@ -227,48 +273,90 @@ def ncu_traffic():
         return {}
 
 
-def roofline_from_stats(stats, steps, cfg):
-    """Dominant kernel = the forward NTT (passes 1 + 2, ~35% of the step):
-    FP64-pipe bound, so achieved butterflies/s against the FP64 FMA rate / 8.
-    The HBM-bound kernels (diagonal MAC, key switches) are listed with their
-    algorithmic GB/s against the measured HBM copy bandwidth."""
+def roofline_from_stats(stats, steps, cfg, floor_bytes, ms_per_step):
+    """SURVEY.md 8(d) roofline of the dominant kernel: the forward NTT
+    (passes 1 + 2, the largest share of the step), against the measured HBM
+    copy bandwidth, with the 8(d) algorithmic bytes: 16 B per coefficient per
+    limb transform (one read + one write of 8 B), i.e. 1 MiB per limb at
+    N = 2^16, times the limb transforms the profiled steps ran.  The FP64-pipe
+    view of the same kernel (achieved butterflies/s against 148 SMs x 64 FP64
+    lanes x clock / 8 ops) and the HBM-bound kernels (diagonal MAC, key
+    switches) are listed beside it; lookup_hbm_frac is the whole step's 8(d)
+    floor bytes (diagonals + keys streamed once) over its time."""
     N, logN = cfg.N, int(round(math.log2(cfg.N)))
     p1, p2 = stats.get("ntt_fwd_p1"), stats.get("ntt_fwd_p2")
+    hbm, hsrc = hbm_peak()
     peak_fp64, src = fp64_peak()
     peak_bfly = peak_fp64 / NTT_FP64_OPS_PER_BFLY / 1e9
-    hbm, hsrc = hbm_peak()
-    out = {"bound": "alu", "kernel": "ntt_fwd (passes 1+2, FP64 pipe)", "achieved": None, "peak": round(peak_bfly, 1),
-           "unit": "Gbutterfly/s", "frac": None, "traffic": None,
-           "peak_source": f"{src} / {NTT_FP64_OPS_PER_BFLY} FP64 ops per exact butterfly"}
+    tr = ncu_traffic()
+    out = {"bound": "hbm", "kernel": "ntt_fwd (passes 1 + 2)", "achieved": None, "peak": hbm, "unit": "GB/s",
+           "frac": None, "traffic": None, "peak_source": hsrc}
     if p1 and p2:
         limbs = p1["bytes"] / (8.0 * N)                 # limb transforms in the profiled steps
         ms = p1["ms"] + p2["ms"]
-        bfly = limbs * (N // 2) * logN
-        ach = bfly / (ms / 1e3) / 1e9
+        alg = 16.0 * N * limbs
+        ach = alg / (ms / 1e3) / 1e9
+        bfly = limbs * (N // 2) * logN / (ms / 1e3) / 1e9
         tot = sum(v["ms"] for v in stats.values())
-        tr = ncu_traffic()
-        out.update({"achieved": round(ach, 1), "frac": round(ach / peak_bfly, 4),
+        trb = tr.get("ntt_fwd_bytes_per_limb")
+        out.update({"achieved": round(ach, 1), "frac": round(ach / hbm, 4),
+                    "traffic": trb, "traffic_unit": "dram bytes read + written per limb transform (ncu --set full, "
+                                                    "profiles/ncu_traffic.json)",
+                    "traffic_commit": tr.get("commit"),
+                    "algorithmic_bytes_per_limb": 16 * N,
                     "launches_per_step": (p1["count"] + p2["count"]) // steps,
                     "limb_transforms_per_step": round(limbs / steps, 1),
                     "avg_transform_us": round(ms * 1e3 / limbs, 4),
                     "share_of_step": round(ms / tot, 3),
-                    "algorithmic_bytes_per_limb": 16 * N,
-                    "traffic": tr.get("ntt_fwd_bytes_per_limb"),
-                    "traffic_unit": "dram bytes per limb transform (ncu, profiles/ncu_traffic.json)",
-                    # ncu sm__pipe_fp64_cycles_active (time-weighted): the pipe is busier than frac
-                    # because reductions and conversions add ~2.75 FP64 ops per 8-op butterfly
-                    "fp64_pipe_frac": tr.get("ntt_fwd_fp64_pipe_frac"),
-                    "fp64_pipe_frac_p1_p2": [tr.get("ntt_fwd_p1_fp64_pipe_frac"), tr.get("ntt_fwd_p2_fp64_pipe_frac")]})
+                    "fp64_view": {"achieved": round(bfly, 1), "peak": round(peak_bfly, 1), "unit": "Gbutterfly/s",
+                                  "frac": round(bfly / peak_bfly, 4),
+                                  "peak_source": f"{src} / {NTT_FP64_OPS_PER_BFLY} FP64 ops per exact butterfly",
+                                  "fp64_pipe_frac_ncu": tr.get("ntt_fwd_fp64_pipe_frac")}})
     hk = {}
-    for k in ("diag_mac", "kip_multi", "kip"):
+    for k in ("diag_mac", "kip_multi", "kip", "kip_giants"):
         v = stats.get(k)
         if v:
             gbs = v["bytes"] / (v["ms"] / 1e3) / 1e9
             hk[k] = {"achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
                      "ms_per_step": round(v["ms"] / steps, 4), "traffic": tr_get(k)}
     out["hbm_kernels"] = hk
-    out["hbm_peak_source"] = hsrc
+    out["lookup_hbm_frac"] = round(floor_bytes / (ms_per_step / 1e3) / 1e9 / hbm, 4)
+    out["lookup_floor_GB"] = round(floor_bytes / 1e9, 3)
     return out
+
+
+def fp64_frac_model(ctx, run, cfg, macs, ms):
+    """FP64-pipe fraction of an ALU-bound run (batch 64, LLM):
+    algorithmic FP64 ops -- 8 per NTT butterfly (limb transforms counted by a
+    profiled pass of `run`), 5 per exact modular MAC (key inner products and
+    diagonal MACs, counted from the plan) -- over the run's time, against
+    148 SMs x 64 FP64 lanes x clock."""
+    ctx.profile(True)
+    run()
+    st = ctx.profile_stats()
+    ctx.profile(False)
+    N, logN = cfg.N, int(round(math.log2(cfg.N)))
+    limbs = sum(st.get(k, {}).get("bytes", 0.0) for k in ("ntt_fwd_p1", "ntt_inv_pa")) / (8.0 * N)
+    ops = limbs * (N // 2) * logN * NTT_FP64_OPS_PER_BFLY + 5.0 * macs
+    peak, src = fp64_peak()
+    return {"fp64_frac_model": round(ops / (ms / 1e3) / peak, 4), "fp64_ops_per_run": ops,
+            "ntt_limb_transforms_per_run": round(limbs), "macs_per_run": macs,
+            "fp64_peak_source": src, "model": "8 FP64 ops per NTT butterfly + 5 per exact MAC (fmath.cuh)"}
+
+
+def lookup_macs(P_info, cfg, info, blocks_per_diag=1):
+    """Exact modular MACs of one lookup: key switches x
+    dnum x (l+1+K) x 2 x N, plus n_diag x 2 x (l+1+K) x N (x blocks sharing a
+    diagonal)."""
+    l, K, N = cfg.level, P_info.K, cfg.N
+    alpha = K
+    dn = -(-(l + 1) // alpha)
+    nl = l + 1 + K
+    rotsum = int(round(math.log2(cfg.n_slots // info.mbar)))
+    dn1 = -(-l // alpha)
+    ks = info.n_rotations - rotsum      # babies + giants of the plan (distinct amounts)
+    return (ks * dn * nl * 2 * N + rotsum * dn1 * (nl - 1) * 2 * N
+            + info.n_diag * blocks_per_diag * 2 * nl * N)
 
 
 def tr_get(k):
@@ -343,7 +431,8 @@ def run_gpu(args, world, rank, local):
         step(i)
     stats = ctx.profile_stats()
     ctx.profile(False)
-    roofline = roofline_from_stats(stats, args.steps, cfg)
+    roofline = roofline_from_stats(stats, args.steps, cfg, info.diag_bytes + rk.nbytes() + 2 * 2 * (cfg.level + 1)
+                                   * cfg.N * 8, ms / args.steps)
     total_kernel_ms = sum(v["ms"] for v in stats.values())
     step_bytes = sum(v["bytes"] for v in stats.values()) / args.steps
     kernels = {k: {"count": v["count"] // args.steps, "ms_per_step": round(v["ms"] / args.steps, 4),
@@ -459,8 +548,17 @@ def batch_lookup(args, ctx, helrm, torch, stream, plan, rk, cts, world, B=64):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / reps
-    return {"batch": B, "ms_per_batch": round(ms, 3), "lookups_per_s": round(world * B * 1e3 / ms, 2),
-            "inputs": f"{len(cts)} encrypted queries cycled"}
+    res = {"batch": B, "ms_per_batch": round(ms, 3), "lookups_per_s": round(world * B * 1e3 / ms, 2),
+           "inputs": f"{len(cts)} encrypted queries cycled"}
+    import synth
+    cfg = synth.config_by_name("criteo")
+
+    def run():
+        for o in helrm.lookup(ctx, plan, rk, batch, B):
+            o.close()
+    info = plan.info()
+    res.update(fp64_frac_model(ctx, run, cfg, B * lookup_macs(ctx.info, cfg, info), ms))
+    return res
 
 
 def shape_lookup(helrm, torch, stream, world, dev, name, reps=5):
@@ -589,7 +687,18 @@ def llm_lookup(args, helrm, torch, stream, world, dev):
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / reps
     tokens = w.indices.shape[1]
-    res = {"tokens_per_lookup": tokens, "ms_per_lookup": round(ms, 3),
+
+    def run():
+        for o in helrm.lookup(ctx, plan, rk, cts):
+            o.close()
+    # the 4 output blocks each apply the 1279 shared diagonals to their own input ct; the
+    # rotation keys of a distinct amount are applied once per input ct (babies) / block (giants)
+    l, K, N = cfg.level, ctx.info.K, cfg.N
+    dn, nl = -(-(l + 1) // K), l + 1 + K
+    nb = info.n1 - 1
+    macs = (info.n_in_cts * nb + info.n_out_cts * info.n2_max) * dn * nl * 2 * N + info.n_diag * 2 * nl * N
+    fp = fp64_frac_model(ctx, run, cfg, macs, ms)
+    res = {"tokens_per_lookup": tokens, **fp, "ms_per_lookup": round(ms, 3),
            "token_lookups_per_s": round(world * tokens * 1e3 / ms, 1), "in_cts": info.n_in_cts,
            "out_cts": info.n_out_cts, "unique_diagonals": info.n_unique, "n1": info.n1,
            "rotation_keys": info.n_rotations, "setup_s": round(setup, 1),
@@ -684,21 +793,27 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        secs = []
-        last = None
+        from oracle import core
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        core.set_threads(cores)
+        smp = OracleSample()
+        ests, spent = [], []
+        parts = None
         for i in range(args.warmup + args.steps):
-            s, sample, cores, parts = oracle_lookup_seconds()
+            est, sp, parts = smp.step()
             if i >= args.warmup:
-                secs.append(s)
-            last = (sample, cores, parts)
-        t = statistics.mean(secs)
+                ests.append(est)
+                spent.append(sp)
+        t = statistics.mean(ests)
         v = 1.0 / t
         line = {"metric": metric, "value": round(v, 6), "unit": "lookups/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 1),
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(spent), 1),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic", "config": config, "impl": "reference",
-                "cpu_baseline": {"value": round(v, 6), "unit": "lookups/s", "cores": last[1], "kind": "oracle",
-                                 "sample": last[0], "parts_s": last[2]},
+                "step_note": "a step is one timed slice of the oracle lookup (ms_per_step is its wall time); value = "
+                             "1 / (phase times scaled by the plan's counts)",
+                "cpu_baseline": {"value": round(v, 6), "unit": "lookups/s", "cores": core.threads(), "kind": "oracle",
+                                 "sample": smp.desc, "est_s_per_lookup": round(t, 2), "parts_s": parts},
                 "e2e": {"value": round(v, 6), "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -714,9 +829,7 @@ def main():
         r = run_gpu(args, world, rank, local)
         cpu = None
         if rank == 0 and world == 1 and not args.skip_cpu_baseline:
-            s, sample, cores, parts = oracle_lookup_seconds()
-            cpu = {"value": round(1.0 / s, 6), "unit": "lookups/s", "cores": cores, "kind": "oracle",
-                   "sample": sample, "parts_s": parts}
+            cpu = oracle_baseline()
     finally:
         sys.stdout.flush()
         os.dup2(saved_stdout, 1)

@@ -94,6 +94,8 @@ helrm_status helrm_params_moduli(const helrm_params* p, uint64_t* q, uint64_t* p
 /* Builds the device twiddle / conversion tables of every prime on `device`;
  * all later GPU work is enqueued on `cuda_stream` (0 = legacy default). */
 helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t cuda_stream, helrm_ctx** out);
+/* Frees the context's device memory pool: every handle created on the
+ * context (keys, ciphertexts, plans) must be destroyed before it. */
 void helrm_ctx_destroy(helrm_ctx* c);
 helrm_status helrm_ctx_sync(helrm_ctx* c);
 /* Number of library kernels launched on this context since creation. */

@@ -38,6 +38,7 @@
 #include "internal.h"
 #include "fmath.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace helrm {
@@ -83,9 +84,11 @@ __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double 
 //   MODE 1 (pass 2): sub-transform = 256-block B; twiddles tw2[B][...]:
 //     [0, 15): phase A, 2^st - 1 + i_loc;  15 + 16 j + t: thread t's phase-B twiddle j.
 // The body of one CTA: tile bx of launch limb `limb`; the pass-1 -> pass-2
-// intermediate of that limb lives at scratch + slot N.  CG: scratch reads
-// bypass L1 (the fused kernel reuses scratch slots inside one launch).
-template <int SLOG, int MODE, bool CG = false>
+// intermediate of that limb lives at scratch + slot N.  (A persistent,
+// double-buffered variant that prefetched the next tile with cp.async while
+// computing this one measured slower: 3 CTAs/SM instead of 4, 7.26 vs 6.81 ms
+// per Criteo lookup, 1640 vs 2091 GB/s in the microbenchmark.)
+template <int SLOG, int MODE>
 __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t limb, size_t slot,
                                              const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
                                              const PrimeDev* __restrict__ primes, const LimbMap& map, size_t limb0,
@@ -119,7 +122,7 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
       } else if (MODE == 0) {
         r[k] = u2d(s[(size_t)e * 256 + gsub]);
       } else {
-        r[k] = __longlong_as_double((long long)(CG ? __ldcg(s + (size_t)gsub * 256 + e) : s[(size_t)gsub * 256 + e]));
+        r[k] = __longlong_as_double((long long)s[(size_t)gsub * 256 + e]);
       }
     }
   }

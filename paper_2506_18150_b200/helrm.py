@@ -169,6 +169,8 @@ class _Handle:
     def __init__(self, h: ctypes.c_void_p, owner=None):
         self.h = h
         self._owner = owner        # keeps the context alive while this handle lives
+        if owner is not None and hasattr(owner, "_children"):
+            owner._children.add(self)   # the C ABI needs every handle destroyed before its context
 
     def close(self):
         if self.h:
@@ -262,11 +264,22 @@ class Context(_Handle):
     _destroy = "helrm_ctx_destroy"
 
     def __init__(self, params: Params, device: int = 0, stream: int = 0):
+        import weakref
         h = ctypes.c_void_p()
         _check(_L.helrm_ctx_create(params.h, device, stream, ctypes.byref(h)))
+        self._children = weakref.WeakSet()
         super().__init__(h)
         self.params = params
         self.info = params.info()
+
+    def close(self):
+        """Destroy the context after every handle created on it (ciphertexts,
+        keys, plans) that is still alive: helrm_ctx_destroy frees the device
+        memory pool those handles live in."""
+        if self.h:
+            for ch in list(self._children):
+                ch.close()
+        super().close()
 
     def sync(self):
         _check(_L.helrm_ctx_sync(self.h))
