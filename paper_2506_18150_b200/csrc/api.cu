@@ -24,9 +24,16 @@
 #include <tuple>
 #include <unordered_map>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 
 using namespace helrm;
+
+namespace helrm {
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
+}  // namespace helrm
 
 namespace {
 thread_local std::string g_last_error;
@@ -1893,6 +1900,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   c->evnext = 0;
   // inputs: ct (q, ci) at X + (q C + ci) 2 nqN (staged by the caller)
   const size_t xs = C * 2 * nqN;   // query stride of the inputs
+  std::unique_ptr<NvtxRange> nv12(new NvtxRange("helrm L1-L2 ModUp + baby steps"));
   // L1 (hoist #1): digits of every input c1 [ci][q][dn][nl][N];  L2: lazy baby steps over Q_l P,
   // baby b of query q at babies + (b Qc + q) 2 nlN
   std::vector<std::map<int, uint64_t*>> ab(C);
@@ -1991,6 +1999,8 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     }
     if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
+  nv12.reset();
+  NvtxRange nv34("helrm L3-L4 inner sums + giant steps");
   // L3 + L4, pipelined over the MAC groups (packs of kGiantPack giants):
   //   context stream: the inner sums (A, B) of a chunk of groups (HBM-bound)
   //   s_ntt:          ModDown(B) + ModUp(B') of the previous one (FP64-bound, hoist #2)
@@ -2285,6 +2295,7 @@ static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t
 // mbar < n; results into S [O][Qc][2][l][N]
 static void lookup_finish(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* Oall, int Qc,
                           uint64_t* S) {
+  NvtxRange nv_("helrm L6-L8 ModDown, rescale, RotSum");
   const Params& P = c->P;
   const uint32_t l = pl->level;
   const size_t N = P.N, nq = l + 1, nlN = (size_t)(l + 1 + P.K) * N, oN = 2 * (size_t)l * N;
@@ -2722,6 +2733,15 @@ helrm_status helrm_comm_init(helrm_ctx* c, const uint8_t* id, int rank, int worl
   });
 }
 
+// the communicator's asynchronous error state (a peer failure, a network error)
+static void nccl_check_async(helrm_ctx* c) {
+  if (!c->comm) return;
+  ncclResult_t r = ncclSuccess;
+  HNCCL(nccl().commGetAsyncError(c->comm, &r));
+  if (r != ncclSuccess && r != ncclInProgress)
+    throw Error(HELRM_ERR_NCCL, std::string("NCCL asynchronous error: ") + nccl().getErrorString(r));
+}
+
 // D20 with the giant pairs split over `parts` partitions: partition r
 // computes the partial Q_l P accumulators of its giant range
 // (helrm_dist_range), the partials are summed as uint64 words without
@@ -2762,8 +2782,10 @@ static void lookup_split(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys*
       int64_t lo = 0, hi = INT64_MAX;
       (void)helrm_dist_range(count_pairs(p), c->world, c->rank, &lo, &hi);
       lookup_double_part(c, p, rk, X.p, 1, lo, hi, O.p);
-      if (c->world > 1)
+      if (c->world > 1) {
         HNCCL(nccl().allReduce(O.p, O.p, owords, ncclUint64, ncclSum, c->comm, c->stream));
+        nccl_check_async(c);
+      }
     }
     // L5: each partial word is < q, so the sum is < parts q < 2^64 (parts < 2^13); reduce mod q
     if (parts > 1)

@@ -97,6 +97,7 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 NcclApi& nccl();
 #define HNCCL(x)                                                                                       \
@@ -181,6 +182,13 @@ inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   HCUDA(cudaLaunchKernelEx(&cfg, k, args...));
 }
 #endif
+
+// NVTX range per lookup stage (D20 L1..L8), visible in Nsight tools and usable
+// as an ncu --nvtx filter; a push/pop pair on the host thread
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+};
 
 // host-side time per call site (HELRM_HOSTPROF=1; diagnostics of launch overhead)
 bool hostprof_on();

@@ -231,9 +231,14 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
       const uint64_t qq = P.rc.q, sv = epi.s[lg], svp = epi.sp[lg];
       const uint64_t* yg = epi.y + pg * epi.ys + lg * (size_t)N + pbase + ((size_t)tp0 << lgs);
       uint64_t* og = epi.out + pg * epi.os + lg * (size_t)N + pbase + ((size_t)tp0 << lgs);
-#pragma unroll 4
+      // all 16 loads of y (and of out when accumulating) in flight at once: the epilogue's
+      // HBM reads otherwise serialise per 4-element group at the end of every CTA
+      uint64_t yv[16];
+#pragma unroll
+      for (int it = 0; it < 16; it++) yv[it] = yg[it * gstep];
+#pragma unroll
       for (int it = 0; it < 16; it++) {
-        uint64_t v = shoup(sub_mod(yg[it * gstep], sp0[256 * it], qq), sv, svp, qq);
+        uint64_t v = shoup(sub_mod(yv[it], sp0[256 * it], qq), sv, svp, qq);
         if (epi.accumulate) v = add_mod(v, og[it * gstep], qq);
         og[it * gstep] = v;
       }
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
     const int n = N >> 1, lgs = log_n - 9, stride = 1 << lgs;
     const int i = tid % 16, g = blockIdx.x * 16 + i;
     const uint64_t* sg = s + (size_t)(g >> lgs) * n + (g & (stride - 1));
-#pragma unroll 4
+#pragma unroll
     for (int idx = tid; idx < kTileElems; idx += kThreads) {   // swizzled gather, as the forward store
       const int tp = idx / 16;
       sm[tp * 16 + (i ^ (tp & 15))] = u2d(sg[(size_t)tp << lgs]);

@@ -22,8 +22,9 @@ NcclApi& nccl() {
     api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
     api.broadcast = (decltype(api.broadcast))dlsym(h, "ncclBroadcast");
     api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+    api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
     api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.broadcast &&
-             api.getErrorString;
+             api.getErrorString && api.commGetAsyncError;
   });
   if (!api.ok) throw Error(HELRM_ERR_NCCL, "libnccl.so.2 not loadable");
   return api;
