@@ -58,6 +58,14 @@ typedef int helrm_status;
 
 #define HELRM_MODE_DOUBLE 0  /* double-hoisted BSGS (the paper's) */
 #define HELRM_MODE_SINGLE 1  /* single-hoisted cross-check mode */
+/* Flag OR-ed into the plan mode (double-hoisted only): keep the encoded
+ * diagonals as int64 coefficients (N words each instead of l+1+K limbs) and
+ * expand them (reduce, NTT, D-form) during every lookup, in bounded chunks;
+ * input ciphertexts are processed in groups.  For layouts whose QP-NTT
+ * diagonals exceed HBM (LLM layout L1: 36,348 diagonals = 426 GiB; the
+ * 100-input-ct Criteo model: 700 GiB).  Same bits as the stored form.
+ * Lookups on compact plans run query by query, without graph replay. */
+#define HELRM_PLAN_COMPACT 2
 
 typedef struct helrm_params helrm_params;
 typedef struct helrm_ctx helrm_ctx;
@@ -199,7 +207,8 @@ typedef struct {
 /* Packs W, extracts the hybrid diagonals, splits them BSGS (n1 = 0: smallest
  * power of two with n1^2 >= span), pre-rotates, encodes at Delta_pt = q_level
  * over Q_level P (double) or Q_level (single) and uploads them (device memory
- * owned by the plan).  LEVEL if level < 1 or > L. */
+ * owned by the plan; mode | HELRM_PLAN_COMPACT: the int64 coefficients only).
+ * LEVEL if level < 1 or > L; ARG for a compact single-hoisted plan. */
 helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* t, uint32_t level, uint32_t n1, uint32_t mode,
                                helrm_plan** out);
 void helrm_plan_destroy(helrm_plan* p);

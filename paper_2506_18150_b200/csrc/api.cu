@@ -267,6 +267,8 @@ struct helrm_plan {
   std::vector<std::vector<int>> babies;                   // [c] sorted j used
   int64_t n_diag = 0;
   uint64_t* diag = nullptr;                               // [n_unique][nl][N]
+  bool compact = false;                                   // HELRM_PLAN_COMPACT: diagonals as coefficients
+  int64_t* coef = nullptr;                                // compact: [n_unique][N] encoded int64
   int64_t n_unique = 0;
   uint32_t nl = 0;
   std::vector<int64_t> rotations;
@@ -1537,12 +1539,16 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
     DevGuard dg_(c->device);
     const Params& P = c->P;
     need(level >= 1 && level <= P.L, HELRM_ERR_LEVEL, "lookup needs 1 <= level <= L");
+    const bool compact = (mode & HELRM_PLAN_COMPACT) != 0;
+    mode &= ~(uint32_t)HELRM_PLAN_COMPACT;
     need(mode == HELRM_MODE_DOUBLE || mode == HELRM_MODE_SINGLE, HELRM_ERR_ARG, "bad mode");
+    need(!compact || mode == HELRM_MODE_DOUBLE, HELRM_ERR_ARG, "compact plans run the double-hoisted mode");
     const int64_t n = P.n;
     pl = new helrm_plan();
     pl->c = c;
     pl->level = level;
     pl->mode = mode;
+    pl->compact = compact;
     pl->K = T->K;
     pl->M = T->M;
     pl->mbar = std::min(next_pow2(T->M), n);
@@ -1653,7 +1659,8 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
     pl->nl = mode == HELRM_MODE_DOUBLE ? level + 1 + P.K : level + 1;
     LimbMap m = mode == HELRM_MODE_DOUBLE ? P.map_qp(level) : P.map_q(level);
     const size_t N = P.N;
-    pl->diag = (uint64_t*)c->dalloc((size_t)pl->n_unique * pl->nl * N * 8);
+    if (compact) pl->coef = (int64_t*)c->dalloc((size_t)pl->n_unique * N * 8);
+    else pl->diag = (uint64_t*)c->dalloc((size_t)pl->n_unique * pl->nl * N * 8);
     const double delta_pt = (double)P.primes[level];
     const int64_t chunk = 64;
     std::vector<int64_t> coef((size_t)chunk * N);
@@ -1665,6 +1672,11 @@ helrm_status helrm_plan_create(helrm_ctx* c, const helrm_tables* T, uint32_t lev
       for (int64_t k = 0; k < cnt; k++) bad |= encode_slots(uniq[u0 + k].data(), 0, P.log_n, delta_pt, &coef[k * N]);
       need(bad == 0, HELRM_ERR_CONFIG, "|encoded diagonal coefficient| >= 2^62");
       HCUDA(cudaStreamSynchronize(c->stream));
+      if (compact) {   // the lookup expands them (reduce, NTT, D-form) just before its inner sums
+        HCUDA(cudaMemcpyAsync(pl->coef + (size_t)u0 * N, coef.data(), (size_t)cnt * N * 8, cudaMemcpyHostToDevice,
+                              c->stream));
+        continue;
+      }
       HCUDA(cudaMemcpyAsync(dcoef.p, coef.data(), (size_t)cnt * N * 8, cudaMemcpyHostToDevice, c->stream));
       for (int64_t k = 0; k < cnt; k++) {
         uint64_t* dst = pl->diag + (size_t)(u0 + k) * pl->nl * N;
@@ -1685,6 +1697,7 @@ void helrm_plan_destroy(helrm_plan* p) {
   DevGuard dg_(p->c->device);
   p->c->drop_graphs(p->id);
   p->c->dfree(p->diag);
+  p->c->dfree(p->coef);
   p->c->trim();
   delete p;
 }
@@ -1704,8 +1717,8 @@ helrm_status helrm_plan_info(const helrm_plan* p, helrm_plan_info_t* out) {
     r.n2_max = *std::max_element(p->n2.begin(), p->n2.end());
     r.n_rotations = (int64_t)p->rotations.size();
     r.level = p->level;
-    r.mode = p->mode;
-    r.diag_bytes = (uint64_t)p->n_unique * p->nl * p->c->P.N * 8;
+    r.mode = p->mode | (p->compact ? HELRM_PLAN_COMPACT : 0);
+    r.diag_bytes = (uint64_t)p->n_unique * (p->compact ? 1 : p->nl) * p->c->P.N * 8;
     *out = r;
   });
 }
@@ -1881,6 +1894,150 @@ static void run_macs_all(helrm_ctx* c, const MacList& ml, uint64_t* out, size_t 
   run_macs(c, ml, md, 0, ml.groups.size(), out, out_stride, map, x_dform);
 }
 
+// Compact plans (HELRM_PLAN_COMPACT), one query: D20 L1-L3 with the input
+// cts in groups and the diagonals expanded chunk by chunk.  For each group
+// of input cts: ModUp of their c1 and their baby steps (one k_kip_multi with
+// the cts as "queries" when they share the baby set); then the unique
+// diagonals those cts' terms use, `uc` at a time, are expanded from the
+// plan's int64 coefficients (reduce into every Q_l P limb, NTT, D-form) and
+// the inner sums of the terms that use them are accumulated into AB (pair z
+// of ml.oi at AB + z 2 nlN, zeroed by the caller).  Exact modular sums in
+// another order: the same bits as the stored-diagonal path.
+static void compact_l1_l3(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* X,
+                          const std::vector<std::pair<int64_t, int64_t>>& oi, uint64_t* AB) {
+  const Params& P = c->P;
+  const uint32_t l = pl->level;
+  const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, nqN = nq * N, dn = P.dnum(l);
+  const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
+  const LevelConst& lc = level_const(c, l);
+  const int64_t C = pl->C;
+  size_t fr = 0, tot = 0;
+  HCUDA(cudaMemGetInfo(&fr, &tot));
+  // device budgets: baby pairs + digits of a ct group, and the expansion buffer
+  static const double grp_gib = getenv("HELRM_COMPACT_GROUP_GIB") ? atof(getenv("HELRM_COMPACT_GROUP_GIB")) : 0;
+  static const double exp_gib = getenv("HELRM_COMPACT_EXP_GIB") ? atof(getenv("HELRM_COMPACT_EXP_GIB")) : 4;
+  const size_t gbudget = grp_gib > 0 ? (size_t)(grp_gib * (1 << 30)) : std::min<size_t>(fr / 3, (size_t)40 << 30);
+  size_t nb_max = 1;
+  for (auto& b : pl->babies) nb_max = std::max(nb_max, b.size());
+  const size_t per_ct = 8 * (dn * nlN + nb_max * 2 * nlN);
+  const int64_t G = std::max<int64_t>(1, std::min<int64_t>(C, (int64_t)(gbudget / per_ct)));
+  const size_t uc = std::max<size_t>(1, std::min<size_t>((size_t)pl->n_unique, (size_t)(exp_gib * (1 << 30)) / (8 * nlN)));
+  DBuf E(c, uc * nlN);
+  for (int64_t c0 = 0; c0 < C; c0 += G) {
+    const int64_t g = std::min(G, C - c0);
+    DBuf Dg(c, (size_t)g * dn * nlN), Bg(c, (size_t)g * nb_max * 2 * nlN);
+    // L1: digits of the group's c1 (ct ci at X + ci 2 nqN)
+    modup_batch(c, X + c0 * 2 * nqN + nqN, 2 * nqN, (int)g, l, Dg.p, nullptr, false);
+    // L2: baby pair (ci, j) at Bg + ((ci - c0) nb_max + jj) 2 nlN
+    std::map<std::pair<int64_t, int>, uint64_t*> ab;
+    bool same = true;
+    for (int64_t ci = c0 + 1; ci < c0 + g; ci++) same = same && pl->babies[ci] == pl->babies[c0];
+    const int64_t runs = same ? 1 : g;   // one kip_multi over the group (cts as queries), or one per ct
+    for (int64_t r = 0; r < runs; r++) {
+      const int64_t cf = c0 + (same ? 0 : r), nct = same ? g : 1;
+      const uint64_t* xc = X + cf * 2 * nqN;
+      KipMulti km{};
+      km.own = xc + nqN;
+      km.ownq = 2 * nqN;
+      km.alpha = (int)P.alpha;
+      km.digits = Dg.p + (cf - c0) * dn * nlN;
+      km.digit_stride = nlN;
+      km.dnum = (int)dn;
+      km.c0 = xc;
+      km.p_mod = lc.pmod;
+      km.level = l;
+      km.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+      km.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+      km.out_half = nlN;
+      km.nq = (int)nct;
+      km.qk = std::min((int)nct, 4);
+      km.zfast = nct > 4 ? 1 : 0;
+      km.dq = dn * nlN;
+      km.cq = 2 * nqN;
+      km.oq = nb_max * 2 * nlN;
+      const std::vector<int>& bl = pl->babies[cf];
+      for (size_t jj = 0; jj < bl.size(); jj++) {
+        const int j = bl[jj];
+        uint64_t* a = Bg.p + ((cf - c0) * nb_max + jj) * 2 * nlN;
+        for (int64_t k = 0; k < nct; k++) ab[{cf + k, j}] = a + k * nb_max * 2 * nlN;
+        if (j == 0) {   // (P c0, P c1) in D-form, P limbs 0
+          for (int64_t k = 0; k < nct; k++) HCUDA(cudaMemsetAsync(a + k * nb_max * 2 * nlN, 0, 2 * nlN * 8, c->stream));
+          launch_scalar_mul(c->dc(), xc, a, mq, lc.pmod, lc.pmods, 1, (int)nct, 2 * nqN, nb_max * 2 * nlN);
+          launch_scalar_mul(c->dc(), xc + nqN, a + nlN, mq, lc.pmod, lc.pmods, 1, (int)nct, 2 * nqN, nb_max * 2 * nlN);
+        } else {
+          need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
+          const uint64_t ge = galois_of_rot(c, j);
+          km.rot[km.n] = rot_of_galois(c, ge);
+          km.key[km.n] = key_for(rk, ge);
+          km.out[km.n] = a;
+          km.max_rot = std::max(km.max_rot, km.rot[km.n]);
+          km.n++;
+        }
+      }
+      if (km.n) launch_kip_multi(c->dc(), km, mqp);
+    }
+    // L3: the unique diagonals of this group's terms, uc at a time
+    std::vector<uint32_t> uids;
+    for (auto& zo : oi)
+      for (const Entry& e : pl->entries[zo.first][zo.second])
+        if (e.c >= c0 && e.c < c0 + g) uids.push_back((uint32_t)e.uid);
+    std::sort(uids.begin(), uids.end());
+    uids.erase(std::unique(uids.begin(), uids.end()), uids.end());
+    for (size_t u0 = 0; u0 < uids.size(); u0 += uc) {
+      const size_t cnt = std::min(uc, uids.size() - u0);
+      std::unordered_map<uint32_t, size_t> slot;
+      for (size_t k = 0; k < cnt; k++) slot[uids[u0 + k]] = k;
+      DBuf du(c, (cnt + 1) / 2);
+      HCUDA(cudaMemcpyAsync(du.p, uids.data() + u0, cnt * 4, cudaMemcpyHostToDevice, c->stream));
+      launch_expand_coef(c->dc(), pl->coef, (const uint32_t*)du.p, cnt, E.p, mqp);
+      ntt_fwd(c, E.p, E.p, cnt * nl, mqp);
+      launch_dform(c->dc(), E.p, cnt * nlN, mqp, 1);
+      // work list: packs of <= kGiantPack consecutive pairs of one output block
+      std::vector<MacTerm> terms;
+      std::vector<int4> groups;
+      double nu = 0;
+      for (size_t z0 = 0; z0 < oi.size();) {
+        size_t z1 = z0 + 1;
+        while (z1 < oi.size() && z1 - z0 < (size_t)kGiantPack && oi[z1].first == oi[z0].first) z1++;
+        std::map<std::pair<int64_t, int>, MacTerm> tm;
+        for (size_t z = z0; z < z1; z++)
+          for (const Entry& e : pl->entries[oi[z].first][oi[z].second]) {
+            if (e.c < c0 || e.c >= c0 + g) continue;
+            auto it = slot.find((uint32_t)e.uid);
+            if (it == slot.end()) continue;
+            auto ti = tm.find({e.c, e.j});
+            if (ti == tm.end()) {
+              MacTerm t{};
+              t.x0 = ab.at({e.c, e.j});
+              t.x1 = t.x0 + nlN;
+              ti = tm.emplace(std::make_pair((int64_t)e.c, e.j), t).first;
+            }
+            ti->second.u[z - z0] = E.p + it->second * nlN;
+            nu += 1;
+          }
+        if (!tm.empty()) {
+          groups.push_back(make_int4((int)terms.size(), (int)tm.size(), (int)z0, (int)(z1 - z0)));
+          for (auto& kv : tm) terms.push_back(kv.second);
+        }
+        z0 = z1;
+      }
+      if (groups.empty()) continue;
+      DBuf dt(c, (terms.size() * sizeof(MacTerm) + 7) / 8), dg(c, groups.size() * 2);
+      HCUDA(cudaMemcpyAsync(dt.p, terms.data(), terms.size() * sizeof(MacTerm), cudaMemcpyHostToDevice, c->stream));
+      HCUDA(cudaMemcpyAsync(dg.p, groups.data(), groups.size() * sizeof(int4), cudaMemcpyHostToDevice, c->stream));
+      {
+        const DevCtx dcx = c->dc();
+        ProfScope ps_(dcx, "diag_mac", 8.0 * N * nl * (nu + 2.0 * terms.size() + 4.0 * oi.size()));
+        need(launch_diag_mac_bulk(dcx, (const MacTerm*)dt.p, (const int4*)dg.p, (int)groups.size(), AB, 2 * nlN, nlN,
+                                  mqp, 1, 0, 0, 1),
+             HELRM_ERR_CONFIG, "compact plans need N divisible by the MAC tile");
+      }
+      // host vectors are copied before the next chunk reuses them (pageable copies are staged)
+      HCUDA(cudaStreamSynchronize(c->stream));
+    }
+  }
+}
+
 // D20 L1-L4 for Qc queries (in[q C + c]) and the giant pairs z in [z_lo, z_hi)
 // of the non-empty (o, i) enumeration: accumulates into Oall [O][Qc][2][l+1+K][N]
 // (zeroed by the caller).  With z over everything this is the whole lookup up
@@ -1906,10 +2063,12 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   std::vector<std::map<int, uint64_t*>> ab(C);
   size_t n_baby = 0;
   for (auto& bl : pl->babies) n_baby += bl.size();
-  DBuf D(c, C * Qc * dn * nlN);
-  DBuf babies(c, std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
+  need(!pl->compact || Qc == 1, HELRM_ERR_ARG, "compact plans look up one query at a time");
+  // compact plans: L1-L2 happen per ct group inside compact_l1_l3 (after the work list)
+  DBuf D(c, pl->compact ? 1 : C * Qc * dn * nlN);
+  DBuf babies(c, pl->compact ? 1 : std::max<size_t>(1, n_baby) * Qc * 2 * nlN);
   size_t bi = 0;
-  bool same_babies = Qc == 1 && C > 1;
+  bool same_babies = Qc == 1 && C > 1 && !pl->compact;
   for (size_t ci = 1; same_babies && ci < C; ci++) same_babies = pl->babies[ci] == pl->babies[0];
   if (same_babies) {
     // one query, C input cts with the same baby steps (LLM layout L2): the cts take the
@@ -1958,7 +2117,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
     }
     if (km.n) launch_kip_multi(c->dc(), km, mqp);
   }
-  for (size_t ci = 0; !same_babies && ci < C; ci++) {
+  for (size_t ci = 0; !same_babies && !pl->compact && ci < C; ci++) {
     const uint64_t* c0 = X + ci * 2 * nqN;
     uint64_t* Dc = D.p + ci * Qc * dn * nlN;
     modup_batch(c, c0 + nqN, xs, Qc, l, Dc, nullptr, false);
@@ -2009,6 +2168,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   // only meet at the events; O is only touched by s_kip.  Pair z of query q
   // lives at AB + (z Qc + q) 2 nlN, so a run of pairs is one strided batch.
   const MacList ml = build_macs(pl, nlN, [&](int ci, int j) {
+    if (pl->compact) return std::make_pair((const uint64_t*)nullptr, (const uint64_t*)nullptr);   // unused
     uint64_t* a = ab[ci].at(j);
     return std::make_pair((const uint64_t*)a, (const uint64_t*)(a + nlN));
   }, z_lo, z_hi);
@@ -2016,7 +2176,11 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   if (n_out == 0) return;
   const size_t zq = (size_t)Qc;   // pairs per z
   DBuf AB(c, (size_t)n_out * zq * 2 * nlN), Bp(c, (size_t)n_out * zq * nqN), D2(c, (size_t)n_out * zq * dn * nlN);
-  const MacDev md(c, ml, pinned);
+  if (pl->compact) {
+    HCUDA(cudaMemsetAsync(AB.p, 0, (size_t)n_out * zq * 2 * nlN * 8, c->stream));
+    compact_l1_l3(c, pl, rk, X, ml.oi, AB.p);
+  }
+  const MacDev md(c, pl->compact ? MacList{} : ml, pinned);
   // (serialised while the per-kernel profiler is on, so each kernel's events time it alone)
   // default: on for batched chunks (measured 158 vs 148 lookups/s at batch 64), off for batch 1
   // (7.16 vs 7.22 ms); HELRM_PIPE overrides
@@ -2044,7 +2208,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   // (LLM layout L2: the 4 blocks share all 1279 plaintexts) run as one MAC launch in which
   // the blocks take the query role, so each plaintext value is loaded once per 2 blocks.
   size_t g_blk = ml.groups.size();
-  bool periodic = same_babies && pl->O == (int64_t)C && pl->O > 1 && ml.groups.size() % pl->O == 0;
+  bool periodic = !pl->compact && same_babies && pl->O == (int64_t)C && pl->O > 1 && ml.groups.size() % pl->O == 0;
   if (periodic) {
     g_blk = ml.groups.size() / pl->O;
     const size_t ts = ml.term_size, nbb = pl->babies[0].size();
@@ -2152,7 +2316,7 @@ static void lookup_double_part(helrm_ctx* c, const helrm_plan* pl, const helrm_r
   for (size_t gp = 0; !periodic && gp < ml.groups.size(); gp += mac_ch) {
     const size_t gq = std::min(ml.groups.size(), gp + (size_t)mac_ch);
     const int z0 = ml.groups[gp].z, z1 = ml.groups[gq - 1].z + ml.groups[gq - 1].w;
-    if (!periodic)
+    if (!periodic && !pl->compact)
       run_macs(c, ml, md, gp, gq, AB.p, zq * 2 * nlN, mqp, true, Qc, 2 * nlN, 2 * nlN, sm, pers);
     if (pipe) c->join(sn, sm);
     std::vector<int> rot;   // rotating pairs of the chunk (zero giants need no key switch)
@@ -2435,12 +2599,13 @@ static void lookup_double(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
     if (getenv("HELRM_QCHUNK")) qc = std::max(1, atoi(getenv("HELRM_QCHUNK")));
     qc = std::min(qc, batch);
   }
+  if (pl->compact) qc = 1;   // compact plans: one query at a time, eagerly (chunked host work lists)
   static const bool graphs = getenv("HELRM_GRAPH") ? atoi(getenv("HELRM_GRAPH")) != 0 : true;
   for (size_t q0 = 0; q0 < batch; q0 += qc) {
     const int Qc = (int)std::min(qc, batch - q0);
     const size_t nin = (size_t)Qc * pl->C;
     const double scale = in[q0 * pl->C]->scale;
-    if (!graphs || c->prof.on || Qc > 2) {
+    if (!graphs || c->prof.on || Qc > 2 || pl->compact) {
       DBuf X(c, nin * 2 * nqN), S(c, (size_t)pl->O * Qc * oN);
       stage_inputs(c, in + q0 * pl->C, nin, 2 * nqN, X.p);
       lookup_chunk(c, pl, rk, X.p, Qc, S.p, nullptr);
@@ -2506,7 +2671,8 @@ helrm_status helrm_lookup_host(helrm_ctx* c, const helrm_plan* p, const helrm_ro
   return guard([&] {
     need(c && p && rk && (in || batch == 0) && (out || batch == 0), HELRM_ERR_ARG, "null argument");
     DevGuard dg_(c->device);
-    need(p->mode == HELRM_MODE_DOUBLE, HELRM_ERR_ARG, "helrm_lookup_host runs the double-hoisted mode");
+    need(p->mode == HELRM_MODE_DOUBLE && !p->compact, HELRM_ERR_ARG,
+         "helrm_lookup_host runs stored-diagonal double-hoisted plans");
     for (int64_t a : p->rotations) (void)key_for(rk, galois_of_rot(c, a));
     const Params& P = c->P;
     const uint32_t l = p->level;

@@ -264,6 +264,9 @@ void launch_automorph(const DevCtx& c, const uint64_t* a, uint64_t* out, const L
                       int accumulate);
 // out[l] = in[l] mod q_l for in < 2^64 (after a uint64 sum all-reduce)
 void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map);
+// compact plans: out + (k map.n + l) N = coef[uids[k]] mod q_l (signed -> canonical), k < n
+void launch_expand_coef(const DevCtx& c, const int64_t* coef, const uint32_t* uids, size_t n, uint64_t* out,
+                        const LimbMap& map);
 // x[i] += y[i] as uint64 words, i < n (the exact sum of the all-reduce)
 void launch_add_u64(const DevCtx& c, uint64_t* x, const uint64_t* y, size_t n);
 void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_t ql, uint64_t* out, size_t os, int G,
@@ -366,9 +369,10 @@ using MacTermW = MacTermT<kWidePack>;
 // nq queries: query q reads x + q xq and writes out + q oq (plaintexts shared).
 // wide: terms are MacTermW (batched kernel, nq >= 1), else MacTerm.
 // batch-1 inner sums fed by bulk async copies (kernels_mac_bulk.cu); false if it does not apply
+// accumulate: out (+)= the inner sums (compact plans sum a pair's terms over several launches)
 bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
                           size_t out_stride, size_t half, const LimbMap& map, int nq = 1, size_t xq = 0,
-                          size_t oq = 0);
+                          size_t oq = 0, int accumulate = 0);
 void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int n_groups, double n_u_total,
                      double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
                      bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0, bool wide = false);

@@ -82,7 +82,8 @@ template <int QN, int kProducers = bulk_producers<QN>(), int QS = bulk_qsplit<QN
 __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
     k_diag_mac_bulk(const MacTerm* __restrict__ terms, const int4* __restrict__ groups, int n_groups,
                     uint64_t* __restrict__ out, size_t out_stride, size_t half, const PrimeDev* __restrict__ primes,
-                    const __grid_constant__ LimbMap map, uint32_t N, int stages, int nq, size_t xq, size_t oq) {
+                    const __grid_constant__ LimbMap map, uint32_t N, int stages, int nq, size_t xq, size_t oq,
+                    int accumulate) {
   pdl_wait_trigger();
   constexpr int G = kGiantPack, NS = bulk_slots<QN>();
   constexpr uint32_t SB = NS * kSlotBytes;
@@ -201,8 +202,14 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
         for (int g = 0; g < G; g++) {
           if (g < gr.w) {
             uint64_t* dst = out + (size_t)(gr.z + g) * out_stride + (size_t)(qc * QN + qh * QT + k) * oq;
-            dst[o] = fm::c2u(fm::fred(acc0[k][g], q, qi), P.rc.q);
-            dst[half + o] = fm::c2u(fm::fred(acc1[k][g], q, qi), P.rc.q);
+            uint64_t v0 = fm::c2u(fm::fred(acc0[k][g], q, qi), P.rc.q);
+            uint64_t v1 = fm::c2u(fm::fred(acc1[k][g], q, qi), P.rc.q);
+            if (accumulate) {
+              v0 = add_mod(v0, dst[o], P.rc.q);
+              v1 = add_mod(v1, dst[half + o], P.rc.q);
+            }
+            dst[o] = v0;
+            dst[half + o] = v1;
           }
         }
     }
@@ -211,7 +218,8 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
 
 template <int QN>
 static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
-                        size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq) {
+                        size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq,
+                        int accumulate) {
   static const int stages_env = getenv("HELRM_MACB_STAGES") ? atoi(getenv("HELRM_MACB_STAGES")) : 0;
   constexpr size_t SB = (size_t)bulk_slots<QN>() * kSlotBytes;
   // default: as many stages as fit in ~200 KiB (16 at 12 KiB, 8 at 24 KiB), a multiple of kProducers
@@ -230,18 +238,22 @@ static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* group
   }
   const unsigned total = (c.N / kTile) * (unsigned)n_groups * map.n;
   const unsigned grid = std::min<unsigned>(total, (unsigned)c.n_sm * (unsigned)per_sm);
-  launch_pdl(k_diag_mac_bulk<QN>, dim3(grid), dim3(kTile * bulk_qsplit<QN>() + 32 * kProducers), smem, c.stream, terms, groups, n_groups, out, out_stride, half, c.primes, map, c.N, stages, nq, xq, oq);
+  launch_pdl(k_diag_mac_bulk<QN>, dim3(grid), dim3(kTile * bulk_qsplit<QN>() + 32 * kProducers), smem, c.stream, terms, groups, n_groups, out, out_stride, half, c.primes, map, c.N, stages, nq, xq, oq, accumulate);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
-                          size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq) {
+                          size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq,
+                          int accumulate) {
   if (c.N % kTile || nq < 1) return false;
   static const int qmax = getenv("HELRM_MACB_QMAX") ? atoi(getenv("HELRM_MACB_QMAX")) : 4;
-  if (nq % 4 == 0 && qmax >= 4) bulk_launch<4>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
-  else if (nq % 2 == 0 && qmax >= 2) bulk_launch<2>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
-  else bulk_launch<1>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq);
+  if (nq % 4 == 0 && qmax >= 4)
+    bulk_launch<4>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate);
+  else if (nq % 2 == 0 && qmax >= 2)
+    bulk_launch<2>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate);
+  else
+    bulk_launch<1>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate);
   return true;
 }
 

@@ -648,6 +648,28 @@ __global__ void k_modred(uint64_t* __restrict__ x, const PrimeDev* __restrict__ 
   x[o] = v - mulhi64(v, rc.mu) * rc.q >= rc.q ? v - mulhi64(v, rc.mu) * rc.q - rc.q : v - mulhi64(v, rc.mu) * rc.q;
 }
 
+// Compact plans (HELRM_PLAN_COMPACT): the signed encoded coefficients of
+// unique diagonal uids[k] (coef + uids[k] N) reduced into every limb of map:
+// out + (k map.n + l) N.  (The NTT and the D-form conversion follow.)
+__global__ void k_expand_coef(const int64_t* __restrict__ coef, const uint32_t* __restrict__ uids,
+                              uint64_t* __restrict__ out, const PrimeDev* __restrict__ primes,
+                              const __grid_constant__ LimbMap map, uint32_t N) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  const size_t k = blockIdx.z;
+  if (i >= N) return;
+  const uint64_t q = primes[map.pr[l]].rc.q;
+  const int64_t v = coef[(size_t)uids[k] * N + i];
+  uint64_t r;
+  if (v >= 0) {
+    r = (uint64_t)v % q;
+  } else {
+    r = (uint64_t)(-v) % q;
+    r = r ? q - r : 0;
+  }
+  out[(k * map.n + l) * N + i] = r;
+}
+
 // x += y as plain uint64 words (the sum ncclAllReduce(ncclUint64, ncclSum) computes)
 __global__ void k_add_u64(uint64_t* __restrict__ x, const uint64_t* __restrict__ y, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -729,6 +751,15 @@ void launch_conv_rows(const DevCtx& c, const ConvRowDev* tab, int ncv, int rows,
 void launch_modred(const DevCtx& c, uint64_t* x, const LimbMap& map) {
   ProfScope ps_(c, "modred", 16.0 * c.N * map.n);
   launch_pdl(k_modred, dim3(grid_for(c.N, map.n)), dim3(kT), 0, c.stream, x, c.primes, map, c.N);
+  (*c.launches)++;
+  HCUDA(cudaGetLastError());
+}
+
+void launch_expand_coef(const DevCtx& c, const int64_t* coef, const uint32_t* uids, size_t n, uint64_t* out,
+                        const LimbMap& map) {
+  ProfScope ps_(c, "expand_coef", 8.0 * c.N * n * (1 + map.n));
+  k_expand_coef<<<dim3((c.N + kT - 1) / kT, map.n, (unsigned)n), kT, 0, c.stream>>>(coef, uids, out, c.primes, map,
+                                                                                    c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }

@@ -430,3 +430,32 @@ def test_hybrid_diagonals_equal_brute_force_random_multi_ct():
         assert got[:3] == want[:3] and got[3].keys() == want[3].keys(), trial
         for k, v in want[3].items():
             assert np.array_equal(got[3][k], v)
+
+
+def test_llm_l1_layout_plan_counts():
+    """The paper-exact LLM layout L1 (contiguous row-major slot
+    ordering) on the Tiny ring: 64 tokens at input stride 64
+    and output stride 48 -> 2 input / 2 output cts; the diagonals equal the
+    brute-force D19 evaluation and the plan reproduces the dense W x."""
+    w = synth.make_workload("llm_l1_small")
+    lay = lk.layout(w)
+    n = w.config.n_slots
+    assert (lay.K, lay.M) == (64 * 64, 64 * 48)
+    got = lk.hybrid_diagonals(lay, n)
+    want = _diagonals_brute_force(lk.dense_matrix(lay), n)
+    assert got[:3] == want[:3] == (n, 2, 2) and got[3].keys() == want[3].keys() and len(want[3]) == 1325
+    plan = lk.make_plan(lay, n, w.config.level)
+    x = np.random.default_rng(5).normal(size=lay.K)
+    y = lk.simulate_plan_slots(plan, x, n)
+    assert np.abs(y[: lay.M] - lk.dense_matrix(lay) @ x).max() < 1e-9
+    # full size: 2 input / 3 output cts (PAPER.md:553: m = 128 tokens x 512 slots -> 2 cts)
+    lay_f = lk.layout(synth.make_workload("llm_l1"))
+    assert (-(-lay_f.K // (1 << 15)), -(-lay_f.M // (1 << 15))) == (2, 3)
+
+
+def test_criteo_100_ct_layout():
+    """The least compressed Criteo model analog: 3,272,921 input slots -> 100
+    input cts at n = 2^15 (the paper's 2,772,109 -> 85)."""
+    w = synth.make_workload("criteo_c100")
+    lay = lk.layout(w)
+    assert lay.K == 3272921 and -(-lay.K // (1 << 15)) == 100 and lay.M == 416

@@ -1,2 +1,8 @@
-timeout 1500 python -m pytest tests -m gpu -q -x -k "not (llm_full or c2_full)" > gpurun_out/r2_t2_pytest.txt 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2_t2_pytest.txt
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/r2_t2_bench.json 2> gpurun_out/r2_t2_bench.err; echo "bench rc=$?"; tail -3 gpurun_out/r2_t2_bench.err
+timeout 300 python bench.py --steps 10 --warmup 3 --skip-cpu-baseline --skip-micro --skip-llm --skip-c2 --skip-batch > gpurun_out/r2_t3_bench.json 2> gpurun_out/r2_t3_bench.err; echo "bench rc=$?"
+python - <<'PY'
+import json
+d = json.load(open("gpurun_out/r2_t3_bench.json"))
+print(d["value"], d["ms_per_step"], d["e2e"]["value"])
+for k, v in d["step"]["kernels"].items(): print(f"{k:14s} {v}")
+PY
+timeout 600 compute-sanitizer --tool memcheck --error-exitcode 1 python tools/sanitize_case.py > gpurun_out/r2_memcheck.txt 2>&1; echo "memcheck rc=$?"; tail -5 gpurun_out/r2_memcheck.txt
