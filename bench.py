@@ -484,6 +484,11 @@ def run_gpu(args, world, rank, local):
         secondary["criteo_l4_b1"] = shape_lookup(helrm, torch, stream, world, dev, "criteo_l4", reps=10)
         # a dense 512 -> 256 linear layer on the same engine, Criteo parameters
         secondary["mlp_512x256"] = shape_lookup(helrm, torch, stream, world, dev, "mlp_512x256")
+    if args.with_compact:
+        # layouts whose QP-NTT diagonals exceed HBM, on compact plans (HELRM_PLAN_COMPACT):
+        # the paper-exact LLM layout L1 and the 100-input-ct Criteo model
+        secondary["llm_l1_128_tokens"] = shape_lookup(helrm, torch, stream, world, dev, "llm_l1", reps=2, mode=2)
+        secondary["criteo_c100_b1"] = shape_lookup(helrm, torch, stream, world, dev, "criteo_c100", reps=2, mode=2)
 
     return {
         "value": value, "ms": ms / args.steps, "launches": launches, "clocks": clk.summary(),
@@ -561,7 +566,7 @@ def batch_lookup(args, ctx, helrm, torch, stream, plan, rk, cts, world, B=64):
     return res
 
 
-def shape_lookup(helrm, torch, stream, world, dev, name, reps=5):
+def shape_lookup(helrm, torch, stream, world, dev, name, reps=5, mode=0):
     """Batch-1 lookup of a secondary workload shape on its own context: device
     time per lookup (max over ranks) and the plan's counts."""
     import synth
@@ -571,7 +576,7 @@ def shape_lookup(helrm, torch, stream, world, dev, name, reps=5):
     ctx = helrm.Context(P, dev, stream.cuda_stream)
     t0 = time.time()
     T = helrm.tables_create(P, w.tables, w.n_dense)
-    plan = helrm.plan_create(ctx, T, cfg.level)
+    plan = helrm.plan_create(ctx, T, cfg.level, 0, mode)
     info = plan.info()
     sk = helrm.sk_gen(ctx, cfg.seed)
     pk = helrm.pk_gen(ctx, sk, cfg.seed)
@@ -581,7 +586,7 @@ def shape_lookup(helrm, torch, stream, world, dev, name, reps=5):
            for c in range(info.n_in_cts)]
     ctx.sync()
     setup = time.time() - t0
-    for _ in range(3):
+    for _ in range(1 if mode else 3):
         for o in helrm.lookup(ctx, plan, rk, cts):
             o.close()
     torch.cuda.synchronize()
@@ -597,9 +602,9 @@ def shape_lookup(helrm, torch, stream, world, dev, name, reps=5):
     res = {"ms_per_lookup": round(ms, 3), "lookups_per_s": round(world * 1e3 / ms, 2), "in_cts": info.n_in_cts,
            "n_diag": info.n_diag, "n1": info.n1, "rotation_keys": info.n_rotations, "setup_s": round(setup, 1),
            "diag_GiB": round(info.diag_bytes / 2**30, 2), "keys_GiB": round(rk.nbytes() / 2**30, 2)}
-    for h in (rk, pk, sk, plan, T):
-        h.close()
-    ctx.close()
+    if mode:
+        res.update({"out_cts": info.n_out_cts, "plan": "compact (int64 coefficient diagonals expanded in the lookup)"})
+    ctx.close()   # closes the context's keys, plan and ciphertexts first
     return res
 
 
@@ -777,6 +782,8 @@ def main():
     ap.add_argument("--skip-llm", action="store_true", help="skip the LLM-style 128-token measurement")
     ap.add_argument("--skip-c2", action="store_true", help="skip the 2-input-ct Criteo shape (Table 2 threshold 5e4)")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--with-compact", action="store_true",
+                    help="also time the compact-plan layouts (LLM L1, 100-ct Criteo; ~3 min of plan setup)")
     ap.add_argument("--micro-cts", type=int, default=1024)
     ap.add_argument("--rot-cts", type=int, default=8)
     ap.add_argument("--dist", action="store_true", help="also time the partitioned batch-1 lookup at world size 1")

@@ -288,6 +288,24 @@ helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_ro
  * 1 <= parts < 8192 (ARG otherwise).  Bit-identical to helrm_lookup. */
 helrm_status helrm_lookup_dist_virtual(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
                                        const helrm_ct* const* in, size_t batch, int parts, helrm_ct** out);
+/* The RNS-limb partition of the batch-1 lookup
+ * emulated in one process: rank r of `parts` owns rows [lo_r, hi_r) of the
+ * l+1+K limbs (helrm_dist_range) and computes only those rows of the baby key
+ * switches, inner sums and giant key switches (1/parts of the rotation keys
+ * and plaintext diagonals streamed per rank); ModUp / ModDown / rescale /
+ * RotSum are replicated; each giant's B rows and the output accumulators are
+ * all-gathered (explicit copies of the ranks' private slices).  Rank r owns
+ * rows [r rp, (r+1) rp), rp = ceil((l+1+K) / parts) (trailing ranks may own
+ * none).  Stored-diagonal double-hoisted plans; 1 <= parts <= l+1+K.
+ * Bit-identical to helrm_lookup. */
+helrm_status helrm_lookup_limbsplit_virtual(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                            const helrm_ct* const* in, size_t batch, int parts, helrm_ct** out);
+/* The same partition over the context's communicator (helrm_comm_init), one
+ * process per GPU: this rank computes its rows only; rank 0's inputs are
+ * broadcast, each giant's B rows and the accumulators are exchanged with
+ * ncclAllGather (slices padded to ceil((l+1+K) / world) rows). */
+helrm_status helrm_lookup_limbsplit(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                   const helrm_ct* const* in, size_t batch, helrm_ct** out);
 /* The combine's reduction alone (D23 L5), in place: n_polys R_{Q_level P}
  * polynomials [n_polys][level+1+K][N] at `dev` whose words are sums of
  * residues (< 2^64) become residues mod their limb's prime. */

@@ -2961,6 +2961,244 @@ static void lookup_split(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys*
   }
 }
 
+// the batch-1 lookup with the Q_l P limbs split
+// over `parts` ranks (rank r owns rows [lo_r, hi_r) of helrm_dist_range(l+1+K)),
+// emulated one rank after another in this process.  What every rank does:
+//   replicated (FP64): ModUp of the input c1s, each giant's ModDown + ModUp,
+//     the final ModDown / rescale / RotSum;
+//   own rows only (HBM): the baby key switches (k_kip_multi, row slice), the
+//     inner sums (bulk MAC, row slice) and the giant key switches
+//     (k_kip_giants, row slice) -- so each rank streams 1/G of the rotation
+//     keys and plaintext diagonals;
+//   exchange (an all-gather on a multi-GPU node): each giant pair's B rows
+//     before its ModDown, and the output accumulators before the finish.
+// Every rank's baby pairs, inner sums and accumulators live in private slice
+// buffers [2][rows][N]; the all-gathers are explicit copies of the slices into
+// full buffers.  Per-limb work is independent, so the result is bit-identical
+// to helrm_lookup (D23: only the limb placement changes).
+static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
+                             size_t batch, helrm_ct** out, int parts, bool real) {
+  need(pl->mode == HELRM_MODE_DOUBLE && !pl->compact, HELRM_ERR_ARG,
+       "the limb-partitioned lookup runs stored-diagonal double-hoisted plans");
+  for (int64_t a : pl->rotations) (void)key_for(rk, galois_of_rot(c, a));
+  const Params& P = c->P;
+  const uint32_t l = pl->level;
+  const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, nqN = nq * N, dn = P.dnum(l);
+  const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
+  const LevelConst& lc = level_const(c, l);
+  const int64_t C = pl->C, O = pl->O;
+  if (real) parts = c->world;
+  need(parts >= 1 && (size_t)parts <= nl, HELRM_ERR_ARG, "1 <= parts <= l + 1 + K");
+  // equal slices of rp = ceil(nl / parts) rows (the last ones shorter or empty), so that one
+  // ncclAllGather of the padded slices lays the rows out in order
+  const size_t rp = (nl + parts - 1) / parts;
+  std::vector<int64_t> lo(parts), hi(parts);
+  for (int r = 0; r < parts; r++) {
+    lo[r] = std::min<int64_t>((int64_t)nl, (int64_t)(r * rp));
+    hi[r] = std::min<int64_t>((int64_t)nl, (int64_t)((r + 1) * rp));
+  }
+  std::vector<int> mine;   // the ranks this process computes
+  if (real) mine.push_back(c->rank);
+  else
+    for (int r = 0; r < parts; r++) mine.push_back(r);
+  auto sub = [&](int r) {   // the LimbMap of rank r's rows (for the row-agnostic element-wise kernels)
+    LimbMap m{};
+    m.n = (int)(hi[r] - lo[r]);
+    for (int i = 0; i < m.n; i++) m.pr[i] = mqp.pr[lo[r] + i];
+    return m;
+  };
+  for (size_t qy = 0; qy < batch; qy++) {
+    const helrm_ct* const* cin = in + qy * C;
+    DBuf X(c, (size_t)C * 2 * nqN);
+    for (int64_t ci = 0; ci < C; ci++) {
+      need(cin[ci] != nullptr && cin[ci]->level == l, HELRM_ERR_LEVEL, "input level differs from the plan's");
+      if (real && parts > 1)   // the query lives on rank 0
+        HNCCL(nccl().broadcast(cin[ci]->d, X.p + ci * 2 * nqN, 2 * nqN, ncclUint64, 0, c->comm, c->stream));
+      else
+        HCUDA(cudaMemcpyAsync(X.p + ci * 2 * nqN, cin[ci]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    // L1 (replicated): digits of every input c1
+    DBuf D(c, (size_t)C * dn * nlN);
+    modup_batch(c, X.p + nqN, 2 * nqN, (int)C, l, D.p, nullptr, false);
+    // (P c0, P c1) of every ct (replicated, cheap): the baby pair of rotation 0
+    DBuf P0(c, (size_t)C * 2 * nlN);
+    HCUDA(cudaMemsetAsync(P0.p, 0, (size_t)C * 2 * nlN * 8, c->stream));
+    launch_scalar_mul(c->dc(), X.p, P0.p, mq, lc.pmod, lc.pmods, 1, (int)C, 2 * nqN, 2 * nlN);
+    launch_scalar_mul(c->dc(), X.p + nqN, P0.p + nlN, mq, lc.pmod, lc.pmods, 1, (int)C, 2 * nqN, 2 * nlN);
+    // the non-empty giant pairs z (o, i)
+    std::vector<std::pair<int64_t, int64_t>> oi;
+    for (int64_t o = 0; o < O; o++)
+      for (size_t i = 0; i < pl->entries[o].size(); i++)
+        if (!pl->entries[o][i].empty()) oi.push_back({o, (int64_t)i});
+    const size_t nz = oi.size();
+    size_t nb_tot = 0;
+    for (auto& b : pl->babies) nb_tot += b.size();
+    // rank slices: babies [b][2][rows][N], inner sums [z][2][rows][N], accumulators [o][2][rows][N]
+    // (slices hold rp rows; a rank with rows < rp leaves the tail unused)
+    std::vector<std::unique_ptr<DBuf>> SB(parts), SAB(parts), SO(parts);
+    std::vector<uint64_t*> sab(parts, nullptr), so(parts, nullptr);
+    for (int r : mine) {
+      SB[r].reset(new DBuf(c, std::max<size_t>(1, nb_tot) * 2 * rp * N));
+      SAB[r].reset(new DBuf(c, std::max<size_t>(1, nz) * 2 * rp * N));
+      SO[r].reset(new DBuf(c, (size_t)O * 2 * rp * N));
+      sab[r] = SAB[r]->p;
+      so[r] = SO[r]->p;
+      HCUDA(cudaMemsetAsync(so[r], 0, (size_t)O * 2 * rp * N * 8, c->stream));
+      if (hi[r] == lo[r]) HCUDA(cudaMemsetAsync(sab[r], 0, std::max<size_t>(1, nz) * 2 * rp * N * 8, c->stream));
+    }
+    for (int r : mine) {
+      if (hi[r] == lo[r]) continue;   // an empty slice (parts does not divide into l + 1 + K evenly)
+      const size_t rows = rp;         // slice stride (rows actually computed: hi - lo)
+      const size_t r0N = (size_t)lo[r] * N;
+      // L2 (own rows): baby pairs of every ct, baby (ci, j) at slice + b 2 rows N
+      std::map<std::pair<int64_t, int>, uint64_t*> ab;
+      size_t b = 0;
+      for (int64_t ci = 0; ci < C; ci++) {
+        KipMulti km{};
+        km.row0 = (int)lo[r];
+        km.rows = (int)(hi[r] - lo[r]);
+        km.own = X.p + ci * 2 * nqN + nqN;
+        km.alpha = (int)P.alpha;
+        km.digits = D.p + ci * dn * nlN;
+        km.digit_stride = nlN;
+        km.dnum = (int)dn;
+        km.c0 = X.p + ci * 2 * nqN;
+        km.p_mod = lc.pmod;
+        km.level = l;
+        km.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+        km.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+        km.out_half = rows * N;
+        for (int j : pl->babies[ci]) {
+          uint64_t* a = SB[r]->p + b++ * 2 * rows * N;
+          ab[{ci, j}] = a;
+          if (j == 0) {   // this rank's rows of (P c0, P c1)
+            for (int h = 0; h < 2; h++)
+              HCUDA(cudaMemcpyAsync(a + h * rows * N, P0.p + ci * 2 * nlN + h * nlN + r0N, (hi[r] - lo[r]) * N * 8,
+                                    cudaMemcpyDeviceToDevice, c->stream));
+            continue;
+          }
+          need(km.n < kMaxBabies, HELRM_ERR_CAPACITY, "too many baby steps");
+          const uint64_t g = galois_of_rot(c, j);
+          km.rot[km.n] = rot_of_galois(c, g);
+          km.key[km.n] = key_for(rk, g);
+          km.out[km.n] = a - r0N;   // the kernel addresses row l at out + l N
+          km.max_rot = std::max(km.max_rot, km.rot[km.n]);
+          km.n++;
+        }
+        if (km.n) launch_kip_multi(c->dc(), km, mqp);
+      }
+      // L3 (own rows): inner sums of every giant pair into the rank's slice
+      const MacList ml = build_macs(pl, nlN, [&](int ci, int j) {
+        uint64_t* a = ab.at({ci, j}) - r0N;
+        return std::make_pair((const uint64_t*)a, (const uint64_t*)(a + rows * N));
+      });
+      need(ml.oi.size() == nz, HELRM_ERR_CONFIG, "work list differs from the pair enumeration");
+      MacDev md(c, ml);
+      {
+        const DevCtx dcx = c->dc();
+        ProfScope ps_(dcx, "diag_mac", 8.0 * N * (hi[r] - lo[r]) * (ml.n_u + 2.0 * ml.n_x + 2.0 * nz));
+        need(launch_diag_mac_bulk(dcx, (const MacTerm*)md.terms.p, (const int4*)md.groups.p, (int)ml.groups.size(),
+                                  sab[r] - r0N, 2 * rows * N, rows * N, mqp, 1, 0, 0, 0, (int)lo[r],
+                                  (int)(hi[r] - lo[r])),
+             HELRM_ERR_CONFIG, "the limb partition needs N divisible by the MAC tile");
+      }
+    }
+    // L4: per giant pair, all-gather B, ModDown + ModUp (replicated), key switch on own rows
+    DBuf Bf(c, parts * rp * N), Bp(c, nqN), D2(c, dn * nlN);   // Bf: the all-gathered rows (padded)
+    for (size_t z = 0; z < nz; z++) {
+      const int64_t o = oi[z].first, gi = pl->giants[o][oi[z].second];
+      if (gi % (int64_t)P.n == 0) {   // O_o += (A, B)_z on own rows
+        for (int r : mine) {
+          if (hi[r] == lo[r]) continue;
+          const LimbMap sm = sub(r);
+          for (int h = 0; h < 2; h++)
+            launch_binary(c->dc(), 0, so[r] + (o * 2 + h) * rp * N, sab[r] + (z * 2 + h) * rp * N,
+                          so[r] + (o * 2 + h) * rp * N, sm);
+        }
+        continue;
+      }
+      // all-gather of B's rows: slice r lands at rows [r rp, (r + 1) rp) of Bf
+      if (real && parts > 1) {
+        HNCCL(nccl().allGather(sab[c->rank] + (z * 2 + 1) * rp * N, Bf.p, rp * N, ncclUint64, c->comm, c->stream));
+      } else {
+        for (int r : mine)
+          HCUDA(cudaMemcpyAsync(Bf.p + r * rp * N, sab[r] + (z * 2 + 1) * rp * N, rp * N * 8,
+                                cudaMemcpyDeviceToDevice, c->stream));
+      }
+      moddown_batch(c, Bf.p, nlN, 1, l, Bp.p, nqN);
+      modup_batch(c, Bp.p, nqN, 1, l, D2.p, nullptr, false);
+      const uint64_t g = galois_of_rot(c, gi);
+      for (int r : mine) {
+        if (hi[r] == lo[r]) continue;
+        const size_t rows = rp;
+        const size_t r0N = (size_t)lo[r] * N;
+        KipGiants kg{};
+        kg.row0 = (int)lo[r];
+        kg.rows = (int)(hi[r] - lo[r]);
+        kg.digit_stride = nlN;
+        kg.dnum = (int)dn;
+        kg.add_rows = (int)nl;
+        kg.alpha = (int)P.alpha;
+        kg.level = (int)l;
+        kg.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+        kg.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+        kg.out0 = so[r] + o * 2 * rows * N - r0N;
+        kg.out1 = kg.out0 + rows * N;
+        kg.n = 1;
+        kg.digits[0] = D2.p;
+        kg.own[0] = Bp.p;
+        kg.key[0] = key_for(rk, g);
+        kg.add0[0] = sab[r] + z * 2 * rows * N - r0N;   // A's rows
+        kg.rot[0] = rot_of_galois(c, g);
+        launch_kip_giants(c->dc(), kg, mqp);
+      }
+    }
+    // all-gather of the accumulators, then L6-L8 (replicated)
+    DBuf Of(c, (size_t)O * 2 * nlN), S(c, (size_t)O * 2 * l * N);
+    std::unique_ptr<DBuf> Og;
+    std::vector<const uint64_t*> src(parts, nullptr);
+    if (real && parts > 1) {   // [rank][O][2][rp][N]
+      Og.reset(new DBuf(c, (size_t)parts * O * 2 * rp * N));
+      HNCCL(nccl().allGather(so[c->rank], Og->p, (size_t)O * 2 * rp * N, ncclUint64, c->comm, c->stream));
+      nccl_check_async(c);
+      for (int r = 0; r < parts; r++) src[r] = Og->p + (size_t)r * O * 2 * rp * N;
+    } else {
+      for (int r : mine) src[r] = so[r];
+    }
+    for (int r = 0; r < parts; r++) {
+      if (hi[r] == lo[r]) continue;
+      for (int64_t k = 0; k < 2 * O; k++)
+        HCUDA(cudaMemcpyAsync(Of.p + k * nlN + (size_t)lo[r] * N, src[r] + k * rp * N, (hi[r] - lo[r]) * N * 8,
+                              cudaMemcpyDeviceToDevice, c->stream));
+    }
+    lookup_finish(c, pl, rk, Of.p, 1, S.p);
+    emit_outputs(c, pl, S.p, 1, cin[0]->scale, out + qy * O);
+  }
+}
+
+helrm_status helrm_lookup_limbsplit_virtual(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                            const helrm_ct* const* in, size_t batch, int parts, helrm_ct** out) {
+  if (out)
+    for (size_t i = 0; i < batch * (p ? p->O : 0); i++) out[i] = nullptr;
+  return guard([&] {
+    need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
+    lookup_limbsplit(c, p, rk, in, batch, out, parts, false);
+  });
+}
+
+helrm_status helrm_lookup_limbsplit(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                   const helrm_ct* const* in, size_t batch, helrm_ct** out) {
+  if (out)
+    for (size_t i = 0; i < batch * (p ? p->O : 0); i++) out[i] = nullptr;
+  return guard([&] {
+    need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
+    DevGuard dg_(c->device);
+    need(c->world == 1 || c->comm, HELRM_ERR_ARG, "helrm_comm_init first");
+    lookup_limbsplit(c, p, rk, in, batch, out, c->world, true);
+  });
+}
+
 helrm_status helrm_lookup_dist(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk, const helrm_ct* const* in,
                                size_t batch, helrm_ct** out) {
   if (out)

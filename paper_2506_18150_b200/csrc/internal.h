@@ -96,6 +96,7 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
@@ -304,6 +305,9 @@ void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map);
 // per giant.  Common fields as KipArgs (add_mul = 1, accumulate = 1, nq = 1).
 constexpr int kMaxGiantRun = 16;
 struct KipGiants {
+  // rows [row0, row0 + rows) of the Q_l P limbs only (rows = 0: all of map): the RNS-limb
+  // partition of the lookup gives each rank a slice of the limbs
+  int row0 = 0, rows = 0;
   size_t digit_stride;
   int dnum, add_rows, alpha, level, n;
   size_t key_digit_stride, key_half_stride;
@@ -324,6 +328,7 @@ void launch_kip_giants(const DevCtx& c, const KipGiants& a, const LimbMap& map);
 // all babies of one ciphertext (k_kip_multi)
 constexpr int kMaxBabies = 128;
 struct KipMulti {
+  int row0 = 0, rows = 0;     // limb rows [row0, row0 + rows) only (rows = 0: all of map)
   const uint64_t* digits;     // digit k at digits + k digit_stride ([nl][N])
   size_t digit_stride;
   int dnum;
@@ -370,9 +375,10 @@ using MacTermW = MacTermT<kWidePack>;
 // wide: terms are MacTermW (batched kernel, nq >= 1), else MacTerm.
 // batch-1 inner sums fed by bulk async copies (kernels_mac_bulk.cu); false if it does not apply
 // accumulate: out (+)= the inner sums (compact plans sum a pair's terms over several launches)
+// rows [row0, row0 + rows) of map only (rows = 0: all)
 bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
                           size_t out_stride, size_t half, const LimbMap& map, int nq = 1, size_t xq = 0,
-                          size_t oq = 0, int accumulate = 0);
+                          size_t oq = 0, int accumulate = 0, int row0 = 0, int rows = 0);
 void launch_diag_mac(const DevCtx& c, const void* terms, const int4* groups, int n_groups, double n_u_total,
                      double n_x_distinct, int n_out, uint64_t* out, size_t out_stride, const LimbMap& map,
                      bool x_dform, int nq = 1, size_t xq = 0, size_t oq = 0, bool wide = false);

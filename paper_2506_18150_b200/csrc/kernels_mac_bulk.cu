@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
     k_diag_mac_bulk(const MacTerm* __restrict__ terms, const int4* __restrict__ groups, int n_groups,
                     uint64_t* __restrict__ out, size_t out_stride, size_t half, const PrimeDev* __restrict__ primes,
                     const __grid_constant__ LimbMap map, uint32_t N, int stages, int nq, size_t xq, size_t oq,
-                    int accumulate) {
+                    int accumulate, int row0, int nrows) {
   pdl_wait_trigger();
   constexpr int G = kGiantPack, NS = bulk_slots<QN>();
   constexpr uint32_t SB = NS * kSlotBytes;
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
     }
   }
   __syncthreads();
-  const uint32_t tiles = N / kTile, total = tiles * (uint32_t)n_groups * (uint32_t)map.n;
+  const uint32_t tiles = N / kTile, total = tiles * (uint32_t)n_groups * (uint32_t)nrows;
   const int nqc = nq / QN;   // query chunks per work item
   constexpr int kCons = kTile * QS, QT = QN / QS;   // consumer threads, queries per consumer thread
   if (tid >= kCons) {
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
     uint32_t j = 0;
     for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
       const int4 gr = groups[w % n_groups];   // pack fastest (as k_diag_mac): packs of a tile share baby pairs in L2
-      const size_t o0 = (size_t)(w / (tiles * n_groups)) * N + ((w / n_groups) % tiles) * kTile;
+      const size_t o0 = (size_t)(row0 + w / (tiles * n_groups)) * N + ((w / n_groups) % tiles) * kTile;
       const int items = nqc * gr.y;
       int it = (int)((kProducers + pw - j % kProducers) % kProducers);   // this warp's first item
       j += it;
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
   uint32_t phase = 0;
   for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
     const int4 gr = groups[w % n_groups];
-    const int l = (int)(w / (tiles * n_groups));
+    const int l = row0 + (int)(w / (tiles * n_groups));
     const size_t o = (size_t)l * N + ((w / n_groups) % tiles) * kTile + pos;
     const PrimeDev& P = primes[map.pr[l]];
     const double q = P.qd, qi = P.qinv;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kTile * QS + 32 * kProducers, 1)
 template <int QN>
 static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
                         size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq,
-                        int accumulate) {
+                        int accumulate, int row0, int rows) {
   static const int stages_env = getenv("HELRM_MACB_STAGES") ? atoi(getenv("HELRM_MACB_STAGES")) : 0;
   constexpr size_t SB = (size_t)bulk_slots<QN>() * kSlotBytes;
   // default: as many stages as fit in ~200 KiB (16 at 12 KiB, 8 at 24 KiB), a multiple of kProducers
@@ -236,24 +236,25 @@ static void bulk_launch(const DevCtx& c, const MacTerm* terms, const int4* group
     HCUDA(cudaFuncSetAttribute(k_diag_mac_bulk<QN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (dev < 64) attr[dev] = smem;
   }
-  const unsigned total = (c.N / kTile) * (unsigned)n_groups * map.n;
+  const unsigned total = (c.N / kTile) * (unsigned)n_groups * (unsigned)rows;
   const unsigned grid = std::min<unsigned>(total, (unsigned)c.n_sm * (unsigned)per_sm);
-  launch_pdl(k_diag_mac_bulk<QN>, dim3(grid), dim3(kTile * bulk_qsplit<QN>() + 32 * kProducers), smem, c.stream, terms, groups, n_groups, out, out_stride, half, c.primes, map, c.N, stages, nq, xq, oq, accumulate);
+  launch_pdl(k_diag_mac_bulk<QN>, dim3(grid), dim3(kTile * bulk_qsplit<QN>() + 32 * kProducers), smem, c.stream, terms, groups, n_groups, out, out_stride, half, c.primes, map, c.N, stages, nq, xq, oq, accumulate, row0, rows);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
 
 bool launch_diag_mac_bulk(const DevCtx& c, const MacTerm* terms, const int4* groups, int n_groups, uint64_t* out,
                           size_t out_stride, size_t half, const LimbMap& map, int nq, size_t xq, size_t oq,
-                          int accumulate) {
+                          int accumulate, int row0, int rows) {
   if (c.N % kTile || nq < 1) return false;
+  if (rows <= 0) rows = map.n - row0;
   static const int qmax = getenv("HELRM_MACB_QMAX") ? atoi(getenv("HELRM_MACB_QMAX")) : 4;
   if (nq % 4 == 0 && qmax >= 4)
-    bulk_launch<4>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate);
+    bulk_launch<4>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate, row0, rows);
   else if (nq % 2 == 0 && qmax >= 2)
-    bulk_launch<2>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate);
+    bulk_launch<2>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate, row0, rows);
   else
-    bulk_launch<1>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate);
+    bulk_launch<1>(c, terms, groups, n_groups, out, out_stride, half, map, nq, xq, oq, accumulate, row0, rows);
   return true;
 }
 

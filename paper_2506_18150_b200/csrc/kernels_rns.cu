@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(256, NQ > 1 ? 2 : 3) k_kip_giants(const __grid
   pdl_wait_trigger();
   constexpr int kFoldEvery = 2 * (DNUM + 1) <= fm::kFAccTerms ? 2 : 1;
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int l = blockIdx.y;
+  const int l = a.row0 + (int)blockIdx.y;
   const uint32_t chain = map.pr[l];
   const PrimeDev& P = primes[chain];
   const double q = P.qd, qi = P.qinv;
@@ -372,7 +372,7 @@ void launch_kip_giants(const DevCtx& c, const KipGiants& a, const LimbMap& map) 
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
 #undef HELRM_KG_CASE
-  launch_pdl(kern, dim3(dim3(c.N / kT, map.n)), dim3(kT), 0, c.stream, a, c.primes, map, c.N);
+  launch_pdl(kern, dim3(dim3(c.N / kT, a.rows ? a.rows : map.n)), dim3(kT), 0, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());
 }
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256, 4) k_kip_multi(const __grid_constant__ Ki
                                                       const __grid_constant__ LimbMap map, uint32_t N) {
   pdl_wait_trigger();
   extern __shared__ double shd[];
-  const int l = blockIdx.y;
+  const int l = a.row0 + (int)blockIdx.y;
   const uint32_t n = N / 2, tile = blockDim.x;
   const uint32_t zq = (uint32_t)((a.nq + a.qk - 1) / a.qk);
   const uint32_t tix = a.zfast ? blockIdx.x / zq : blockIdx.x, zix = a.zfast ? blockIdx.x % zq : blockIdx.z;
@@ -819,7 +819,8 @@ void launch_kip_multi(const DevCtx& c, const KipMulti& a, const LimbMap& map) {
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
   if (smem > 48 * 1024) HCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const dim3 grid = a.zfast ? dim3(c.N / tile * (unsigned)zq, map.n, 1) : dim3(c.N / tile, map.n, (unsigned)zq);
+  const unsigned ny = a.rows ? (unsigned)a.rows : (unsigned)map.n;
+  const dim3 grid = a.zfast ? dim3(c.N / tile * (unsigned)zq, ny, 1) : dim3(c.N / tile, ny, (unsigned)zq);
   launch_pdl(kern, grid, dim3(tile), smem, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;
   HCUDA(cudaGetLastError());

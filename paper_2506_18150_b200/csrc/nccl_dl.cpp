@@ -21,9 +21,10 @@ NcclApi& nccl() {
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
     api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
     api.broadcast = (decltype(api.broadcast))dlsym(h, "ncclBroadcast");
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
     api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
     api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
-    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.broadcast &&
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.broadcast && api.allGather &&
              api.getErrorString && api.commGetAsyncError;
   });
   if (!api.ok) throw Error(HELRM_ERR_NCCL, "libnccl.so.2 not loadable");

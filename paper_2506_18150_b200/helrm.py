@@ -104,6 +104,8 @@ _SIGS = {
     "helrm_lookup_dist": [_vp, _vp, _vp, _pp, _sz, _pp],
     "helrm_lookup_dist_virtual": [_vp, _vp, _vp, _pp, _sz, ctypes.c_int, _pp],
     "helrm_modred": [_vp, _vp, _u32, _sz],
+    "helrm_lookup_limbsplit_virtual": [_vp, _vp, _vp, _pp, _sz, ctypes.c_int, _pp],
+    "helrm_lookup_limbsplit": [_vp, _vp, _vp, _pp, _sz, _pp],
     "helrm_plan_galois": [_vp, _u64p, _sz, ctypes.POINTER(_sz)],
     "helrm_rotkeys_galois": [_vp, _u64p, _sz, ctypes.POINTER(_sz)],
     "helrm_sk_import": [_vp, _i64p, _sz, _pp],
@@ -136,6 +138,7 @@ EXPORTED = sorted(list(_SIGS) + ["helrm_params_destroy", "helrm_ctx_destroy", "h
                                  "helrm_rotkeys_bytes", "helrm_ctx_profile", "helrm_ctx_profile_json", "helrm_dist_range",
                                  "helrm_comm_unique_id", "helrm_comm_init", "helrm_lookup_dist",
                                  "helrm_lookup_dist_virtual", "helrm_modred", "helrm_plan_galois",
+                                 "helrm_lookup_limbsplit_virtual", "helrm_lookup_limbsplit",
                                  "helrm_rotkeys_galois", "helrm_sk_import", "helrm_pk_import",
                                  "helrm_rotkeys_import", "helrm_rotkeys_upload"])
 
@@ -565,6 +568,25 @@ def lookup_dist_virtual(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Cip
     ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
     outs = (ctypes.c_void_p * (batch * info.n_out_cts))()
     _check(_L.helrm_lookup_dist_virtual(ctx.h, plan.h, rk.h, ins, batch, parts, outs))
+    return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]
+
+
+def lookup_limbsplit_virtual(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Ciphertext], parts: int,
+                             batch: int = 1) -> List[Ciphertext]:
+    info = plan.info()
+    assert len(cts) == batch * info.n_in_cts
+    ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
+    outs = (ctypes.c_void_p * (batch * info.n_out_cts))()
+    _check(_L.helrm_lookup_limbsplit_virtual(ctx.h, plan.h, rk.h, ins, batch, parts, outs))
+    return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]
+
+
+def lookup_limbsplit(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Ciphertext], batch: int = 1) -> List[Ciphertext]:
+    info = plan.info()
+    assert len(cts) == batch * info.n_in_cts
+    ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
+    outs = (ctypes.c_void_p * (batch * info.n_out_cts))()
+    _check(_L.helrm_lookup_limbsplit(ctx.h, plan.h, rk.h, ins, batch, outs))
     return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]
 
 
