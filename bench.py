@@ -472,6 +472,8 @@ def run_gpu(args, world, rank, local):
         secondary["criteo_b64"] = batch_lookup(args, ctx, helrm, torch, stream, plan, rk, cts, world)
     if world > 1 or args.dist:
         secondary["dist_b1"] = dist_b1(args, ctx, helrm, torch, stream, plan, rk, cts, world, rank)
+    if world == 1 and not args.skip_batch:
+        secondary["limb_split_projection"] = limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg)
     if not args.skip_micro:
         secondary.update(micro(args, ctx, helrm, torch, stream, sk, cfg, world))
     if not args.skip_llm:
@@ -530,6 +532,47 @@ def dist_b1(args, ctx, helrm, torch, stream, plan, rk, cts, world, rank):
     ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
     return {"ms_per_lookup": round(ms, 4), "lookups_per_s": round(1e3 / ms, 3), "world": world,
             "partition": "giant range per rank, NCCL allreduce(uint64, sum) + mod-q kernel"}
+
+
+def limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg, parts_list=(2, 4, 8)):
+    """SURVEY.md 8(e)/(f) rank 1 on one GPU: the RNS-limb partition
+    (helrm_lookup_limbsplit; bit-exact through helrm_lookup_limbsplit_virtual
+    in the GPU tests).  Every rank's kernels (its rows of the ModUp / ModDown
+    conversions and NTTs, baby key switches, inner sums and giant key
+    switches, plus the replicated INTTs of the input and of B's P rows and the
+    replicated finish) are timed per rank with CUDA events through
+    helrm_limbsplit_rank_work; projected device time on `parts` GPUs = the
+    slowest rank + the all-gathers (each giant pair's B rows and B' y-form
+    rows, and the accumulators: the bytes a rank receives, over NVLink at the
+    measured 770 GB/s peer-copy rate of B200_PROFILING.md; collective latency
+    not included).  A model with measured parts: no multi-GPU box was
+    available."""
+    info = plan.info()
+    N, l = cfg.N, cfg.level
+    nl = l + 1 + ctx.info.K
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {}
+    for parts in parts_list:
+        rank_ms = []
+        for r in range(parts):
+            for _ in range(2):
+                for o in helrm.limbsplit_rank_work(ctx, plan, rk, [cts[0]], parts, r):
+                    o.close()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for o in helrm.limbsplit_rank_work(ctx, plan, rk, [cts[0]], parts, r):
+                o.close()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            rank_ms.append(e0.elapsed_time(e1))
+        rp = -(-nl // parts)
+        n_rot_pairs = info.n2_max * info.n_out_cts - 1   # every giant pair but giant 0 rotates (Criteo: 15)
+        recv = (n_rot_pairs * 2 + 2 * info.n_out_cts) * (parts - 1) * rp * N * 8
+        proj = max(rank_ms) + recv / 770e9 * 1e3
+        res[str(parts)] = {"projected_ms": round(proj, 3), "rank_ms_max": round(max(rank_ms), 3),
+                           "rank_ms_min": round(min(rank_ms), 3), "allgather_recv_MB": round(recv / 1e6, 1),
+                           "projected_lookups_per_s": round(1e3 / proj, 1)}
+    return {"model": " ".join(limb_split_projection.__doc__.split()), "per_parts": res}
 
 
 def batch_lookup(args, ctx, helrm, torch, stream, plan, rk, cts, world, B=64):

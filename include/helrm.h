@@ -306,6 +306,12 @@ helrm_status helrm_lookup_limbsplit_virtual(helrm_ctx* c, const helrm_plan* p, c
  * ncclAllGather (slices padded to ceil((l+1+K) / world) rows). */
 helrm_status helrm_lookup_limbsplit(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
                                    const helrm_ct* const* in, size_t batch, helrm_ct** out);
+/* Timing harness of the partition (no multi-GPU node needed): enqueues
+ * exactly the kernels rank `rank` of `parts` runs for one query, with every
+ * exchange skipped -- the outputs are NOT a lookup result.  bench.py times it
+ * per rank to project the partitioned lookup's device time. */
+helrm_status helrm_limbsplit_rank_work(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                       const helrm_ct* const* in, int parts, int rank, helrm_ct** out);
 /* The combine's reduction alone (D23 L5), in place: n_polys R_{Q_level P}
  * polynomials [n_polys][level+1+K][N] at `dev` whose words are sums of
  * residues (< 2^64) become residues mod their limb's prime. */

@@ -109,6 +109,18 @@ struct helrm_ctx {
   std::map<int, LevelConst> lconst;
   std::map<std::pair<int, int>, uint32_t*> modup_lidx;   // (level, G) -> NTT limb table of modup_batch
   std::map<std::pair<int, int>, uint32_t*> pm_lidx;      // (G, n) -> prime-major limb table
+  // row-slice tables of the RNS-limb partition, keyed by (level, first row, end row, G)
+  struct SliceTabs {
+    ConvRowDev* up_tab = nullptr;   // [dnum][up_rows]: ModUp conversion rows of digit k inside the slice
+    int up_rows = 0;
+    uint32_t* up_lidx = nullptr;    // ModUp NTT limbs (g dnum + k) nl + r, r in the slice, outside digit k
+    size_t n_up = 0;
+    ConvRowDev* dn_tab = nullptr;   // ModDown conversion rows: Q rows of the slice
+    int dn_rows = 0;
+    uint32_t* q_lidx = nullptr;     // the slice's Q rows g nq + r (INTT / ModDown NTT)
+    size_t n_q = 0;
+  };
+  std::map<std::tuple<int, int, int, int>, SliceTabs> slices;
   // CUDA-graph replay of the double-hoisted lookup (one graph per plan, key
   // set and query-chunk size): the ~400 launches, allocations and copies of a
   // lookup are enqueued once at capture; a replay costs one graph launch.
@@ -517,6 +529,71 @@ static const uint32_t* pm_lidx(helrm_ctx* c, int G, uint32_t n) {
   c->owned.push_back(d);
   c->pm_lidx.emplace(key, d);
   return d;
+}
+
+// Row-slice tables for rows [r0, r1) of the Q_l P limbs and G polynomials
+// (the RNS-limb partition): the ModUp conversion rows of each digit that fall
+// in the slice (padded per digit), the ModUp NTT limbs of the slice, and the
+// slice's Q rows for the ModDown conversion, the INTTs and the ModDown NTT.
+static const helrm_ctx::SliceTabs& slice_tabs(helrm_ctx* c, uint32_t l, int r0, int r1, int G) {
+  auto key = std::make_tuple((int)l, r0, r1, G);
+  auto it = c->slices.find(key);
+  if (it != c->slices.end()) return it->second;
+  const Params& P = c->P;
+  const LevelConst& lc = level_const(c, l);
+  const uint32_t nl = l + 1 + P.K, nq = l + 1, dn = P.dnum(l);
+  helrm_ctx::SliceTabs t;
+  std::vector<ConvRowDev> ut((size_t)dn * lc.modup_rows);
+  HCUDA(cudaMemcpy(ut.data(), lc.modup_tab, ut.size() * sizeof(ConvRowDev), cudaMemcpyDeviceToHost));
+  std::vector<std::vector<ConvRowDev>> per(dn);
+  for (uint32_t k = 0; k < dn; k++)
+    for (int j = 0; j < lc.modup_rows; j++) {
+      const ConvRowDev& e = ut[(size_t)k * lc.modup_rows + j];
+      if (e.out_row >= r0 && e.out_row < r1) per[k].push_back(e);
+    }
+  size_t mx = 1;
+  for (auto& v : per) mx = std::max(mx, v.size());
+  std::vector<ConvRowDev> st(dn * mx);
+  for (uint32_t k = 0; k < dn; k++)
+    for (size_t j = 0; j < mx; j++) {
+      if (j < per[k].size()) {
+        st[k * mx + j] = per[k][j];
+      } else {   // padding: nothing written
+        st[k * mx + j] = ut[(size_t)k * lc.modup_rows];
+        st[k * mx + j].out_row = -1;
+      }
+    }
+  t.up_rows = (int)mx;
+  std::vector<uint32_t> up, ql;
+  for (int r = r0; r < r1; r++)
+    for (int g = 0; g < G; g++) {
+      for (uint32_t k = 0; k < dn; k++) {
+        const uint32_t lo = k * P.alpha, hi = std::min((k + 1) * P.alpha, nq);
+        if ((uint32_t)r < lo || (uint32_t)r >= hi) up.push_back(((uint32_t)g * dn + k) * nl + (uint32_t)r);
+      }
+      if ((uint32_t)r < nq) ql.push_back((uint32_t)g * nq + (uint32_t)r);
+    }
+  std::vector<ConvRowDev> dt;
+  const int q1 = std::min<int>(r1, (int)nq);
+  if (q1 > r0) {
+    dt.resize(q1 - r0);
+    HCUDA(cudaMemcpy(dt.data(), lc.moddown_tab + r0, dt.size() * sizeof(ConvRowDev), cudaMemcpyDeviceToHost));
+  }
+  auto up_dev = [&](const void* h, size_t bytes) {
+    void* d = c->dalloc(std::max<size_t>(bytes, 16));
+    if (bytes) HCUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->owned.push_back(d);
+    return d;
+  };
+  t.up_tab = (ConvRowDev*)up_dev(st.data(), st.size() * sizeof(ConvRowDev));
+  t.up_lidx = (uint32_t*)up_dev(up.data(), up.size() * 4);
+  t.n_up = up.size();
+  t.dn_tab = (ConvRowDev*)up_dev(dt.data(), dt.size() * sizeof(ConvRowDev));
+  t.dn_rows = (int)dt.size();
+  t.q_lidx = (uint32_t*)up_dev(ql.data(), ql.size() * 4);
+  t.n_q = ql.size();
+  HCUDA(cudaStreamSynchronize(c->stream));
+  return c->slices.emplace(key, t).first->second;
 }
 
 // copy_own = false: the digit's own limbs of out are left unwritten; the key
@@ -2977,7 +3054,7 @@ static void lookup_split(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys*
 // full buffers.  Per-limb work is independent, so the result is bit-identical
 // to helrm_lookup (D23: only the limb placement changes).
 static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
-                             size_t batch, helrm_ct** out, int parts, bool real) {
+                             size_t batch, helrm_ct** out, int parts, bool real, int only_rank = -1) {
   need(pl->mode == HELRM_MODE_DOUBLE && !pl->compact, HELRM_ERR_ARG,
        "the limb-partitioned lookup runs stored-diagonal double-hoisted plans");
   for (int64_t a : pl->rotations) (void)key_for(rk, galois_of_rot(c, a));
@@ -2998,7 +3075,9 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
     hi[r] = std::min<int64_t>((int64_t)nl, (int64_t)((r + 1) * rp));
   }
   std::vector<int> mine;   // the ranks this process computes
-  if (real) mine.push_back(c->rank);
+  const bool timing = only_rank >= 0;   // one rank's kernels only, exchanges skipped (a timing harness)
+  if (timing) mine.push_back(only_rank);
+  else if (real) mine.push_back(c->rank);
   else
     for (int r = 0; r < parts; r++) mine.push_back(r);
   auto sub = [&](int r) {   // the LimbMap of rank r's rows (for the row-agnostic element-wise kernels)
@@ -3017,9 +3096,18 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
       else
         HCUDA(cudaMemcpyAsync(X.p + ci * 2 * nqN, cin[ci]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
     }
-    // L1 (replicated): digits of every input c1
-    DBuf D(c, (size_t)C * dn * nlN);
-    modup_batch(c, X.p + nqN, 2 * nqN, (int)C, l, D.p, nullptr, false);
+    // L1: every rank converts the (replicated) y-form of the input c1s into its own rows of
+    // the digits: D row r of digit k is written by the rank owning row r
+    DBuf D(c, (size_t)C * dn * nlN), Y(c, (size_t)C * nqN);
+    launch_ntt_inv(c->dc(), X.p + nqN, Y.p, c->scratch, (size_t)C * nq, mq, 2 * nqN, nqN, lc.modup_post,
+                   pm_lidx(c, (int)C, (uint32_t)nq));
+    for (int r : mine) {
+      if (hi[r] == lo[r]) continue;
+      const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], (int)C);
+      launch_conv_rows(c->dc(), st.up_tab, (int)dn, st.up_rows, (int)P.alpha, Y.p, nqN, D.p, dn * nlN, nlN, (int)C,
+                       mqp);
+      if (st.n_up) launch_ntt_fwd(c->dc(), D.p, D.p, c->scratch, st.n_up, mqp, 0, 0, true, st.up_lidx);
+    }
     // (P c0, P c1) of every ct (replicated, cheap): the baby pair of rotation 0
     DBuf P0(c, (size_t)C * 2 * nlN);
     HCUDA(cudaMemsetAsync(P0.p, 0, (size_t)C * 2 * nlN * 8, c->stream));
@@ -3104,7 +3192,9 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
       }
     }
     // L4: per giant pair, all-gather B, ModDown + ModUp (replicated), key switch on own rows
-    DBuf Bf(c, parts * rp * N), Bp(c, nqN), D2(c, dn * nlN);   // Bf: the all-gathered rows (padded)
+    // Bf: all-gathered B rows; Bp: B' (each rank's Q rows); Y2: B' in y-form, all-gathered
+    DBuf Bf(c, parts * rp * N), Bp(c, nqN), D2(c, dn * nlN), Y2(c, parts * rp * N), yP(c, (size_t)P.K * N),
+        T(c, nqN);
     for (size_t z = 0; z < nz; z++) {
       const int64_t o = oi[z].first, gi = pl->giants[o][oi[z].second];
       if (gi % (int64_t)P.n == 0) {   // O_o += (A, B)_z on own rows
@@ -3125,8 +3215,35 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
           HCUDA(cudaMemcpyAsync(Bf.p + r * rp * N, sab[r] + (z * 2 + 1) * rp * N, rp * N * 8,
                                 cudaMemcpyDeviceToDevice, c->stream));
       }
-      moddown_batch(c, Bf.p, nlN, 1, l, Bp.p, nqN);
-      modup_batch(c, Bp.p, nqN, 1, l, D2.p, nullptr, false);
+      // ModDown (D16) of B: the P rows to y-form (replicated, K limbs), then each rank converts
+      // and transforms its own Q rows, the epilogue writing (B - t) P^-1 into Bp
+      launch_ntt_inv(c->dc(), Bf.p + nqN, yP.p, c->scratch, P.K, P.map_range(P.L + 1, P.K), P.K * N, P.K * N,
+                     lc.moddown_post, nullptr);
+      for (int r : mine) {
+        const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], 1);
+        if (st.n_q == 0) continue;
+        launch_conv_rows(c->dc(), st.dn_tab, 1, st.dn_rows, (int)P.K, yP.p, P.K * N, T.p, nqN, 0, 1, mq);
+        NttEpi epi;
+        epi.y = Bf.p;
+        epi.ys = nlN;
+        epi.out = Bp.p;
+        epi.os = nqN;
+        epi.s = lc.pinv;
+        epi.sp = lc.pinvs;
+        launch_ntt_fwd(c->dc(), T.p, T.p, c->scratch, st.n_q, mq, 0, 0, true, st.q_lidx, &epi);
+        // ModUp (D15) of B': its own Q rows into y-form
+        launch_ntt_inv(c->dc(), Bp.p, Y2.p, c->scratch, st.n_q, mq, nqN, nqN, lc.modup_post, st.q_lidx);
+      }
+      if (real && parts > 1) {   // all-gather of B' (y-form) rows: slice r lands at rows [r rp, (r + 1) rp)
+        HNCCL(nccl().allGather(Y2.p + (size_t)lo[c->rank] * N, Y2.p, rp * N, ncclUint64, c->comm, c->stream));
+      }
+      for (int r : mine) {   // each rank's rows of the digits of B'
+        if (hi[r] == lo[r]) continue;
+        const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], 1);
+        launch_conv_rows(c->dc(), st.up_tab, (int)dn, st.up_rows, (int)P.alpha, Y2.p, nqN, D2.p, dn * nlN, nlN, 1,
+                         mqp);
+        if (st.n_up) launch_ntt_fwd(c->dc(), D2.p, D2.p, c->scratch, st.n_up, mqp, 0, 0, true, st.up_lidx);
+      }
       const uint64_t g = galois_of_rot(c, gi);
       for (int r : mine) {
         if (hi[r] == lo[r]) continue;
@@ -3166,7 +3283,7 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
       for (int r : mine) src[r] = so[r];
     }
     for (int r = 0; r < parts; r++) {
-      if (hi[r] == lo[r]) continue;
+      if (hi[r] == lo[r] || !src[r]) continue;   // (timing harness: the other ranks' rows are absent)
       for (int64_t k = 0; k < 2 * O; k++)
         HCUDA(cudaMemcpyAsync(Of.p + k * nlN + (size_t)lo[r] * N, src[r] + k * rp * N, (hi[r] - lo[r]) * N * 8,
                               cudaMemcpyDeviceToDevice, c->stream));
@@ -3184,6 +3301,17 @@ helrm_status helrm_lookup_limbsplit_virtual(helrm_ctx* c, const helrm_plan* p, c
     need(c && p && rk && in && out, HELRM_ERR_ARG, "null argument");
     DevGuard dg_(c->device);
     lookup_limbsplit(c, p, rk, in, batch, out, parts, false);
+  });
+}
+
+helrm_status helrm_limbsplit_rank_work(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys* rk,
+                                       const helrm_ct* const* in, int parts, int rank, helrm_ct** out) {
+  if (out)
+    for (int64_t i = 0; i < (p ? p->O : 0); i++) out[i] = nullptr;
+  return guard([&] {
+    need(c && p && rk && in && out && parts >= 1 && rank >= 0 && rank < parts, HELRM_ERR_ARG, "bad argument");
+    DevGuard dg_(c->device);
+    lookup_limbsplit(c, p, rk, in, 1, out, parts, false, rank);
   });
 }
 

@@ -106,6 +106,7 @@ _SIGS = {
     "helrm_modred": [_vp, _vp, _u32, _sz],
     "helrm_lookup_limbsplit_virtual": [_vp, _vp, _vp, _pp, _sz, ctypes.c_int, _pp],
     "helrm_lookup_limbsplit": [_vp, _vp, _vp, _pp, _sz, _pp],
+    "helrm_limbsplit_rank_work": [_vp, _vp, _vp, _pp, ctypes.c_int, ctypes.c_int, _pp],
     "helrm_plan_galois": [_vp, _u64p, _sz, ctypes.POINTER(_sz)],
     "helrm_rotkeys_galois": [_vp, _u64p, _sz, ctypes.POINTER(_sz)],
     "helrm_sk_import": [_vp, _i64p, _sz, _pp],
@@ -139,6 +140,7 @@ EXPORTED = sorted(list(_SIGS) + ["helrm_params_destroy", "helrm_ctx_destroy", "h
                                  "helrm_comm_unique_id", "helrm_comm_init", "helrm_lookup_dist",
                                  "helrm_lookup_dist_virtual", "helrm_modred", "helrm_plan_galois",
                                  "helrm_lookup_limbsplit_virtual", "helrm_lookup_limbsplit",
+                                 "helrm_limbsplit_rank_work",
                                  "helrm_rotkeys_galois", "helrm_sk_import", "helrm_pk_import",
                                  "helrm_rotkeys_import", "helrm_rotkeys_upload"])
 
@@ -587,6 +589,16 @@ def lookup_limbsplit(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Cipher
     ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
     outs = (ctypes.c_void_p * (batch * info.n_out_cts))()
     _check(_L.helrm_lookup_limbsplit(ctx.h, plan.h, rk.h, ins, batch, outs))
+    return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]
+
+
+def limbsplit_rank_work(ctx: Context, plan: Plan, rk: RotKeys, cts: Sequence[Ciphertext], parts: int,
+                        rank: int) -> List[Ciphertext]:
+    """Timing harness: rank `rank`'s kernels of the limb partition (outputs are not a lookup)."""
+    info = plan.info()
+    ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
+    outs = (ctypes.c_void_p * info.n_out_cts)()
+    _check(_L.helrm_limbsplit_rank_work(ctx.h, plan.h, rk.h, ins, parts, rank, outs))
     return [Ciphertext(ctypes.c_void_p(o), ctx) for o in outs]
 
 
