@@ -783,20 +783,30 @@ def micro(args, ctx, helrm, torch, stream, sk, cfg, world):
     nbytes = 16.0 * N * limbs
     del buf
     torch.cuda.empty_cache()
-    # hoisted rotations: amounts 1..64, keys for all of them
+    # hoisted rotations: amounts 1..64, keys for all of them, amortised over the cts
+    # (helrm_rotate_hoisted_batch: one ModUp per ct, one key switch per amount over all cts)
     amounts = list(range(1, 65))
     rk = helrm.rotkeys_gen(ctx, sk, sorted({pow(5, a, 2 * N) for a in amounts}), cfg.seed)
     n_rot_cts = args.rot_cts
     cts = [helrm.ct_random(ctx, cfg.seed, i, L) for i in range(n_rot_cts)]
-    ring = [helrm.ct_alloc(ctx, L) for _ in range(4)]
-    helrm.rotate_hoisted(ctx, rk, cts[0], amounts[:4], ring)
+    ring = 2 * n_rot_cts
+    out = torch.empty(ring * 2 * (L + 1) * N, dtype=torch.uint64, device="cuda")
+    helrm.rotate_hoisted_batch(ctx, rk, cts, amounts[:2], out, ring)
     torch.cuda.synchronize()
     ev[0].record(stream)
-    for c in cts:
-        helrm.rotate_hoisted(ctx, rk, c, amounts, ring)
+    helrm.rotate_hoisted_batch(ctx, rk, cts, amounts, out, ring)
     ev[1].record(stream)
     torch.cuda.synchronize()
     rot_ms = ev[0].elapsed_time(ev[1])
+    # one ct at a time (helrm_rotate_hoisted: the keys are re-read for every ct)
+    ring1 = [helrm.ct_alloc(ctx, L) for _ in range(4)]
+    ev[2].record(stream)
+    for c in cts[:4]:
+        helrm.rotate_hoisted(ctx, rk, c, amounts, ring1)
+    ev[3].record(stream)
+    torch.cuda.synchronize()
+    rot1_ms = ev[2].elapsed_time(ev[3])
+    del out
     rot_ms = max_over_ranks(rot_ms, world)
     fwd_ms = max_over_ranks(fwd_ms, world)
     inv_ms = max_over_ranks(inv_ms, world)
@@ -809,6 +819,7 @@ def micro(args, ctx, helrm, torch, stream, sk, cfg, world):
         "ntt_cts": n_cts,
         "rotations_per_s": round(world * n_rot_cts * len(amounts) / (rot_ms / 1e3), 1),
         "rotation_cts": n_rot_cts,
+        "rotations_per_s_one_ct_at_a_time": round(world * 4 * len(amounts) / (rot1_ms / 1e3), 1),
         "rotation_keys_GiB": round(rk.nbytes() / 2**30, 2),
     }
 
@@ -828,7 +839,7 @@ def main():
     ap.add_argument("--with-compact", action="store_true",
                     help="also time the compact-plan layouts (LLM L1, 100-ct Criteo; ~3 min of plan setup)")
     ap.add_argument("--micro-cts", type=int, default=1024)
-    ap.add_argument("--rot-cts", type=int, default=8)
+    ap.add_argument("--rot-cts", type=int, default=32)
     ap.add_argument("--dist", action="store_true", help="also time the partitioned batch-1 lookup at world size 1")
     ap.add_argument("--ncu-step", action="store_true", help="profile one lookup in a cudaProfiler range and exit")
     args = ap.parse_args()

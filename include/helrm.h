@@ -260,6 +260,15 @@ helrm_status helrm_rotate(helrm_ctx* c, const helrm_rotkeys* rk, const helrm_ct*
  * input's level, e.g. by helrm_ct_import or helrm_ct_alloc). */
 helrm_status helrm_rotate_hoisted(helrm_ctx* c, const helrm_rotkeys* rk, const helrm_ct* in, const int64_t* amounts,
                                   size_t n_amounts, helrm_ct* const* out_ring, size_t ring);
+/* Hoisted rotations of n cts with the keys amortised over them (SURVEY.md
+ * 8(d) microbench unit): every ct's ModUp once; per amount one key switch
+ * over all n cts (each key value loaded once) and one batched ModDown.
+ * Rotate(in[j], amounts[i]) is written to the device buffer `out` (borrowed,
+ * NTT slot order, [ring][2][level+1][N]) at slot (i n + j) % ring; ring must
+ * be a multiple of n (ARG); all cts at one level (LEVEL).  Bit-identical to
+ * helrm_rotate. */
+helrm_status helrm_rotate_hoisted_batch(helrm_ctx* c, const helrm_rotkeys* rk, const helrm_ct* const* in, size_t n,
+                                        const int64_t* amounts, size_t n_amounts, uint64_t* out, size_t ring);
 helrm_status helrm_ct_alloc(helrm_ctx* c, uint32_t level, double scale, helrm_ct** out);
 /* Microbench input: limbs of cts drawn UniformMod from D9 streams
  * (purpose 9, a = ct, b = poly, c = limb), written in NTT form. */

@@ -2924,6 +2924,60 @@ helrm_status helrm_rotate_hoisted(helrm_ctx* c, const helrm_rotkeys* rk, const h
   });
 }
 
+// SURVEY.md 8(d) "hoisted rotation, keys amortised": ModUp of every input ct
+// once (hoist), then per amount ONE key switch over all cts (k_kip with the
+// cts as queries: each key value is loaded once for all of them, lazy
+// P phi(c0) added) and one ModDown batched over the 2 n polynomials, written
+// straight into the caller's device ring: (amount i, ct j) ->
+// out + ((i n + j) % ring) 2 (l+1) N, NTT slot order.
+helrm_status helrm_rotate_hoisted_batch(helrm_ctx* c, const helrm_rotkeys* rk, const helrm_ct* const* in, size_t n,
+                                        const int64_t* amounts, size_t n_amounts, uint64_t* out, size_t ring) {
+  return guard([&] {
+    need(c && rk && in && amounts && out && n > 0 && ring > 0 && ring % n == 0, HELRM_ERR_ARG,
+         "bad argument (ring must be a multiple of the number of cts)");
+    DevGuard dg_(c->device);
+    const Params& P = c->P;
+    const uint32_t l = in[0]->level;
+    for (size_t j = 0; j < n; j++) need(in[j] && in[j]->level == l, HELRM_ERR_LEVEL, "input cts at different levels");
+    const size_t N = P.N, nq = l + 1, nqN = nq * N, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
+    const LevelConst& lc = level_const(c, l);
+    DBuf X(c, n * 2 * nqN), D(c, n * dn * nlN), T(c, n * 2 * nlN);
+    stage_inputs(c, in, n, 2 * nqN, X.p);
+    modup_batch(c, X.p + nqN, 2 * nqN, (int)n, l, D.p, nullptr, false);   // hoisted: once per ct
+    for (size_t i = 0; i < n_amounts; i++) {
+      uint64_t* o = out + ((i * n) % ring) * 2 * nqN;
+      const uint64_t g = galois_of_rot(c, amounts[i]);
+      if (g == 1) {   // Rotate(ct, 0) = ct
+        HCUDA(cudaMemcpyAsync(o, X.p, n * 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
+        continue;
+      }
+      KipArgs a{};
+      a.digits = D.p;
+      a.digit_stride = nlN;
+      a.dnum = (int)dn;
+      a.key = key_for(rk, g);
+      a.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+      a.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+      a.add0 = X.p;                     // lazy rotation: P phi(c0) + KS0, KS1
+      a.add_rows = (int)nq;
+      a.add_mul = lc.pmod;
+      a.rot = rot_of_galois(c, g);
+      a.out0 = T.p;
+      a.out1 = T.p + nlN;
+      a.nq = (int)n;
+      a.dq = dn * nlN;
+      a.aq = 2 * nqN;
+      a.oq = 2 * nlN;
+      a.own = X.p + nqN;
+      a.ownq = 2 * nqN;
+      a.alpha = (int)P.alpha;
+      a.level = (int)l;
+      launch_kip(c->dc(), a, P.map_qp(l));
+      moddown_batch(c, T.p, nlN, (int)(2 * n), l, o, nqN);
+    }
+  });
+}
+
 helrm_status helrm_ct_random(helrm_ctx* c, uint64_t seed, uint32_t ct_index, uint32_t level, helrm_ct** out) {
   if (out) *out = nullptr;
   return guard([&] {

@@ -19,8 +19,11 @@
 // contiguous runs; pass-2 twiddles are stored in per-block, per-thread order
 // so each thread reads its 15 phase-B twiddles contiguously.  Inverse = the
 // Gentleman-Sande mirror.  Between the passes the data live in a scratch
-// buffer of <= 32 MiB per chunk of limbs, which stays L2-resident: HBM sees
-// one read and one write per coefficient per transform.
+// buffer of up to 512 limbs (256 MiB at N = 2^16) per launch: launches up to
+// ~200 limbs keep it in the 126 MB L2, the large ModUp launches do not (ncu:
+// 1.96 MB of DRAM traffic per limb transform against the algorithmic
+// 1 MiB); 64 MiB chunks keep it in L2 but lose more to partial waves
+// (profiles/r01_ab_chunk.txt).
 //
 // Butterfly arithmetic runs on the FP64 pipe (fmath.cuh, q < 2^51): residues
 // are exact integer-valued doubles, the product Y W = h + l is split exactly
@@ -189,7 +192,7 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
     for (int k = 0; k < kEPT; k++) r[k] = cred(r[k], q, qi);
   }
   if (P1) {
-    // centred doubles into the (L2-resident) scratch, natural row positions
+    // centred doubles into the scratch, natural row positions
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const int e = SLOG > 4 ? kEPT * t + k : t + TS * k;

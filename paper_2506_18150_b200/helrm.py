@@ -98,6 +98,7 @@ _SIGS = {
     "helrm_rescale": [_vp, _vp, _pp],
     "helrm_rotate": [_vp, _vp, _vp, _i64, _pp],
     "helrm_rotate_hoisted": [_vp, _vp, _vp, _i64p, _sz, _pp, _sz],
+    "helrm_rotate_hoisted_batch": [_vp, _vp, _pp, _sz, _i64p, _sz, _vp, _sz],
     "helrm_dist_range": [_i64, ctypes.c_int, ctypes.c_int, _i64p, _i64p],
     "helrm_comm_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
     "helrm_comm_init": [_vp, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int],
@@ -140,7 +141,7 @@ EXPORTED = sorted(list(_SIGS) + ["helrm_params_destroy", "helrm_ctx_destroy", "h
                                  "helrm_comm_unique_id", "helrm_comm_init", "helrm_lookup_dist",
                                  "helrm_lookup_dist_virtual", "helrm_modred", "helrm_plan_galois",
                                  "helrm_lookup_limbsplit_virtual", "helrm_lookup_limbsplit",
-                                 "helrm_limbsplit_rank_work",
+                                 "helrm_limbsplit_rank_work", "helrm_rotate_hoisted_batch",
                                  "helrm_rotkeys_galois", "helrm_sk_import", "helrm_pk_import",
                                  "helrm_rotkeys_import", "helrm_rotkeys_upload"])
 
@@ -543,6 +544,16 @@ def rotate_hoisted(ctx: Context, rk: RotKeys, ct: Ciphertext, amounts: Sequence[
     a = np.ascontiguousarray(np.array(list(amounts), dtype=np.int64))
     r = (ctypes.c_void_p * len(ring))(*[c.h for c in ring])
     _check(_L.helrm_rotate_hoisted(ctx.h, rk.h, ct.h, a.ctypes.data_as(_i64p), a.size, r, len(ring)))
+
+
+def rotate_hoisted_batch(ctx: Context, rk: RotKeys, cts: Sequence[Ciphertext], amounts: Sequence[int], dev_out,
+                         ring: int):
+    """helrm_rotate_hoisted_batch: Rotate(cts[j], amounts[i]) -> dev_out slot (i n + j) % ring,
+    [ring][2][level+1][N] uint64 (NTT slot order)."""
+    a = np.ascontiguousarray(np.array(list(amounts), dtype=np.int64))
+    ins = (ctypes.c_void_p * len(cts))(*[c.h for c in cts])
+    _check(_L.helrm_rotate_hoisted_batch(ctx.h, rk.h, ins, len(cts), a.ctypes.data_as(_i64p), a.size, _devptr(dev_out),
+                                         ring))
 
 
 # ---------------------------------------------------------------- multi-GPU
