@@ -339,7 +339,9 @@ def fp64_frac_model(ctx, run, cfg, macs, ms):
     limbs = sum(st.get(k, {}).get("bytes", 0.0) for k in ("ntt_fwd_p1", "ntt_inv_pa")) / (8.0 * N)
     ops = limbs * (N // 2) * logN * NTT_FP64_OPS_PER_BFLY + 5.0 * macs
     peak, src = fp64_peak()
+    kern = {k: round(v["ms"], 3) for k, v in sorted(st.items(), key=lambda kv: -kv[1]["ms"])[:8]}
     return {"fp64_frac_model": round(ops / (ms / 1e3) / peak, 4), "fp64_ops_per_run": ops,
+            "profiled_kernel_ms": kern,
             "ntt_limb_transforms_per_run": round(limbs), "macs_per_run": macs,
             "fp64_peak_source": src, "model": "8 FP64 ops per NTT butterfly + 5 per exact MAC (fmath.cuh)"}
 

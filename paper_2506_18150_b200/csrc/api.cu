@@ -3324,8 +3324,8 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
         launch_kip_giants(c->dc(), kg, mqp);
       }
     }
-    // all-gather of the accumulators, then L6-L8 (replicated)
-    DBuf Of(c, (size_t)O * 2 * nlN), S(c, (size_t)O * 2 * l * N);
+    // all-gather of the accumulators
+    DBuf Of(c, (size_t)O * 2 * nlN);
     std::unique_ptr<DBuf> Og;
     std::vector<const uint64_t*> src(parts, nullptr);
     if (real && parts > 1) {   // [rank][O][2][rp][N]
@@ -3342,8 +3342,137 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
         HCUDA(cudaMemcpyAsync(Of.p + k * nlN + (size_t)lo[r] * N, src[r] + k * rp * N, (hi[r] - lo[r]) * N * 8,
                               cudaMemcpyDeviceToDevice, c->stream));
     }
-    lookup_finish(c, pl, rk, Of.p, 1, S.p);
-    emit_outputs(c, pl, S.p, 1, cin[0]->scale, out + qy * O);
+    // L6-L8 on each rank's rows.  Ownership follows the primes: at level l - 1 (after the
+    // rescale drops q_l) rank r owns rows [lo1, hi1) = its rows with those above l moved down.
+    const uint32_t l1 = l - 1;
+    const size_t nq1 = l, nl1 = l + P.K, nl1N = nl1 * N, nq1N = nq1 * N, dn1 = P.dnum(l1);
+    const LimbMap mq1 = P.map_q(l1), mqp1 = P.map_qp(l1);
+    const LevelConst& lc1 = level_const(c, l1);
+    std::vector<int64_t> lo1(parts), hi1(parts);
+    for (int r = 0; r < parts; r++) {
+      lo1[r] = lo[r] - (lo[r] > (int64_t)l ? 1 : 0);
+      hi1[r] = hi[r] - (hi[r] > (int64_t)l ? 1 : 0);
+    }
+    // exchange: every rank's rows [a_r, b_r) of npoly polynomials (poly stride ps) to all ranks
+    // (one ncclBroadcast per owner, grouped); the emulation's ranks share the buffer already
+    auto share = [&](uint64_t* buf, const std::vector<int64_t>& a, const std::vector<int64_t>& b, int npoly,
+                     size_t ps) {
+      if (!(real && parts > 1)) return;
+      HNCCL(nccl().groupStart());
+      for (int r = 0; r < parts; r++)
+        for (int k = 0; k < npoly; k++)
+          if (b[r] > a[r])
+            HNCCL(nccl().broadcast(buf + k * ps + (size_t)a[r] * N, buf + k * ps + (size_t)a[r] * N,
+                                   (size_t)(b[r] - a[r]) * N, ncclUint64, r, c->comm, c->stream));
+      HNCCL(nccl().groupEnd());
+    };
+    std::vector<int64_t> qa(parts), qb(parts), pa(parts), pb(parts), la(parts), lb(parts);
+    DBuf R(c, 2 * nqN), S1(c, (size_t)O * 2 * nq1N), yP2(c, 2 * (size_t)P.K * N), T2(c, 2 * nqN), xl(c, 2 * N),
+        rr(c, 2 * nq1N), Yr(c, nq1N), Dr(c, dn1 * nl1N), K2(c, 2 * nl1N);
+    for (int64_t o = 0; o < O; o++) {
+      const uint64_t* Oo = Of.p + o * 2 * nlN;
+      uint64_t* So = S1.p + o * 2 * nq1N;
+      // L6 ModDown of both halves: P rows to y-form (replicated), own Q rows converted + NTT
+      launch_ntt_inv(c->dc(), Oo + nqN, yP2.p, c->scratch, 2 * P.K, P.map_range(P.L + 1, P.K), nlN, P.K * N,
+                     lc.moddown_post, nullptr);
+      for (int r : mine) {
+        const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], 2);
+        if (st.n_q == 0) continue;
+        launch_conv_rows(c->dc(), st.dn_tab, 1, st.dn_rows, (int)P.K, yP2.p, P.K * N, T2.p, nqN, 0, 2, mq);
+        NttEpi epi;
+        epi.y = Oo;
+        epi.ys = nlN;
+        epi.out = R.p;
+        epi.os = nqN;
+        epi.s = lc.pinv;
+        epi.sp = lc.pinvs;
+        launch_ntt_fwd(c->dc(), T2.p, T2.p, c->scratch, st.n_q, mq, 0, 0, true, st.q_lidx, &epi);
+      }
+      // L7 rescale: row l of both halves (its owner's) to everyone, then each rank's rows i < l
+      for (int r = 0; r < parts; r++) {
+        la[r] = std::max<int64_t>(lo[r], (int64_t)l);
+        lb[r] = std::min<int64_t>(hi[r], (int64_t)l + 1);
+      }
+      if (!timing) share(R.p, la, lb, 2, nqN);
+      ntt_inv(c, R.p + (size_t)l * N, xl.p, 2, P.map_range(l, 1), nqN, N);
+      launch_rescale_prep(c->dc(), xl.p, N, P.primes[l], rr.p, nq1N, 2, mq1);
+      for (int r : mine) {
+        const helrm_ctx::SliceTabs& st = slice_tabs(c, l1, (int)lo1[r], (int)hi1[r], 2);
+        if (st.n_q == 0) continue;
+        NttEpi epi;
+        epi.y = R.p;
+        epi.ys = nqN;
+        epi.out = So;
+        epi.os = nq1N;
+        epi.s = lc.qlinv;
+        epi.sp = lc.qlinvs;
+        launch_ntt_fwd(c->dc(), rr.p, rr.p, c->scratch, st.n_q, mq1, 0, 0, false, st.q_lidx, &epi);
+      }
+      // L8 RotSum at level l - 1, every rotation on the ranks' rows
+      for (int r = 0; r < parts; r++) {
+        qa[r] = lo1[r];
+        qb[r] = std::min<int64_t>(hi1[r], (int64_t)nq1);
+        pa[r] = std::max<int64_t>(lo1[r], (int64_t)nq1);
+        pb[r] = hi1[r];
+      }
+      for (int64_t amt = pl->mbar; amt < (int64_t)P.n; amt *= 2) {
+        const uint64_t g = galois_of_rot(c, amt);
+        // ModUp of c1: own Q rows to y-form, shared, own rows of the digits
+        for (int r : mine) {
+          const helrm_ctx::SliceTabs& st = slice_tabs(c, l1, (int)lo1[r], (int)hi1[r], 1);
+          if (st.n_q) launch_ntt_inv(c->dc(), So + nq1N, Yr.p, c->scratch, st.n_q, mq1, nq1N, nq1N, lc1.modup_post,
+                                     st.q_lidx);
+        }
+        if (!timing) share(Yr.p, qa, qb, 1, nq1N);
+        for (int r : mine) {
+          if (hi1[r] == lo1[r]) continue;
+          const helrm_ctx::SliceTabs& st = slice_tabs(c, l1, (int)lo1[r], (int)hi1[r], 1);
+          launch_conv_rows(c->dc(), st.up_tab, (int)dn1, st.up_rows, (int)P.alpha, Yr.p, nq1N, Dr.p, dn1 * nl1N,
+                           nl1N, 1, mqp1);
+          if (st.n_up) launch_ntt_fwd(c->dc(), Dr.p, Dr.p, c->scratch, st.n_up, mqp1, 0, 0, true, st.up_lidx);
+          // lazy key switch on own rows: (P phi(c0) + KS0, KS1)
+          KipArgs a{};
+          a.row0 = (int)lo1[r];
+          a.rows = (int)(hi1[r] - lo1[r]);
+          a.digits = Dr.p;
+          a.digit_stride = nl1N;
+          a.dnum = (int)dn1;
+          a.key = key_for(rk, g);
+          a.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+          a.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+          a.add0 = So;
+          a.add_rows = (int)nq1;
+          a.add_mul = lc1.pmod;
+          a.rot = rot_of_galois(c, g);
+          a.out0 = K2.p;
+          a.out1 = K2.p + nl1N;
+          a.own = So + nq1N;
+          a.alpha = (int)P.alpha;
+          a.level = (int)l1;
+          launch_kip(c->dc(), a, mqp1);
+        }
+        // ModDown of (KS0, KS1): their P rows shared, own Q rows accumulated into the ct
+        if (!timing) share(K2.p, pa, pb, 2, nl1N);
+        launch_ntt_inv(c->dc(), K2.p + nq1N, yP2.p, c->scratch, 2 * P.K, P.map_range(P.L + 1, P.K), nl1N, P.K * N,
+                       lc1.moddown_post, nullptr);
+        for (int r : mine) {
+          const helrm_ctx::SliceTabs& st = slice_tabs(c, l1, (int)lo1[r], (int)hi1[r], 2);
+          if (st.n_q == 0) continue;
+          launch_conv_rows(c->dc(), st.dn_tab, 1, st.dn_rows, (int)P.K, yP2.p, P.K * N, T2.p, nq1N, 0, 2, mq1);
+          NttEpi epi;
+          epi.y = K2.p;
+          epi.ys = nl1N;
+          epi.out = So;
+          epi.os = nq1N;
+          epi.s = lc1.pinv;
+          epi.sp = lc1.pinvs;
+          epi.accumulate = 1;   // ct += Rotate(ct)
+          launch_ntt_fwd(c->dc(), T2.p, T2.p, c->scratch, st.n_q, mq1, 0, 0, true, st.q_lidx, &epi);
+        }
+      }
+      if (!timing) share(So, qa, qb, 2, nq1N);   // the output ct's rows to every rank
+    }
+    emit_outputs(c, pl, S1.p, 1, cin[0]->scale, out + qy * O);
   }
 }
 

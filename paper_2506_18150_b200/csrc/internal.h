@@ -99,6 +99,8 @@ struct NcclApi {
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
 };
 NcclApi& nccl();
 #define HNCCL(x)                                                                                       \
@@ -274,6 +276,7 @@ void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_
                          const LimbMap& map);
 
 struct KipArgs {
+  int row0 = 0, rows = 0;     // limb rows [row0, row0 + rows) only (rows = 0: all of map)
   const uint64_t* digits;     // digit k of the switched polynomial at digits + k digit_stride ([nl][N], NTT slot order)
   size_t digit_stride;
   int dnum;

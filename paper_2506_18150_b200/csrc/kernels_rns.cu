@@ -213,10 +213,10 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
                                              const __grid_constant__ LimbMap map, uint32_t N) {
   pdl_wait_trigger();
   // work item w = (tile, limb); a grid smaller than the work loops (persistent CTAs)
-  const uint32_t tiles = N / blockDim.x, total = tiles * (uint32_t)map.n;
+  const uint32_t tiles = N / blockDim.x, total = tiles * (uint32_t)(a.rows ? a.rows : map.n);
   for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
   const uint32_t p = (w % tiles) * blockDim.x + threadIdx.x;
-  const int l = (int)(w / tiles);
+  const int l = a.row0 + (int)(w / tiles);
   const uint32_t chain = map.pr[l];
   const PrimeDev& P = primes[chain];
   const double q = P.qd, qi = P.qinv;
@@ -794,7 +794,7 @@ void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
     case 7: kern = b ? k_kip<7, 2> : k_kip<7, 1>; break;
     default: throw Error(HELRM_ERR_CONFIG, "key switch supports dnum <= 7");
   }
-  const unsigned total = (c.N / kT) * map.n;
+  const unsigned total = (c.N / kT) * (unsigned)(a.rows ? a.rows : map.n);
   const unsigned grid = c.persist > 0 ? std::min<unsigned>(total, (unsigned)c.n_sm * c.persist) : total;
   launch_pdl(kern, dim3(grid), dim3(kT), 0, c.stream, a, c.primes, map, c.N);
   (*c.launches)++;

@@ -24,8 +24,10 @@ NcclApi& nccl() {
     api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
     api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
     api.commGetAsyncError = (decltype(api.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
     api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.broadcast && api.allGather &&
-             api.getErrorString && api.commGetAsyncError;
+             api.getErrorString && api.commGetAsyncError && api.groupStart && api.groupEnd;
   });
   if (!api.ok) throw Error(HELRM_ERR_NCCL, "libnccl.so.2 not loadable");
   return api;

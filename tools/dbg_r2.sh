@@ -1,4 +1,14 @@
-timeout 900 python -m pytest tests/test_gpu_boundary.py -m gpu -q -x -k "hoisted_batch" > gpurun_out/r2_rotb.txt 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/r2_rotb.txt
-timeout 600 python bench.py --steps 3 --warmup 3 --skip-cpu-baseline --skip-batch --skip-llm --skip-c2 > gpurun_out/r2_micro.json 2>/dev/null; echo "bench rc=$?"
-python -c "
-import json; d=json.load(open('gpurun_out/r2_micro.json')); s=d['secondary']; print({k: s[k] for k in s if 'rot' in k or 'ntt' in k})"
+timeout 1200 python -m pytest tests/test_gpu_boundary.py -m gpu -q -x -k "limb" > gpurun_out/r2_limb.txt 2>&1; echo "pytest rc=$?"; tail -30 gpurun_out/r2_limb.txt | grep -v "^  " | tail -12
+timeout 600 python - <<'PY'
+import sys, json
+sys.argv = ["bench.py"]
+import torch, synth, bench
+from paper_2506_18150_b200 import helrm
+w = synth.make_workload("criteo", batch=1); cfg = w.config
+P = helrm.params_from_config(cfg); stream = torch.cuda.Stream(); ctx = helrm.Context(P, 0, stream.cuda_stream)
+T = helrm.tables_create(P, w.tables, w.n_dense); plan = helrm.plan_create(ctx, T, cfg.level)
+sk = helrm.sk_gen(ctx, cfg.seed); pk = helrm.pk_gen(ctx, sk, cfg.seed); rk = helrm.rotkeys_gen(ctx, sk, plan.galois(), cfg.seed)
+x = helrm.encode_query(T, w.indices[0], w.dense[0], cfg.n_slots)
+cts = [helrm.encrypt(ctx, pk, x, cfg.level, (cfg.seed << 20))]
+print(json.dumps(bench.limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg, (1, 2, 4, 8))["per_parts"], indent=1))
+PY
