@@ -1998,7 +1998,8 @@ static void compact_l1_l3(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkey
   for (auto& b : pl->babies) nb_max = std::max(nb_max, b.size());
   const size_t per_ct = 8 * (dn * nlN + nb_max * 2 * nlN);
   const int64_t G = std::max<int64_t>(1, std::min<int64_t>(C, (int64_t)(gbudget / per_ct)));
-  const size_t uc = std::max<size_t>(1, std::min<size_t>((size_t)pl->n_unique, (size_t)(exp_gib * (1 << 30)) / (8 * nlN)));
+  const size_t uc = std::max<size_t>(1, std::min<size_t>({(size_t)pl->n_unique, (size_t)65535,
+                                                          (size_t)(exp_gib * (1 << 30)) / (8 * nlN)}));
   DBuf E(c, uc * nlN);
   for (int64_t c0 = 0; c0 < C; c0 += G) {
     const int64_t g = std::min(G, C - c0);
@@ -3289,7 +3290,8 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
         launch_ntt_inv(c->dc(), Bp.p, Y2.p, c->scratch, st.n_q, mq, nqN, nqN, lc.modup_post, st.q_lidx);
       }
       if (real && parts > 1) {   // all-gather of B' (y-form) rows: slice r lands at rows [r rp, (r + 1) rp)
-        HNCCL(nccl().allGather(Y2.p + (size_t)lo[c->rank] * N, Y2.p, rp * N, ncclUint64, c->comm, c->stream));
+        // (in place: the rank's slice sits at rank rp rows, also for a trailing empty rank)
+        HNCCL(nccl().allGather(Y2.p + (size_t)c->rank * rp * N, Y2.p, rp * N, ncclUint64, c->comm, c->stream));
       }
       for (int r : mine) {   // each rank's rows of the digits of B'
         if (hi[r] == lo[r]) continue;

@@ -145,3 +145,36 @@ def test_compact_chunking_knobs(knobs):
                         os.path.join(here, "test_gpu_compact.py") + "::test_llm_l1_small_compact_matches_oracle"],
                        env=dict(os.environ, **knobs), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@gpu
+def test_compact_plan_batch_and_errors(torch_mod):
+    """A batch on a compact plan runs query by query and equals the stored
+    plan's batched lookup; the serving path and the limb partition reject
+    compact plans (ARG), and a compact single-hoisted plan is refused."""
+    E = env("uci", torch_mod)
+    h, w = E.h, synth.make_workload("uci", batch=3)
+    cfg = w.config
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    plan_s = h.plan_create(E.ctx, T, cfg.level)
+    plan_c = h.plan_create(E.ctx, T, cfg.level, 0, COMPACT)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan_s.galois(), cfg.seed)
+    cts = []
+    for q in range(3):
+        x = h.encode_query(T, w.indices[q], w.dense[q], cfg.n_slots)
+        cts.append(h.encrypt(E.ctx, pk, x, cfg.level, (cfg.seed << 20) | q))
+    for a, b in zip(h.lookup(E.ctx, plan_c, rk, cts, 3), h.lookup(E.ctx, plan_s, rk, cts, 3)):
+        assert np.array_equal(h.ct_export(E.ctx, a), h.ct_export(E.ctx, b))
+    coeff = np.ascontiguousarray(h.ct_export(E.ctx, cts[0]).reshape(-1))
+    out = np.zeros(2 * cfg.level * cfg.N, dtype=np.uint64)
+    with pytest.raises(h.HelrmError) as e:
+        h.lookup_host(E.ctx, plan_c, rk, [coeff], 1.0, 1, [out])
+    assert e.value.code == 10
+    with pytest.raises(h.HelrmError) as e:
+        h.lookup_limbsplit_virtual(E.ctx, plan_c, rk, cts[:1], 2)
+    assert e.value.code == 10
+    with pytest.raises(h.HelrmError) as e:
+        h.plan_create(E.ctx, T, cfg.level, 0, COMPACT | 1)
+    assert e.value.code == 10

@@ -1,14 +1,4 @@
-timeout 1200 python -m pytest tests/test_gpu_boundary.py -m gpu -q -x -k "limb" > gpurun_out/r2_limb.txt 2>&1; echo "pytest rc=$?"; tail -30 gpurun_out/r2_limb.txt | grep -v "^  " | tail -12
-timeout 600 python - <<'PY'
-import sys, json
-sys.argv = ["bench.py"]
-import torch, synth, bench
-from paper_2506_18150_b200 import helrm
-w = synth.make_workload("criteo", batch=1); cfg = w.config
-P = helrm.params_from_config(cfg); stream = torch.cuda.Stream(); ctx = helrm.Context(P, 0, stream.cuda_stream)
-T = helrm.tables_create(P, w.tables, w.n_dense); plan = helrm.plan_create(ctx, T, cfg.level)
-sk = helrm.sk_gen(ctx, cfg.seed); pk = helrm.pk_gen(ctx, sk, cfg.seed); rk = helrm.rotkeys_gen(ctx, sk, plan.galois(), cfg.seed)
-x = helrm.encode_query(T, w.indices[0], w.dense[0], cfg.n_slots)
-cts = [helrm.encrypt(ctx, pk, x, cfg.level, (cfg.seed << 20))]
-print(json.dumps(bench.limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg, (1, 2, 4, 8))["per_parts"], indent=1))
-PY
+timeout 600 python bench.py --steps 3 --warmup 3 --skip-cpu-baseline --skip-micro --skip-c2 > gpurun_out/r2_b64.json 2>/dev/null; echo "bench rc=$?"
+python -c "
+import json; d=json.load(open('gpurun_out/r2_b64.json')); s=d['secondary']
+for k in ('criteo_b64','llm_128_tokens'): print(k, json.dumps({kk: s[k][kk] for kk in s[k] if kk in ('ms_per_batch','ms_per_lookup','fp64_frac_model','profiled_kernel_ms','ntt_limb_transforms_per_run')}))"
