@@ -290,6 +290,7 @@ struct KipArgs {
   uint64_t* out0;             // [nl][N]
   uint64_t* out1;
   int accumulate;             // out += result (else out = result)
+  int halves = 3;             // 1: out0 only (b keys, add0), 2: out1 only (a keys), 3: both
   // queries sharing the key (batched lookups): query q uses digits + q dq,
   // add0 + q aq and writes out0/out1 + q oq; the key is loaded once for all
   int nq = 1;

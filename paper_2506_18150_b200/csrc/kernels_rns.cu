@@ -227,15 +227,17 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
   const uint64_t* og = a.own ? a.own + (size_t)l * N + sp : nullptr;
   const bool add = a.add0 != nullptr && l < a.add_rows;
   const double amul = add && a.add_mul ? fm::u2c(a.add_mul[l], q) : 1.0;
+  const bool h0 = a.halves & 1, h1 = a.halves & 2;   // which outputs (and key halves) this launch computes
   uint64_t kv0[DNUM], kv1[DNUM];
 #pragma unroll
   for (int k = 0; k < DNUM; k++) {
+    kv0[k] = kv1[k] = 0;
     if (a.nq == 1) {
-      kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
-      kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
+      if (h0) kv0[k] = __ldcs(kb + (size_t)k * a.key_digit_stride);
+      if (h1) kv1[k] = __ldcs(kb + (size_t)k * a.key_digit_stride + a.key_half_stride);
     } else {
-      kv0[k] = kb[(size_t)k * a.key_digit_stride];
-      kv1[k] = kb[(size_t)k * a.key_digit_stride + a.key_half_stride];
+      if (h0) kv0[k] = kb[(size_t)k * a.key_digit_stride];
+      if (h1) kv1[k] = kb[(size_t)k * a.key_digit_stride + a.key_half_stride];
     }
   }
   const size_t o = (size_t)l * N + p;
@@ -250,10 +252,10 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
 #pragma unroll
         for (int k = 0; k < DNUM; k++)
           dv[r][k] = k == kown ? og[(size_t)(q0 + r) * a.ownq] : dq[(size_t)k * a.digit_stride];
-        av[r] = add ? a.add0[(size_t)(q0 + r) * a.aq + (size_t)l * N + sp] : 0;
+        av[r] = add && h0 ? a.add0[(size_t)(q0 + r) * a.aq + (size_t)l * N + sp] : 0;
         // the accumulated outputs are fetched with the operands (one memory round trip per thread)
-        pv0[r] = a.accumulate ? a.out0[(size_t)(q0 + r) * a.oq + o] : 0;
-        pv1[r] = a.accumulate ? a.out1[(size_t)(q0 + r) * a.oq + o] : 0;
+        pv0[r] = a.accumulate && h0 ? a.out0[(size_t)(q0 + r) * a.oq + o] : 0;
+        pv1[r] = a.accumulate && h1 ? a.out1[(size_t)(q0 + r) * a.oq + o] : 0;
       }
     }
 #pragma unroll
@@ -263,19 +265,17 @@ __global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs 
 #pragma unroll
         for (int k = 0; k < DNUM; k++) {
           const double d = fm::u2d(dv[r][k]);
-          fm::fmac(acc0, d, fm::bits2d(kv0[k]));
-          fm::fmac(acc1, d, fm::bits2d(kv1[k]));
+          if (h0) fm::fmac(acc0, d, fm::bits2d(kv0[k]));
+          if (h1) fm::fmac(acc1, d, fm::bits2d(kv1[k]));
         }
         if (add) fm::fmac(acc0, fm::u2d(av[r]), amul);
         uint64_t r0 = fm::c2u(fm::fred(acc0, q, qi), P.rc.q), r1 = fm::c2u(fm::fred(acc1, q, qi), P.rc.q);
-        uint64_t* o0 = a.out0 + (size_t)(q0 + r) * a.oq + o;
-        uint64_t* o1 = a.out1 + (size_t)(q0 + r) * a.oq + o;
         if (a.accumulate) {
           r0 = add_mod(r0, pv0[r], P.rc.q);
           r1 = add_mod(r1, pv1[r], P.rc.q);
         }
-        *o0 = r0;
-        *o1 = r1;
+        if (h0) a.out0[(size_t)(q0 + r) * a.oq + o] = r0;
+        if (h1) a.out1[(size_t)(q0 + r) * a.oq + o] = r1;
       }
     }
   }
@@ -780,8 +780,9 @@ void launch_rescale_prep(const DevCtx& c, const uint64_t* xl, size_t xs, uint64_
 }
 
 void launch_kip(const DevCtx& c, const KipArgs& a, const LimbMap& map) {
-  ProfScope ps_(c, "kip", 8.0 * c.N * (2.0 * a.dnum * map.n + a.nq * (a.dnum * map.n + (a.add0 ? a.add_rows : 0) +
-                                                                      (a.accumulate ? 4 : 2) * map.n)));
+  const double nh = a.halves == 3 ? 2.0 : 1.0;
+  ProfScope ps_(c, "kip", 8.0 * c.N * (nh * a.dnum * map.n + a.nq * (a.dnum * map.n + (a.add0 ? a.add_rows : 0) +
+                                                                      (a.accumulate ? 2 : 1) * nh * map.n)));
   decltype(&k_kip<1, 1>) kern = nullptr;
   const bool b = a.nq > 1;
   switch (a.dnum) {
