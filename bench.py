@@ -540,22 +540,23 @@ def limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg, parts_l
     """SURVEY.md 8(e)/(f) rank 1 on one GPU: the RNS-limb partition
     (helrm_lookup_limbsplit; bit-exact through helrm_lookup_limbsplit_virtual
     in the GPU tests).  Every rank's kernels (its rows of the ModUp / ModDown
-    conversions and NTTs, baby key switches, inner sums and giant key
-    switches, plus the replicated INTTs of the input and of B's P rows and the
-    replicated finish) are timed per rank with CUDA events through
-    helrm_limbsplit_rank_work; projected device time on `parts` GPUs = the
-    slowest rank + the all-gathers (each giant pair's B rows and B' y-form
-    rows, and the accumulators: the bytes a rank receives, over NVLink at the
-    measured 770 GB/s peer-copy rate of B200_PROFILING.md; collective latency
-    not included).  A model with measured parts: no multi-GPU box was
-    available."""
+    conversions and NTTs, baby key switches, inner sums, giant and RotSum key
+    switches, rescale, plus the small replicated INTTs) are run per rank
+    through helrm_limbsplit_rank_work and timed with CUDA events around the
+    call (eager: host work and launch gaps included -- the partitioned path
+    is not graph-replayed, so this is conservative; one rank doing all rows
+    takes 8.3 ms against the graph-replayed lookup's 6.8).  Projected device
+    time on `parts` GPUs = the slowest rank + the all-gathered / broadcast
+    bytes a rank receives over NVLink at the measured 770 GB/s peer-copy rate
+    of B200_PROFILING.md (collective latency excluded).  A model with
+    measured parts: no multi-GPU box was available."""
     info = plan.info()
     N, l = cfg.N, cfg.level
     nl = l + 1 + ctx.info.K
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     res = {}
     for parts in parts_list:
-        rank_ms = []
+        wall = []
         for r in range(parts):
             for _ in range(2):
                 for o in helrm.limbsplit_rank_work(ctx, plan, rk, [cts[0]], parts, r):
@@ -566,14 +567,20 @@ def limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg, parts_l
                 o.close()
             e1.record(stream)
             torch.cuda.synchronize()
-            rank_ms.append(e0.elapsed_time(e1))
+            wall.append(e0.elapsed_time(e1))
         rp = -(-nl // parts)
         n_rot_pairs = info.n2_max * info.n_out_cts - 1   # every giant pair but giant 0 rotates (Criteo: 15)
-        recv = (n_rot_pairs * 2 + 2 * info.n_out_cts) * (parts - 1) * rp * N * 8
-        proj = max(rank_ms) + recv / 770e9 * 1e3
-        res[str(parts)] = {"projected_ms": round(proj, 3), "rank_ms_max": round(max(rank_ms), 3),
-                           "rank_ms_min": round(min(rank_ms), 3), "allgather_recv_MB": round(recv / 1e6, 1),
-                           "projected_lookups_per_s": round(1e3 / proj, 1)}
+        rotsum = max(0, int(round(math.log2(cfg.n_slots // info.mbar))))
+        # B rows + B' y-form rows per rotating pair, the accumulators, and in the finish the
+        # rescale row, each RotSum rotation's c1 y-form rows and key-switch P rows, the output rows
+        recv_rows = (n_rot_pairs * 2 * rp + 2 * info.n_out_cts * rp) * (parts - 1)
+        recv_rows += info.n_out_cts * (2 + rotsum * (l + 2 * ctx.info.K) + 2 * l) * (parts - 1) / parts
+        recv = recv_rows * N * 8
+        xfer = recv / 770e9 * 1e3
+        res[str(parts)] = {"projected_ms": round(max(wall) + xfer, 3),
+                           "projected_lookups_per_s": round(1e3 / (max(wall) + xfer), 1),
+                           "rank_ms_max": round(max(wall), 3), "rank_ms_min": round(min(wall), 3),
+                           "exchange_recv_MB": round(recv / 1e6, 1)}
     return {"model": " ".join(limb_split_projection.__doc__.split()), "per_parts": res}
 
 

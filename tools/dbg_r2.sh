@@ -1,9 +1,18 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_boundary.py -m gpu -q -x -k "lookup or golden or batched or rotate or host or extraction or dense" > gpurun_out/r2_rs.txt 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r2_rs.txt
-for v in "HELRM_ROTSUM_SPLIT=0" "X=1" "HELRM_ROTSUM_SPLIT=0" "X=1"; do
-  env $v timeout 300 python bench.py --steps 20 --warmup 5 --skip-cpu-baseline --skip-micro --skip-batch --skip-llm --skip-c2 > gpurun_out/ab_tmp.json 2>/dev/null
-  python - "$v" <<'PY'
-import json, sys
-d = json.load(open("gpurun_out/ab_tmp.json"))
-print(f"{sys.argv[1]:40s} step {d['ms_per_step']:.3f} ms e2e {d['e2e']['value']}", flush=True)
+timeout 900 python - <<'PY'
+import sys, json
+sys.argv = ["bench.py"]
+import torch, synth, bench
+from paper_2506_18150_b200 import helrm
+w = synth.make_workload("criteo", batch=1); cfg = w.config
+P = helrm.params_from_config(cfg); stream = torch.cuda.Stream(); ctx = helrm.Context(P, 0, stream.cuda_stream)
+T = helrm.tables_create(P, w.tables, w.n_dense); plan = helrm.plan_create(ctx, T, cfg.level)
+sk = helrm.sk_gen(ctx, cfg.seed); pk = helrm.pk_gen(ctx, sk, cfg.seed); rk = helrm.rotkeys_gen(ctx, sk, plan.galois(), cfg.seed)
+x = helrm.encode_query(T, w.indices[0], w.dense[0], cfg.n_slots)
+cts = [helrm.encrypt(ctx, pk, x, cfg.level, (cfg.seed << 20))]
+# reference: the single-GPU lookup's kernel sum vs its graph time
+ctx.profile(True)
+for o in helrm.lookup(ctx, plan, rk, cts): o.close()
+st = ctx.profile_stats(); ctx.profile(False)
+print("single-GPU lookup kernel sum ms", round(sum(v["ms"] for v in st.values()), 3))
+print(json.dumps(bench.limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg, (1, 2, 4, 8))["per_parts"], indent=1))
 PY
-done
