@@ -34,7 +34,10 @@ def main(path):
         a["time"] += t
         if col_fp64 is not None:
             a["fp64_x_time"] += t * float(r[col_fp64].replace(",", ""))
-    res = {"source": path, "kernels": agg}
+    import os
+    commit = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], capture_output=True, text=True,
+                            cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__)))).stdout.strip()
+    res = {"source": path, "commit": commit, "kernels": agg}
     p1 = [v for k, v in agg.items() if k.startswith("k_ntt_fwd<8, 0") or k.startswith("k_ntt_fwd<8, 2")]
     p2 = [v for k, v in agg.items() if k.startswith("k_ntt_fwd<8, 1")]
     if p1 and p2:
