@@ -2610,13 +2610,19 @@ static helrm_ctx::LookupGraph& graph_entry(helrm_ctx* c, const helrm_plan* pl, c
 
 // G.X -> G.S on the context stream: eagerly on the first use (creates every
 // cached constant), captured into a CUDA graph on the second, replayed after
-static void run_graph_chunk(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, helrm_ctx::LookupGraph& G,
-                            int Qc) {
+// G.X -> G.S through body(pinned) on the context stream: eagerly on the first
+// use (creates every cached constant), captured into a CUDA graph on the
+// second, replayed after.  body enqueues on c->stream only (side streams are
+// forked from and joined back to it); pinned != null during the capture (host
+// work lists are staged there, so the graph re-uploads them from pinned memory).
+}  // extern "C" (template below)
+template <class F>
+static void run_graph(helrm_ctx* c, helrm_ctx::LookupGraph& G, F body) {
   if (G.exec) {
     HCUDA(cudaGraphLaunch(G.exec, c->stream));
     c->launches += G.launches;
   } else if (G.uses == 0 || G.failed) {
-    lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
+    body((void**)nullptr);
   } else {
     // capture on the private stream (the context stream may be the legacy
     // default stream, which cannot be captured), ordered after the staging
@@ -2628,7 +2634,7 @@ static void run_graph_chunk(helrm_ctx* c, const helrm_plan* pl, const helrm_rotk
     cudaError_t e = cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
       try {
-        lookup_chunk(c, pl, rk, G.X, Qc, G.S, &G.pinned);
+        body(&G.pinned);
       } catch (...) {
         cudaStreamEndCapture(c->s_cap, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -2646,13 +2652,20 @@ static void run_graph_chunk(helrm_ctx* c, const helrm_plan* pl, const helrm_rotk
       G.exec = nullptr;
       G.failed = true;
       c->launches = l0;
-      lookup_chunk(c, pl, rk, G.X, Qc, G.S, nullptr);
+      body((void**)nullptr);
     } else {
       G.launches = c->launches - l0;
       HCUDA(cudaGraphLaunch(G.exec, c->stream));
     }
   }
   G.uses++;
+}
+
+extern "C" {
+
+static void run_graph_chunk(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, helrm_ctx::LookupGraph& G,
+                            int Qc) {
+  run_graph(c, G, [&](void** pinned) { lookup_chunk(c, pl, rk, G.X, Qc, G.S, pinned); });
 }
 
 // device words one query of a batched double-hoisted lookup keeps live
@@ -3113,6 +3126,14 @@ static void lookup_split(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys*
 // buffers [2][rows][N]; the all-gathers are explicit copies of the slices into
 // full buffers.  Per-limb work is independent, so the result is bit-identical
 // to helrm_lookup (D23: only the limb placement changes).
+static void limbsplit_body(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* Xin,
+                           uint64_t* Sout, int parts, bool real, int only_rank, void** pinned);
+
+// per-rank pinned staging of the MAC work lists (graph capture of the limb split)
+static size_t limbsplit_pinned_per_rank(const helrm_plan* pl) {
+  return (size_t)pl->n_diag * sizeof(MacTerm) + (size_t)count_pairs(pl) * sizeof(int4) + 256;
+}
+
 static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const helrm_ct* const* in,
                              size_t batch, helrm_ct** out, int parts, bool real, int only_rank = -1) {
   need(pl->mode == HELRM_MODE_DOUBLE && !pl->compact, HELRM_ERR_ARG,
@@ -3120,12 +3141,45 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
   for (int64_t a : pl->rotations) (void)key_for(rk, galois_of_rot(c, a));
   const Params& P = c->P;
   const uint32_t l = pl->level;
+  const size_t N = P.N, nqN = (size_t)(l + 1) * N, oN = 2 * (size_t)l * N;
+  const int64_t C = pl->C, O = pl->O;
+  if (real) parts = c->world;
+  need(parts >= 1 && (size_t)parts <= l + 1 + P.K, HELRM_ERR_ARG, "1 <= parts <= l + 1 + K");
+  // one graph per (plan, key set, partition, mode): staged inputs X, outputs S
+  const int mode = only_rank >= 0 ? 2 : real ? 1 : 0;
+  helrm_ctx::LookupGraph& G = c->graphs[std::make_tuple(pl->id, rk->id, 100000 + parts * 1000 + mode * 100 +
+                                                          std::max(0, only_rank))];
+  if (!G.X) {
+    G.X = (uint64_t*)c->dalloc((size_t)C * 2 * nqN * 8);
+    G.S = (uint64_t*)c->dalloc((size_t)O * oN * 8);
+    HCUDA(cudaMallocHost(&G.pinned, limbsplit_pinned_per_rank(pl) * parts));
+  }
+  static const bool graphs = getenv("HELRM_GRAPH") ? atoi(getenv("HELRM_GRAPH")) != 0 : true;
+  for (size_t qy = 0; qy < batch; qy++) {
+    const helrm_ct* const* cin = in + qy * C;
+    for (int64_t ci = 0; ci < C; ci++) {
+      need(cin[ci] != nullptr && cin[ci]->level == l, HELRM_ERR_LEVEL, "input level differs from the plan's");
+      if (real && parts > 1)   // the query lives on rank 0
+        HNCCL(nccl().broadcast(cin[ci]->d, G.X + ci * 2 * nqN, 2 * nqN, ncclUint64, 0, c->comm, c->stream));
+      else
+        HCUDA(cudaMemcpyAsync(G.X + ci * 2 * nqN, cin[ci]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    auto body = [&](void** pinned) { limbsplit_body(c, pl, rk, G.X, G.S, parts, real, only_rank, pinned); };
+    if (graphs && !c->prof.on) run_graph(c, G, body);
+    else body(nullptr);
+    emit_outputs(c, pl, G.S, 1, cin[0]->scale, out + qy * O);
+  }
+}
+
+// the whole limb-partitioned lookup of one staged query Xin -> Sout [O][2][l][N]
+static void limbsplit_body(helrm_ctx* c, const helrm_plan* pl, const helrm_rotkeys* rk, const uint64_t* Xin,
+                           uint64_t* Sout, int parts, bool real, int only_rank, void** pinned) {
+  const Params& P = c->P;
+  const uint32_t l = pl->level;
   const size_t N = P.N, nq = l + 1, nl = l + 1 + P.K, nlN = nl * N, nqN = nq * N, dn = P.dnum(l);
   const LimbMap mqp = P.map_qp(l), mq = P.map_q(l);
   const LevelConst& lc = level_const(c, l);
   const int64_t C = pl->C, O = pl->O;
-  if (real) parts = c->world;
-  need(parts >= 1 && (size_t)parts <= nl, HELRM_ERR_ARG, "1 <= parts <= l + 1 + K");
   // equal slices of rp = ceil(nl / parts) rows (the last ones shorter or empty), so that one
   // ncclAllGather of the padded slices lays the rows out in order
   const size_t rp = (nl + parts - 1) / parts;
@@ -3146,16 +3200,10 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
     for (int i = 0; i < m.n; i++) m.pr[i] = mqp.pr[lo[r] + i];
     return m;
   };
-  for (size_t qy = 0; qy < batch; qy++) {
-    const helrm_ct* const* cin = in + qy * C;
-    DBuf X(c, (size_t)C * 2 * nqN);
-    for (int64_t ci = 0; ci < C; ci++) {
-      need(cin[ci] != nullptr && cin[ci]->level == l, HELRM_ERR_LEVEL, "input level differs from the plan's");
-      if (real && parts > 1)   // the query lives on rank 0
-        HNCCL(nccl().broadcast(cin[ci]->d, X.p + ci * 2 * nqN, 2 * nqN, ncclUint64, 0, c->comm, c->stream));
-      else
-        HCUDA(cudaMemcpyAsync(X.p + ci * 2 * nqN, cin[ci]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
-    }
+  {
+    struct {
+      const uint64_t* p;
+    } X{Xin};
     // L1: every rank converts the (replicated) y-form of the input c1s into its own rows of
     // the digits: D row r of digit k is written by the rank owning row r
     DBuf D(c, (size_t)C * dn * nlN), Y(c, (size_t)C * nqN);
@@ -3241,7 +3289,8 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
         return std::make_pair((const uint64_t*)a, (const uint64_t*)(a + rows * N));
       });
       need(ml.oi.size() == nz, HELRM_ERR_CONFIG, "work list differs from the pair enumeration");
-      MacDev md(c, ml);
+      void* pr = pinned ? (char*)*pinned + (size_t)r * limbsplit_pinned_per_rank(pl) : nullptr;
+      MacDev md(c, ml, pinned ? &pr : nullptr);
       {
         const DevCtx dcx = c->dc();
         ProfScope ps_(dcx, "diag_mac", 8.0 * N * (hi[r] - lo[r]) * (ml.n_u + 2.0 * ml.n_x + 2.0 * nz));
@@ -3251,84 +3300,112 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
              HELRM_ERR_CONFIG, "the limb partition needs N divisible by the MAC tile");
       }
     }
-    // L4: per giant pair, all-gather B, ModDown + ModUp (replicated), key switch on own rows
-    // Bf: all-gathered B rows; Bp: B' (each rank's Q rows); Y2: B' in y-form, all-gathered
-    DBuf Bf(c, parts * rp * N), Bp(c, nqN), D2(c, dn * nlN), Y2(c, parts * rp * N), yP(c, (size_t)P.K * N),
-        T(c, nqN);
+    // L4, batched over the rotating giant pairs: all-gather every pair's B rows, ModDown of
+    // all of them on each rank's Q rows, B' to y-form on those rows, all-gather, each rank's
+    // rows of the digits of every B', then the giant key switches in runs on own rows.
+    std::vector<size_t> rot;   // rotating pairs (g_i != 0)
     for (size_t z = 0; z < nz; z++) {
       const int64_t o = oi[z].first, gi = pl->giants[o][oi[z].second];
-      if (gi % (int64_t)P.n == 0) {   // O_o += (A, B)_z on own rows
-        for (int r : mine) {
-          if (hi[r] == lo[r]) continue;
-          const LimbMap sm = sub(r);
-          for (int h = 0; h < 2; h++)
-            launch_binary(c->dc(), 0, so[r] + (o * 2 + h) * rp * N, sab[r] + (z * 2 + h) * rp * N,
-                          so[r] + (o * 2 + h) * rp * N, sm);
-        }
+      if (gi % (int64_t)P.n != 0) {
+        rot.push_back(z);
         continue;
       }
-      // all-gather of B's rows: slice r lands at rows [r rp, (r + 1) rp) of Bf
+      for (int r : mine) {   // O_o += (A, B)_z on own rows
+        if (hi[r] == lo[r]) continue;
+        const LimbMap sm = sub(r);
+        for (int h = 0; h < 2; h++)
+          launch_binary(c->dc(), 0, so[r] + (o * 2 + h) * rp * N, sab[r] + (z * 2 + h) * rp * N,
+                        so[r] + (o * 2 + h) * rp * N, sm);
+      }
+    }
+    const size_t nr = rot.size(), fs = (size_t)parts * rp * N;   // padded full stride per polynomial
+    if (nr) {
+      DBuf Bf(c, nr * fs), Bp(c, nr * nqN), D2(c, nr * dn * nlN), Y2(c, nr * fs), yP(c, nr * P.K * N),
+          T(c, nr * nqN);
+      // all-gather of every rotating pair's B rows: slice r of pair t at Bf + t fs + r rp N
       if (real && parts > 1) {
-        HNCCL(nccl().allGather(sab[c->rank] + (z * 2 + 1) * rp * N, Bf.p, rp * N, ncclUint64, c->comm, c->stream));
+        HNCCL(nccl().groupStart());
+        for (size_t t = 0; t < nr; t++)
+          HNCCL(nccl().allGather(sab[c->rank] + (rot[t] * 2 + 1) * rp * N, Bf.p + t * fs, rp * N, ncclUint64, c->comm,
+                                 c->stream));
+        HNCCL(nccl().groupEnd());
       } else {
         for (int r : mine)
-          HCUDA(cudaMemcpyAsync(Bf.p + r * rp * N, sab[r] + (z * 2 + 1) * rp * N, rp * N * 8,
-                                cudaMemcpyDeviceToDevice, c->stream));
+          for (size_t t = 0; t < nr; t++)
+            HCUDA(cudaMemcpyAsync(Bf.p + t * fs + r * rp * N, sab[r] + (rot[t] * 2 + 1) * rp * N, rp * N * 8,
+                                  cudaMemcpyDeviceToDevice, c->stream));
       }
-      // ModDown (D16) of B: the P rows to y-form (replicated, K limbs), then each rank converts
-      // and transforms its own Q rows, the epilogue writing (B - t) P^-1 into Bp
-      launch_ntt_inv(c->dc(), Bf.p + nqN, yP.p, c->scratch, P.K, P.map_range(P.L + 1, P.K), P.K * N, P.K * N,
+      // ModDown (D16): every B's P rows to y-form (replicated), own Q rows converted + NTT + epilogue
+      launch_ntt_inv(c->dc(), Bf.p + nqN, yP.p, c->scratch, nr * P.K, P.map_range(P.L + 1, P.K), fs, P.K * N,
                      lc.moddown_post, nullptr);
       for (int r : mine) {
-        const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], 1);
+        const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], (int)nr);
         if (st.n_q == 0) continue;
-        launch_conv_rows(c->dc(), st.dn_tab, 1, st.dn_rows, (int)P.K, yP.p, P.K * N, T.p, nqN, 0, 1, mq);
+        launch_conv_rows(c->dc(), st.dn_tab, 1, st.dn_rows, (int)P.K, yP.p, P.K * N, T.p, nqN, 0, (int)nr, mq);
         NttEpi epi;
         epi.y = Bf.p;
-        epi.ys = nlN;
+        epi.ys = fs;
         epi.out = Bp.p;
         epi.os = nqN;
         epi.s = lc.pinv;
         epi.sp = lc.pinvs;
         launch_ntt_fwd(c->dc(), T.p, T.p, c->scratch, st.n_q, mq, 0, 0, true, st.q_lidx, &epi);
-        // ModUp (D15) of B': its own Q rows into y-form
-        launch_ntt_inv(c->dc(), Bp.p, Y2.p, c->scratch, st.n_q, mq, nqN, nqN, lc.modup_post, st.q_lidx);
+        // ModUp (D15) of B': own Q rows into y-form, rows at the padded positions of Y2
+        launch_ntt_inv(c->dc(), Bp.p, Y2.p, c->scratch, st.n_q, mq, nqN, fs, lc.modup_post, st.q_lidx);
       }
-      if (real && parts > 1) {   // all-gather of B' (y-form) rows: slice r lands at rows [r rp, (r + 1) rp)
-        // (in place: the rank's slice sits at rank rp rows, also for a trailing empty rank)
-        HNCCL(nccl().allGather(Y2.p + (size_t)c->rank * rp * N, Y2.p, rp * N, ncclUint64, c->comm, c->stream));
+      if (real && parts > 1) {   // all-gather of the y-form rows (in place: slice r at r rp rows)
+        HNCCL(nccl().groupStart());
+        for (size_t t = 0; t < nr; t++)
+          HNCCL(nccl().allGather(Y2.p + t * fs + (size_t)c->rank * rp * N, Y2.p + t * fs, rp * N, ncclUint64, c->comm,
+                                 c->stream));
+        HNCCL(nccl().groupEnd());
       }
-      for (int r : mine) {   // each rank's rows of the digits of B'
+      for (int r : mine) {   // each rank's rows of the digits of every B'
         if (hi[r] == lo[r]) continue;
-        const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], 1);
-        launch_conv_rows(c->dc(), st.up_tab, (int)dn, st.up_rows, (int)P.alpha, Y2.p, nqN, D2.p, dn * nlN, nlN, 1,
-                         mqp);
+        const helrm_ctx::SliceTabs& st = slice_tabs(c, l, (int)lo[r], (int)hi[r], (int)nr);
+        launch_conv_rows(c->dc(), st.up_tab, (int)dn, st.up_rows, (int)P.alpha, Y2.p, fs, D2.p, dn * nlN, nlN,
+                         (int)nr, mqp);
         if (st.n_up) launch_ntt_fwd(c->dc(), D2.p, D2.p, c->scratch, st.n_up, mqp, 0, 0, true, st.up_lidx);
       }
-      const uint64_t g = galois_of_rot(c, gi);
+      // giant key switches on own rows, in runs of one output block (k_kip_giants row slice)
       for (int r : mine) {
         if (hi[r] == lo[r]) continue;
         const size_t rows = rp;
         const size_t r0N = (size_t)lo[r] * N;
         KipGiants kg{};
-        kg.row0 = (int)lo[r];
-        kg.rows = (int)(hi[r] - lo[r]);
-        kg.digit_stride = nlN;
-        kg.dnum = (int)dn;
-        kg.add_rows = (int)nl;
-        kg.alpha = (int)P.alpha;
-        kg.level = (int)l;
-        kg.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
-        kg.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
-        kg.out0 = so[r] + o * 2 * rows * N - r0N;
-        kg.out1 = kg.out0 + rows * N;
-        kg.n = 1;
-        kg.digits[0] = D2.p;
-        kg.own[0] = Bp.p;
-        kg.key[0] = key_for(rk, g);
-        kg.add0[0] = sab[r] + z * 2 * rows * N - r0N;   // A's rows
-        kg.rot[0] = rot_of_galois(c, g);
-        launch_kip_giants(c->dc(), kg, mqp);
+        int64_t cur_o = -1;
+        auto flush = [&]() {
+          if (kg.n == 0) return;
+          kg.row0 = (int)lo[r];
+          kg.rows = (int)(hi[r] - lo[r]);
+          kg.digit_stride = nlN;
+          kg.dnum = (int)dn;
+          kg.add_rows = (int)nl;
+          kg.alpha = (int)P.alpha;
+          kg.level = (int)l;
+          kg.key_digit_stride = (size_t)2 * (P.L + 1 + P.K) * N;
+          kg.key_half_stride = (size_t)(P.L + 1 + P.K) * N;
+          kg.out0 = so[r] + cur_o * 2 * rows * N - r0N;
+          kg.out1 = kg.out0 + rows * N;
+          launch_kip_giants(c->dc(), kg, mqp);
+          kg.n = 0;
+        };
+        for (size_t t = 0; t < nr; t++) {
+          const size_t z = rot[t];
+          const int64_t o = oi[z].first, gi = pl->giants[o][oi[z].second];
+          if (o != cur_o || kg.n == kMaxGiantRun) {
+            flush();
+            cur_o = o;
+          }
+          const uint64_t g = galois_of_rot(c, gi);
+          kg.digits[kg.n] = D2.p + t * dn * nlN;
+          kg.own[kg.n] = Bp.p + t * nqN;
+          kg.key[kg.n] = key_for(rk, g);
+          kg.add0[kg.n] = sab[r] + z * 2 * rows * N - r0N;   // A's rows
+          kg.rot[kg.n] = rot_of_galois(c, g);
+          kg.n++;
+        }
+        flush();
       }
     }
     // all-gather of the accumulators
@@ -3479,7 +3556,7 @@ static void lookup_limbsplit(helrm_ctx* c, const helrm_plan* pl, const helrm_rot
       }
       if (!timing) share(So, qa, qb, 2, nq1N);   // the output ct's rows to every rank
     }
-    emit_outputs(c, pl, S1.p, 1, cin[0]->scale, out + qy * O);
+    HCUDA(cudaMemcpyAsync(Sout, S1.p, (size_t)O * 2 * nq1N * 8, cudaMemcpyDeviceToDevice, c->stream));
   }
 }
 
