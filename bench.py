@@ -532,8 +532,25 @@ def dist_b1(args, ctx, helrm, torch, stream, plan, rk, cts, world, rank):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
-    return {"ms_per_lookup": round(ms, 4), "lookups_per_s": round(1e3 / ms, 3), "world": world,
-            "partition": "giant range per rank, NCCL allreduce(uint64, sum) + mod-q kernel"}
+    res = {"ms_per_lookup": round(ms, 4), "lookups_per_s": round(1e3 / ms, 3), "world": world,
+           "partition": "giant range per rank, NCCL allreduce(uint64, sum) + mod-q kernel"}
+    # the RNS-limb partition on the same communicator
+    for _ in range(max(3, args.warmup)):
+        for o in helrm.lookup_limbsplit(ctx, plan, rk, [cts[0]]):
+            o.close()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for _ in range(args.steps):
+        for o in helrm.lookup_limbsplit(ctx, plan, rk, [cts[0]]):
+            o.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms2 = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+    res["limb_split"] = {"ms_per_lookup": round(ms2, 4), "lookups_per_s": round(1e3 / ms2, 3),
+                         "partition": "Q_l P rows per rank; ModUp / ModDown / key switches / inner sums on own rows; "
+                                      "NCCL all-gathers + broadcasts of the exchanged rows"}
+    return res
 
 
 def limb_split_projection(ctx, helrm, torch, stream, plan, rk, cts, cfg, parts_list=(2, 4, 8)):
