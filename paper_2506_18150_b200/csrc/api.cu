@@ -3074,16 +3074,19 @@ static void lookup_split(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys*
   const size_t nlN = (size_t)(p->level + 1 + P.K) * P.N, nqN = (size_t)(p->level + 1) * P.N;
   const size_t owords = (size_t)p->O * 2 * nlN;
   const int parts = virt > 0 ? virt : c->world;
-  for (size_t q = 0; q < batch; q++) {
-    const helrm_ct* const* cin = in + q * p->C;
-    DBuf O(c, owords), X(c, (size_t)p->C * 2 * nqN), S(c, (size_t)p->O * 2 * p->level * P.N);
-    for (int64_t ci = 0; ci < p->C; ci++) {
-      need(cin[ci] != nullptr && cin[ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's");
-      if (virt == 0 && c->world > 1)   // the query lives on rank 0: broadcast it into every rank's staging buffer
-        HNCCL(nccl().broadcast(cin[ci]->d, X.p + ci * 2 * nqN, 2 * nqN, ncclUint64, 0, c->comm, c->stream));
-      else
-        HCUDA(cudaMemcpyAsync(X.p + ci * 2 * nqN, cin[ci]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
-    }
+  // graph entry of (plan, key set, split): staged inputs X, outputs S, one pinned MAC-list region per part
+  helrm_ctx::LookupGraph& G = c->graphs[std::make_tuple(p->id, rk->id, 300000 + parts * 10 + (virt > 0 ? 1 : 0))];
+  size_t nbb = 0;
+  for (auto& b : p->babies) nbb = std::max(nbb, b.size());
+  const size_t per_part = (size_t)p->n_diag * sizeof(MacTermW) + count_pairs(p) * sizeof(int4) +
+                          (size_t)count_pairs(p) * nbb * 8 + 64;
+  if (!G.X) {
+    G.X = (uint64_t*)c->dalloc((size_t)p->C * 2 * nqN * 8);
+    G.S = (uint64_t*)c->dalloc((size_t)p->O * 2 * p->level * P.N * 8);
+    HCUDA(cudaMallocHost(&G.pinned, per_part * parts));
+  }
+  auto body = [&](void** pinned) {
+    DBuf O(c, owords);
     HCUDA(cudaMemsetAsync(O.p, 0, owords * 8, c->stream));
     if (virt > 0) {
       DBuf part(c, owords);
@@ -3091,23 +3094,35 @@ static void lookup_split(helrm_ctx* c, const helrm_plan* p, const helrm_rotkeys*
         int64_t lo = 0, hi = 0;
         (void)helrm_dist_range(count_pairs(p), virt, r, &lo, &hi);
         HCUDA(cudaMemsetAsync(part.p, 0, owords * 8, c->stream));
-        lookup_double_part(c, p, rk, X.p, 1, lo, hi, part.p);
+        void* pr = pinned ? (char*)*pinned + (size_t)r * per_part : nullptr;
+        lookup_double_part(c, p, rk, G.X, 1, lo, hi, part.p, pinned ? &pr : nullptr);
         launch_add_u64(c->dc(), O.p, part.p, owords);   // the all-reduce's exact uint64 sum
       }
     } else {
       int64_t lo = 0, hi = INT64_MAX;
       (void)helrm_dist_range(count_pairs(p), c->world, c->rank, &lo, &hi);
-      lookup_double_part(c, p, rk, X.p, 1, lo, hi, O.p);
-      if (c->world > 1) {
-        HNCCL(nccl().allReduce(O.p, O.p, owords, ncclUint64, ncclSum, c->comm, c->stream));
-        nccl_check_async(c);
-      }
+      lookup_double_part(c, p, rk, G.X, 1, lo, hi, O.p, pinned);
+      if (c->world > 1) HNCCL(nccl().allReduce(O.p, O.p, owords, ncclUint64, ncclSum, c->comm, c->stream));
     }
     // L5: each partial word is < q, so the sum is < parts q < 2^64 (parts < 2^13); reduce mod q
     if (parts > 1)
       for (int64_t h = 0; h < 2 * p->O; h++) launch_modred(c->dc(), O.p + (size_t)h * nlN, P.map_qp(p->level));
-    lookup_finish(c, p, rk, O.p, 1, S.p);
-    emit_outputs(c, p, S.p, 1, cin[0]->scale, out + q * p->O);
+    lookup_finish(c, p, rk, O.p, 1, G.S);
+  };
+  static const bool graphs = getenv("HELRM_GRAPH") ? atoi(getenv("HELRM_GRAPH")) != 0 : true;
+  for (size_t q = 0; q < batch; q++) {
+    const helrm_ct* const* cin = in + q * p->C;
+    for (int64_t ci = 0; ci < p->C; ci++) {
+      need(cin[ci] != nullptr && cin[ci]->level == p->level, HELRM_ERR_LEVEL, "input level differs from the plan's");
+      if (virt == 0 && c->world > 1)   // the query lives on rank 0: broadcast it into every rank's staging buffer
+        HNCCL(nccl().broadcast(cin[ci]->d, G.X + ci * 2 * nqN, 2 * nqN, ncclUint64, 0, c->comm, c->stream));
+      else
+        HCUDA(cudaMemcpyAsync(G.X + ci * 2 * nqN, cin[ci]->d, 2 * nqN * 8, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (graphs && !c->prof.on && !p->compact) run_graph(c, G, body);
+    else body(nullptr);
+    if (virt == 0 && c->world > 1) nccl_check_async(c);
+    emit_outputs(c, p, G.S, 1, cin[0]->scale, out + q * p->O);
   }
 }
 
