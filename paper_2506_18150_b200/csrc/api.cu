@@ -888,11 +888,15 @@ helrm_status helrm_ctx_create(const helrm_params* p, int device, uintptr_t strea
         ipw[k] = mulm(ipw[k - 1], ipsi, q);
       }
       double* base = &tw[i * per];
+      // centred twiddles (|w| <= q/2): the butterflies' mmul then accepts inputs below 4q
+      // (kernels_ntt.cu), which halves the lazy reductions
+      auto cen = [&](uint64_t w) { return w > q / 2 ? (double)w - (double)q : (double)w; };
       auto put = [&](double* dst, size_t j, size_t idx) {
-        dst[2 * j] = (double)pw[br[idx]];
-        dst[2 * j + 1] = (double)pw[br[idx]] / (double)q;
-        dst[2 * N + 512 + 2 * j] = (double)ipw[br[idx]];
-        dst[2 * N + 512 + 2 * j + 1] = (double)ipw[br[idx]] / (double)q;
+        const double w = cen(pw[br[idx]]), iw = cen(ipw[br[idx]]);
+        dst[2 * j] = w;
+        dst[2 * j + 1] = w / (double)q;
+        dst[2 * N + 512 + 2 * j] = iw;
+        dst[2 * N + 512 + 2 * j + 1] = iw / (double)q;
       };
       for (size_t idx = 0; idx < 256; idx++) put(base, idx, idx);  // pass 1 (natural index < 256)
       double* t2 = base + 512;

@@ -29,8 +29,10 @@
 // are exact integer-valued doubles, the product Y W = h + l is split exactly
 // with an FMA, the quotient k = rint(Y W / q) comes from one FMA against the
 // precomputed W/q (round-to-nearest via the 1.5 2^52 shift), and
-// r = (h - k q) + l is exact; values stay in (-2q, 2q) by centred
-// reductions.  Measured on B200: ~2.7x the modmul throughput of 64-bit
+// r = (h - k q) + l is exact.  The twiddles are stored centred (|W| <= q/2,
+// |W/q| <= 1/2), so mmul accepts any |Y| < 4q < 2^52 and returns |r| <= 0.75 q;
+// values stay below 4q by centred reductions (every fourth forward stage on
+// the additive inputs, every other inverse stage on the sums).  Measured on B200: ~2.7x the modmul throughput of 64-bit
 // integer Shoup (profiles/r01_peak_int.txt).
 //
 // Limb selection: limb v of a launch is limb lidx[v] of the layout when a
@@ -74,9 +76,13 @@ __device__ __forceinline__ void ct_bfly(double& x, double& y, double2 w, double 
   x = a + r;
   y = a - r;
 }
+// R: reduce the sum.  Alternating R = true / false from the first stage of a
+// pass keeps |x|, |y| < 1.5 q before a reducing stage (so |x - y| < 3q) and
+// < 0.75 q + ... before a lazy one; every pass ends below 1.5 q.
+template <bool R>
 __device__ __forceinline__ void gs_bfly(double& x, double& y, double2 w, double q, double qi) {
   const double s = x + y, dd = x - y;
-  x = cred(s, q, qi);
+  x = R ? cred(s, q, qi) : s;
   y = mmul(dd, w.x, w.y, q);
 }
 }  // namespace
@@ -131,13 +137,13 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
   }
   // phase A: stages 0..3 on layout e = t + TS k (twiddles independent of t)
   // Lazy reduction: a butterfly's product term is reduced by mmul (|r| <= 0.75 q for any
-  // |y| < 2^51), so only the additive inputs grow, by 0.75 q per stage.  Reducing the
-  // additive inputs (half the elements) before every even stage keeps every value below
-  // 2 q < 2^51 (q < 2^50): half the reductions of reducing everything every other stage.
+  // |y| < 4q, centred twiddles), so only the additive inputs grow, by 0.75 q per stage.
+  // Reducing the additive inputs (half the elements) before stages 0 and 4 keeps every
+  // value below 0.5 q + 4 x 0.75 q = 3.5 q < 2^52 (q < 2^50).
 #pragma unroll
   for (int st = 0; st < 4; st++) {
     const int half = 8 >> st;
-    if ((st & 1) == 0) {
+    if ((st & 3) == 0) {
 #pragma unroll
       for (int k = 0; k < kEPT; k++)
         if ((k & half) == 0) r[k] = cred(r[k], q, qi);
@@ -168,7 +174,7 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
 #pragma unroll
     for (int st = 4; st < SLOG; st++) {
       const int half = S >> (st + 1);
-      if ((st & 1) == 0) {
+      if ((st & 3) == 0) {
 #pragma unroll
         for (int k = 0; k < kEPT; k++)
           if ((k & half) == 0) r[k] = cred(r[k], q, qi);
@@ -185,7 +191,7 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
       }
     }
   }
-  // pass 1 hands values below 2 q to pass 2 (whose first stage reduces its additive inputs);
+  // pass 1 hands values below 3.5 q to pass 2 (whose first stage reduces its additive inputs);
   // pass 2 reduces everything once before canonicalising
   if (!P1) {
 #pragma unroll
@@ -339,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
           double2 w;
           if (MODE == 0) w = twB[(1 << st) + (e >> (SLOG - st))];
           else w = twB[((1 << (st - 4)) - 1 + (k >> (SLOG - st))) * 16];
-          gs_bfly(r[k], r[k + half], w, q, qi);
+          if (((SLOG - 1 - st) & 1) == 0) gs_bfly<true>(r[k], r[k + half], w, q, qi);
+          else gs_bfly<false>(r[k], r[k + half], w, q, qi);
         }
       }
     }
@@ -364,7 +371,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
     for (int k = 0; k < kEPT; k++) {
       if ((k & half) == 0) {
         const double2 w = MODE == 0 ? twA[(1 << st) + (k >> (4 - st))] : twA[(1 << st) - 1 + (k >> (4 - st))];
-        gs_bfly(r[k], r[k + half], w, q, qi);
+        if (((SLOG - 1 - st) & 1) == 0) gs_bfly<true>(r[k], r[k + half], w, q, qi);
+        else gs_bfly<false>(r[k], r[k + half], w, q, qi);
       }
     }
   }
