@@ -128,6 +128,46 @@ def test_ntt_matches_oracle(name, torch_mod):
 
 
 @gpu
+@pytest.mark.parametrize("name", ["tiny_a", "criteo"])
+def test_ntt_extreme_inputs_match_oracle(name, torch_mod):
+    """The lazy reductions of the butterflies (values kept below 4q between
+    reductions, centred twiddles) on inputs of maximal magnitude: constant
+    q - 1, constant (q +- 1)/2, alternating 0 / q - 1, one-hot q - 1, and
+    random draws from {0, 1, (q-1)/2, (q+1)/2, q - 2, q - 1}, for the forward
+    and the inverse transform against the oracle."""
+    E = env(name, torch_mod)
+    PO = E.PO
+    primes = PO.q + PO.p
+    N = PO.N
+    rng = np.random.default_rng(5)
+    pats = []
+    for q in primes:
+        q = np.uint64(q)
+        alt = np.zeros(N, dtype=np.uint64)
+        alt[::2] = q - np.uint64(1)
+        one = np.zeros(N, dtype=np.uint64)
+        one[N // 3] = q - np.uint64(1)
+        pick = np.array([0, 1, (int(q) - 1) // 2, (int(q) + 1) // 2, int(q) - 2, int(q) - 1], dtype=np.uint64)
+        pats.append([np.full(N, q - np.uint64(1)), np.full(N, (q - np.uint64(1)) // np.uint64(2)),
+                     np.full(N, (q + np.uint64(1)) // np.uint64(2)), alt, one, pick[rng.integers(0, 6, N)]])
+    n_pat = len(pats[0])
+    a = np.stack([np.stack([pats[l][k] for l in range(len(primes))]) for k in range(n_pat)])   # [pat][limb][N]
+    perm = _slot_to_natural(N)
+    d = E.dev(a.reshape(n_pat * len(primes), N))
+    E.h.ntt_fwd(E.ctx, d, 0, len(primes), n_pat)
+    got = E.host(d).reshape(n_pat, len(primes), N)
+    for k in range(n_pat):
+        assert np.array_equal(got[k][:, perm], core.ntt(a[k], primes, PO)), k
+    # inverse of the same extreme values placed in slot order (as NTT-form data)
+    d = E.dev(a.reshape(n_pat * len(primes), N))
+    E.h.ntt_inv(E.ctx, d, 0, len(primes), n_pat)
+    got = E.host(d).reshape(n_pat, len(primes), N)
+    for k in range(n_pat):
+        natural = a[k][:, perm]              # the oracle's natural order of the slot-order input
+        assert np.array_equal(got[k], core.intt(natural, primes, PO)), k
+
+
+@gpu
 @pytest.mark.parametrize("name", ["tiny_a", "uci"])
 def test_keys_and_encryption_match_oracle(name, torch_mod):
     E = env(name, torch_mod)
