@@ -488,6 +488,10 @@ def run_gpu(args, world, rank, local):
         secondary["criteo_l4_b1"] = shape_lookup(helrm, torch, stream, world, dev, "criteo_l4", reps=10)
         # a dense 512 -> 256 linear layer on the same engine, Criteo parameters
         secondary["mlp_512x256"] = shape_lookup(helrm, torch, stream, world, dev, "mlp_512x256")
+        # the paper's Table-1 shape: GPT-2 d = 768, p = 16, l = 32 (its CPU
+        # BSGS: 3.17 s, another machine -- context, not a target)
+        secondary["table1_gpt2_p16_l32"] = shape_lookup(helrm, torch, stream, world, dev, "table1")
+        secondary["table1_gpt2_p16_l32"]["paper_cpu_bsgs_s"] = 3.17
     if args.with_compact:
         # layouts whose QP-NTT diagonals exceed HBM, on compact plans (HELRM_PLAN_COMPACT):
         # the paper-exact LLM layout L1 and the 100-input-ct Criteo model

@@ -163,10 +163,14 @@ typedef struct {
   int64_t k;          /* rows of the (virtual) original table, >= 1 */
   int64_t d;          /* embedding dimension, >= 1 */
   int64_t p;          /* digit base; 0 = never compress; compress iff k > p */
-  const double* w;    /* (k <= p or p == 0 ? k : p * ceil(log_p k)) x d, row-major;
+  const double* w;    /* (uncompressed ? k : p * l) x d, row-major (l below);
                          rows [t p, (t+1) p) are sub-table t (LSD-first digits) */
   int64_t in_off;     /* input slot offset, -1 = contiguous default (D19) */
   int64_t out_off;    /* output slot offset, -1 = contiguous default */
+  int64_t l;          /* digit count: 0 = ceil(log_p k); > 0 (p >= 2): exactly l digits,
+                         LAYOUT unless p^l >= k -- shapes whose p^l exceeds the int64 row
+                         range, e.g. PAPER.md:361's p = 16, l = 32 (the weights then have
+                         p l rows and the high digits of every index are 0) */
 } helrm_table_desc;
 
 /* Copies the weights in (blocks sharing one `w` pointer are deduplicated);

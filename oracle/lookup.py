@@ -77,14 +77,18 @@ class Layout:
 
 def layout(workload) -> Layout:
     """D19 input/output layout: table b is uncompressed iff k_b <= p_b (or
-    p_b = 0), segment width k_b; else l_b digits, width p_b l_b, digit t
+    p_b = 0) and no digit count is given, segment width k_b; else l_b digits
+    (ceil(log_p k_b), or the table's explicit l >= that), width p_b l_b, digit t
     one-hot at [t p_b, (t+1) p_b) of the segment.  Default offsets are the
     paper's contiguous layout."""
     blocks = []
     I, R = workload.n_dense, 0
     for t in workload.tables:
-        comp = t.p != 0 and t.k > t.p
-        l = n_digits(t.k, t.p) if comp else 1
+        lx = getattr(t, "l", 0)          # explicit digit count (the boundary's int64 k caps ceil(log_p k))
+        comp = t.p != 0 and (t.k > t.p or lx > 0)
+        if comp and lx > 0 and t.p ** lx < t.k:
+            raise ValueError("HELRM_ERR_LAYOUT: p^l < k")
+        l = (lx or n_digits(t.k, t.p)) if comp else 1
         w = t.p * l if comp else t.k
         if t.weights.shape != (w, t.d):
             raise ValueError("HELRM_ERR_LAYOUT: table weights have the wrong shape")

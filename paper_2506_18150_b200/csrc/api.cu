@@ -1396,17 +1396,22 @@ helrm_status helrm_tables_create(const helrm_params* p, const helrm_table_desc* 
     int64_t I = n_dense, R = 0;
     for (size_t b = 0; b < n_tables; b++) {
       const helrm_table_desc& d = t[b];
-      need(d.k >= 1 && d.d >= 1 && d.p >= 0 && d.w, HELRM_ERR_CONFIG, "bad table description");
+      need(d.k >= 1 && d.d >= 1 && d.p >= 0 && d.l >= 0 && d.w, HELRM_ERR_CONFIG, "bad table description");
       Block B{};
       B.k = d.k;
       B.d = d.d;
       B.p = d.p;
-      B.comp = d.p != 0 && d.k > d.p;
+      B.comp = d.p != 0 && (d.k > d.p || d.l > 0);
       B.l = 1;
       if (B.comp) {
         need(d.p >= 2, HELRM_ERR_CONFIG, "digit base must be >= 2");
         __int128 cap = d.p;
         while (cap < d.k) { cap *= d.p; B.l++; }
+        if (d.l > 0) {   // explicit digit count: p^l >= k, i.e. l >= ceil(log_p k)
+          need(d.l >= B.l, HELRM_ERR_LAYOUT, "p^l < k");
+          need(d.p * d.l <= ((int64_t)1 << 40), HELRM_ERR_CONFIG, "digit segment too wide");
+          B.l = d.l;
+        }
       }
       B.w = B.comp ? d.p * B.l : d.k;
       B.I = d.in_off < 0 ? I : d.in_off;

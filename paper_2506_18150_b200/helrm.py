@@ -44,7 +44,8 @@ class ParamsInfo(ctypes.Structure):
 
 class TableDesc(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int64), ("d", ctypes.c_int64), ("p", ctypes.c_int64),
-                ("w", ctypes.POINTER(ctypes.c_double)), ("in_off", ctypes.c_int64), ("out_off", ctypes.c_int64)]
+                ("w", ctypes.POINTER(ctypes.c_double)), ("in_off", ctypes.c_int64), ("out_off", ctypes.c_int64),
+                ("l", ctypes.c_int64)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -238,7 +239,7 @@ class Tables(_Handle):
 
 
 def tables_create(params: Params, tables: Sequence, n_dense: int) -> Tables:
-    """tables: objects with k, d, p, weights (float64 rows x d), in_off, out_off."""
+    """tables: objects with k, d, p, weights (float64 rows x d), in_off, out_off, l."""
     keep = []
     arr = (TableDesc * len(tables))()
     seen = {}
@@ -251,6 +252,7 @@ def tables_create(params: Params, tables: Sequence, n_dense: int) -> Tables:
         arr[i].k, arr[i].d, arr[i].p = t.k, t.d, t.p
         arr[i].w = _dptr(w)
         arr[i].in_off, arr[i].out_off = getattr(t, "in_off", -1), getattr(t, "out_off", -1)
+        arr[i].l = getattr(t, "l", 0)
     h = ctypes.c_void_p()
     _check(_L.helrm_tables_create(params.h, arr, len(tables), n_dense, ctypes.byref(h)))
     return Tables(h)

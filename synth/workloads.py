@@ -46,7 +46,7 @@ CRITEO_VOCAB_SEED = 230
 
 CONFIG_NAMES = ("tiny_a", "tiny_b", "uci", "criteo", "criteo_b64", "criteo_c2", "criteo_c2_small", "llm",
                 "llm_small", "llm_gen", "llm_gen_small", "tiny_dnum7", "criteo_c17", "criteo_c9_small", "criteo_l4", "mlp_small",
-                "llm_l1", "llm_l1_small", "criteo_c100",
+                "llm_l1", "llm_l1_small", "criteo_c100", "table1", "table1_small",
                 "mlp_512x256", "microbench")
 
 
@@ -74,6 +74,7 @@ class Table:
     in_off: int = -1            # explicit input slot offset, -1 = contiguous default
     out_off: int = -1           # explicit output slot offset, -1 = contiguous default
     weight_id: int = -1         # blocks sharing one weight array carry the same id
+    l: int = 0                  # explicit digit count (p^l >= k), 0 = ceil(log_p k)
 
 
 @dataclasses.dataclass
@@ -158,6 +159,15 @@ _CONFIGS = {
     # "table" is the weight matrix W (in x out, one row per input slot), the input a dense
     # encrypted vector x, the output W^T x
     "mlp_small": Config("mlp_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
+    # the paper's Table-1 shape: one GPT-2 table
+    # (d = 768) decomposed base p = 16 into l = 32 digits -> p l = 512 one-hot input slots and
+    # 768 outputs, one ct each way (the paper: "BSGS 3.17" s on its CPU).  16^32 rows do not
+    # fit the boundary's int64 row index, so the table declares k = 2^63 - 1 rows with an
+    # explicit digit count l = 32 (Table.l): the server-side matrix (32 sub-tables of
+    # 16 x 768) is the paper's, and digits 16..31 of a query are always 0.  LLM ring and
+    # level; table1_small: 16^8 rows, base 16 (8 digits), d = 48 on the Tiny ring.
+    "table1": Config("table1", 16, [(50, 20)], [(50, 4)], 40, 19, 1),
+    "table1_small": Config("table1_small", 12, [(40, 1), (30, 2)], [(40, 1)], 30, 2, 1),
     "mlp_512x256": Config("mlp_512x256", 16, [(50, 24)], [(50, 4)], 40, 23, 1),
     "microbench": Config("microbench", 16, [(50, 24)], [(50, 4)], 40, 23, 1, batch=1024),
 }
@@ -220,6 +230,11 @@ def make_workload(name: str, batch: Optional[int] = None) -> Workload:
         fan_in, fan_out = (64, 32) if name == "mlp_small" else (512, 256)
         w = rng.normal(0.0, 1.0 / np.sqrt(fan_in), size=(fan_in, fan_out))
         return Workload(cfg, [Table(fan_in, fan_out, 0, w)], 0, np.zeros((B, 1), dtype=np.int64), np.zeros((B, 0)))
+    if name in ("table1", "table1_small"):
+        k, d, p, l = (2**63 - 1, 768, 16, 32) if name == "table1" else (16**8, 48, 16, 0)
+        w = rng.normal(0.0, 0.02, size=(p * (l or 8), d))
+        idx = rng.integers(0, k, size=(B, 1), dtype=np.int64)
+        return Workload(cfg, [Table(k, d, p, w, l=l)], 0, idx, np.zeros((B, 0)))
     if name in ("llm_l1", "llm_l1_small"):
         V, d, p, m = (50257, 768, 256, 128) if name == "llm_l1" else (1000, 48, 32, 64)
         w = rng.normal(0.0, 0.02, size=(subtable_rows(V, p), d))

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 def test_host_side_matches_oracle_on_cpu():
     """CPU: primes/psi (D2/D3), table layout and the client query (S0)."""
     from paper_2506_18150_b200 import helrm
-    for name in ("tiny_a", "tiny_b", "uci", "criteo"):
+    for name in ("table1", "table1_small", "tiny_a", "tiny_b", "uci", "criteo"):
         w = synth.make_workload(name)
         P = helrm.params_from_config(w.config)
         PO = core.params_from_config(w.config)
@@ -52,6 +52,9 @@ def test_host_side_matches_oracle_on_cpu():
     with pytest.raises(helrm.HelrmError) as e:
         helrm.encode_query(T, [10**9] * 26, [], lay.K)
     assert e.value.code == 5
+    with pytest.raises(helrm.HelrmError) as e:      # explicit digit count with p^l < k
+        helrm.tables_create(P, [synth.Table(1000, 4, 4, np.zeros((16, 4)), l=4)], 0)
+    assert e.value.code == 6
 
 
 gpu = pytest.mark.gpu
@@ -286,7 +289,7 @@ def _gpu_lookup(E, w, mode=0, n1=0):
 @pytest.mark.parametrize("name,mode", [("tiny_a", 0), ("tiny_b", 0), ("uci", 0), ("uci", 1), ("tiny_b", 1),
                                        ("llm_small", 0), ("llm_small", 1), ("criteo_c2_small", 0),
                                        ("llm_gen_small", 0), ("tiny_dnum7", 0), ("tiny_dnum7", 1),
-                                       ("criteo_c9_small", 0)])
+                                       ("criteo_c9_small", 0), ("table1_small", 0)])
 def test_lookup_bit_exact_vs_oracle(name, mode, torch_mod):
     E = env(name, torch_mod)
     w = synth.make_workload(name)
@@ -416,6 +419,30 @@ def test_llm_gen_full_size_decryption(torch_mod):
     _golden_outputs(E, "llm_gen", outs[0])
     lay = lk.layout(w)
     z = E.h.decrypt_decode(E.ctx, sk, outs[0][0])
+    assert np.abs(z[: lay.M] - lk.gather(lay, w.indices[0])).max() < 1e-3
+
+
+@gpu
+def test_table1_shape_full_size(torch_mod):
+    """The paper's Table-1 shape at full size (GPT-2 d = 768,
+    p = 16, l = 32 -> 512 one-hot slots, one ct in and out) on the LLM ring:
+    plan counts and the decrypted output against the 32-digit gather."""
+    E = env("llm", torch_mod)
+    h, w = E.h, synth.make_workload("table1")
+    cfg = w.config
+    T = h.tables_create(E.P, w.tables, w.n_dense)
+    plan = h.plan_create(E.ctx, T, cfg.level)
+    info = plan.info()
+    assert (info.K, info.M, info.n_in_cts, info.n_out_cts, info.mbar) == (512, 768, 1, 1, 1024)
+    sk = h.sk_gen(E.ctx, cfg.seed)
+    pk = h.pk_gen(E.ctx, sk, cfg.seed)
+    rk = h.rotkeys_gen(E.ctx, sk, plan.galois(), cfg.seed)
+    x = h.encode_query(T, w.indices[0], w.dense[0], cfg.n_slots)
+    assert x.sum() == 32
+    ct = h.encrypt(E.ctx, pk, x, cfg.level, cfg.seed << 20)
+    out = h.lookup(E.ctx, plan, rk, [ct])
+    lay = lk.layout(w)
+    z = h.decrypt_decode(E.ctx, sk, out[0])
     assert np.abs(z[: lay.M] - lk.gather(lay, w.indices[0])).max() < 1e-3
 
 

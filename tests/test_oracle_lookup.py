@@ -459,3 +459,38 @@ def test_criteo_100_ct_layout():
     w = synth.make_workload("criteo_c100")
     lay = lk.layout(w)
     assert lay.K == 3272921 and -(-lay.K // (1 << 15)) == 100 and lay.M == 416
+
+
+def test_table1_shape_layout_and_digits():
+    """The paper's Table-1 shape (p = 16, l = 32, d = 768,
+    "p l = 512 slots"): 512 one-hot input slots, 768 outputs, one ct each way;
+    the query has one 1 per 16-slot digit segment (32 ones, LSD first) and the
+    gather is the sum of the 32 sub-table rows.  An explicit l below
+    ceil(log_p k) is a layout error."""
+    w = synth.make_workload("table1")
+    lay = lk.layout(w)
+    assert (lay.K, lay.M) == (512, 768)
+    b = lay.blocks[0]
+    assert (b.compressed, b.l, b.w) == (True, 32, 512)
+    i = int(w.indices[0, 0])
+    x = lk.encode_query(lay, w.indices[0], w.dense[0])
+    digits = lk.digit_decompose(i, 16, 32)
+    assert x.sum() == 32 and all(x[t * 16 + dg] == 1 for t, dg in enumerate(digits))
+    assert all(dg == 0 for dg in digits[16:])              # i < 2^63 < 16^16
+    y = lk.gather(lay, w.indices[0])
+    assert np.allclose(y, sum(w.tables[0].weights[t * 16 + dg] for t, dg in enumerate(digits)), atol=0)
+    plan = lk.make_plan(lay, 1 << 15, 19)
+    assert (plan.C, plan.O, plan.mbar) == (1, 1, 1024)
+    bad = types.SimpleNamespace(tables=[synth.Table(1000, 4, 4, np.zeros((16, 4)), l=4)], n_dense=0)
+    with pytest.raises(ValueError, match="LAYOUT"):
+        lk.layout(bad)                                      # 4^4 = 256 < 1000
+
+
+def test_table1_small_lookup_decrypts_to_gather():
+    """Table-1 shape on the Tiny ring (16^8 rows, base 16, 8 digits, d = 48):
+    the oracle lookup decrypts to the digit gather."""
+    w = synth.make_workload("table1_small")
+    run = lk.run_config(w)
+    assert (run.lay.K, run.lay.M, run.lay.blocks[0].l) == (128, 48, 8)
+    z = core.decrypt_decode(run.P, run.sk, run.outs[0][0])
+    assert np.abs(z[: run.lay.M] - lk.gather(run.lay, w.indices[0])).max() < 1e-3
