@@ -628,14 +628,13 @@ static void modup_batch(helrm_ctx* c, const uint64_t* in, size_t in_stride, int 
 // D16 for G polynomials: y_g = y + g ys ([l+1+K][N]) -> out_g = out + g os ([l+1][N])
 // (accumulate: out += ModDown(y); the finishing (y - t) P^-1 runs in the NTT's pass-2 epilogue)
 static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uint32_t l, uint64_t* out, size_t os,
-                          cudaStream_t st = nullptr, bool accumulate = false, uint64_t* scratch = nullptr) {
+                          cudaStream_t st = nullptr, bool accumulate = false) {
   const Params& P = c->P;
   const size_t N = P.N, nq = l + 1;
   const LevelConst& lc = level_const(c, l);
   if (!st) st = c->stream;
-  if (!scratch) scratch = c->scratch;
   DBuf yp(c, G * P.K * N, st), t(c, G * nq * N, st);
-  launch_ntt_inv(c->dc(st), y + nq * N, yp.p, scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
+  launch_ntt_inv(c->dc(st), y + nq * N, yp.p, c->scratch, G * P.K, P.map_range(P.L + 1, P.K), ys, P.K * N,
                  lc.moddown_post, pm_lidx(c, G, P.K));
   launch_conv_rows(c->dc(st), lc.moddown_tab, 1, (int)nq, (int)P.K, yp.p, P.K * N, t.p, nq * N, 0, G, P.map_q(l));
   NttEpi epi;
@@ -646,7 +645,7 @@ static void moddown_batch(helrm_ctx* c, const uint64_t* y, size_t ys, int G, uin
   epi.s = lc.pinv;
   epi.sp = lc.pinvs;
   epi.accumulate = accumulate ? 1 : 0;
-  launch_ntt_fwd(c->dc(st), t.p, t.p, scratch, G * nq, P.map_q(l), 0, 0, true, pm_lidx(c, G, (uint32_t)nq), &epi);
+  launch_ntt_fwd(c->dc(st), t.p, t.p, c->scratch, G * nq, P.map_q(l), 0, 0, true, pm_lidx(c, G, (uint32_t)nq), &epi);
 }
 
 static void modup(helrm_ctx* c, const uint64_t* in, uint32_t l, int k, uint64_t* out) {
@@ -2511,20 +2510,11 @@ static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t
   if (mbar >= n) return;
   const size_t N = P.N, nq = l + 1, nqN = nq * N, nl = l + 1 + P.K, nlN = nl * N, dn = P.dnum(l);
   const LevelConst& lc = level_const(c, l);
-  // The next rotation needs c1 first (its ModUp) and c0 only in its key switch (P phi(c0) is
-  // added there), so the c0 half of each ModDown runs on a side stream, beside the next
-  // rotation's INTT / conversion / NTT, with its own NTT scratch; the key switch waits for it.
-  // (Splitting the key switch itself into halves measured slower: 7.23 vs 6.91-7.06 ms per
-  // Criteo lookup -- the digits are read twice.)  HELRM_ROTSUM_SPLIT=0: both halves in one
-  // ModDown on the context stream.
-  static const int split_env = getenv("HELRM_ROTSUM_SPLIT") ? atoi(getenv("HELRM_ROTSUM_SPLIT")) : 1;
-  const bool split = split_env != 0 && c->s_mac != nullptr && Qc <= 4;
-  cudaStream_t side = c->s_mac;
+  // (splitting every rotation into a c1 chain on the context stream and a c0 chain on a side
+  // stream, the halves of each key switch separate, measured slower: 7.23 vs 6.91-7.06 ms per
+  // Criteo lookup -- the digits are read twice and the ModDowns lose their 2-poly batching)
   {
     DBuf D(c, (size_t)Qc * dn * nlN), T(c, (size_t)Qc * 2 * nlN);
-    DBuf scr(c, split ? std::min<size_t>(ntt_scratch_words(P.log_n), (size_t)Qc * nq * N) : 0);
-    if (split) c->join(side, c->stream);   // the side stream's buffers are allocated on the context stream
-    bool pending = false;
     for (int64_t r = mbar; r < n; r *= 2) {
       const uint64_t g = galois_of_rot(c, r);
       modup_batch(c, S + nqN, 2 * nqN, Qc, l, D.p, nullptr, false);
@@ -2550,18 +2540,9 @@ static void rot_sum_batch(helrm_ctx* c, uint64_t* S, int Qc, uint32_t l, int64_t
       a.dq = dn * nlN;
       a.aq = 2 * nqN;
       a.oq = 2 * nlN;
-      if (pending) c->join(c->stream, side);   // c0 updated and T free before the key switch
       launch_kip(c->dc(), a, P.map_qp(l));
-      if (split) {
-        c->join(side, c->stream);
-        moddown_batch(c, T.p + nlN, 2 * nlN, Qc, l, S + nqN, 2 * nqN, nullptr, true);   // c1 += ...
-        moddown_batch(c, T.p, 2 * nlN, Qc, l, S, 2 * nqN, side, true, scr.p);          // c0 += ...
-        pending = true;
-      } else {
-        moddown_batch(c, T.p, nlN, 2 * Qc, l, S, nqN, nullptr, true);   // S += Rotate(S)
-      }
+      moddown_batch(c, T.p, nlN, 2 * Qc, l, S, nqN, nullptr, true);   // S += Rotate(S)
     }
-    if (pending) c->join(c->stream, side);
   }
 }
 
