@@ -105,7 +105,7 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
                                              const uint8_t* __restrict__ tpos, const uint32_t* __restrict__ lidx,
                                              const NttEpi& epi) {
   constexpr int S = 1 << SLOG, TS = S / kEPT, SUBS = kThreads / TS;
-  constexpr bool P1 = MODE != 1;  // MODE 2: pass 1 on centred doubles (conversion output)
+  constexpr bool P1 = MODE != 1;  // MODE 2: pass 1 on integer-valued doubles below 4q (conversion output)
   const int N = 1 << log_n;
   const size_t gl = lidx ? lidx[limb0 + limb] : limb0 + limb;
   const int pr = map.pr[gl % map.n];

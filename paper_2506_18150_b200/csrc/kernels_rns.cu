@@ -134,7 +134,8 @@ __global__ void k_automorph(const uint64_t* __restrict__ a, uint64_t* __restrict
   out[o] = accumulate ? add_mod(out[o], v, primes[map.pr[l]].rc.q) : v;
 }
 
-// D14 from y-form sources: out_gk[r][i] = sum_b y_g[row0 + b][i] cf_kr[b] mod q_r for
+// D14 from y-form sources: out_gk[r][i] = sum_b y_g[row0 + b][i] cf_kr[b] mod q_r (as an
+// integer-valued double below 4q, not yet reduced when nb <= 4) for
 // every row r (the table also reproduces a digit's own rows); the CTA stages
 // its conversion's table in shared memory, each thread loads its nb sources
 // once and produces all rows.  grid (N/256, G ncv).
@@ -172,8 +173,10 @@ __global__ void __launch_bounds__(256) k_conv_rows(const ConvRowDev* __restrict_
     for (int u = 0; u < PT; u++) {
       double acc = 0.0;
 #pragma unroll
-      for (int b = 0; b < NB; b++) acc += fm::mmul(v[u][b], cf[b].x, cf[b].y, q);  // each in [-q/2, q/2]
-      o[(size_t)orow * N + 256 * u] = (uint64_t)__double_as_longlong(fm::cred(acc, q, qi));
+      for (int b = 0; b < NB; b++) acc += fm::mmul(v[u][b], cf[b].x, cf[b].y, q);  // each |.| <= 0.75 q
+      // every conversion output feeds a forward NTT (MODE 2), whose butterflies take inputs
+      // below 4q: with NB <= 4 terms |acc| <= 3q, so the final reduction is left to it
+      o[(size_t)orow * N + 256 * u] = (uint64_t)__double_as_longlong(NB <= 4 ? acc : fm::cred(acc, q, qi));
     }
   }
 }
