@@ -164,7 +164,10 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
       if (P1) sm[e * SUBS + sub] = r[k];
       else sm[sub * kBlkPad + pidx(e)] = r[k];
     }
-    __syncthreads();
+    // pass 2: a 256-point block is held by 16 consecutive threads (half a warp) in its own
+    // shared-memory rows, so the exchange only needs the warp; pass 1's columns span the CTA
+    if (P1) __syncthreads();
+    else __syncwarp();
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const int e = kEPT * t + k;
@@ -357,7 +360,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_ntt_inv(const uint64_t* __restr
       if (MODE == 0) sm[e * SUBS + sub] = r[k];
       else sm[sub * kBlkPad + pidx(e)] = r[k];
     }
-    __syncthreads();
+    if (MODE == 0) __syncthreads();
+    else __syncwarp();   // pass A: each block's rows belong to its half-warp (as the forward pass 2)
 #pragma unroll
     for (int k = 0; k < kEPT; k++) {
       const int e = t + TS * k;
