@@ -135,6 +135,20 @@ __device__ __forceinline__ void ntt_fwd_body(double* sm, unsigned bx, size_t lim
       }
     }
   }
+  if (!P1 && epi.out != nullptr && (tid & 15) == 0) {
+    // fused ModDown / rescale epilogue: its y (and out) lines towards L2 now, so the reads at
+    // the end of the CTA do not add an HBM round trip (one thread per 128-byte line)
+    const int lgs = log_n - 9, g = (int)bx * 16;
+    const size_t pbase = (size_t)(g >> lgs) * (size_t)(N >> 1) + (g & ((1 << lgs) - 1));
+    const size_t gstep = (size_t)16 << lgs, pg = gl / map.n, lg = gl % map.n;
+    const uint64_t* yg = epi.y + pg * epi.ys + lg * (size_t)N + pbase + ((size_t)(tid / 16) << lgs);
+    const uint64_t* og = epi.out + pg * epi.os + lg * (size_t)N + pbase + ((size_t)(tid / 16) << lgs);
+#pragma unroll
+    for (int it = 0; it < 16; it++) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(yg + it * gstep));
+      if (epi.accumulate) asm volatile("prefetch.global.L2 [%0];" ::"l"(og + it * gstep));
+    }
+  }
   // phase A: stages 0..3 on layout e = t + TS k (twiddles independent of t)
   // Lazy reduction: a butterfly's product term is reduced by mmul (|r| <= 0.75 q for any
   // |y| < 4q, centred twiddles), so only the additive inputs grow, by 0.75 q per stage.
