@@ -212,7 +212,7 @@ __global__ void k_rescale_prep(const uint64_t* __restrict__ xl, size_t xs, uint6
 // flight before the first product (a runtime bound made the compiler convert
 // each digit right after its load, serialising the memory latency).
 template <int DNUM, int QR>
-__global__ void __launch_bounds__(256, 3) k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
+__global__ void __launch_bounds__(256, QR == 1 ? 4 : 3) k_kip(const __grid_constant__ KipArgs a, const PrimeDev* __restrict__ primes,
                                              const __grid_constant__ LimbMap map, uint32_t N) {
   pdl_wait_trigger();
   // work item w = (tile, limb); a grid smaller than the work loops (persistent CTAs)
