@@ -131,6 +131,26 @@ def test_criteo_100_ct_full_size(torch_mod):
 
 
 @gpu
+def test_criteo_17_ct_full_size(torch_mod):
+    """The 10^2x Criteo model analog (569,545 slots, 18
+    input cts; ours 535,963 slots = 17 cts, 8704 diagonals = 119 GiB in
+    QP-NTT form) on a compact plan: plan counts and the decrypted output
+    against the gather.  (The stored-plan form, 166 GiB of HBM in use, runs
+    alone: tests/manual/c17_check.py, profiles/r01_c17.txt.)"""
+    E = env("criteo", torch_mod)
+    h, w = E.h, synth.make_workload("criteo_c17")
+    T, plan, sk, rk, cts = _setup(E, w, True)
+    info = plan.info()
+    assert (info.n_in_cts, info.n_diag, info.n1) == (17, 8704, 32)
+    out = h.lookup(E.ctx, plan, rk, cts)
+    lay = lk.layout(w)
+    z = h.decrypt_decode(E.ctx, sk, out[0])
+    assert np.abs(z[: lay.M] - lk.gather(lay, w.indices[0])).max() < 1e-3
+    for c in cts:
+        c.close()
+
+
+@gpu
 @pytest.mark.parametrize("knobs", [{"HELRM_COMPACT_GROUP_GIB": "0.001", "HELRM_COMPACT_EXP_GIB": "0.001"},
                                    {"HELRM_COMPACT_GROUP_GIB": "0.02", "HELRM_COMPACT_EXP_GIB": "0.01"}])
 def test_compact_chunking_knobs(knobs):
