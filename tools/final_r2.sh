@@ -12,6 +12,6 @@ if [ $rc -eq 0 ]; then
     python bench.py --ncu-step --warmup 3 --skip-cpu-baseline > gpurun_out/r2_final_ncu_full.log 2>&1
   echo "ncu full rc=$?"
   python tools/ncu_traffic.py /tmp/r2_full.ncu-rep > gpurun_out/r2_final_ncu_traffic.json 2>&1
-  python tools/ncu_summary.py /tmp/r2_full.ncu-rep 40 > gpurun_out/r2_final_ncu_full_summary.txt 2>&1
+  python tools/ncu_summary.py /tmp/r2_full.ncu-rep 400 > gpurun_out/r2_final_ncu_full_summary.txt 2>&1
   python tools/launch_summary.py gpurun_out/r2_final_launches.csv > gpurun_out/r2_final_launch_summary.txt 2>&1
 fi
